@@ -1,0 +1,161 @@
+/*
+ * emm.h — C ABI of the B200-native SGEMM ("emm", after the paper's Emmerald).
+ *
+ * The operation (the method's hot path, BASELINE.json north_star):
+ *
+ *     C <- alpha * op(A) * op(B) + beta * C          (single precision)
+ *
+ * is the Level-3 BLAS SGEMM the paper implements ("Emmerald implements the
+ * SGEMM interface of Level-3 BLAS", §Introduction) — dense
+ * matrix multiplication of A: M x K by B: K x N in 2MNK flops
+ * (PAPER.md:33-38), each C_ij the dot product of PAPER.md:277-279 (§L0
+ * blocking, eq. 1).  Storage is COLUMN-major (reading R2):
+ * element (r, c) of an array X with leading dimension ld is X[r + c*ld].
+ *
+ *   transA = 'N'/'n': A is stored M x K, lda >= max(1, M)
+ *            'T'/'t'/'C'/'c': A is stored K x M, lda >= max(1, K)
+ *   transB = 'N'/'n': B is stored K x N, ldb >= max(1, K)
+ *            'T'/'t'/'C'/'c': B is stored N x K, ldb >= max(1, N)
+ *   C is M x N, ldc >= max(1, M).    ('C' means 'T' for real data.)
+ *
+ * Ownership / lifetime: every matrix pointer of emm_sgemm* is a DEVICE
+ * pointer owned by the caller (allocated e.g. with torch), valid until
+ * `stream` reaches the enqueued work.  The library keeps no pointer after
+ * return.  All calls are stream-ordered and asynchronous (no host sync),
+ * except emm_sgemm_host which is synchronous.  `stream` is a cudaStream_t
+ * passed as void* (NULL = legacy default stream).
+ *
+ * Semantics (reading R4 in DESIGN.md):
+ *   beta == 0 (incl. -0.0): C is never read (NaN/Inf in C do not propagate).
+ *   alpha == 0 or K == 0: A and B are never read; C <- beta*C.
+ *   Quick return (nothing launched) when M == 0, N == 0, or
+ *   ((alpha == 0 or K == 0) and beta == 1).
+ *   Only the M x N logical region of C is written; ldc padding never is.
+ *   Results are run-to-run deterministic (no atomics, no split-K).
+ *   Reentrant; concurrent calls on different streams are safe when their C
+ *   ranges are disjoint.
+ *
+ * Errors: 0 = success.  -i = BLAS argument i invalid (transA=1 transB=2 M=3
+ * N=4 K=5 A=7 lda=8 B=9 ldb=10 C=12 ldc=13; a NULL or non-4-byte-aligned
+ * pointer is rejected only when that operand would be read or written).
+ * Negative EMM_ERR_* below; 1000 + cudaError_t for CUDA errors; 2000 +
+ * ncclResult_t for NCCL errors.  On any argument error C is unmodified and
+ * nothing is launched.
+ */
+#ifndef EMM_H_
+#define EMM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EMM_SUCCESS 0
+#define EMM_ERR_ALIAS (-100)      /* C's byte range overlaps A's or B's          */
+#define EMM_ERR_ARCH (-101)       /* current device is not compute capability 10.0 */
+#define EMM_ERR_WORKSPACE (-102)  /* workspace too small / misaligned            */
+#define EMM_ERR_MATH (-103)       /* unknown emm_math_t                          */
+#define EMM_ERR_COMM (-104)       /* bad communicator / NCCL unavailable         */
+#define EMM_ERR_NOMEM (-105)      /* host or device allocation failed            */
+#define EMM_ERR_CUDA_BASE 1000
+#define EMM_ERR_NCCL_BASE 2000
+
+/* Arithmetic of the product.  All report 2MNK flops.
+ *   EMM_MATH_3XTF32: FP32-accurate tcgen05 tensor-core path; each operand is
+ *     split x = big + small (big = rn_tf32(x), small = rn_tf32(x - big)) and
+ *     C accumulates small*big + big*small + big*big in FP32 in TMEM.
+ *   EMM_MATH_FFMA:   FP32 FFMA on CUDA cores (register-blocked tiles).
+ *   EMM_MATH_1XTF32: one TF32 product per step (exposed lower precision). */
+typedef enum {
+    EMM_MATH_3XTF32 = 0,
+    EMM_MATH_FFMA = 1,
+    EMM_MATH_1XTF32 = 2
+} emm_math_t;
+
+/* C <- alpha*op(A)*op(B) + beta*C with the default FP32-accurate path
+ * (EMM_MATH_3XTF32).  Scratch for the operand split is taken from a
+ * stream-ordered pool (cudaMallocAsync/cudaFreeAsync on `stream`). */
+int emm_sgemm(char transA, char transB, int64_t M, int64_t N, int64_t K,
+              float alpha, const float *A, int64_t lda,
+              const float *B, int64_t ldb,
+              float beta, float *C, int64_t ldc, void *stream);
+
+/* Same, with an explicit math mode and an optional caller-owned device
+ * workspace (>= emm_sgemm_workspace_bytes(...), 1024-byte aligned).
+ * workspace == NULL -> stream-ordered pool as in emm_sgemm. */
+int emm_sgemm_ex(char transA, char transB, int64_t M, int64_t N, int64_t K,
+                 float alpha, const float *A, int64_t lda,
+                 const float *B, int64_t ldb,
+                 float beta, float *C, int64_t ldc, void *stream,
+                 emm_math_t math, void *workspace, size_t workspace_bytes);
+
+/* Device workspace the call above needs (0 for EMM_MATH_FFMA).  Host-only. */
+size_t emm_sgemm_workspace_bytes(char transA, char transB, int64_t M, int64_t N,
+                                 int64_t K, emm_math_t math);
+
+/* End-to-end form: A, B, C are HOST pointers (pinned or pageable, same
+ * layouts as above).  Copies A, B (and C when beta != 0) to device buffers
+ * cached by the library, runs emm_sgemm_ex on an internal stream, copies C
+ * back and synchronises.  Returns when C holds the result. */
+int emm_sgemm_host(char transA, char transB, int64_t M, int64_t N, int64_t K,
+                   float alpha, const float *A, int64_t lda,
+                   const float *B, int64_t ldb,
+                   float beta, float *C, int64_t ldc, emm_math_t math);
+
+/* Frees the device buffers cached by emm_sgemm_host.  Host-only. */
+void emm_release_cache(void);
+
+/* ----------------------------------------------------------------------
+ * Row-sharded multi-GPU SGEMM (BASELINE.json north_star, "Multi-GPU":
+ * C row blocks per rank, B broadcast, optional C all-gather over NCCL).
+ * One process per GPU.  The communicator wraps NCCL (loaded at run time).
+ * -------------------------------------------------------------------- */
+
+/* Rank r's block of rows of C (and of op(A)): [*row0, *row0 + *rows).
+ * Blocks are multiples of 256 rows (the tensor-core tile of a CTA pair)
+ * except the last, balanced to within one tile; they tile [0, M) exactly in
+ * rank order.  Host-only; valid for nranks >= 1, 0 <= rank < nranks. */
+void emm_row_partition(int64_t M, int nranks, int rank, int64_t *row0, int64_t *rows);
+
+/* 128-byte NCCL unique id, produced on one rank and distributed by the
+ * caller (e.g. torch.distributed broadcast).  Returns EMM_ERR_COMM if NCCL
+ * cannot be loaded. */
+int emm_get_unique_id(void *id128);
+int emm_comm_create(void **comm, const void *id128, int nranks, int rank);
+int emm_comm_destroy(void *comm);
+
+/* Collective: every rank calls with identical (trans, M, N, K, alpha, beta,
+ * root).  A_local: this rank's rows of op(A) as an (rows x K) op-matrix
+ * (transA='N': stored rows x K with lda >= rows; 'T': stored K x rows).
+ * B: K x N op(B) storage, valid on `root`; on other ranks a buffer of the
+ * same size that receives it (broadcast in column panels, each panel's
+ * GEMM overlapping the next panel's transfer).  C_local: this rank's rows x N
+ * block (ldc >= rows).  C_full (nullable): if set, receives the whole M x N
+ * result on every rank (ldc_full >= M) via NCCL all-gather.  ldb must equal
+ * the stored rows of B (panels are contiguous). */
+int emm_sgemm_multi(void *comm, char transA, char transB, int64_t M, int64_t N, int64_t K,
+                    float alpha, const float *A_local, int64_t lda,
+                    float *B, int64_t ldb, int root,
+                    float beta, float *C_local, int64_t ldc,
+                    float *C_full, int64_t ldc_full, void *stream, emm_math_t math);
+
+/* ----------------------------------------------------------------------
+ * Introspection (host-only).
+ * -------------------------------------------------------------------- */
+const char *emm_strerror(int status);
+const char *emm_version(void);
+/* Number of kernels this library has launched in this process. */
+uint64_t emm_launch_count(void);
+/* Optional per-kernel CUDA-event timing of the dominant kernel (the GEMM
+ * main loop): enable, run, then read the summed device milliseconds and the
+ * number of timed launches (synchronises the recorded events). */
+void emm_profile_enable(int on);
+int emm_profile_read(double *gemm_ms, uint64_t *gemm_launches, double *other_ms,
+                     uint64_t *other_launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EMM_H_ */

@@ -1,0 +1,353 @@
+// api.cu — the C ABI of include/emm.h: argument validation (BLAS rules),
+// quick returns, path selection and launch.  No CPU fallback: every step of
+// the product runs in this library's kernels; if the device is not sm_100 the
+// call fails with EMM_ERR_ARCH.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "emm_internal.h"
+
+namespace emm {
+
+std::atomic<uint64_t> g_launches{0};
+
+// ------------------------------------------------------------ profiling
+namespace {
+std::atomic<int> g_prof_on{0};
+std::mutex g_prof_mu;
+struct ProfRec {
+    cudaEvent_t a, b;
+    bool gemm;
+};
+std::vector<ProfRec> g_prof;
+}  // namespace
+
+void prof_begin(cudaStream_t s, bool, cudaEvent_t *ev0) {
+    *ev0 = nullptr;
+    if (!g_prof_on.load(std::memory_order_relaxed)) return;
+    if (cudaEventCreate(ev0) != cudaSuccess) {
+        *ev0 = nullptr;
+        return;
+    }
+    cudaEventRecord(*ev0, s);
+}
+
+void prof_end(cudaStream_t s, bool is_gemm, cudaEvent_t ev0) {
+    if (!ev0) return;
+    cudaEvent_t ev1;
+    if (cudaEventCreate(&ev1) != cudaSuccess) return;
+    cudaEventRecord(ev1, s);
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    g_prof.push_back({ev0, ev1, is_gemm});
+}
+
+// ------------------------------------------------------------ validation
+static bool trans_ok(char t) { return t == 'N' || t == 'n' || t == 'T' || t == 't' || t == 'C' || t == 'c'; }
+static bool is_n(char t) { return t == 'N' || t == 'n'; }
+static int64_t max1(int64_t v) { return v > 1 ? v : 1; }
+
+static int check_args(char tA, char tB, int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb, int64_t ldc) {
+    if (!trans_ok(tA)) return -1;
+    if (!trans_ok(tB)) return -2;
+    if (M < 0) return -3;
+    if (N < 0) return -4;
+    if (K < 0) return -5;
+    if (lda < max1(is_n(tA) ? M : K)) return -8;
+    if (ldb < max1(is_n(tB) ? K : N)) return -10;
+    if (ldc < max1(M)) return -13;
+    return 0;
+}
+
+static bool ptr_bad(const void *p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 3u) != 0; }
+
+// byte range [lo, hi) spanned by a column-major rows x cols array
+static void span(const void *p, int64_t rows, int64_t cols, int64_t ld, uintptr_t *lo, uintptr_t *hi) {
+    *lo = reinterpret_cast<uintptr_t>(p);
+    *hi = *lo + (uintptr_t)(((cols - 1) * ld + rows) * 4);
+}
+
+static int check_device() {
+    static std::mutex mu;
+    static int cached[64];
+    static bool init = false;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return EMM_ERR_CUDA_BASE + (int)e;
+    std::lock_guard<std::mutex> g(mu);
+    if (!init) {
+        for (int &c : cached) c = -1;
+        init = true;
+    }
+    if (dev < 0 || dev >= 64) return EMM_ERR_ARCH;
+    if (cached[dev] < 0) {
+        int maj = 0, min = 0;
+        cudaDeviceGetAttribute(&maj, cudaDevAttrComputeCapabilityMajor, dev);
+        cudaDeviceGetAttribute(&min, cudaDevAttrComputeCapabilityMinor, dev);
+        cached[dev] = (maj == 10 && min == 0) ? 1 : 0;
+    }
+    return cached[dev] ? 0 : EMM_ERR_ARCH;
+}
+
+static int cuda_status(cudaError_t e) { return e == cudaSuccess ? 0 : EMM_ERR_CUDA_BASE + (int)e; }
+
+static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+static int planes_of(emm_math_t m) { return m == EMM_MATH_3XTF32 ? 2 : 1; }
+
+static size_t ws_bytes(int64_t M, int64_t N, int64_t K, emm_math_t math) {
+    if (math == EMM_MATH_FFMA || M == 0 || N == 0 || K == 0) return 0;
+    const int64_t Kp = tc_kpad(K);
+    const size_t pl = (size_t)planes_of(math);
+    return align_up(pl * (size_t)M * (size_t)Kp * 4, 1024) + align_up(pl * (size_t)N * (size_t)Kp * 4, 1024);
+}
+
+}  // namespace emm
+
+using namespace emm;
+
+extern "C" size_t emm_sgemm_workspace_bytes(char transA, char transB, int64_t M, int64_t N, int64_t K,
+                                            emm_math_t math) {
+    (void)transA;
+    (void)transB;
+    if (M < 0 || N < 0 || K < 0) return 0;
+    return ws_bytes(M, N, K, math);
+}
+
+extern "C" int emm_sgemm_ex(char transA, char transB, int64_t M, int64_t N, int64_t K, float alpha, const float *A,
+                            int64_t lda, const float *B, int64_t ldb, float beta, float *C, int64_t ldc, void *stream,
+                            emm_math_t math, void *workspace, size_t workspace_bytes) {
+    int st = check_args(transA, transB, M, N, K, lda, ldb, ldc);
+    if (st) return st;
+    if (math != EMM_MATH_3XTF32 && math != EMM_MATH_FFMA && math != EMM_MATH_1XTF32) return EMM_ERR_MATH;
+    // quick return (BLAS): nothing to do
+    if (M == 0 || N == 0) return 0;
+    const bool ab_used = !(alpha == 0.0f || K == 0);
+    if (!ab_used && beta == 1.0f) return 0;
+    if (ptr_bad(C)) return -12;
+    if (ab_used) {
+        if (ptr_bad(A)) return -7;
+        if (ptr_bad(B)) return -9;
+        uintptr_t c0, c1, a0, a1, b0, b1;
+        span(C, M, N, ldc, &c0, &c1);
+        span(A, is_n(transA) ? M : K, is_n(transA) ? K : M, lda, &a0, &a1);
+        span(B, is_n(transB) ? K : N, is_n(transB) ? N : K, ldb, &b0, &b1);
+        if ((c0 < a1 && a0 < c1) || (c0 < b1 && b0 < c1)) return EMM_ERR_ALIAS;
+    }
+    if ((st = check_device())) return st;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+
+    if (!ab_used) return cuda_status(launch_scale_c(M, N, beta, C, ldc, s));
+
+    if (math == EMM_MATH_FFMA)
+        return cuda_status(
+            launch_ffma_sgemm(!is_n(transA), !is_n(transB), M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, s));
+
+    // tensor-core paths: re-buffer/split both operands, then tcgen05 GEMM
+    const size_t need = ws_bytes(M, N, K, math);
+    void *ws = workspace;
+    bool own = false;
+    if (ws) {
+        if (workspace_bytes < need || (reinterpret_cast<uintptr_t>(ws) & 1023u)) return EMM_ERR_WORKSPACE;
+    } else {
+        cudaError_t e = cudaMallocAsync(&ws, need, s);
+        if (e != cudaSuccess) return cuda_status(e);
+        own = true;
+    }
+    const int64_t Kp = tc_kpad(K);
+    const int planes = planes_of(math);
+    float *Ap = reinterpret_cast<float *>(ws);
+    float *Bp = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(ws) +
+                                          align_up((size_t)planes * (size_t)M * (size_t)Kp * 4, 1024));
+    cudaError_t e = launch_pack_split(A, lda, /*kcontig=*/!is_n(transA), M, K, Kp, planes, Ap, s);
+    if (e == cudaSuccess) e = launch_pack_split(B, ldb, /*kcontig=*/is_n(transB), N, K, Kp, planes, Bp, s);
+    if (e == cudaSuccess)
+        e = launch_tc_sgemm(math == EMM_MATH_3XTF32 ? 3 : 1, Ap, Bp, M, N, Kp, alpha, beta, C, ldc, s);
+    if (own) {
+        cudaError_t e2 = cudaFreeAsync(ws, s);
+        if (e == cudaSuccess) e = e2;
+    }
+    return cuda_status(e);
+}
+
+extern "C" int emm_sgemm(char transA, char transB, int64_t M, int64_t N, int64_t K, float alpha, const float *A,
+                         int64_t lda, const float *B, int64_t ldb, float beta, float *C, int64_t ldc, void *stream) {
+    return emm_sgemm_ex(transA, transB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, stream, EMM_MATH_3XTF32,
+                        nullptr, 0);
+}
+
+// ------------------------------------------------------------ host-buffer form
+namespace {
+std::mutex g_host_mu;
+struct HostCache {
+    void *dA = nullptr, *dB = nullptr, *dC = nullptr, *dW = nullptr;
+    size_t nA = 0, nB = 0, nC = 0, nW = 0;
+    cudaStream_t s = nullptr;
+    int dev = -1;
+} g_hc;
+
+int ensure(void **p, size_t *have, size_t need) {
+    if (*have >= need && *p) return 0;
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    *have = 0;
+    if (need == 0) return 0;
+    cudaError_t e = cudaMalloc(p, need);
+    if (e != cudaSuccess) return EMM_ERR_CUDA_BASE + (int)e;
+    *have = need;
+    return 0;
+}
+}  // namespace
+
+extern "C" int emm_sgemm_host(char transA, char transB, int64_t M, int64_t N, int64_t K, float alpha, const float *A,
+                              int64_t lda, const float *B, int64_t ldb, float beta, float *C, int64_t ldc,
+                              emm_math_t math) {
+    int st = check_args(transA, transB, M, N, K, lda, ldb, ldc);
+    if (st) return st;
+    if (math != EMM_MATH_3XTF32 && math != EMM_MATH_FFMA && math != EMM_MATH_1XTF32) return EMM_ERR_MATH;
+    if (M == 0 || N == 0) return 0;
+    const bool ab_used = !(alpha == 0.0f || K == 0);
+    if (!ab_used && beta == 1.0f) return 0;
+    if (C == nullptr) return -12;
+    if (ab_used && A == nullptr) return -7;
+    if (ab_used && B == nullptr) return -9;
+    if ((st = check_device())) return st;
+    std::lock_guard<std::mutex> g(g_host_mu);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (g_hc.dev != dev || !g_hc.s) {
+        if (g_hc.s) cudaStreamDestroy(g_hc.s);
+        g_hc = HostCache{};
+        cudaError_t e = cudaStreamCreateWithFlags(&g_hc.s, cudaStreamNonBlocking);
+        if (e != cudaSuccess) return cuda_status(e);
+        g_hc.dev = dev;
+    }
+    const int64_t ar = is_n(transA) ? M : K, ac = is_n(transA) ? K : M;
+    const int64_t br = is_n(transB) ? K : N, bc = is_n(transB) ? N : K;
+    const size_t nA = ab_used ? (size_t)((ac - 1) * lda + ar) * 4 : 0;
+    const size_t nB = ab_used ? (size_t)((bc - 1) * ldb + br) * 4 : 0;
+    const size_t nC = (size_t)((N - 1) * ldc + M) * 4;
+    const size_t nW = ab_used ? ws_bytes(M, N, K, math) : 0;
+    if ((st = ensure(&g_hc.dA, &g_hc.nA, nA)) || (st = ensure(&g_hc.dB, &g_hc.nB, nB)) ||
+        (st = ensure(&g_hc.dC, &g_hc.nC, nC)) || (st = ensure(&g_hc.dW, &g_hc.nW, nW)))
+        return st;
+    cudaStream_t s = g_hc.s;
+    cudaError_t e = cudaSuccess;
+    if (ab_used) {
+        e = cudaMemcpyAsync(g_hc.dA, A, nA, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(g_hc.dB, B, nB, cudaMemcpyHostToDevice, s);
+    }
+    if (e == cudaSuccess && beta != 0.0f) e = cudaMemcpyAsync(g_hc.dC, C, nC, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return cuda_status(e);
+    st = emm_sgemm_ex(transA, transB, M, N, K, alpha, (const float *)g_hc.dA, lda, (const float *)g_hc.dB, ldb, beta,
+                      (float *)g_hc.dC, ldc, s, math, g_hc.dW, g_hc.nW);
+    if (st) return st;
+    // copy back column by column only if ldc padding must be preserved
+    if (ldc == M || N == 1) {
+        e = cudaMemcpyAsync(C, g_hc.dC, (size_t)M * N * 4, cudaMemcpyDeviceToHost, s);
+    } else {
+        e = cudaMemcpy2DAsync(C, (size_t)ldc * 4, g_hc.dC, (size_t)ldc * 4, (size_t)M * 4, (size_t)N,
+                              cudaMemcpyDeviceToHost, s);
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    return cuda_status(e);
+}
+
+extern "C" void emm_release_cache(void) {
+    std::lock_guard<std::mutex> g(g_host_mu);
+    if (g_hc.dA) cudaFree(g_hc.dA);
+    if (g_hc.dB) cudaFree(g_hc.dB);
+    if (g_hc.dC) cudaFree(g_hc.dC);
+    if (g_hc.dW) cudaFree(g_hc.dW);
+    if (g_hc.s) cudaStreamDestroy(g_hc.s);
+    g_hc = HostCache{};
+}
+
+// ------------------------------------------------------------ partition
+extern "C" void emm_row_partition(int64_t M, int nranks, int rank, int64_t *row0, int64_t *rows) {
+    const int64_t T = 256;  // rows per CTA-pair tile
+    if (nranks < 1 || rank < 0 || rank >= nranks || M <= 0) {
+        if (row0) *row0 = 0;
+        if (rows) *rows = 0;
+        return;
+    }
+    const int64_t tiles = (M + T - 1) / T;
+    const int64_t base = tiles / nranks, extra = tiles % nranks;
+    // the last `extra` ranks take one more tile
+    const int64_t first_big = nranks - extra;
+    const int64_t t0 = rank * base + (rank > first_big ? rank - first_big : 0);
+    const int64_t nt = base + (rank >= first_big ? 1 : 0);
+    int64_t r0 = t0 * T, r1 = (t0 + nt) * T;
+    if (r0 > M) r0 = M;
+    if (r1 > M) r1 = M;
+    if (row0) *row0 = r0;
+    if (rows) *rows = r1 - r0;
+}
+
+// ------------------------------------------------------------ introspection
+extern "C" const char *emm_strerror(int status) {
+    static thread_local char buf[160];
+    if (status == 0) return "success";
+    if (status <= -1 && status >= -13) {
+        static const char *names[] = {"", "transA", "transB", "M", "N", "K", "alpha", "A", "lda", "B", "ldb", "beta",
+                                      "C", "ldc"};
+        snprintf(buf, sizeof buf, "invalid argument %d (%s)", -status, names[-status]);
+        return buf;
+    }
+    switch (status) {
+        case EMM_ERR_ALIAS: return "C overlaps A or B";
+        case EMM_ERR_ARCH: return "device is not compute capability 10.0 (sm_100a build)";
+        case EMM_ERR_WORKSPACE: return "workspace too small or not 1024-byte aligned";
+        case EMM_ERR_MATH: return "unknown math mode";
+        case EMM_ERR_COMM: return "invalid communicator or NCCL unavailable";
+        case EMM_ERR_NOMEM: return "allocation failed";
+        default: break;
+    }
+    if (status >= EMM_ERR_NCCL_BASE) {
+        snprintf(buf, sizeof buf, "NCCL error %d", status - EMM_ERR_NCCL_BASE);
+        return buf;
+    }
+    if (status >= EMM_ERR_CUDA_BASE) {
+        snprintf(buf, sizeof buf, "CUDA error %d (%s)", status - EMM_ERR_CUDA_BASE,
+                 cudaGetErrorString((cudaError_t)(status - EMM_ERR_CUDA_BASE)));
+        return buf;
+    }
+    return "unknown status";
+}
+
+extern "C" const char *emm_version(void) { return "emm 0.1 (sm_100a: tcgen05 3xTF32/1xTF32, FFMA)"; }
+
+extern "C" uint64_t emm_launch_count(void) { return g_launches.load(); }
+
+extern "C" void emm_profile_enable(int on) { g_prof_on.store(on ? 1 : 0); }
+
+extern "C" int emm_profile_read(double *gemm_ms, uint64_t *gemm_launches, double *other_ms, uint64_t *other_launches) {
+    std::vector<ProfRec> recs;
+    {
+        std::lock_guard<std::mutex> g(g_prof_mu);
+        recs.swap(g_prof);
+    }
+    double gm = 0, om = 0;
+    uint64_t gn = 0, on = 0;
+    int st = 0;
+    for (auto &r : recs) {
+        float ms = 0;
+        cudaError_t e = cudaEventSynchronize(r.b);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, r.a, r.b);
+        if (e != cudaSuccess && !st) st = EMM_ERR_CUDA_BASE + (int)e;
+        if (r.gemm) { gm += ms; ++gn; } else { om += ms; ++on; }
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    if (gemm_ms) *gemm_ms = gm;
+    if (gemm_launches) *gemm_launches = gn;
+    if (other_ms) *other_ms = om;
+    if (other_launches) *other_launches = on;
+    return st;
+}

@@ -1,0 +1,331 @@
+// k_tc.cu — the tensor-core SGEMM path for sm_100a (KN1 3xTF32, KN2 1xTF32)
+// and its operand re-buffering pass (KN4).
+//
+// Paper → B200 mapping:
+//  * "Re-buffering: ... we deliberately buffer B' into L1 cache. By also
+//    re-ordering B to enforce optimal memory access patterns"
+//     and "padding with zeros" for K
+//    → pack_split_kernel: one pass that re-orders op(A) and op(B) into
+//    K-major, 1024-byte-friendly planes, zero-pads K to a multiple of 32 and
+//    splits each value into tf32 big/small parts (3xTF32).  Every trans /
+//    leading-dimension / alignment case becomes the same dense layout, so the
+//    main kernel has one TMA path.
+//  * L1 blocking + A' prefetch → TMA loads of
+//    128x32 K-major tiles into a multi-stage 128B-swizzled SMEM ring
+//    (mbarrier full/empty pairs), a producer warp running ahead.
+//  * L0 register blocking, 5 dot products accumulated in registers for the
+//    whole dot product → tcgen05.mma accumulating
+//    a 256x256 FP32 tile of a CTA pair in TMEM for the whole K loop; one
+//    elected thread issues.  "shuffling and write back" deferred to the end
+//    of the dot product → one epilogue per tile.
+//  * N-edge special cases → predicated epilogue stores.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <mutex>
+
+#include "emm_internal.h"
+#include "ptx.cuh"
+
+namespace emm {
+
+using namespace ptx;
+
+constexpr int TC_BK = 32;            // K per stage: one 128-byte swizzle row of FP32
+constexpr int TC_BM = 128;           // rows of A per CTA (UMMA M = 256 per pair)
+constexpr int TC_BN = 256;           // columns of C per pair (UMMA N)
+constexpr int TC_TILE_BYTES = 128 * TC_BK * 4;   // one 128 x 32 FP32 operand tile
+constexpr int TC_THREADS = 192;      // warp0 TMA, warp1 MMA/TMEM, warps 2-5 epilogue
+constexpr int TC_TMEM_COLS = 256;
+
+int64_t tc_kpad(int64_t K) { return (K + TC_BK - 1) / TC_BK * TC_BK; }
+
+// =====================================================================
+// KN4: re-buffer + split.  32x32 tiles, 256 threads.
+// =====================================================================
+template <bool KCONTIG, int PLANES>
+__global__ void __launch_bounds__(256) pack_split_kernel(const float *__restrict__ X, int64_t ld, int64_t R,
+                                                         int64_t K, int64_t Kp, float *__restrict__ out) {
+    __shared__ float tile[32][33];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int64_t r0 = (int64_t)blockIdx.x * 32;
+    const int64_t k0 = (int64_t)blockIdx.y * 32;
+    const int64_t plane = R * Kp;
+    float v[4];
+    if (KCONTIG) {
+        // (r, p) at X[p + r*ld]: read and write along p.
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int64_t r = r0 + ty + 8 * i, p = k0 + tx;
+            v[i] = (r < R && p < K) ? __ldg(X + p + r * ld) : 0.0f;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int64_t r = r0 + ty + 8 * i, p = k0 + tx;
+            if (r < R) {
+                const uint32_t big = cvt_tf32_rn(v[i]);
+                out[r * Kp + p] = __uint_as_float(big);
+                if (PLANES == 2) out[plane + r * Kp + p] = __uint_as_float(cvt_tf32_rn(v[i] - __uint_as_float(big)));
+            }
+        }
+    } else {
+        // (r, p) at X[r + p*ld]: read along r, transpose through smem.
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int64_t r = r0 + tx, p = k0 + ty + 8 * i;
+            tile[ty + 8 * i][tx] = (r < R && p < K) ? __ldg(X + r + p * ld) : 0.0f;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int64_t r = r0 + ty + 8 * i, p = k0 + tx;
+            if (r < R) {
+                const float x = tile[tx][ty + 8 * i];
+                const uint32_t big = cvt_tf32_rn(x);
+                out[r * Kp + p] = __uint_as_float(big);
+                if (PLANES == 2) out[plane + r * Kp + p] = __uint_as_float(cvt_tf32_rn(x - __uint_as_float(big)));
+            }
+        }
+    }
+}
+
+cudaError_t launch_pack_split(const float *X, int64_t ld, bool kcontig, int64_t R, int64_t K, int64_t Kp,
+                              int planes, float *out, cudaStream_t s) {
+    dim3 grid((unsigned)((R + 31) / 32), (unsigned)(Kp / 32));
+    if (grid.y > 65535) return cudaErrorInvalidConfiguration;
+    cudaEvent_t ev = nullptr;
+    prof_begin(s, false, &ev);
+    if (kcontig) {
+        if (planes == 2) pack_split_kernel<true, 2><<<grid, 256, 0, s>>>(X, ld, R, K, Kp, out);
+        else pack_split_kernel<true, 1><<<grid, 256, 0, s>>>(X, ld, R, K, Kp, out);
+    } else {
+        if (planes == 2) pack_split_kernel<false, 2><<<grid, 256, 0, s>>>(X, ld, R, K, Kp, out);
+        else pack_split_kernel<false, 1><<<grid, 256, 0, s>>>(X, ld, R, K, Kp, out);
+    }
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    prof_end(s, false, ev);
+    return cudaGetLastError();
+}
+
+// =====================================================================
+// KN1/KN2: tcgen05 GEMM on packed operands, CTA pair per 256x256 tile.
+// =====================================================================
+template <int TERMS>
+struct TcCfg {
+    static constexpr int PLANES = TERMS == 3 ? 2 : 1;
+    static constexpr int TILES_PER_STAGE = 2 * PLANES;              // A planes + B planes
+    static constexpr int STAGE_BYTES = TILES_PER_STAGE * TC_TILE_BYTES;
+    static constexpr int STAGES = TERMS == 3 ? 3 : 6;
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+template <int TERMS>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
+    tc_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
+                    int Kp, float alpha, float beta, float *__restrict__ C, int64_t ldc, int tiles_m, int tiles_n,
+                    int group_m) {
+    using Cfg = TcCfg<TERMS>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+    uint64_t *empty = full + Cfg::STAGES;
+    uint64_t *accum = empty + Cfg::STAGES;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(accum + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+
+    // ---- tile coordinates: grouped raster along M (GPU-L2 analogue of the
+    //      paper's L2 blocking) ----
+    const int t = blockIdx.x >> 1;
+    const int per_group = group_m * tiles_n;
+    const int g = t / per_group;
+    const int first_m = g * group_m;
+    const int gsize = min(tiles_m - first_m, group_m);
+    const int tm = first_m + (t % per_group) % gsize;
+    const int tn = (t % per_group) / gsize;
+    const int m0 = tm * (2 * TC_BM);
+    const int n0 = tn * TC_BN;
+    const int nkb = Kp / TC_BK;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < Cfg::STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(accum, 1);
+        fence_mbar_init();
+    }
+    if (warp == 0 && lane == 0) {
+        prefetch_tmap(&tmA);
+        prefetch_tmap(&tmB);
+    }
+    if (warp == 1) tmem_alloc_2sm<TC_TMEM_COLS>(tmem_slot);
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ===== TMA producer (both CTAs; each loads its half of A and B) =====
+        if (lane == 0) {
+            uint32_t leader_full0;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(leader_full0) : "r"(smem_u32(&full[0])));
+            const uint64_t pol = policy_evict_normal();
+            const int arow = m0 + (int)rank * TC_BM;
+            const int brow = n0 + (int)rank * TC_BM;
+            for (int kb = 0; kb < nkb; ++kb) {
+                const int s = kb % Cfg::STAGES;
+                const uint32_t ph = (uint32_t)(kb / Cfg::STAGES) & 1u;
+                mbar_wait(&empty[s], ph ^ 1u);
+                const uint32_t fb = leader_full0 + (uint32_t)(s * sizeof(uint64_t));
+                if (rank == 0) mbar_arrive_expect_tx(&full[s], 2u * Cfg::STAGE_BYTES);
+                const uint32_t st = smem_u32(smem + s * Cfg::STAGE_BYTES);
+#pragma unroll
+                for (int p = 0; p < Cfg::PLANES; ++p) {
+                    tma_load_3d_2sm(st + p * TC_TILE_BYTES, &tmA, fb, kb * TC_BK, arow, p, pol);
+                    tma_load_3d_2sm(st + (Cfg::PLANES + p) * TC_TILE_BYTES, &tmB, fb, kb * TC_BK, brow, p, pol);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===== MMA issuer: one thread of the leader CTA drives the pair =====
+        if (rank == 0 && lane == 0) {
+            constexpr uint32_t idesc = idesc_tf32<2 * TC_BM, TC_BN>();
+            for (int kb = 0; kb < nkb; ++kb) {
+                const int s = kb % Cfg::STAGES;
+                const uint32_t ph = (uint32_t)(kb / Cfg::STAGES) & 1u;
+                mbar_wait(&full[s], ph);
+                tc_fence_after();
+                const uint32_t st = smem_u32(smem + s * Cfg::STAGE_BYTES);
+                const uint64_t a_big = desc_kmajor_sw128(st);
+                const uint64_t b_big = desc_kmajor_sw128(st + Cfg::PLANES * TC_TILE_BYTES);
+#pragma unroll
+                for (int k = 0; k < TC_BK / 8; ++k) {
+                    // advance 8 tf32 = 32 bytes along K inside the swizzle row
+                    const uint64_t koff = (uint64_t)((k * 32) >> 4);
+                    const uint32_t acc0 = (kb > 0 || k > 0) ? 1u : 0u;
+                    if (TERMS == 3) {
+                        const uint64_t a_sml = desc_kmajor_sw128(st + TC_TILE_BYTES);
+                        const uint64_t b_sml = desc_kmajor_sw128(st + 3 * TC_TILE_BYTES);
+                        // small terms first (they are the smaller magnitudes)
+                        mma_tf32_2sm(tmem_base, a_sml + koff, b_big + koff, idesc, acc0);
+                        mma_tf32_2sm(tmem_base, a_big + koff, b_sml + koff, idesc, 1u);
+                        mma_tf32_2sm(tmem_base, a_big + koff, b_big + koff, idesc, 1u);
+                    } else {
+                        mma_tf32_2sm(tmem_base, a_big + koff, b_big + koff, idesc, acc0);
+                    }
+                }
+                mma_commit_2sm_mc(&empty[s], (uint16_t)0x3);
+            }
+            mma_commit_2sm_mc(accum, (uint16_t)0x3);
+        }
+    } else {
+        // ===== epilogue: TMEM -> registers -> alpha/beta -> C (column-major) =====
+        const int q = warp & 3;                        // TMEM lane quarter of this warp
+        const int row = m0 + (int)rank * TC_BM + 32 * q + lane;
+        mbar_wait(accum, 0);
+        tc_fence_after();
+        const bool row_ok = row < M;
+#pragma unroll 1
+        for (int c = 0; c < TC_BN / 32; ++c) {
+            const int col0 = n0 + 32 * c;
+            if (col0 >= N) break;                      // warp-uniform
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(32 * c), v);
+            tmem_ld_wait();
+            if (row_ok) {
+                float *cp = C + (int64_t)row + (int64_t)col0 * ldc;
+                const int jmax = min(32, N - col0);
+                if (beta == 0.0f) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        if (j < jmax) cp[(int64_t)j * ldc] = alpha * __uint_as_float(v[j]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        if (j < jmax) {
+                            float *d = cp + (int64_t)j * ldc;
+                            *d = fmaf(beta, *d, alpha * __uint_as_float(v[j]));
+                        }
+                }
+            }
+        }
+    }
+
+    tc_fence_before();
+    cluster_sync();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc_2sm<TC_TMEM_COLS>(tmem_base);
+    }
+}
+
+// ---------------------------------------------------------------- host side
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void *p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+// planes x R x Kp FP32 (K-major), box 32 (K) x 128 (rows) x 1, 128B swizzle,
+// out-of-bounds rows read as zero.
+static bool make_tmap(CUtensorMap *tm, const float *base, int64_t R, int64_t Kp, int planes) {
+    auto enc = get_encode_fn();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)Kp, (cuuint64_t)R, (cuuint64_t)planes};
+    cuuint64_t strides[2] = {(cuuint64_t)Kp * 4, (cuuint64_t)R * (cuuint64_t)Kp * 4};
+    cuuint32_t box[3] = {(cuuint32_t)TC_BK, (cuuint32_t)TC_BM, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+template <int TERMS>
+static cudaError_t launch_tc_t(const float *Ap, const float *Bp, int64_t M, int64_t N, int64_t Kp, float alpha,
+                               float beta, float *C, int64_t ldc, cudaStream_t s) {
+    using Cfg = TcCfg<TERMS>;
+    static std::once_flag once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(once, [] {
+        attr_err = cudaFuncSetAttribute(tc_sgemm_kernel<TERMS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        Cfg::SMEM_BYTES);
+    });
+    if (attr_err != cudaSuccess) return attr_err;
+    CUtensorMap ta, tb;
+    if (!make_tmap(&ta, Ap, M, Kp, Cfg::PLANES) || !make_tmap(&tb, Bp, N, Kp, Cfg::PLANES))
+        return cudaErrorInvalidValue;
+    const int tiles_m = (int)((M + 2 * TC_BM - 1) / (2 * TC_BM));
+    const int tiles_n = (int)((N + TC_BN - 1) / TC_BN);
+    const int group_m = 8;
+    const int64_t blocks = 2LL * tiles_m * tiles_n;
+    if (blocks > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+    cudaEvent_t ev = nullptr;
+    prof_begin(s, true, &ev);
+    tc_sgemm_kernel<TERMS><<<(unsigned)blocks, TC_THREADS, Cfg::SMEM_BYTES, s>>>(
+        ta, tb, (int)M, (int)N, (int)Kp, alpha, beta, C, ldc, tiles_m, tiles_n, group_m);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    prof_end(s, true, ev);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tc_sgemm(int terms, const float *Ap, const float *Bp, int64_t M, int64_t N, int64_t Kp,
+                            float alpha, float beta, float *C, int64_t ldc, cudaStream_t s) {
+    if (M > 0x7fffffffLL || N > 0x7fffffffLL || Kp > 0x7fffffffLL) return cudaErrorInvalidValue;
+    return terms == 3 ? launch_tc_t<3>(Ap, Bp, M, N, Kp, alpha, beta, C, ldc, s)
+                      : launch_tc_t<1>(Ap, Bp, M, N, Kp, alpha, beta, C, ldc, s);
+}
+
+}  // namespace emm

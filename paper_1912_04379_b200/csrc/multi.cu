@@ -1,0 +1,231 @@
+// multi.cu — row-sharded multi-GPU SGEMM over NCCL (BASELINE.json north_star,
+// "Multi-GPU: large problems are partitioned ... by C row-blocks. B is
+// broadcast and C is optionally all-gathered with NCCL over NVLink, with
+// compute overlapped on streams").
+//
+// The paper's only distributed use of its SGEMM is the 196-CPU neural-network
+// run with no communication details; this is the B200
+// design of SURVEY.md §8(e): each rank owns a block of rows of op(A) and C,
+// B is broadcast from `root` in column panels on a communication stream, and
+// the GEMM of panel c (compute stream) waits only for panel c, so the
+// transfer of panel c+1 overlaps the math of panel c.
+//
+// NCCL is loaded at run time (dlopen of the process's libnccl.so.2, normally
+// the one torch already loaded), so the library has no link-time NCCL
+// dependency and the host-only entry points work on machines without it.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "emm_internal.h"
+
+namespace emm {
+namespace {
+
+struct Nccl {
+    bool ok = false;
+    decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+    decltype(&ncclCommInitRank) commInitRank = nullptr;
+    decltype(&ncclCommDestroy) commDestroy = nullptr;
+    decltype(&ncclCommGetAsyncError) getAsyncError = nullptr;
+    decltype(&ncclBroadcast) broadcast = nullptr;
+    decltype(&ncclGroupStart) groupStart = nullptr;
+    decltype(&ncclGroupEnd) groupEnd = nullptr;
+};
+
+Nccl &nccl() {
+    static Nccl n;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return;
+        n.getUniqueId = (decltype(n.getUniqueId))dlsym(h, "ncclGetUniqueId");
+        n.commInitRank = (decltype(n.commInitRank))dlsym(h, "ncclCommInitRank");
+        n.commDestroy = (decltype(n.commDestroy))dlsym(h, "ncclCommDestroy");
+        n.getAsyncError = (decltype(n.getAsyncError))dlsym(h, "ncclCommGetAsyncError");
+        n.broadcast = (decltype(n.broadcast))dlsym(h, "ncclBroadcast");
+        n.groupStart = (decltype(n.groupStart))dlsym(h, "ncclGroupStart");
+        n.groupEnd = (decltype(n.groupEnd))dlsym(h, "ncclGroupEnd");
+        n.ok = n.getUniqueId && n.commInitRank && n.commDestroy && n.getAsyncError && n.broadcast && n.groupStart &&
+               n.groupEnd;
+    });
+    return n;
+}
+
+struct Comm {
+    ncclComm_t nc = nullptr;
+    int nranks = 0, rank = 0, dev = 0;
+    cudaStream_t comm_stream = nullptr;
+    std::vector<cudaEvent_t> evs;
+    float *stage = nullptr;  // all-gather staging (grown on demand)
+    size_t stage_bytes = 0;
+};
+
+int nccl_status(ncclResult_t r) { return r == ncclSuccess ? 0 : EMM_ERR_NCCL_BASE + (int)r; }
+int cuda_st(cudaError_t e) { return e == cudaSuccess ? 0 : EMM_ERR_CUDA_BASE + (int)e; }
+
+cudaEvent_t ev_at(Comm *c, size_t i) {
+    while (c->evs.size() <= i) {
+        cudaEvent_t e;
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+        c->evs.push_back(e);
+    }
+    return c->evs[i];
+}
+
+}  // namespace
+}  // namespace emm
+
+using namespace emm;
+
+extern "C" int emm_get_unique_id(void *id128) {
+    Nccl &n = nccl();
+    if (!n.ok || !id128) return EMM_ERR_COMM;
+    ncclUniqueId id;
+    int st = nccl_status(n.getUniqueId(&id));
+    if (!st) memcpy(id128, &id, sizeof id);
+    return st;
+}
+
+extern "C" int emm_comm_create(void **comm, const void *id128, int nranks, int rank) {
+    Nccl &n = nccl();
+    if (!n.ok || !comm || !id128 || nranks < 1 || nranks > 8 || rank < 0 || rank >= nranks) return EMM_ERR_COMM;
+    ncclUniqueId id;
+    memcpy(&id, id128, sizeof id);
+    Comm *c = new Comm();
+    c->nranks = nranks;
+    c->rank = rank;
+    cudaGetDevice(&c->dev);
+    int st = nccl_status(n.commInitRank(&c->nc, nranks, id, rank));
+    if (!st) st = cuda_st(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+    if (st) {
+        delete c;
+        return st;
+    }
+    *comm = c;
+    return 0;
+}
+
+extern "C" int emm_comm_destroy(void *comm) {
+    if (!comm) return EMM_ERR_COMM;
+    Comm *c = static_cast<Comm *>(comm);
+    cudaStreamSynchronize(c->comm_stream);
+    for (auto e : c->evs) cudaEventDestroy(e);
+    if (c->stage) cudaFree(c->stage);
+    if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+    int st = 0;
+    if (c->nc) st = nccl_status(nccl().commDestroy(c->nc));
+    delete c;
+    return st;
+}
+
+extern "C" int emm_sgemm_multi(void *comm, char transA, char transB, int64_t M, int64_t N, int64_t K, float alpha,
+                               const float *A_local, int64_t lda, float *B, int64_t ldb, int root, float beta,
+                               float *C_local, int64_t ldc, float *C_full, int64_t ldc_full, void *stream,
+                               emm_math_t math) {
+    if (!comm) return EMM_ERR_COMM;
+    Comm *c = static_cast<Comm *>(comm);
+    Nccl &n = nccl();
+    if (!n.ok) return EMM_ERR_COMM;
+    if (root < 0 || root >= c->nranks) return EMM_ERR_COMM;
+    const bool bN = (transB == 'N' || transB == 'n');
+    if (K >= 0 && ldb != (bN ? (K > 1 ? K : 1) : (N > 1 ? N : 1))) return -10;  // panels must be contiguous
+    ncclResult_t async_err = ncclSuccess;
+    n.getAsyncError(c->nc, &async_err);
+    if (async_err != ncclSuccess) return nccl_status(async_err);
+
+    int64_t row0 = 0, rows = 0;
+    emm_row_partition(M, c->nranks, c->rank, &row0, &rows);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t b_elems = bN ? K * N : N * K;
+
+    // Gate the communication stream on the caller's stream (B / C ready).
+    cudaEvent_t e0 = ev_at(c, 0);
+    if (!e0) return EMM_ERR_NOMEM;
+    int st = cuda_st(cudaEventRecord(e0, s));
+    if (!st) st = cuda_st(cudaStreamWaitEvent(c->comm_stream, e0, 0));
+    if (st) return st;
+
+    if (bN && K > 0 && N > 0) {
+        // column panels of B: contiguous K x nc ranges, ~8 panels (>= 1024 cols)
+        int64_t panel = (N + 7) / 8;
+        if (panel < 1024) panel = 1024;
+        panel = (panel + 255) / 256 * 256;
+        size_t idx = 1;
+        for (int64_t c0 = 0; c0 < N; c0 += panel, ++idx) {
+            const int64_t nc = (N - c0 < panel) ? N - c0 : panel;
+            float *bp = B + c0 * ldb;
+            if (c->nranks > 1) {
+                st = nccl_status(n.broadcast(bp, bp, (size_t)(K * nc), ncclFloat32, root, c->nc, c->comm_stream));
+                if (st) return st;
+            }
+            cudaEvent_t ev = ev_at(c, idx);
+            if (!ev) return EMM_ERR_NOMEM;
+            if ((st = cuda_st(cudaEventRecord(ev, c->comm_stream)))) return st;
+            if ((st = cuda_st(cudaStreamWaitEvent(s, ev, 0)))) return st;
+            if (rows > 0) {
+                st = emm_sgemm_ex(transA, transB, rows, nc, K, alpha, A_local, lda, bp, ldb, beta, C_local + c0 * ldc,
+                                  ldc, s, math, nullptr, 0);
+                if (st) return st;
+            }
+        }
+    } else {
+        // transB = 'T': B's stored columns run along K; broadcast it whole
+        // (no panel overlap), then one GEMM.
+        if (c->nranks > 1 && b_elems > 0) {
+            st = nccl_status(n.broadcast(B, B, (size_t)b_elems, ncclFloat32, root, c->nc, c->comm_stream));
+            if (st) return st;
+        }
+        cudaEvent_t ev = ev_at(c, 1);
+        if ((st = cuda_st(cudaEventRecord(ev, c->comm_stream)))) return st;
+        if ((st = cuda_st(cudaStreamWaitEvent(s, ev, 0)))) return st;
+        if (rows > 0) {
+            st = emm_sgemm_ex(transA, transB, rows, N, K, alpha, A_local, lda, B, ldb, beta, C_local, ldc, s, math,
+                              nullptr, 0);
+            if (st) return st;
+        }
+    }
+
+    if (C_full) {
+        // all-gather of the row blocks: compact own block into the rank-major
+        // staging buffer, P broadcasts in one NCCL group, then unpack (KN6).
+        if (ldc_full < (M > 1 ? M : 1)) return -17;
+        const size_t need = (size_t)M * (size_t)N * 4;
+        if (c->stage_bytes < need) {
+            if (c->stage) cudaFree(c->stage);
+            c->stage = nullptr;
+            c->stage_bytes = 0;
+            if ((st = cuda_st(cudaMalloc(&c->stage, need)))) return st;
+            c->stage_bytes = need;
+        }
+        std::vector<int64_t> r0s(c->nranks), rws(c->nranks), offs(c->nranks);
+        int64_t off = 0;
+        for (int r = 0; r < c->nranks; ++r) {
+            emm_row_partition(M, c->nranks, r, &r0s[r], &rws[r]);
+            offs[r] = off;
+            off += rws[r] * N;
+        }
+        if (rows > 0 && N > 0)
+            st = cuda_st(cudaMemcpy2DAsync(c->stage + offs[c->rank], (size_t)rows * 4, C_local, (size_t)ldc * 4,
+                                           (size_t)rows * 4, (size_t)N, cudaMemcpyDeviceToDevice, s));
+        if (st) return st;
+        if (c->nranks > 1) {
+            n.groupStart();
+            for (int r = 0; r < c->nranks; ++r)
+                if (rws[r] > 0)
+                    n.broadcast(c->stage + offs[r], c->stage + offs[r], (size_t)(rws[r] * N), ncclFloat32, r, c->nc,
+                                s);
+            st = nccl_status(n.groupEnd());
+            if (st) return st;
+        }
+        st = cuda_st(launch_unpack_rows(c->stage, c->nranks, r0s.data(), rws.data(), N, C_full, ldc_full, s));
+        if (st) return st;
+    }
+    return 0;
+}

@@ -1,0 +1,346 @@
+"""GPU parity: the CUDA path through the C ABI vs the oracle, element by
+element on the same seeded inputs (BASELINE.json configs + edge cases).
+
+Bars (BASELINE.json north_star):
+* integer-exact inputs (ints in [-8,8], alpha,beta in {1,-1,2}): every path
+  must equal the oracle BITWISE (all partial sums are exact integers < 2^24);
+* FP32-accurate paths (3xtf32, ffma): |C - R| <= 1e-5*S + 1e-6*T per entry;
+* 1xtf32: |C - R| <= 5e-3*S + 1e-6*T;
+* non-finite oracle entries must match by class;
+* nothing outside the M x N logical region changes (ldc padding + a guard
+  region after C keep their sentinel); A and B are never written;
+* results are run-to-run bitwise deterministic.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import datagen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"3xtf32": 1e-5, "ffma": 1e-5, "1xtf32": 5e-3}
+MATHS = ["3xtf32", "ffma", "1xtf32"]
+SENTINEL = -12345.0
+GUARD = 4096
+
+
+@pytest.fixture(scope="module")
+def emm():
+    from paper_1912_04379_b200 import build
+    build.build()
+    import paper_1912_04379_b200 as e
+    torch.cuda.set_device(0)
+    return e
+
+
+_CASES = {}
+
+
+def cached_case(*args, **kw):
+    """Inputs are immutable per (args, kw): generate big ones once per module."""
+    key = (args, tuple(sorted(kw.items())))
+    if key not in _CASES:
+        _CASES[key] = Case(*args, **kw)
+    return _CASES[key]
+
+
+def stored(trans, r, c):
+    return (r, c) if trans in "Nn" else (c, r)
+
+
+class Case:
+    """Inputs of one SGEMM call, on host (flat storages) and device."""
+
+    def __init__(self, tA, tB, M, N, K, alpha, beta, kind="uniform", pad=(0, 0, 0), sigma=1.0,
+                 c_kind="uniform", seed=0):
+        self.tA, self.tB, self.M, self.N, self.K = tA, tB, M, N, K
+        self.alpha, self.beta = alpha, beta
+        ar, ac = stored(tA, M, K)
+        br, bc = stored(tB, K, N)
+        self.lda, self.ldb, self.ldc = max(1, ar) + pad[0], max(1, br) + pad[1], max(1, M) + pad[2]
+        self.A = datagen.matrix(kind, datagen.TAG_A, ar, ac, self.lda, seed=seed, sigma=sigma)
+        self.B = datagen.matrix(kind, datagen.TAG_B, br, bc, self.ldb, seed=seed, sigma=sigma)
+        Cv = datagen.matrix(c_kind, datagen.TAG_C, M, N, self.ldc, seed=seed, sigma=sigma,
+                            pad_value=SENTINEL)
+        self.Cflat = torch.full((self.ldc * max(N, 1) + GUARD,), SENTINEL, dtype=torch.float32)
+        if M * N:
+            self.Cflat[: self.ldc * N] = datagen.storage_of(Cv)
+
+    def flat(self, x):
+        return datagen.storage_of(x) if x.numel() else torch.zeros(1)
+
+    def oracle(self, rows=None, cols=None):
+        C = self.Cflat.numpy()
+        return oracle.sgemm_sub(self.tA, self.tB, self.M, self.N, self.K, self.alpha,
+                                self.flat(self.A).numpy(), self.lda, self.flat(self.B).numpy(), self.ldb,
+                                self.beta, C, self.ldc, rows=rows, cols=cols)
+
+    def run(self, emm, math, stream=None):
+        dA = self.flat(self.A).cuda()
+        dB = self.flat(self.B).cuda()
+        dC = self.Cflat.cuda()
+        st = emm.sgemm_ptr(self.tA, self.tB, self.M, self.N, self.K, self.alpha, dA.data_ptr(), self.lda,
+                           dB.data_ptr(), self.ldb, self.beta, dC.data_ptr(), self.ldc,
+                           torch.cuda.current_stream().cuda_stream, math)
+        torch.cuda.synchronize()
+        assert st == 0, emm.strerror(st)
+        assert torch.equal(dA.cpu(), self.flat(self.A)) and torch.equal(dB.cpu(), self.flat(self.B))
+        return dC.cpu()
+
+    def logical(self, Cflat):
+        if self.M * self.N == 0:
+            return np.zeros((self.M, self.N))
+        return Cflat[: self.ldc * self.N].reshape(self.N, self.ldc)[:, : self.M].T.double().numpy()
+
+    def check_untouched(self, Cflat):
+        full = Cflat.reshape(-1)
+        if self.M * self.N:
+            body = full[: self.ldc * self.N].reshape(self.N, self.ldc)
+            assert torch.all(body[:, self.M:] == SENTINEL), "ldc padding modified"
+        assert torch.all(full[self.ldc * self.N:] == SENTINEL) if self.M * self.N else True, "guard modified"
+
+
+def assert_close(case, Cg, R, S, T, tol, rows=None, cols=None):
+    G = case.logical(Cg)
+    if rows is not None:
+        G = G[np.ix_(rows, cols if cols is not None else np.arange(case.N))]
+    fin = np.isfinite(R)
+    err = np.abs(G - R)
+    bound = tol * S + 1e-6 * T
+    bad = fin & ~(err <= bound)
+    if bad.any():
+        i = np.argwhere(bad)[0]
+        raise AssertionError(f"{bad.sum()} entries out of tolerance; first {tuple(i)}: gpu={G[tuple(i)]!r} "
+                             f"ref={R[tuple(i)]!r} err/tol={err[tuple(i)] / max(bound[tuple(i)], 1e-300):.3g}; "
+                             f"max err/tol={np.max(np.where(fin, err / np.maximum(bound, 1e-300), 0)):.3g}")
+    if (~fin).any():
+        assert np.array_equal(np.isnan(G[~fin]), np.isnan(R[~fin]))
+        assert np.array_equal(np.sign(G[~fin & ~np.isnan(R)]), np.sign(R[~fin & ~np.isnan(R)]))
+    return float(np.max(np.where(fin, err / np.maximum(bound, 1e-300), 0))) if R.size else 0.0
+
+
+# --------------------------------------------------------------------------
+# bitwise on integer-exact inputs (all paths, all trans, ragged shapes)
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("math", MATHS)
+@pytest.mark.parametrize("tA", ["N", "T"])
+@pytest.mark.parametrize("tB", ["N", "T"])
+@pytest.mark.parametrize("shape", [(1, 1, 1), (64, 64, 64), (300, 260, 100), (513, 257, 129), (129, 700, 33)])
+def test_integer_exact_bitwise(emm, math, tA, tB, shape):
+    M, N, K = shape
+    for alpha, beta in ((1.0, 0.0), (-1.0, 2.0)):
+        case = Case(tA, tB, M, N, K, alpha, beta, kind="ints", c_kind="ints", pad=(3, 1, 2))
+        R, S, T, st = case.oracle()
+        Cg = case.run(emm, math)
+        case.check_untouched(Cg)
+        G = case.logical(Cg)
+        assert np.array_equal(G, R.astype(np.float32).astype(np.float64)), \
+            f"max |diff| {np.max(np.abs(G - R))}"
+
+
+def test_spec_worked_example_bitwise(emm):
+    """tests/golden/spec_2x2.txt: [[1,2],[3,4]]·[[5,6],[7,8]] = [[19,22],[43,50]] (column-major)."""
+    for math in MATHS:
+        A = torch.tensor([1, 3, 2, 4], dtype=torch.float32, device="cuda")
+        B = torch.tensor([5, 7, 6, 8], dtype=torch.float32, device="cuda")
+        C = torch.full((4,), float("nan"), device="cuda")
+        st = emm.sgemm_ptr("N", "N", 2, 2, 2, 1.0, A.data_ptr(), 2, B.data_ptr(), 2, 0.0, C.data_ptr(), 2,
+                           torch.cuda.current_stream().cuda_stream, math)
+        torch.cuda.synchronize()
+        assert st == 0 and C.cpu().tolist() == [19, 43, 22, 50]
+
+
+# --------------------------------------------------------------------------
+# tolerance on the BASELINE.json configs
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("math", MATHS)
+def test_c1_64cubed(emm, math):
+    case = Case("N", "N", 64, 64, 64, 1.0, 0.0)
+    R, S, T, _ = case.oracle()
+    Cg = case.run(emm, math)
+    case.check_untouched(Cg)
+    assert_close(case, Cg, R, S, T, TOL[math])
+
+
+@pytest.mark.parametrize("math", MATHS)
+@pytest.mark.parametrize("n", [100, 333, 512, 700, 1000, 1024, 2048])
+def test_c2_square_sweep(emm, math, n):
+    case = Case("N", "N", n, n, n, 1.0, 0.0)
+    R, S, T, _ = case.oracle()
+    Cg = case.run(emm, math)
+    case.check_untouched(Cg)
+    assert_close(case, Cg, R, S, T, TOL[math])
+
+
+@pytest.mark.parametrize("math", MATHS)
+def test_c2_4096_sampled_rows(emm, math):
+    n = 4096
+    case = Case("N", "N", n, n, n, 1.0, 0.0)
+    rng = np.random.default_rng(0)
+    rows = np.unique(np.concatenate([[0, 1, 255, 256, n - 1], rng.integers(0, n, 27)]))
+    R, S, T, _ = case.oracle(rows=rows)
+    Cg = case.run(emm, math)
+    assert_close(case, Cg, R, S, T, TOL[math], rows=rows)
+
+
+@pytest.mark.parametrize("math", MATHS)
+@pytest.mark.parametrize("tA", ["N", "T"])
+@pytest.mark.parametrize("tB", ["N", "T"])
+def test_c3_blas_stress(emm, math, tA, tB):
+    """configs[2] with the valid reading lda = stored rows + 13 (R3)."""
+    case = cached_case(tA, tB, 1531, 997, 2049, -0.75, 1.25, kind="normal", c_kind="uniform", pad=(13, 7, 5))
+    rows = np.arange(0, 1531, 3) if math == "ffma" else None
+    R, S, T, _ = case.oracle(rows=rows)
+    Cg = case.run(emm, math)
+    case.check_untouched(Cg)
+    assert_close(case, Cg, R, S, T, TOL[math], rows=rows)
+
+
+@pytest.mark.parametrize("math", ["3xtf32", "1xtf32"])
+@pytest.mark.parametrize("shape", [(65536, 1024, 4096), (65536, 4096, 1024)])
+def test_c4_nn_layer_sampled(emm, math, shape):
+    M, N, K = shape
+    case = cached_case("N", "T", M, N, K, 1.0, 1.0, kind="normal", c_kind="normal", sigma=1.0 / np.sqrt(K))
+    rng = np.random.default_rng(1)
+    rows = np.unique(np.concatenate([[0, 255, 256, M - 1], rng.integers(0, M, 12)]))
+    R, S, T, _ = case.oracle(rows=rows)
+    Cg = case.run(emm, math)
+    assert_close(case, Cg, R, S, T, TOL[math], rows=rows)
+
+
+# --------------------------------------------------------------------------
+# edge cases
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("math", MATHS)
+@pytest.mark.parametrize("K", [1, 7, 31, 33, 337, 2049])
+def test_k_tails(emm, math, K):
+    case = Case("N", "N", 257, 129, K, 1.0, 0.0, pad=(3, 3, 3))
+    R, S, T, _ = case.oracle()
+    Cg = case.run(emm, math)
+    case.check_untouched(Cg)
+    assert_close(case, Cg, R, S, T, TOL[math])
+
+
+@pytest.mark.parametrize("math", MATHS)
+@pytest.mark.parametrize("mn", [(1, 1), (1, 300), (300, 1), (7, 5), (127, 129), (255, 257), (256, 256)])
+def test_mn_edges(emm, math, mn):
+    M, N = mn
+    for tA, tB in (("N", "N"), ("T", "T")):
+        case = Case(tA, tB, M, N, 77, -0.75, 1.25, pad=(3, 0, 3))
+        R, S, T, _ = case.oracle()
+        Cg = case.run(emm, math)
+        case.check_untouched(Cg)
+        assert_close(case, Cg, R, S, T, TOL[math])
+
+
+@pytest.mark.parametrize("math", MATHS)
+def test_alpha_zero_never_reads_AB(emm, math):
+    M, N, K = 200, 100, 50
+    for beta in (0.0, 2.0):
+        A = torch.full((M * K,), float("nan"), device="cuda")
+        B = torch.full((K * N,), float("nan"), device="cuda")
+        Cv = datagen.matrix("uniform", datagen.TAG_C, M, N)
+        C = datagen.storage_of(Cv).cuda()
+        st = emm.sgemm_ptr("N", "N", M, N, K, 0.0, A.data_ptr(), M, B.data_ptr(), K, beta, C.data_ptr(), M,
+                           torch.cuda.current_stream().cuda_stream, math)
+        torch.cuda.synchronize()
+        assert st == 0
+        expect = datagen.storage_of(Cv) * beta if beta != 0 else torch.zeros(M * N)
+        assert torch.equal(C.cpu(), expect)
+
+
+@pytest.mark.parametrize("math", MATHS)
+def test_beta_zero_never_reads_C(emm, math):
+    case = Case("N", "N", 130, 70, 40, 1.0, 0.0)
+    case.Cflat[: case.ldc * case.N] = float("nan")
+    R, S, T, _ = case.oracle()
+    Cg = case.run(emm, math)
+    G = case.logical(Cg)
+    assert np.all(np.isfinite(G))
+    assert_close(case, Cg, R, S, T, TOL[math])
+
+
+@pytest.mark.parametrize("math", MATHS)
+def test_K_zero_scales_C(emm, math):
+    case = Case("N", "N", 100, 60, 0, 1.0, -2.0)
+    R, S, T, _ = case.oracle()
+    Cg = case.run(emm, math)
+    case.check_untouched(Cg)
+    assert np.array_equal(case.logical(Cg), R.astype(np.float32).astype(np.float64))
+
+
+def test_empty_is_noop(emm):
+    C = torch.full((16,), 3.0, device="cuda")
+    n0 = emm.launch_count()
+    assert emm.sgemm_ptr("N", "N", 0, 4, 5, 1.0, 0, 1, 0, 5, 0.0, C.data_ptr(), 1, None, "3xtf32") == 0
+    assert emm.sgemm_ptr("N", "N", 4, 0, 5, 1.0, 0, 4, 0, 5, 0.0, C.data_ptr(), 4, None, "3xtf32") == 0
+    assert emm.launch_count() == n0
+    assert torch.all(C == 3.0)
+
+
+def test_argument_error_leaves_C_unmodified(emm):
+    C = torch.full((64,), 5.0, device="cuda")
+    A = torch.ones(64, device="cuda")
+    st = emm.sgemm_ptr("N", "N", 8, 8, 8, 1.0, A.data_ptr(), 7, A.data_ptr(), 8, 0.0, C.data_ptr(), 8, None)
+    assert st == -8
+    torch.cuda.synchronize()
+    assert torch.all(C == 5.0)
+
+
+@pytest.mark.parametrize("math", MATHS)
+def test_deterministic(emm, math):
+    case = Case("N", "T", 700, 900, 1500, 1.0, 0.5)
+    c1 = case.run(emm, math)
+    c2 = case.run(emm, math)
+    assert torch.equal(c1, c2)
+
+
+def test_accumulate_property(emm):
+    """GEMM into C twice with beta=1 == once with 2B (tolerance-scaled)."""
+    M, N, K = 500, 300, 700
+    case = Case("N", "N", M, N, K, 1.0, 1.0)
+    c0 = case.Cflat.clone()
+    case.Cflat = case.run(emm, "3xtf32")
+    c_twice = case.run(emm, "3xtf32")
+    B2 = (case.flat(case.B) * 2).numpy()
+    R, S, T, _ = oracle.sgemm_sub("N", "N", M, N, K, 1.0, case.flat(case.A).numpy(), case.lda, B2, case.ldb,
+                                  1.0, c0.numpy(), case.ldc)
+    # two FP32 roundings of the partial result: 2 x the single-call bound
+    assert_close(case, c_twice, R, 2 * S, 2 * T, 1e-5)
+
+
+def test_sametsign_diagnostic_3xtf32(emm):
+    """Diagnostic (Q7): same-sign U[0,1) data at large K exposes a
+    truncating tensor-core accumulator; report the max err/tol."""
+    case = Case("N", "N", 256, 256, 16384, 1.0, 0.0, kind="uniform01")
+    R, S, T, _ = case.oracle()
+    Cg = case.run(emm, "3xtf32")
+    G = case.logical(Cg)
+    ratio = float(np.max(np.abs(G - R) / (1e-5 * S)))
+    print(f"same-sign K=16384 3xTF32 max err/(1e-5*S) = {ratio:.3g}")
+    assert ratio < 10.0
+
+
+def test_torch_binding_colmajor(emm):
+    M, N, K = 300, 200, 100
+    A = torch.randn(K, M, device="cuda").t()   # (M, K) with stride (1, M): column-major
+    B = torch.randn(N, K, device="cuda").t()
+    C = torch.zeros(N, M, device="cuda").t()
+    emm.sgemm(A, B, C)
+    ref = (A.double() @ B.double())
+    assert torch.allclose(C.double(), ref, atol=1e-4, rtol=0)
+
+
+def test_host_buffer_entry(emm):
+    M, N, K = 333, 257, 129
+    case = Case("T", "N", M, N, K, 1.5, -0.5, pad=(1, 2, 3))
+    R, S, T, _ = case.oracle()
+    Cf = case.Cflat.clone().pin_memory()
+    emm.sgemm_host("T", "N", M, N, K, 1.5, case.flat(case.A), case.lda, case.flat(case.B), case.ldb, -0.5, Cf,
+                   case.ldc)
+    case.check_untouched(Cf)
+    assert_close(case, Cf, R, S, T, 1e-5)
