@@ -1,0 +1,370 @@
+#!/usr/bin/env python
+"""bench.py — the measured step of the emm SGEMM hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl emm|reference] [--math 3xtf32|ffma|1xtf32]
+                    [--size S]
+
+Workload (BASELINE.json configs[4], the configuration its metric — GFLOP/s at
+1/2/4/8 B200 — is quoted on): square SGEMM M=N=K=32768, FP32, column-major,
+transA=transB='N', alpha=1, beta=0, A and B uniform[-1,1) from seed 0
+(datagen), 4 GiB per operand.  One STEP = one full pass of the hot path on
+that problem: emm_sgemm_ex = re-buffer/split of A and B (KN4) + the tcgen05
+3xTF32 GEMM (KN1), i.e. every row of SURVEY.md §8(a).  At N > 1 the problem
+is row-sharded (emm_row_partition) and each step is emm_sgemm_multi: B
+broadcast from rank 0 over NCCL in column panels overlapped with the
+per-panel GEMMs ("scaling": "strong": total work fixed).
+
+* value: 2MNK * steps / (max over ranks of the CUDA-event time of the K
+  timed steps), inputs resident in HBM.  Inputs (12.9 GB) exceed the 126 MB
+  L2, so no flush is needed between steps (stated in config).
+* e2e: the same metric through the C-ABI host-buffer entry emm_sgemm_host
+  (pinned host A, B in; C out) — copies inside the timed region.
+* roofline: the dominant kernel (tc_sgemm_kernel), algorithmic flops 2MNK per
+  launch / its CUDA-event duration on the launching stream, against the
+  3xTF32-effective tensor peak = measured bf16 peak x (1.1/2.25 nominal
+  tf32/bf16) / 3.
+* cpu_baseline: the oracle (oracle/oracle.c) on a bounded sample of output
+  rows of the same workload, all host cores, rank 0 at N=1 only.
+* --impl reference: the oracle itself, timed as the reference arm.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SGEMM GFLOP/s (2MNK/t) and % of FP32/TF32 roofline at 1/2/4/8 B200"
+TF32_PER_BF16 = 1.1 / 2.25          # nominal dense ratio, B200_PROFILING.md table
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="emm", choices=["emm", "reference"])
+    p.add_argument("--math", default="3xtf32", choices=["3xtf32", "ffma", "1xtf32"])
+    p.add_argument("--size", type=int, default=32768)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--cpu-rows", type=int, default=0, help="oracle sample rows (0 = auto)")
+    return p.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            mp = json.load(f)
+        return mp["bf16_tflops"], mp.get("bf16_tflops_sustained", mp["bf16_tflops"]), mp.get("hbm_gbs"), "measured"
+    except Exception:
+        return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+def workload_config(n, args, world):
+    return {"workload": f"BASELINE configs[4]: SGEMM M=N=K={n}, FP32 column-major, transA=transB=N, "
+                        f"alpha=1, beta=0, A,B ~ U[-1,1) seed 0"
+                        + (f", row-sharded over {world} GPUs, B broadcast (NCCL)" if world > 1 else ""),
+            "M": n, "N": n, "K": n, "transA": "N", "transB": "N", "alpha": 1.0, "beta": 0.0,
+            "math": args.math, "global_batch": None, "seq_len": None,
+            "parallelism": f"rows{world}" if world > 1 else "single",
+            "l2": "inputs (3 x 4 GiB) exceed the 126 MB L2: no flush between steps"}
+
+
+# --------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower() in ("active", "1", "yes"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------------- oracle
+def cpu_oracle_sample(n, nrows, seed_rows=0):
+    """Time the oracle on `nrows` sampled output rows of the workload
+    (compact A rows, full B on the host).  Returns (gflops, seconds, cores)."""
+    import numpy as np
+    import datagen
+    import oracle
+    import torch
+    rows = np.linspace(0, n - 1, nrows).astype(np.int64)
+    A_s = datagen.submatrix("uniform", datagen.TAG_A, n, n, rows)            # nrows x K, lda = nrows
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    B = datagen.storage_of(datagen.matrix("uniform", datagen.TAG_B, n, n, device=dev)).cpu().numpy()
+    cores = oracle.default_threads()
+    t0 = time.perf_counter()
+    R, S, T, st = oracle.sgemm_sub("N", "N", nrows, n, n, 1.0, datagen.storage_of(A_s).numpy(), nrows,
+                                   B, n, 0.0, None, nrows, nthreads=cores)
+    dt = time.perf_counter() - t0
+    assert st == 0
+    return 2.0 * nrows * n * n / dt / 1e9, dt, cores
+
+
+def auto_rows(n):
+    # ~10-20 s of oracle work on the host: rate ~0.6 GFLOP/s per core (j-p-i FP64 loop)
+    cores = len(os.sched_getaffinity(0))
+    rate = 0.6e9 * cores
+    r = int(15.0 * rate / (2.0 * n * n))
+    return max(4, min(256, r))
+
+
+# --------------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    n = args.size
+    rows = args.cpu_rows or max(4, auto_rows(n) // 4)
+    times = []
+    for i in range(args.warmup + args.steps):
+        g, dt, cores = cpu_oracle_sample(n, rows)
+        if i >= args.warmup:
+            times.append(dt)
+    tot = sum(times)
+    gflops = 2.0 * rows * n * n * len(times) / tot / 1e9
+    line = {"metric": METRIC, "value": gflops, "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference", "config": workload_config(n, args, 1),
+            "cpu_baseline": {"value": gflops, "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
+                             "sample": f"{rows} output rows x {n} cols (all of K={n}) of the workload per step"},
+            "e2e": {"value": gflops, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------- emm arm
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import numpy as np
+    import torch
+    import datagen
+    import paper_1912_04379_b200 as emm
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", init_method="env://", device_id=dev)
+    n = args.size
+    M = N = K = n
+    flops = 2.0 * M * N * K
+    stream = torch.cuda.Stream(dev)
+
+    # ---- inputs resident in HBM (generated on the device, bit-identical to host datagen)
+    r0, rows = emm.row_partition(M, world, rank) if world > 1 else (0, M)
+    A = datagen.submatrix("uniform", datagen.TAG_A, M, K, torch.arange(r0, r0 + rows), device=dev) \
+        if world > 1 else datagen.matrix("uniform", datagen.TAG_A, M, K, device=dev)
+    if world == 1 or rank == 0:
+        B = datagen.matrix("uniform", datagen.TAG_B, K, N, device=dev)
+    else:
+        B = torch.empty((N, K), dtype=torch.float32, device=dev).t()
+    C = torch.empty((N, max(rows, 1)), dtype=torch.float32, device=dev).t()[:rows, :]
+    ws = None
+    if world == 1:
+        nbytes = emm.workspace_bytes("N", "N", M, N, K, args.math)
+        ws = torch.empty(max(nbytes // 4 + 256, 1), dtype=torch.float32, device=dev) if nbytes else None
+        if ws is not None and ws.data_ptr() % 1024:
+            ws = ws[(1024 - ws.data_ptr() % 1024) // 4:]
+    comm = emm.Comm(rank, world) if world > 1 else None
+
+    def step():
+        if world > 1:
+            emm.sgemm_multi(comm, M, N, K, A, B, C, 1.0, 0.0, math=args.math, stream=stream)
+        else:
+            emm.sgemm_ex(A, B, C, 1.0, 0.0, math=args.math, workspace=ws, stream=stream)
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize(dev)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+    barrier()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    emm.profile_enable(True)
+    emm.profile_read()
+    l0 = emm.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    ev0.record(stream)
+    with torch.cuda.stream(stream):
+        for _ in range(args.steps):
+            step()
+    ev1.record(stream)
+    barrier()
+    launches = emm.launch_count() - l0
+    ms = ev0.elapsed_time(ev1)
+    gemm_ms, gemm_n, other_ms, other_n = emm.profile_read()
+    emm.profile_enable(False)
+    clk = clocks.stop()
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = flops * args.steps / (ms / 1e3) / 1e9
+
+    bf16, bf16_sus, hbm, src = peaks()
+    tf32_sus = bf16_sus * TF32_PER_BF16
+    tf32_burst = bf16 * TF32_PER_BF16
+    if args.math == "3xtf32":
+        peak, peak_b, pname = tf32_sus / 3.0, tf32_burst / 3.0, "3xTF32-effective (TF32/3)"
+    elif args.math == "1xtf32":
+        peak, peak_b, pname = tf32_sus, tf32_burst, "TF32"
+    else:
+        sm = torch.cuda.get_device_properties(dev).multi_processor_count
+        peak = peak_b = sm * 256 * 1965e6 / 1e12
+        pname = "FP32 FFMA (SMs x 256 flop/clk x 1965 MHz)"
+    flops_rank = 2.0 * rows * N * K
+    kernel_ms = gemm_ms / max(gemm_n, 1)
+    per_launch_flops = flops_rank / max(gemm_n // max(args.steps, 1), 1)
+    achieved = per_launch_flops / (kernel_ms / 1e3) / 1e12 if kernel_ms > 0 else None
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        try:
+            with open(tp) as f:
+                traffic = json.load(f).get(f"{args.math}_{n}")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor" if args.math != "ffma" else "alu", "achieved": achieved, "peak": peak,
+                "unit": "TFLOP/s", "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "peak_kind": f"{pname}, from {src} bf16 sustained {bf16_sus} TF x 1.1/2.25",
+                "peak_burst": peak_b, "frac_burst": (achieved / peak_b) if achieved else None,
+                "kernel": "tc_sgemm_kernel" if args.math != "ffma" else "ffma_sgemm_kernel",
+                "kernel_ms": kernel_ms, "kernel_share_of_step": (gemm_ms / ms) if ms > 0 else None,
+                "other_kernels_ms_per_step": other_ms / args.steps}
+
+    # ---- e2e through the C-ABI host-buffer entry (copies inside the timed region)
+    e2e = None
+    if not args.no_e2e and world == 1:
+        del ws
+        torch.cuda.empty_cache()
+        hA = datagen.storage_of(A).cpu().pin_memory()
+        hB = datagen.storage_of(B).cpu().pin_memory()
+        hC = torch.empty(M * N, dtype=torch.float32).pin_memory()
+        emm.sgemm_host("N", "N", M, N, K, 1.0, hA, M, hB, K, 0.0, hC, M, math=args.math)  # warm (allocs)
+        e_steps = max(1, min(args.steps, 3))
+        t0 = time.perf_counter()
+        for _ in range(e_steps):
+            emm.sgemm_host("N", "N", M, N, K, 1.0, hA, M, hB, K, 0.0, hC, M, math=args.math)
+        dt = time.perf_counter() - t0
+        e2e = {"value": flops * e_steps / dt / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": 4 * (M * K + K * N),
+               "d2h_bytes_per_step": 4 * M * N, "steps": e_steps,
+               "api": "emm_sgemm_host (pinned host A,B -> device, C -> host, synchronous)"}
+        # spot-check the e2e result against the device result on a few entries
+        Cd = C[:64, :64].cpu()
+        hv = hC.reshape(N, M)[:64, :64].t()
+        assert torch.equal(Cd, hv), "e2e result differs from device result"
+        del hA, hB, hC
+        emm.release_cache()
+    elif not args.no_e2e and world > 1:
+        hA = datagen.storage_of(A).cpu().pin_memory() if rows else None
+        hB = datagen.storage_of(B).cpu().pin_memory() if rank == 0 else None
+        hC = torch.empty(max(rows, 1) * N, dtype=torch.float32).pin_memory()
+        e_steps = max(1, min(args.steps, 3))
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(e_steps):
+            with torch.cuda.stream(stream):
+                if rows:
+                    datagen.storage_of(A).copy_(hA, non_blocking=True)
+                if rank == 0:
+                    datagen.storage_of(B).copy_(hB, non_blocking=True)
+                step()
+                hC[: rows * N].copy_(C.t().reshape(-1) if rows else hC[:0], non_blocking=True)
+            stream.synchronize()
+        barrier()
+        dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(dt, op=torch.distributed.ReduceOp.MAX)
+        e2e = {"value": flops * e_steps / float(dt.item()) / 1e9, "unit": "GFLOP/s",
+               "h2d_bytes_per_step": 4 * (M * K + K * N), "d2h_bytes_per_step": 4 * M * N, "steps": e_steps,
+               "api": "H2D copies + emm_sgemm_multi + D2H, per rank"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        nrows = args.cpu_rows or auto_rows(n)
+        g, dt, cores = cpu_oracle_sample(n, nrows)
+        cpu = {"value": g, "unit": "GFLOP/s", "cores": cores, "kind": "oracle", "seconds": dt,
+               "sample": f"{nrows} evenly spaced output rows x all {n} columns (full K={n}) of the workload"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": workload_config(n, args, world), "roofline": roofline, "cpu_baseline": cpu,
+                "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+                "pct_of_roofline": 100.0 * value / 1e3 / (peak * world) if peak else None}
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

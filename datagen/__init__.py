@@ -133,5 +133,25 @@ def matrix(kind: str, tag: int, rows: int, cols: int, ld: int | None = None, *,
 
 def storage_of(x: torch.Tensor) -> torch.Tensor:
     """The full ld*cols storage (padding included) behind a matrix() view."""
-    ld = x.stride(1) if x.dim() == 2 and x.shape[1] > 1 else max(1, x.shape[0])
+    ld = x.stride(1)          # matrix() views keep stride (1, ld) even for one column
     return torch.as_strided(x, (x.shape[1] * ld,), (1,), x.storage_offset())
+
+
+def submatrix(kind: str, tag: int, rows: int, cols: int, row_idx, col_idx=None, *, seed: int = 0,
+              sigma: float = 1.0, device="cpu") -> torch.Tensor:
+    """Selected rows (and columns) of the rows x cols matrix ``matrix(kind,
+    tag, rows, cols)`` would give, as a compact column-major (len(row_idx),
+    len(col_idx)) tensor — same values element for element, without
+    generating the rest (for sampled oracle checks and row-sharded ranks)."""
+    dev = torch.device(device)
+    gen_dev = torch.device("cpu") if kind == "normal" else dev
+    r = torch.as_tensor(row_idx, dtype=torch.int64, device=gen_dev).reshape(-1)
+    c = (torch.arange(cols, dtype=torch.int64, device=gen_dev) if col_idx is None
+         else torch.as_tensor(col_idx, dtype=torch.int64, device=gen_dev).reshape(-1))
+    out = torch.empty((c.numel(), r.numel()), dtype=torch.float32, device=dev)
+    cchunk = max(1, (1 << 26) // max(1, r.numel()))
+    for c0 in range(0, c.numel(), cchunk):
+        cc = c[c0:c0 + cchunk]
+        idx = cc[:, None] * rows + r[None, :]
+        out[c0:c0 + cc.numel()] = _values(kind, idx, tag, seed, sigma).to(dev)
+    return out.t()
