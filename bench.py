@@ -134,21 +134,32 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------- oracle
-def cpu_oracle_sample(n, nrows, seed_rows=0):
+_ORACLE_INPUTS = {}
+
+
+def oracle_inputs(n, nrows, gen_device):
+    """Compact sampled rows of A and the full B on the host (cached)."""
+    key = (n, nrows)
+    if key not in _ORACLE_INPUTS:
+        import numpy as np
+        import datagen
+        rows = np.linspace(0, n - 1, nrows).astype(np.int64)
+        A_s = datagen.storage_of(datagen.submatrix("uniform", datagen.TAG_A, n, n, rows)).numpy()
+        B = datagen.storage_of(datagen.matrix("uniform", datagen.TAG_B, n, n, device=gen_device)).cpu().numpy()
+        _ORACLE_INPUTS.clear()
+        _ORACLE_INPUTS[key] = (A_s, B)
+    return _ORACLE_INPUTS[key]
+
+
+def cpu_oracle_sample(n, nrows, gen_device="cpu"):
     """Time the oracle on `nrows` sampled output rows of the workload
     (compact A rows, full B on the host).  Returns (gflops, seconds, cores)."""
-    import numpy as np
-    import datagen
     import oracle
-    import torch
-    rows = np.linspace(0, n - 1, nrows).astype(np.int64)
-    A_s = datagen.submatrix("uniform", datagen.TAG_A, n, n, rows)            # nrows x K, lda = nrows
-    dev = "cuda" if torch.cuda.is_available() else "cpu"
-    B = datagen.storage_of(datagen.matrix("uniform", datagen.TAG_B, n, n, device=dev)).cpu().numpy()
+    A_s, B = oracle_inputs(n, nrows, gen_device)
     cores = oracle.default_threads()
     t0 = time.perf_counter()
-    R, S, T, st = oracle.sgemm_sub("N", "N", nrows, n, n, 1.0, datagen.storage_of(A_s).numpy(), nrows,
-                                   B, n, 0.0, None, nrows, nthreads=cores)
+    R, S, T, st = oracle.sgemm_sub("N", "N", nrows, n, n, 1.0, A_s, nrows, B, n, 0.0, None, nrows,
+                                   nthreads=cores)
     dt = time.perf_counter() - t0
     assert st == 0
     return 2.0 * nrows * n * n / dt / 1e9, dt, cores
@@ -349,7 +360,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         nrows = args.cpu_rows or auto_rows(n)
-        g, dt, cores = cpu_oracle_sample(n, nrows)
+        g, dt, cores = cpu_oracle_sample(n, nrows, gen_device=dev)
         cpu = {"value": g, "unit": "GFLOP/s", "cores": cores, "kind": "oracle", "seconds": dt,
                "sample": f"{nrows} evenly spaced output rows x all {n} columns (full K={n}) of the workload"}
 
