@@ -38,8 +38,6 @@ constexpr int TC_BK = 32;            // K per stage: one 128-byte swizzle row of
 constexpr int TC_BM = 128;           // rows of A per CTA (UMMA M = 256 per pair)
 constexpr int TC_BN = 256;           // columns of C per pair (UMMA N)
 constexpr int TC_TILE_BYTES = 128 * TC_BK * 4;   // one 128 x 32 FP32 operand tile
-constexpr int TC_THREADS = 192;      // warp0 TMA, warp1 MMA/TMEM, warps 2-5 epilogue
-constexpr int TC_TMEM_COLS = 256;
 
 int64_t tc_kpad(int64_t K) { return (K + TC_BK - 1) / TC_BK * TC_BK; }
 
@@ -112,7 +110,20 @@ cudaError_t launch_pack_split(const float *X, int64_t ld, bool kcontig, int64_t 
 
 // =====================================================================
 // KN1/KN2: tcgen05 GEMM on packed operands, CTA pair per 256x256 tile.
+//
+// Accumulation precision (Q7, measured on B200): the tensor core
+// adds each MMA's result into the TMEM accumulator with truncation, which on
+// same-sign data biases a K=16384 sum by ~1.8e-4 relative.  So the K loop is
+// cut into chunks of `kc_stages` stages: each chunk accumulates in one of two
+// TMEM buffers (ping-pong, 2 x 256 columns) and the epilogue warps drain the
+// finished buffer into FP32 registers with round-to-nearest adds while the
+// MMAs run on the other buffer ("promotion"), bounding the truncation bias
+// to one chunk.
 // =====================================================================
+constexpr int TC_EPI_WARPS = 8;                               // 2 per TMEM lane quarter
+constexpr int TC_THREADS_P = 64 + 32 * TC_EPI_WARPS;          // 320
+constexpr int TC_TMEM_COLS_P = 512;                           // 2 accumulator buffers
+
 template <int TERMS>
 struct TcCfg {
     static constexpr int PLANES = TERMS == 3 ? 2 : 1;
@@ -123,17 +134,18 @@ struct TcCfg {
 };
 
 template <int TERMS>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
     tc_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                     int Kp, float alpha, float beta, float *__restrict__ C, int64_t ldc, int tiles_m, int tiles_n,
-                    int group_m) {
+                    int group_m, int kc_stages) {
     using Cfg = TcCfg<TERMS>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
     uint64_t *empty = full + Cfg::STAGES;
-    uint64_t *accum = empty + Cfg::STAGES;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(accum + 1);
+    uint64_t *acc_full = empty + Cfg::STAGES;     // [2]
+    uint64_t *acc_empty = acc_full + 2;           // [2] (leader's counts both CTAs' epilogue warps)
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
@@ -150,20 +162,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     const int m0 = tm * (2 * TC_BM);
     const int n0 = tn * TC_BN;
     const int nkb = Kp / TC_BK;
+    const int nchunks = (nkb + kc_stages - 1) / kc_stages;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < Cfg::STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(accum, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&acc_full[b], 1);
+            mbar_init(&acc_empty[b], 2 * TC_EPI_WARPS);
+        }
         fence_mbar_init();
     }
     if (warp == 0 && lane == 0) {
         prefetch_tmap(&tmA);
         prefetch_tmap(&tmB);
     }
-    if (warp == 1) tmem_alloc_2sm<TC_TMEM_COLS>(tmem_slot);
+    if (warp == 1) tmem_alloc_2sm<TC_TMEM_COLS_P>(tmem_slot);
     tc_fence_before();
     cluster_sync();
     tc_fence_after();
@@ -196,6 +212,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         if (rank == 0 && lane == 0) {
             constexpr uint32_t idesc = idesc_tf32<2 * TC_BM, TC_BN>();
             for (int kb = 0; kb < nkb; ++kb) {
+                const int chunk = kb / kc_stages;
+                const int b = chunk & 1;
+                const bool first = (kb % kc_stages) == 0;
+                const bool last = (kb % kc_stages) == kc_stages - 1 || kb == nkb - 1;
+                const uint32_t dt = tmem_base + (uint32_t)(b * TC_BN);
+                if (first) {   // the epilogue has drained this buffer (both CTAs)
+                    mbar_wait(&acc_empty[b], (((uint32_t)chunk >> 1) & 1u) ^ 1u);
+                    tc_fence_after();
+                }
                 const int s = kb % Cfg::STAGES;
                 const uint32_t ph = (uint32_t)(kb / Cfg::STAGES) & 1u;
                 mbar_wait(&full[s], ph);
@@ -207,51 +232,67 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
                 for (int k = 0; k < TC_BK / 8; ++k) {
                     // advance 8 tf32 = 32 bytes along K inside the swizzle row
                     const uint64_t koff = (uint64_t)((k * 32) >> 4);
-                    const uint32_t acc0 = (kb > 0 || k > 0) ? 1u : 0u;
+                    const uint32_t acc0 = (first && k == 0) ? 0u : 1u;
                     if (TERMS == 3) {
                         const uint64_t a_sml = desc_kmajor_sw128(st + TC_TILE_BYTES);
                         const uint64_t b_sml = desc_kmajor_sw128(st + 3 * TC_TILE_BYTES);
                         // small terms first (they are the smaller magnitudes)
-                        mma_tf32_2sm(tmem_base, a_sml + koff, b_big + koff, idesc, acc0);
-                        mma_tf32_2sm(tmem_base, a_big + koff, b_sml + koff, idesc, 1u);
-                        mma_tf32_2sm(tmem_base, a_big + koff, b_big + koff, idesc, 1u);
+                        mma_tf32_2sm(dt, a_sml + koff, b_big + koff, idesc, acc0);
+                        mma_tf32_2sm(dt, a_big + koff, b_sml + koff, idesc, 1u);
+                        mma_tf32_2sm(dt, a_big + koff, b_big + koff, idesc, 1u);
                     } else {
-                        mma_tf32_2sm(tmem_base, a_big + koff, b_big + koff, idesc, acc0);
+                        mma_tf32_2sm(dt, a_big + koff, b_big + koff, idesc, acc0);
                     }
                 }
                 mma_commit_2sm_mc(&empty[s], (uint16_t)0x3);
+                if (last) mma_commit_2sm_mc(&acc_full[b], (uint16_t)0x3);
             }
-            mma_commit_2sm_mc(accum, (uint16_t)0x3);
         }
     } else {
-        // ===== epilogue: TMEM -> registers -> alpha/beta -> C (column-major) =====
+        // ===== epilogue: TMEM -> FP32 registers (promotion) -> alpha/beta -> C =====
         const int q = warp & 3;                        // TMEM lane quarter of this warp
+        const int h = (warp - 2) >> 2;                 // column half (128 columns)
         const int row = m0 + (int)rank * TC_BM + 32 * q + lane;
-        mbar_wait(accum, 0);
-        tc_fence_after();
-        const bool row_ok = row < M;
-#pragma unroll 1
-        for (int c = 0; c < TC_BN / 32; ++c) {
-            const int col0 = n0 + 32 * c;
-            if (col0 >= N) break;                      // warp-uniform
-            uint32_t v[32];
-            tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(32 * c), v);
-            tmem_ld_wait();
-            if (row_ok) {
-                float *cp = C + (int64_t)row + (int64_t)col0 * ldc;
-                const int jmax = min(32, N - col0);
-                if (beta == 0.0f) {
+        uint32_t leader_empty0;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(leader_empty0) : "r"(smem_u32(&acc_empty[0])));
+        float acc[128];
 #pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        if (j < jmax) cp[(int64_t)j * ldc] = alpha * __uint_as_float(v[j]);
-                } else {
+        for (int j = 0; j < 128; ++j) acc[j] = 0.0f;
+        for (int chunk = 0; chunk < nchunks; ++chunk) {
+            const int b = chunk & 1;
+            mbar_wait(&acc_full[b], ((uint32_t)chunk >> 1) & 1u);
+            tc_fence_after();
+            const uint32_t tb = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(b * TC_BN + h * 128);
 #pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        if (j < jmax) {
-                            float *d = cp + (int64_t)j * ldc;
-                            *d = fmaf(beta, *d, alpha * __uint_as_float(v[j]));
-                        }
-                }
+            for (int c = 0; c < 4; ++c) {
+                uint32_t v[32];
+                tmem_ld_32x32b_x32(tb + (uint32_t)(32 * c), v);
+                tmem_ld_wait();
+#pragma unroll
+                for (int j = 0; j < 32; ++j) acc[32 * c + j] += __uint_as_float(v[j]);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                const uint32_t eb = leader_empty0 + (uint32_t)(b * sizeof(uint64_t));
+                asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(eb) : "memory");
+            }
+        }
+        if (row < M) {
+            const int col0 = n0 + h * 128;
+            float *cp = C + (int64_t)row + (int64_t)col0 * ldc;
+            const int jmax = min(128, N - col0);
+            if (beta == 0.0f) {
+#pragma unroll
+                for (int j = 0; j < 128; ++j)
+                    if (j < jmax) cp[(int64_t)j * ldc] = alpha * acc[j];
+            } else {
+#pragma unroll
+                for (int j = 0; j < 128; ++j)
+                    if (j < jmax) {
+                        float *d = cp + (int64_t)j * ldc;
+                        *d = fmaf(beta, *d, alpha * acc[j]);
+                    }
             }
         }
     }
@@ -260,7 +301,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     cluster_sync();
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc_2sm<TC_TMEM_COLS>(tmem_base);
+        tmem_dealloc_2sm<TC_TMEM_COLS_P>(tmem_base);
     }
 }
 
@@ -314,8 +355,10 @@ static cudaError_t launch_tc_t(const float *Ap, const float *Bp, int64_t M, int6
     if (blocks > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
     cudaEvent_t ev = nullptr;
     prof_begin(s, true, &ev);
-    tc_sgemm_kernel<TERMS><<<(unsigned)blocks, TC_THREADS, Cfg::SMEM_BYTES, s>>>(
-        ta, tb, (int)M, (int)N, (int)Kp, alpha, beta, C, ldc, tiles_m, tiles_n, group_m);
+    // promotion chunk: 256 of K for 3xTF32 (8 stages), none for 1xTF32
+    const int kc_stages = TERMS == 3 ? 256 / TC_BK : 0x3fffffff;
+    tc_sgemm_kernel<TERMS><<<(unsigned)blocks, TC_THREADS_P, Cfg::SMEM_BYTES, s>>>(
+        ta, tb, (int)M, (int)N, (int)Kp, alpha, beta, C, ldc, tiles_m, tiles_n, group_m, kc_stages);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     prof_end(s, true, ev);
     return cudaGetLastError();

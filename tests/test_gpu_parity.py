@@ -88,7 +88,9 @@ class Case:
                            torch.cuda.current_stream().cuda_stream, math)
         torch.cuda.synchronize()
         assert st == 0, emm.strerror(st)
-        assert torch.equal(dA.cpu(), self.flat(self.A)) and torch.equal(dB.cpu(), self.flat(self.B))
+        # A and B (NaN padding included) are never written: compare bit patterns
+        assert torch.equal(dA.cpu().view(torch.int32), self.flat(self.A).view(torch.int32))
+        assert torch.equal(dB.cpu().view(torch.int32), self.flat(self.B).view(torch.int32))
         return dC.cpu()
 
     def logical(self, Cflat):
@@ -313,16 +315,18 @@ def test_accumulate_property(emm):
     assert_close(case, c_twice, R, 2 * S, 2 * T, 1e-5)
 
 
-def test_sametsign_diagnostic_3xtf32(emm):
-    """Diagnostic (Q7): same-sign U[0,1) data at large K exposes a
-    truncating tensor-core accumulator; report the max err/tol."""
-    case = Case("N", "N", 256, 256, 16384, 1.0, 0.0, kind="uniform01")
+@pytest.mark.parametrize("math", ["3xtf32", "ffma"])
+@pytest.mark.parametrize("K", [4096, 32768])
+def test_same_sign_accumulation(emm, math, K):
+    """Same-sign U[0,1) data at large K (Q7): a truncating
+    tensor-core accumulator biases the sum (measured 17.6x over the bound at
+    K=16384 without promotion); with FP32 promotion every 256 of K the FP32-
+    accurate bound 1e-5*S must hold here too."""
+    case = cached_case("N", "N", 256, 256, K, 1.0, 0.0, kind="uniform01")
     R, S, T, _ = case.oracle()
-    Cg = case.run(emm, "3xtf32")
-    G = case.logical(Cg)
-    ratio = float(np.max(np.abs(G - R) / (1e-5 * S)))
-    print(f"same-sign K=16384 3xTF32 max err/(1e-5*S) = {ratio:.3g}")
-    assert ratio < 10.0
+    Cg = case.run(emm, math)
+    r = assert_close(case, Cg, R, S, T, 1e-5)
+    print(f"same-sign K={K} {math}: max err/tol = {r:.3g}")
 
 
 def test_torch_binding_colmajor(emm):
