@@ -150,17 +150,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
 
-    // ---- tile coordinates: grouped raster along M (GPU-L2 analogue of the
-    //      paper's L2 blocking) ----
-    const int t = blockIdx.x >> 1;
-    const int per_group = group_m * tiles_n;
-    const int g = t / per_group;
-    const int first_m = g * group_m;
-    const int gsize = min(tiles_m - first_m, group_m);
-    const int tm = first_m + (t % per_group) % gsize;
-    const int tn = (t % per_group) / gsize;
-    const int m0 = tm * (2 * TC_BM);
-    const int n0 = tn * TC_BN;
+    // ---- persistent schedule: cluster `cid` walks tiles cid, cid+nclus, ...
+    //      in grouped raster order along M (GPU-L2 analogue of the paper's L2
+    //      blocking): consecutive tile indices (one "wave"
+    //      of clusters) cover a compact group_m x ~(nclus/group_m) block.
+    const int nclus = (int)(gridDim.x >> 1);
+    const int cid = (int)(blockIdx.x >> 1);
+    const int total_tiles = tiles_m * tiles_n;
+    auto tile_origin = [&](int t, int &m0, int &n0) {
+        const int per_group = group_m * tiles_n;
+        const int g = t / per_group;
+        const int first_m = g * group_m;
+        const int gsize = min(tiles_m - first_m, group_m);
+        const int tm = first_m + (t % per_group) % gsize;
+        const int tn = (t % per_group) / gsize;
+        m0 = tm * (2 * TC_BM);
+        n0 = tn * TC_BN;
+    };
     const int nkb = Kp / TC_BK;
     const int nchunks = (nkb + kc_stages - 1) / kc_stages;
 
@@ -191,19 +197,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
             uint32_t leader_full0;
             asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(leader_full0) : "r"(smem_u32(&full[0])));
             const uint64_t pol = policy_evict_normal();
-            const int arow = m0 + (int)rank * TC_BM;
-            const int brow = n0 + (int)rank * TC_BM;
-            for (int kb = 0; kb < nkb; ++kb) {
-                const int s = kb % Cfg::STAGES;
-                const uint32_t ph = (uint32_t)(kb / Cfg::STAGES) & 1u;
-                mbar_wait(&empty[s], ph ^ 1u);
-                const uint32_t fb = leader_full0 + (uint32_t)(s * sizeof(uint64_t));
-                if (rank == 0) mbar_arrive_expect_tx(&full[s], 2u * Cfg::STAGE_BYTES);
-                const uint32_t st = smem_u32(smem + s * Cfg::STAGE_BYTES);
+            int it = 0;
+            for (int t = cid; t < total_tiles; t += nclus) {
+                int m0, n0;
+                tile_origin(t, m0, n0);
+                const int arow = m0 + (int)rank * TC_BM;
+                const int brow = n0 + (int)rank * TC_BM;
+                for (int kb = 0; kb < nkb; ++kb, ++it) {
+                    const int s = it % Cfg::STAGES;
+                    const uint32_t ph = (uint32_t)(it / Cfg::STAGES) & 1u;
+                    mbar_wait(&empty[s], ph ^ 1u);
+                    const uint32_t fb = leader_full0 + (uint32_t)(s * sizeof(uint64_t));
+                    if (rank == 0) mbar_arrive_expect_tx(&full[s], 2u * Cfg::STAGE_BYTES);
+                    const uint32_t st = smem_u32(smem + s * Cfg::STAGE_BYTES);
 #pragma unroll
-                for (int p = 0; p < Cfg::PLANES; ++p) {
-                    tma_load_3d_2sm(st + p * TC_TILE_BYTES, &tmA, fb, kb * TC_BK, arow, p, pol);
-                    tma_load_3d_2sm(st + (Cfg::PLANES + p) * TC_TILE_BYTES, &tmB, fb, kb * TC_BK, brow, p, pol);
+                    for (int p = 0; p < Cfg::PLANES; ++p) {
+                        tma_load_3d_2sm(st + p * TC_TILE_BYTES, &tmA, fb, kb * TC_BK, arow, p, pol);
+                        tma_load_3d_2sm(st + (Cfg::PLANES + p) * TC_TILE_BYTES, &tmB, fb, kb * TC_BK, brow, p, pol);
+                    }
                 }
             }
         }
@@ -211,88 +222,98 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
         // ===== MMA issuer: one thread of the leader CTA drives the pair =====
         if (rank == 0 && lane == 0) {
             constexpr uint32_t idesc = idesc_tf32<2 * TC_BM, TC_BN>();
-            for (int kb = 0; kb < nkb; ++kb) {
-                const int chunk = kb / kc_stages;
-                const int b = chunk & 1;
-                const bool first = (kb % kc_stages) == 0;
-                const bool last = (kb % kc_stages) == kc_stages - 1 || kb == nkb - 1;
-                const uint32_t dt = tmem_base + (uint32_t)(b * TC_BN);
-                if (first) {   // the epilogue has drained this buffer (both CTAs)
-                    mbar_wait(&acc_empty[b], (((uint32_t)chunk >> 1) & 1u) ^ 1u);
+            int it = 0, ch = 0;   // global stage / chunk counters (continue across tiles)
+            for (int t = cid; t < total_tiles; t += nclus) {
+                for (int kb = 0; kb < nkb; ++kb, ++it) {
+                    const bool first = (kb % kc_stages) == 0;
+                    const bool last = (kb % kc_stages) == kc_stages - 1 || kb == nkb - 1;
+                    const int b = ch & 1;
+                    const uint32_t dt = tmem_base + (uint32_t)(b * TC_BN);
+                    if (first) {   // the epilogue has drained this buffer (both CTAs)
+                        mbar_wait(&acc_empty[b], (((uint32_t)ch >> 1) & 1u) ^ 1u);
+                        tc_fence_after();
+                    }
+                    const int s = it % Cfg::STAGES;
+                    const uint32_t ph = (uint32_t)(it / Cfg::STAGES) & 1u;
+                    mbar_wait(&full[s], ph);
                     tc_fence_after();
-                }
-                const int s = kb % Cfg::STAGES;
-                const uint32_t ph = (uint32_t)(kb / Cfg::STAGES) & 1u;
-                mbar_wait(&full[s], ph);
-                tc_fence_after();
-                const uint32_t st = smem_u32(smem + s * Cfg::STAGE_BYTES);
-                const uint64_t a_big = desc_kmajor_sw128(st);
-                const uint64_t b_big = desc_kmajor_sw128(st + Cfg::PLANES * TC_TILE_BYTES);
+                    const uint32_t st = smem_u32(smem + s * Cfg::STAGE_BYTES);
+                    const uint64_t a_big = desc_kmajor_sw128(st);
+                    const uint64_t b_big = desc_kmajor_sw128(st + Cfg::PLANES * TC_TILE_BYTES);
 #pragma unroll
-                for (int k = 0; k < TC_BK / 8; ++k) {
-                    // advance 8 tf32 = 32 bytes along K inside the swizzle row
-                    const uint64_t koff = (uint64_t)((k * 32) >> 4);
-                    const uint32_t acc0 = (first && k == 0) ? 0u : 1u;
-                    if (TERMS == 3) {
-                        const uint64_t a_sml = desc_kmajor_sw128(st + TC_TILE_BYTES);
-                        const uint64_t b_sml = desc_kmajor_sw128(st + 3 * TC_TILE_BYTES);
-                        // small terms first (they are the smaller magnitudes)
-                        mma_tf32_2sm(dt, a_sml + koff, b_big + koff, idesc, acc0);
-                        mma_tf32_2sm(dt, a_big + koff, b_sml + koff, idesc, 1u);
-                        mma_tf32_2sm(dt, a_big + koff, b_big + koff, idesc, 1u);
-                    } else {
-                        mma_tf32_2sm(dt, a_big + koff, b_big + koff, idesc, acc0);
+                    for (int k = 0; k < TC_BK / 8; ++k) {
+                        // advance 8 tf32 = 32 bytes along K inside the swizzle row
+                        const uint64_t koff = (uint64_t)((k * 32) >> 4);
+                        const uint32_t acc0 = (first && k == 0) ? 0u : 1u;
+                        if (TERMS == 3) {
+                            const uint64_t a_sml = desc_kmajor_sw128(st + TC_TILE_BYTES);
+                            const uint64_t b_sml = desc_kmajor_sw128(st + 3 * TC_TILE_BYTES);
+                            // small terms first (they are the smaller magnitudes)
+                            mma_tf32_2sm(dt, a_sml + koff, b_big + koff, idesc, acc0);
+                            mma_tf32_2sm(dt, a_big + koff, b_sml + koff, idesc, 1u);
+                            mma_tf32_2sm(dt, a_big + koff, b_big + koff, idesc, 1u);
+                        } else {
+                            mma_tf32_2sm(dt, a_big + koff, b_big + koff, idesc, acc0);
+                        }
+                    }
+                    mma_commit_2sm_mc(&empty[s], (uint16_t)0x3);
+                    if (last) {
+                        mma_commit_2sm_mc(&acc_full[b], (uint16_t)0x3);
+                        ++ch;
                     }
                 }
-                mma_commit_2sm_mc(&empty[s], (uint16_t)0x3);
-                if (last) mma_commit_2sm_mc(&acc_full[b], (uint16_t)0x3);
             }
         }
     } else {
         // ===== epilogue: TMEM -> FP32 registers (promotion) -> alpha/beta -> C =====
         const int q = warp & 3;                        // TMEM lane quarter of this warp
         const int h = (warp - 2) >> 2;                 // column half (128 columns)
-        const int row = m0 + (int)rank * TC_BM + 32 * q + lane;
         uint32_t leader_empty0;
         asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(leader_empty0) : "r"(smem_u32(&acc_empty[0])));
-        float acc[128];
+        int ch = 0;
+        for (int t = cid; t < total_tiles; t += nclus) {
+            int m0, n0;
+            tile_origin(t, m0, n0);
+            const int row = m0 + (int)rank * TC_BM + 32 * q + lane;
+            float acc[128];
 #pragma unroll
-        for (int j = 0; j < 128; ++j) acc[j] = 0.0f;
-        for (int chunk = 0; chunk < nchunks; ++chunk) {
-            const int b = chunk & 1;
-            mbar_wait(&acc_full[b], ((uint32_t)chunk >> 1) & 1u);
-            tc_fence_after();
-            const uint32_t tb = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(b * TC_BN + h * 128);
+            for (int j = 0; j < 128; ++j) acc[j] = 0.0f;
+            for (int c2 = 0; c2 < nchunks; ++c2, ++ch) {
+                const int b = ch & 1;
+                mbar_wait(&acc_full[b], ((uint32_t)ch >> 1) & 1u);
+                tc_fence_after();
+                const uint32_t tb = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(b * TC_BN + h * 128);
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                uint32_t v[32];
-                tmem_ld_32x32b_x32(tb + (uint32_t)(32 * c), v);
-                tmem_ld_wait();
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t v[32];
+                    tmem_ld_32x32b_x32(tb + (uint32_t)(32 * c), v);
+                    tmem_ld_wait();
 #pragma unroll
-                for (int j = 0; j < 32; ++j) acc[32 * c + j] += __uint_as_float(v[j]);
+                    for (int j = 0; j < 32; ++j) acc[32 * c + j] += __uint_as_float(v[j]);
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    const uint32_t eb = leader_empty0 + (uint32_t)(b * sizeof(uint64_t));
+                    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(eb) : "memory");
+                }
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) {
-                const uint32_t eb = leader_empty0 + (uint32_t)(b * sizeof(uint64_t));
-                asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(eb) : "memory");
-            }
-        }
-        if (row < M) {
-            const int col0 = n0 + h * 128;
-            float *cp = C + (int64_t)row + (int64_t)col0 * ldc;
-            const int jmax = min(128, N - col0);
-            if (beta == 0.0f) {
+            if (row < M) {
+                const int col0 = n0 + h * 128;
+                float *cp = C + (int64_t)row + (int64_t)col0 * ldc;
+                const int jmax = min(128, N - col0);
+                if (beta == 0.0f) {
 #pragma unroll
-                for (int j = 0; j < 128; ++j)
-                    if (j < jmax) cp[(int64_t)j * ldc] = alpha * acc[j];
-            } else {
+                    for (int j = 0; j < 128; ++j)
+                        if (j < jmax) cp[(int64_t)j * ldc] = alpha * acc[j];
+                } else {
 #pragma unroll
-                for (int j = 0; j < 128; ++j)
-                    if (j < jmax) {
-                        float *d = cp + (int64_t)j * ldc;
-                        *d = fmaf(beta, *d, alpha * acc[j]);
-                    }
+                    for (int j = 0; j < 128; ++j)
+                        if (j < jmax) {
+                            float *d = cp + (int64_t)j * ldc;
+                            *d = fmaf(beta, *d, alpha * acc[j]);
+                        }
+                }
             }
         }
     }
@@ -351,8 +372,16 @@ static cudaError_t launch_tc_t(const float *Ap, const float *Bp, int64_t M, int6
     const int tiles_m = (int)((M + 2 * TC_BM - 1) / (2 * TC_BM));
     const int tiles_n = (int)((N + TC_BN - 1) / TC_BN);
     const int group_m = 8;
-    const int64_t blocks = 2LL * tiles_m * tiles_n;
-    if (blocks > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+    static int num_sms = 0;
+    if (!num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int64_t tiles = (int64_t)tiles_m * tiles_n;
+    if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+    const int64_t clusters = tiles < num_sms / 2 ? tiles : num_sms / 2;   // persistent: one pair per 2 SMs
+    const int64_t blocks = 2 * clusters;
     cudaEvent_t ev = nullptr;
     prof_begin(s, true, &ev);
     // promotion chunk: 256 of K for 3xTF32 (8 stages), none for 1xTF32
