@@ -105,7 +105,8 @@ static size_t ws_bytes(int64_t M, int64_t N, int64_t K, emm_math_t math) {
     if (math == EMM_MATH_FFMA || M == 0 || N == 0 || K == 0) return 0;
     const int64_t Kp = tc_kpad(K);
     const size_t pl = (size_t)planes_of(math);
-    return align_up(pl * (size_t)M * (size_t)Kp * 4, 1024) + align_up(pl * (size_t)N * (size_t)Kp * 4, 1024);
+    return align_up(pl * (size_t)M * (size_t)Kp * 4, 1024) + align_up(pl * (size_t)N * (size_t)Kp * 4, 1024) +
+           1024 /* wave-lockstep counter */;
 }
 
 }  // namespace emm
@@ -167,8 +168,9 @@ extern "C" int emm_sgemm_ex(char transA, char transB, int64_t M, int64_t N, int6
                                           align_up((size_t)planes * (size_t)M * (size_t)Kp * 4, 1024));
     cudaError_t e = launch_pack_split(A, lda, /*kcontig=*/!is_n(transA), M, K, Kp, planes, Ap, s);
     if (e == cudaSuccess) e = launch_pack_split(B, ldb, /*kcontig=*/is_n(transB), N, K, Kp, planes, Bp, s);
+    unsigned int *ctr = reinterpret_cast<unsigned int *>(reinterpret_cast<uint8_t *>(ws) + need - 1024);
     if (e == cudaSuccess)
-        e = launch_tc_sgemm(math == EMM_MATH_3XTF32 ? 3 : 1, Ap, Bp, M, N, Kp, alpha, beta, C, ldc, s);
+        e = launch_tc_sgemm(math == EMM_MATH_3XTF32 ? 3 : 1, Ap, Bp, M, N, Kp, alpha, beta, C, ldc, ctr, s);
     if (own) {
         cudaError_t e2 = cudaFreeAsync(ws, s);
         if (e == cudaSuccess) e = e2;

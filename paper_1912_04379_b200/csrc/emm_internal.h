@@ -25,8 +25,10 @@ void prof_end(cudaStream_t s, bool is_gemm, cudaEvent_t ev0);
 cudaError_t launch_pack_split(const float *X, int64_t ld, bool kcontig, int64_t R, int64_t K, int64_t Kp,
                               int planes, float *out, cudaStream_t s);
 // C <- alpha * Ap * Bp^T + beta*C on the packed operands (tcgen05, 2-CTA).
+// wave_ctr: 4 bytes of device scratch owned by this call (zeroed here,
+// stream-ordered) for the producers' wave lockstep; NULL disables it.
 cudaError_t launch_tc_sgemm(int terms, const float *Ap, const float *Bp, int64_t M, int64_t N, int64_t Kp,
-                            float alpha, float beta, float *C, int64_t ldc, cudaStream_t s);
+                            float alpha, float beta, float *C, int64_t ldc, unsigned int *wave_ctr, cudaStream_t s);
 int64_t tc_kpad(int64_t K);
 
 // ---- CUDA-core path (k_ffma.cu) ------------------------------------------

@@ -137,7 +137,7 @@ template <int TERMS>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
     tc_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                     int Kp, float alpha, float beta, float *__restrict__ C, int64_t ldc, int tiles_m, int tiles_n,
-                    int group_m, int kc_stages) {
+                    int group_m, int kc_stages, unsigned int *__restrict__ wave_ctr) {
     using Cfg = TcCfg<TERMS>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -198,7 +198,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
             asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(leader_full0) : "r"(smem_u32(&full[0])));
             const uint64_t pol = policy_evict_normal();
             int it = 0;
-            for (int t = cid; t < total_tiles; t += nclus) {
+            unsigned int done_target = 0;   // CTAs that finished issuing waves 0..w-1
+            for (int t = cid, w = 0; t < total_tiles; t += nclus, ++w) {
+                if (w > 0 && wave_ctr) {
+                    // Wave lockstep: start loading wave w only when every CTA
+                    // has issued all loads of wave w-1, so the ~17 operand
+                    // panels a wave shares stream through L2 once (all CTAs
+                    // are co-resident: grid <= SMs, 1 CTA per SM).
+                    const long long t0 = clock64();
+                    while (true) {
+                        unsigned int v;
+                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(wave_ctr) : "memory");
+                        if (v >= done_target) break;
+                        __nanosleep(128);
+                        if (clock64() - t0 > 40000000000LL) __trap();
+                    }
+                }
+                {
+                    const int active = min(nclus, total_tiles - w * nclus);
+                    done_target += 2u * (unsigned)active;
+                }
                 int m0, n0;
                 tile_origin(t, m0, n0);
                 const int arow = m0 + (int)rank * TC_BM;
@@ -216,6 +235,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
                         tma_load_3d_2sm(st + (Cfg::PLANES + p) * TC_TILE_BYTES, &tmB, fb, kb * TC_BK, brow, p, pol);
                     }
                 }
+                if (wave_ctr) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(wave_ctr) : "memory");
             }
         }
     } else if (warp == 1) {
@@ -357,7 +377,7 @@ static bool make_tmap(CUtensorMap *tm, const float *base, int64_t R, int64_t Kp,
 
 template <int TERMS>
 static cudaError_t launch_tc_t(const float *Ap, const float *Bp, int64_t M, int64_t N, int64_t Kp, float alpha,
-                               float beta, float *C, int64_t ldc, cudaStream_t s) {
+                               float beta, float *C, int64_t ldc, unsigned int *wave_ctr, cudaStream_t s) {
     using Cfg = TcCfg<TERMS>;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
@@ -387,17 +407,21 @@ static cudaError_t launch_tc_t(const float *Ap, const float *Bp, int64_t M, int6
     // promotion chunk: 256 of K for 3xTF32 (8 stages), none for 1xTF32
     const int kc_stages = TERMS == 3 ? 256 / TC_BK : 0x3fffffff;
     tc_sgemm_kernel<TERMS><<<(unsigned)blocks, TC_THREADS_P, Cfg::SMEM_BYTES, s>>>(
-        ta, tb, (int)M, (int)N, (int)Kp, alpha, beta, C, ldc, tiles_m, tiles_n, group_m, kc_stages);
+        ta, tb, (int)M, (int)N, (int)Kp, alpha, beta, C, ldc, tiles_m, tiles_n, group_m, kc_stages, wave_ctr);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     prof_end(s, true, ev);
     return cudaGetLastError();
 }
 
 cudaError_t launch_tc_sgemm(int terms, const float *Ap, const float *Bp, int64_t M, int64_t N, int64_t Kp,
-                            float alpha, float beta, float *C, int64_t ldc, cudaStream_t s) {
+                            float alpha, float beta, float *C, int64_t ldc, unsigned int *wave_ctr, cudaStream_t s) {
     if (M > 0x7fffffffLL || N > 0x7fffffffLL || Kp > 0x7fffffffLL) return cudaErrorInvalidValue;
-    return terms == 3 ? launch_tc_t<3>(Ap, Bp, M, N, Kp, alpha, beta, C, ldc, s)
-                      : launch_tc_t<1>(Ap, Bp, M, N, Kp, alpha, beta, C, ldc, s);
+    if (wave_ctr) {
+        cudaError_t e = cudaMemsetAsync(wave_ctr, 0, sizeof(unsigned int), s);
+        if (e != cudaSuccess) return e;
+    }
+    return terms == 3 ? launch_tc_t<3>(Ap, Bp, M, N, Kp, alpha, beta, C, ldc, wave_ctr, s)
+                      : launch_tc_t<1>(Ap, Bp, M, N, Kp, alpha, beta, C, ldc, wave_ctr, s);
 }
 
 }  // namespace emm

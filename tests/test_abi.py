@@ -118,8 +118,8 @@ def test_row_partition_c5(emm):
 def test_workspace_bytes(emm):
     assert emm.workspace_bytes("N", "N", 64, 64, 64, "ffma") == 0
     # 3xTF32: 2 planes of M x Kp and N x Kp floats, Kp = K rounded up to 32
-    assert emm.workspace_bytes("N", "N", 256, 128, 33, "3xtf32") == 2 * 4 * 64 * (256 + 128)
-    assert emm.workspace_bytes("N", "T", 256, 128, 32, "1xtf32") == 4 * 32 * (256 + 128)
+    assert emm.workspace_bytes("N", "N", 256, 128, 33, "3xtf32") == 2 * 4 * 64 * (256 + 128) + 1024
+    assert emm.workspace_bytes("N", "T", 256, 128, 32, "1xtf32") == 4 * 32 * (256 + 128) + 1024
 
 
 def test_strerror_and_version(emm):
