@@ -119,6 +119,11 @@ void emm_release_cache(void);
  * rank order.  Host-only; valid for nranks >= 1, 0 <= rank < nranks. */
 void emm_row_partition(int64_t M, int nranks, int rank, int64_t *row0, int64_t *rows);
 
+/* Width (columns) of the B column panels emm_sgemm_multi broadcasts one at a
+ * time (the last panel may be narrower): ~N/8, >= 1024, multiple of 256.
+ * Host-only. */
+int64_t emm_multi_panel_cols(int64_t N);
+
 /* 128-byte NCCL unique id, produced on one rank and distributed by the
  * caller (e.g. torch.distributed broadcast).  Returns EMM_ERR_COMM if NCCL
  * cannot be loaded. */

@@ -22,5 +22,8 @@ from .emm import (  # noqa: F401
     version,
     workspace_bytes,
     Comm,
+    broadcast_unique_id,
+    get_unique_id,
+    multi_panel_cols,
     sgemm_multi,
 )

@@ -53,7 +53,7 @@ static bool trans_ok(char t) { return t == 'N' || t == 'n' || t == 'T' || t == '
 static bool is_n(char t) { return t == 'N' || t == 'n'; }
 static int64_t max1(int64_t v) { return v > 1 ? v : 1; }
 
-static int check_args(char tA, char tB, int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb, int64_t ldc) {
+int check_args(char tA, char tB, int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb, int64_t ldc) {
     if (!trans_ok(tA)) return -1;
     if (!trans_ok(tB)) return -2;
     if (M < 0) return -3;
@@ -73,7 +73,7 @@ static void span(const void *p, int64_t rows, int64_t cols, int64_t ld, uintptr_
     *hi = *lo + (uintptr_t)(((cols - 1) * ld + rows) * 4);
 }
 
-static int check_device() {
+int check_device() {
     static std::mutex mu;
     static int cached[64];
     static bool init = false;
@@ -97,7 +97,7 @@ static int check_device() {
 
 static int cuda_status(cudaError_t e) { return e == cudaSuccess ? 0 : EMM_ERR_CUDA_BASE + (int)e; }
 
-static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 static int planes_of(emm_math_t m) { return m == EMM_MATH_3XTF32 ? 2 : 1; }
 

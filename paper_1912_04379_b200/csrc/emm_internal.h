@@ -10,6 +10,11 @@
 
 namespace emm {
 
+// BLAS argument rules (0 or -i) and the sm_100 device check (api.cu).
+int check_args(char tA, char tB, int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb, int64_t ldc);
+int check_device();
+size_t align_up(size_t v, size_t a);
+
 // Launch accounting (every kernel launch of the library increments it).
 extern std::atomic<uint64_t> g_launches;
 

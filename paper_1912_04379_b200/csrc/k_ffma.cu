@@ -20,14 +20,23 @@ namespace emm {
 
 constexpr int FB_M = 128, FB_N = 128, FB_K = 16, FB_THREADS = 256;
 constexpr int FB_PAD = 4;
+// Promotion: every FB_PROMOTE K-tiles (256 of K) the 64 register partial sums
+// are added (round-to-nearest) into a per-thread master copy in SMEM and
+// restarted, so sequential FP32 rounding error grows with 256 + K/256 terms
+// instead of K (same-sign data at K = 32768 otherwise exceeds 1e-5 * S).
+constexpr int FB_PROMOTE = 16;
+constexpr int FB_SMEM_BYTES = (2 * FB_K * (FB_M + FB_PAD) + 2 * FB_K * (FB_N + FB_PAD) + 64 * FB_THREADS) * 4;
 
 template <bool TA, bool TB>
 __global__ void __launch_bounds__(FB_THREADS) ffma_sgemm_kernel(int64_t M, int64_t N, int64_t K, float alpha,
                                                                 const float *__restrict__ A, int64_t lda,
                                                                 const float *__restrict__ B, int64_t ldb, float beta,
                                                                 float *__restrict__ C, int64_t ldc) {
-    __shared__ __align__(16) float As[2][FB_K][FB_M + FB_PAD];
-    __shared__ __align__(16) float Bs[2][FB_K][FB_N + FB_PAD];
+    extern __shared__ __align__(16) float fb_smem[];
+    float(*As)[FB_K][FB_M + FB_PAD] = reinterpret_cast<float(*)[FB_K][FB_M + FB_PAD]>(fb_smem);
+    float(*Bs)[FB_K][FB_N + FB_PAD] =
+        reinterpret_cast<float(*)[FB_K][FB_N + FB_PAD]>(fb_smem + 2 * FB_K * (FB_M + FB_PAD));
+    float *master = fb_smem + 2 * FB_K * (FB_M + FB_PAD) + 2 * FB_K * (FB_N + FB_PAD);   // [64][256]
     const int tid = threadIdx.x;
     const int64_t m0 = (int64_t)blockIdx.x * FB_M;
     const int64_t n0 = (int64_t)blockIdx.y * FB_N;
@@ -81,6 +90,9 @@ __global__ void __launch_bounds__(FB_THREADS) ffma_sgemm_kernel(int64_t M, int64
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[i][j] = 0.0f;
 
+#pragma unroll
+    for (int e = 0; e < 64; ++e) master[e * FB_THREADS + tid] = 0.0f;
+
     float ra[8], rb[8];
     load_a(0, ra);
     load_b(0, rb);
@@ -113,8 +125,21 @@ __global__ void __launch_bounds__(FB_THREADS) ffma_sgemm_kernel(int64_t M, int64
             store_a(buf ^ 1, ra);
             store_b(buf ^ 1, rb);
         }
+        if ((kt + 1) % FB_PROMOTE == 0 || !more) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    master[(i * 8 + j) * FB_THREADS + tid] += acc[i][j];
+                    acc[i][j] = 0.0f;
+                }
+        }
         __syncthreads();
     }
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = master[(i * 8 + j) * FB_THREADS + tid];
 
     // epilogue: alpha*acc + beta*C (C not read when beta == 0), predicated
 #pragma unroll
@@ -138,12 +163,25 @@ cudaError_t launch_ffma_sgemm(bool tA, bool tB, int64_t M, int64_t N, int64_t K,
     const int64_t gx = (M + FB_M - 1) / FB_M, gy = (N + FB_N - 1) / FB_N;
     if (gx > 0x7fffffffLL || gy > 65535) return cudaErrorInvalidConfiguration;
     dim3 grid((unsigned)gx, (unsigned)gy);
+    static cudaError_t attr = [] {
+        cudaError_t e = cudaSuccess;
+        auto set = [&](const void *f) {
+            cudaError_t r = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, FB_SMEM_BYTES);
+            if (r != cudaSuccess) e = r;
+        };
+        set((const void *)ffma_sgemm_kernel<false, false>);
+        set((const void *)ffma_sgemm_kernel<false, true>);
+        set((const void *)ffma_sgemm_kernel<true, false>);
+        set((const void *)ffma_sgemm_kernel<true, true>);
+        return e;
+    }();
+    if (attr != cudaSuccess) return attr;
     cudaEvent_t ev = nullptr;
     prof_begin(s, true, &ev);
-    if (!tA && !tB) ffma_sgemm_kernel<false, false><<<grid, FB_THREADS, 0, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
-    else if (!tA && tB) ffma_sgemm_kernel<false, true><<<grid, FB_THREADS, 0, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
-    else if (tA && !tB) ffma_sgemm_kernel<true, false><<<grid, FB_THREADS, 0, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
-    else ffma_sgemm_kernel<true, true><<<grid, FB_THREADS, 0, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    if (!tA && !tB) ffma_sgemm_kernel<false, false><<<grid, FB_THREADS, FB_SMEM_BYTES, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    else if (!tA && tB) ffma_sgemm_kernel<false, true><<<grid, FB_THREADS, FB_SMEM_BYTES, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    else if (tA && !tB) ffma_sgemm_kernel<true, false><<<grid, FB_THREADS, FB_SMEM_BYTES, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    else ffma_sgemm_kernel<true, true><<<grid, FB_THREADS, FB_SMEM_BYTES, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     prof_end(s, true, ev);
     return cudaGetLastError();

@@ -84,6 +84,13 @@ cudaEvent_t ev_at(Comm *c, size_t i) {
 
 using namespace emm;
 
+extern "C" int64_t emm_multi_panel_cols(int64_t N) {
+    // ~8 panels, each >= 1024 columns and a multiple of the 256-wide tile
+    int64_t panel = (N + 7) / 8;
+    if (panel < 1024) panel = 1024;
+    return (panel + 255) / 256 * 256;
+}
+
 extern "C" int emm_get_unique_id(void *id128) {
     Nccl &n = nccl();
     if (!n.ok || !id128) return EMM_ERR_COMM;
@@ -152,45 +159,67 @@ extern "C" int emm_sgemm_multi(void *comm, char transA, char transB, int64_t M, 
     if (!st) st = cuda_st(cudaStreamWaitEvent(c->comm_stream, e0, 0));
     if (st) return st;
 
-    if (bN && K > 0 && N > 0) {
-        // column panels of B: contiguous K x nc ranges, ~8 panels (>= 1024 cols)
-        int64_t panel = (N + 7) / 8;
-        if (panel < 1024) panel = 1024;
-        panel = (panel + 255) / 256 * 256;
+    const bool nA = (transA == 'N' || transA == 'n');
+    if ((st = check_args(transA, transB, rows, N, K, lda, ldb, ldc > 0 ? ldc : 1))) return st;
+    if ((st = check_device())) return st;
+    const bool ab_used = !(alpha == 0.0f || K == 0);
+    const bool tc = math != EMM_MATH_FFMA && ab_used;
+    // Tensor-core paths: re-buffer/split this rank's A rows ONCE, then per
+    // B panel: wait for its broadcast, re-buffer the panel, GEMM.
+    void *ws = nullptr;
+    float *Ap = nullptr, *Bp = nullptr;
+    unsigned int *ctr = nullptr;
+    const int64_t Kp = tc_kpad(K);
+    const int planes = math == EMM_MATH_3XTF32 ? 2 : 1;
+    const int64_t panel = bN ? emm_multi_panel_cols(N) : N;
+    if (tc && rows > 0 && N > 0) {
+        const size_t a_bytes = align_up((size_t)planes * rows * Kp * 4, 1024);
+        const size_t b_bytes = align_up((size_t)planes * panel * Kp * 4, 1024);
+        if ((st = cuda_st(cudaMallocAsync(&ws, a_bytes + b_bytes + 1024, s)))) return st;
+        Ap = reinterpret_cast<float *>(ws);
+        Bp = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(ws) + a_bytes);
+        ctr = reinterpret_cast<unsigned int *>(reinterpret_cast<uint8_t *>(ws) + a_bytes + b_bytes);
+        st = cuda_st(launch_pack_split(A_local, lda, /*kcontig=*/!nA, rows, K, Kp, planes, Ap, s));
+    }
+    auto panel_gemm = [&](const float *bp, int64_t nc, float *cp) -> int {
+        if (rows == 0 || nc == 0) return 0;
+        if (!tc)   // FFMA, or alpha == 0 / K == 0 (C <- beta*C)
+            return emm_sgemm_ex(transA, transB, rows, nc, K, alpha, A_local, lda, bp, ldb, beta, cp, ldc, s, math,
+                                nullptr, 0);
+        cudaError_t e = launch_pack_split(bp, ldb, /*kcontig=*/bN, nc, K, Kp, planes, Bp, s);
+        if (e == cudaSuccess)
+            e = launch_tc_sgemm(planes == 2 ? 3 : 1, Ap, Bp, rows, nc, Kp, alpha, beta, cp, ldc, ctr, s);
+        return cuda_st(e);
+    };
+
+    if (!st && bN && N > 0) {
+        // column panels of B: contiguous K x nc ranges (emm_multi_panel_cols);
+        // the GEMM of panel c waits only for panel c's broadcast.
         size_t idx = 1;
-        for (int64_t c0 = 0; c0 < N; c0 += panel, ++idx) {
+        for (int64_t c0 = 0; c0 < N && !st; c0 += panel, ++idx) {
             const int64_t nc = (N - c0 < panel) ? N - c0 : panel;
             float *bp = B + c0 * ldb;
-            if (c->nranks > 1) {
-                st = nccl_status(n.broadcast(bp, bp, (size_t)(K * nc), ncclFloat32, root, c->nc, c->comm_stream));
-                if (st) return st;
-            }
+            if (K > 0) st = nccl_status(n.broadcast(bp, bp, (size_t)(K * nc), ncclFloat32, root, c->nc, c->comm_stream));
             cudaEvent_t ev = ev_at(c, idx);
-            if (!ev) return EMM_ERR_NOMEM;
-            if ((st = cuda_st(cudaEventRecord(ev, c->comm_stream)))) return st;
-            if ((st = cuda_st(cudaStreamWaitEvent(s, ev, 0)))) return st;
-            if (rows > 0) {
-                st = emm_sgemm_ex(transA, transB, rows, nc, K, alpha, A_local, lda, bp, ldb, beta, C_local + c0 * ldc,
-                                  ldc, s, math, nullptr, 0);
-                if (st) return st;
-            }
+            if (!st && !ev) st = EMM_ERR_NOMEM;
+            if (!st) st = cuda_st(cudaEventRecord(ev, c->comm_stream));
+            if (!st) st = cuda_st(cudaStreamWaitEvent(s, ev, 0));
+            if (!st) st = panel_gemm(bp, nc, C_local + c0 * ldc);
         }
-    } else {
+    } else if (!st && N > 0) {
         // transB = 'T': B's stored columns run along K; broadcast it whole
         // (no panel overlap), then one GEMM.
-        if (c->nranks > 1 && b_elems > 0) {
-            st = nccl_status(n.broadcast(B, B, (size_t)b_elems, ncclFloat32, root, c->nc, c->comm_stream));
-            if (st) return st;
-        }
+        if (b_elems > 0) st = nccl_status(n.broadcast(B, B, (size_t)b_elems, ncclFloat32, root, c->nc, c->comm_stream));
         cudaEvent_t ev = ev_at(c, 1);
-        if ((st = cuda_st(cudaEventRecord(ev, c->comm_stream)))) return st;
-        if ((st = cuda_st(cudaStreamWaitEvent(s, ev, 0)))) return st;
-        if (rows > 0) {
-            st = emm_sgemm_ex(transA, transB, rows, N, K, alpha, A_local, lda, B, ldb, beta, C_local, ldc, s, math,
-                              nullptr, 0);
-            if (st) return st;
-        }
+        if (!st) st = cuda_st(cudaEventRecord(ev, c->comm_stream));
+        if (!st) st = cuda_st(cudaStreamWaitEvent(s, ev, 0));
+        if (!st) st = panel_gemm(B, N, C_local);
     }
+    if (ws) {
+        int st2 = cuda_st(cudaFreeAsync(ws, s));
+        if (!st) st = st2;
+    }
+    if (st) return st;
 
     if (C_full) {
         // all-gather of the row blocks: compact own block into the rank-major
@@ -215,7 +244,7 @@ extern "C" int emm_sgemm_multi(void *comm, char transA, char transB, int64_t M, 
             st = cuda_st(cudaMemcpy2DAsync(c->stage + offs[c->rank], (size_t)rows * 4, C_local, (size_t)ldc * 4,
                                            (size_t)rows * 4, (size_t)N, cudaMemcpyDeviceToDevice, s));
         if (st) return st;
-        if (c->nranks > 1) {
+        {
             n.groupStart();
             for (int r = 0; r < c->nranks; ++r)
                 if (rws[r] > 0)

@@ -50,6 +50,8 @@ def lib() -> ctypes.CDLL:
     L.emm_release_cache.restype = None
     L.emm_row_partition.argtypes = [i64, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]
     L.emm_row_partition.restype = None
+    L.emm_multi_panel_cols.argtypes = [i64]
+    L.emm_multi_panel_cols.restype = i64
     L.emm_get_unique_id.argtypes = [vp]
     L.emm_get_unique_id.restype = i32
     L.emm_comm_create.argtypes = [ctypes.POINTER(vp), vp, i32, i32]
@@ -108,6 +110,19 @@ def row_partition(M: int, nranks: int, rank: int):
     r0, n = ctypes.c_int64(), ctypes.c_int64()
     lib().emm_row_partition(M, nranks, rank, ctypes.byref(r0), ctypes.byref(n))
     return r0.value, n.value
+
+
+def multi_panel_cols(N: int) -> int:
+    return int(lib().emm_multi_panel_cols(N))
+
+
+def get_unique_id() -> bytes:
+    """128-byte NCCL unique id (raises EmmError if NCCL cannot be loaded)."""
+    idbuf = (ctypes.c_uint8 * 128)()
+    st = lib().emm_get_unique_id(ctypes.cast(idbuf, ctypes.c_void_p))
+    if st:
+        raise EmmError(st, "emm_get_unique_id")
+    return bytes(idbuf)
 
 
 def workspace_bytes(transA, transB, M, N, K, math="3xtf32") -> int:
@@ -180,6 +195,18 @@ def sgemm_host(transA, transB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, mat
         raise EmmError(st, "emm_sgemm_host")
 
 
+def broadcast_unique_id(rank: int, group=None) -> bytes:
+    """Rank 0 creates the NCCL id; every rank of the torch.distributed group
+    receives the same 128 bytes (the bootstrap of emm_comm_create)."""
+    import torch
+    import torch.distributed as dist
+    raw = get_unique_id() if rank == 0 else bytes(128)
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else "cpu"
+    t = torch.tensor(list(raw), dtype=torch.uint8, device=dev)
+    dist.broadcast(t, 0, group=group)
+    return bytes(t.cpu().tolist())
+
+
 class Comm:
     """NCCL communicator for emm_sgemm_multi, bootstrapped over an existing
     torch.distributed process group (the 128-byte id is broadcast with it)."""
@@ -187,15 +214,7 @@ class Comm:
     def __init__(self, rank: int, nranks: int, group=None):
         import torch
         import torch.distributed as dist
-        idbuf = (ctypes.c_uint8 * 128)()
-        if rank == 0:
-            st = lib().emm_get_unique_id(ctypes.cast(idbuf, ctypes.c_void_p))
-            if st:
-                raise EmmError(st, "emm_get_unique_id")
-        dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else "cpu"
-        t = torch.tensor(list(bytes(idbuf)), dtype=torch.uint8, device=dev)
-        dist.broadcast(t, 0, group=group)
-        raw = bytes(t.cpu().tolist())
+        raw = broadcast_unique_id(rank, group)
         idbuf = (ctypes.c_uint8 * 128).from_buffer_copy(raw)
         h = ctypes.c_void_p()
         st = lib().emm_comm_create(ctypes.byref(h), ctypes.cast(idbuf, ctypes.c_void_p), nranks, rank)
