@@ -166,11 +166,12 @@ def cpu_oracle_sample(n, nrows, gen_device="cpu"):
 
 
 def auto_rows(n):
-    # ~10-20 s of oracle work on the host: rate ~0.6 GFLOP/s per core (j-p-i FP64 loop)
+    # ~15 s of oracle work on the host: the j-p-i FP64 loop ran at ~2.8 GFLOP/s
+    # per core on the B200 box (16 cores, round 1)
     cores = len(os.sched_getaffinity(0))
-    rate = 0.6e9 * cores
+    rate = 2.8e9 * cores
     r = int(15.0 * rate / (2.0 * n * n))
-    return max(4, min(256, r))
+    return max(4, min(512, r))
 
 
 # --------------------------------------------------------------------- reference arm

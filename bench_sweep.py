@@ -1,0 +1,113 @@
+#!/usr/bin/env python
+"""Per-config measurements for BASELINE.md §5 (not the driver's bench line).
+
+For every BASELINE.json config and math path: median and min device time of
+single emm_sgemm_ex calls (CUDA events on the launching stream, L2 flushed
+before each timed call by writing a 2x L2-sized buffer),
+GFLOP/s = 2MNK/t, % of the path's roofline, and GB/s of compulsory traffic
+4(MK + KN + MN [+ MN if beta != 0]) for the latency/HBM-side shapes.
+
+    python bench_sweep.py [--reps 20] [--out profiles/r01_sweep.jsonl]
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import datagen  # noqa: E402
+import paper_1912_04379_b200 as emm  # noqa: E402
+
+
+def peaks():
+    with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+        mp = json.load(f)
+    tf32 = mp["bf16_tflops"] * 1.1 / 2.25
+    return {"3xtf32": tf32 / 3, "1xtf32": tf32, "ffma": 148 * 256 * 1.965e9 / 1e12}
+
+
+def configs():
+    out = [("c1", "N", "N", 64, 64, 64, 1.0, 0.0, (0, 0, 0), "uniform")]
+    for n in (100, 333, 512, 700, 1000, 1024, 2048, 4096, 8192):
+        out.append((f"c2-{n}", "N", "N", n, n, n, 1.0, 0.0, (0, 0, 0), "uniform"))
+    for tA in "NT":
+        for tB in "NT":
+            out.append((f"c3-{tA}{tB}", tA, tB, 1531, 997, 2049, -0.75, 1.25, (13, 7, 5), "normal"))
+    out.append(("c4-i", "N", "T", 65536, 1024, 4096, 1.0, 1.0, (0, 0, 0), "normal"))
+    out.append(("c4-ii", "N", "T", 65536, 4096, 1024, 1.0, 1.0, (0, 0, 0), "normal"))
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_sweep.jsonl"))
+    ap.add_argument("--maths", default="3xtf32,1xtf32,ffma")
+    ap.add_argument("--only", default="")
+    args = ap.parse_args()
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    flush = torch.empty(2 * l2 // 4, dtype=torch.float32, device=dev)
+    pk = peaks()
+    stream = torch.cuda.current_stream(dev)
+    lines = []
+    for name, tA, tB, M, N, K, alpha, beta, pad, kind in configs():
+        if args.only and not name.startswith(args.only):
+            continue
+        ar, ac = (M, K) if tA == "N" else (K, M)
+        br, bc = (K, N) if tB == "N" else (N, K)
+        sig = 1.0 if not name.startswith("c4") else 1.0 / K ** 0.5
+        gdev = dev if kind != "normal" else "cpu"
+        A = datagen.matrix(kind, datagen.TAG_A, ar, ac, ar + pad[0], sigma=sig, device=gdev)
+        B = datagen.matrix(kind, datagen.TAG_B, br, bc, br + pad[1], sigma=sig, device=gdev)
+        C0 = datagen.matrix("uniform" if kind != "normal" or not name.startswith("c4") else "normal",
+                            datagen.TAG_C, M, N, M + pad[2], sigma=sig, device=gdev)
+        dA, dB, dC = (datagen.storage_of(x).to(dev) for x in (A, B, C0))
+        for math in args.maths.split(","):
+            nbytes = emm.workspace_bytes(tA, tB, M, N, K, math)
+            ws = torch.empty(nbytes // 4 + 512, dtype=torch.float32, device=dev) if nbytes else None
+            wsp = 0
+            if ws is not None:
+                wsp = ws.data_ptr() + (-ws.data_ptr()) % 1024
+
+            def call():
+                st = emm.sgemm_ptr(tA, tB, M, N, K, alpha, dA.data_ptr(), ar + pad[0], dB.data_ptr(), br + pad[1],
+                                   beta, dC.data_ptr(), M + pad[2], stream.cuda_stream, math,
+                                   wsp or None, nbytes)
+                assert st == 0, emm.strerror(st)
+            for _ in range(3):
+                call()
+            ts = []
+            for _ in range(args.reps):
+                flush.zero_()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                call()
+                e1.record(stream)
+                e1.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            med = statistics.median(ts)
+            fl = 2.0 * M * N * K
+            byt = 4.0 * (M * K + K * N + M * N + (M * N if beta != 0 else 0))
+            rec = {"config": name, "math": math, "M": M, "N": N, "K": K, "transA": tA, "transB": tB,
+                   "median_ms": med, "min_ms": min(ts), "gflops": fl / med / 1e6,
+                   "pct_roofline": 100.0 * fl / med / 1e9 / pk[math], "gbs": byt / med / 1e6,
+                   "roofline_tflops": pk[math], "l2_flushed": True, "reps": args.reps}
+            print(json.dumps(rec), flush=True)
+            lines.append(rec)
+            del ws
+        del dA, dB, dC
+        torch.cuda.empty_cache()
+    with open(args.out, "w") as f:
+        for r in lines:
+            f.write(json.dumps(r) + "\n")
+
+
+if __name__ == "__main__":
+    main()
