@@ -8,6 +8,7 @@
 #include <atomic>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -101,13 +102,38 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 static int planes_of(emm_math_t m) { return m == EMM_MATH_3XTF32 ? 2 : 1; }
 
-static size_t ws_bytes(int64_t M, int64_t N, int64_t K, emm_math_t math) {
-    if (math == EMM_MATH_FFMA || M == 0 || N == 0 || K == 0) return 0;
+// Problems below this many flops are latency-bound (a few microseconds of
+// launches dominate; the paper's "overhead of setting up buffers is
+// prohibitive" regime): one FFMA launch, which is FP32-accurate.
+// EMM_SMALL_FLOPS (environment) overrides the threshold; 0 disables it.
+static bool small_problem(int64_t M, int64_t N, int64_t K) {
+    double thr = (double)(1 << 24);
+    if (const char *e = getenv("EMM_SMALL_FLOPS")) thr = atof(e);
+    return 2.0 * (double)M * (double)N * (double)K <= thr;
+}
+
+// Workspace of the tensor-core paths:
+//   [Ap: planes*M*Kp | Bp: planes*N*Kp | split-K partials: S*M*N | counter]
+struct WsLayout {
+    size_t a_off, b_off, p_off, ctr_off, total;
+    int splits;
+};
+
+static WsLayout ws_layout(int64_t M, int64_t N, int64_t K, emm_math_t math) {
+    WsLayout L{0, 0, 0, 0, 0, 1};
+    if (math == EMM_MATH_FFMA || M == 0 || N == 0 || K == 0 || small_problem(M, N, K)) return L;
     const int64_t Kp = tc_kpad(K);
     const size_t pl = (size_t)planes_of(math);
-    return align_up(pl * (size_t)M * (size_t)Kp * 4, 1024) + align_up(pl * (size_t)N * (size_t)Kp * 4, 1024) +
-           1024 /* wave-lockstep counter */;
+    L.splits = tc_splits(M, N, K);
+    L.a_off = 0;
+    L.b_off = align_up(pl * (size_t)M * (size_t)Kp * 4, 1024);
+    L.p_off = L.b_off + align_up(pl * (size_t)N * (size_t)Kp * 4, 1024);
+    L.ctr_off = L.p_off + (L.splits > 1 ? align_up((size_t)L.splits * M * N * 4, 1024) : 0);
+    L.total = L.ctr_off + 1024;
+    return L;
 }
+
+static size_t ws_bytes(int64_t M, int64_t N, int64_t K, emm_math_t math) { return ws_layout(M, N, K, math).total; }
 
 }  // namespace emm
 
@@ -146,31 +172,34 @@ extern "C" int emm_sgemm_ex(char transA, char transB, int64_t M, int64_t N, int6
 
     if (!ab_used) return cuda_status(launch_scale_c(M, N, beta, C, ldc, s));
 
-    if (math == EMM_MATH_FFMA)
+    if (math == EMM_MATH_FFMA || small_problem(M, N, K))
         return cuda_status(
             launch_ffma_sgemm(!is_n(transA), !is_n(transB), M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, s));
 
-    // tensor-core paths: re-buffer/split both operands, then tcgen05 GEMM
-    const size_t need = ws_bytes(M, N, K, math);
+    // tensor-core paths: re-buffer/split both operands (one launch), then the
+    // persistent tcgen05 GEMM (+ the split-K reduce for sub-wave problems)
+    const WsLayout L = ws_layout(M, N, K, math);
     void *ws = workspace;
     bool own = false;
     if (ws) {
-        if (workspace_bytes < need || (reinterpret_cast<uintptr_t>(ws) & 1023u)) return EMM_ERR_WORKSPACE;
+        if (workspace_bytes < L.total || (reinterpret_cast<uintptr_t>(ws) & 1023u)) return EMM_ERR_WORKSPACE;
     } else {
-        cudaError_t e = cudaMallocAsync(&ws, need, s);
+        cudaError_t e = cudaMallocAsync(&ws, L.total, s);
         if (e != cudaSuccess) return cuda_status(e);
         own = true;
     }
     const int64_t Kp = tc_kpad(K);
     const int planes = planes_of(math);
-    float *Ap = reinterpret_cast<float *>(ws);
-    float *Bp = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(ws) +
-                                          align_up((size_t)planes * (size_t)M * (size_t)Kp * 4, 1024));
-    cudaError_t e = launch_pack_split(A, lda, /*kcontig=*/!is_n(transA), M, K, Kp, planes, Ap, s);
-    if (e == cudaSuccess) e = launch_pack_split(B, ldb, /*kcontig=*/is_n(transB), N, K, Kp, planes, Bp, s);
-    unsigned int *ctr = reinterpret_cast<unsigned int *>(reinterpret_cast<uint8_t *>(ws) + need - 1024);
+    uint8_t *w = reinterpret_cast<uint8_t *>(ws);
+    float *Ap = reinterpret_cast<float *>(w + L.a_off);
+    float *Bp = reinterpret_cast<float *>(w + L.b_off);
+    float *Pp = reinterpret_cast<float *>(w + L.p_off);
+    unsigned int *ctr = reinterpret_cast<unsigned int *>(w + L.ctr_off);
+    cudaError_t e = launch_pack_split2(A, lda, /*kcontig=*/!is_n(transA), M, B, ldb, /*kcontig=*/is_n(transB), N, K,
+                                       Kp, planes, Ap, Bp, ctr, s);
     if (e == cudaSuccess)
-        e = launch_tc_sgemm(math == EMM_MATH_3XTF32 ? 3 : 1, Ap, Bp, M, N, Kp, alpha, beta, C, ldc, ctr, s);
+        e = launch_tc_sgemm(math == EMM_MATH_3XTF32 ? 3 : 1, Ap, Bp, M, N, Kp, alpha, beta, C, ldc, ctr, L.splits, Pp,
+                            s);
     if (own) {
         cudaError_t e2 = cudaFreeAsync(ws, s);
         if (e == cudaSuccess) e = e2;

@@ -29,12 +29,21 @@ void prof_end(cudaStream_t s, bool is_gemm, cudaEvent_t ev0);
 // kcontig: element (r, p) at X[p + r*ld]; else at X[r + p*ld].
 cudaError_t launch_pack_split(const float *X, int64_t ld, bool kcontig, int64_t R, int64_t K, int64_t Kp,
                               int planes, float *out, cudaStream_t s);
-// C <- alpha * Ap * Bp^T + beta*C on the packed operands (tcgen05, 2-CTA).
-// wave_ctr: 4 bytes of device scratch owned by this call (zeroed here,
-// stream-ordered) for the producers' wave lockstep; NULL disables it.
+// Both operands in one launch (B may be NULL); also zeroes *wave_ctr.
+cudaError_t launch_pack_split2(const float *A, int64_t lda, bool a_kcontig, int64_t M, const float *B, int64_t ldb,
+                               bool b_kcontig, int64_t N, int64_t K, int64_t Kp, int planes, float *Aout, float *Bout,
+                               unsigned int *wave_ctr, cudaStream_t s);
+// C <- alpha * Ap * Bp^T + beta*C on the packed operands (tcgen05, 2-CTA,
+// persistent).  wave_ctr: 4 bytes of device scratch owned by this call, ZERO
+// when the kernel starts (launch_pack_split2 zeroes it), for the producers'
+// wave lockstep; NULL disables it.  splits > 1: split-K with raw partials in
+// `partial` (splits x M x N floats) and a fixed-order reduce launch.
 cudaError_t launch_tc_sgemm(int terms, const float *Ap, const float *Bp, int64_t M, int64_t N, int64_t Kp,
-                            float alpha, float beta, float *C, int64_t ldc, unsigned int *wave_ctr, cudaStream_t s);
+                            float alpha, float beta, float *C, int64_t ldc, unsigned int *wave_ctr, int splits,
+                            float *partial, cudaStream_t s);
 int64_t tc_kpad(int64_t K);
+int tc_splits(int64_t M, int64_t N, int64_t K);
+int tc_num_sms();
 
 // ---- CUDA-core path (k_ffma.cu) ------------------------------------------
 cudaError_t launch_ffma_sgemm(bool tA, bool tB, int64_t M, int64_t N, int64_t K, float alpha, const float *A,

@@ -42,19 +42,34 @@ constexpr int TC_TILE_BYTES = 128 * TC_BK * 4;   // one 128 x 32 FP32 operand ti
 int64_t tc_kpad(int64_t K) { return (K + TC_BK - 1) / TC_BK * TC_BK; }
 
 // =====================================================================
-// KN4: re-buffer + split.  32x32 tiles, 256 threads.
+// KN4: re-buffer + split of BOTH operands in one launch (blockIdx.z = 0: A,
+// 1: B).  32x32 tiles, 256 threads.  Block (0,0,0) also zeroes the GEMM's
+// wave-lockstep counter (stream-ordered before the GEMM).
 // =====================================================================
-template <bool KCONTIG, int PLANES>
-__global__ void __launch_bounds__(256) pack_split_kernel(const float *__restrict__ X, int64_t ld, int64_t R,
-                                                         int64_t K, int64_t Kp, float *__restrict__ out) {
+struct PackOperand {
+    const float *X;
+    int64_t ld, R;
+    int kcontig;      // element (r, p) at X[p + r*ld] (1) or X[r + p*ld] (0)
+    float *out;       // planes x R x Kp
+};
+
+template <int PLANES>
+__global__ void __launch_bounds__(256) pack_split_kernel(PackOperand opA, PackOperand opB, int64_t K, int64_t Kp,
+                                                         unsigned int *wave_ctr) {
     __shared__ float tile[32][33];
+    const PackOperand &op = blockIdx.z == 0 ? opA : opB;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const int64_t r0 = (int64_t)blockIdx.x * 32;
     const int64_t k0 = (int64_t)blockIdx.y * 32;
+    if (wave_ctr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0) *wave_ctr = 0u;
+    if (r0 >= op.R) return;                               // block-uniform
+    const float *__restrict__ X = op.X;
+    float *__restrict__ out = op.out;
+    const int64_t R = op.R, ld = op.ld;
     const int64_t plane = R * Kp;
-    float v[4];
-    if (KCONTIG) {
+    if (op.kcontig) {
         // (r, p) at X[p + r*ld]: read and write along p.
+        float v[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const int64_t r = r0 + ty + 8 * i, p = k0 + tx;
@@ -90,22 +105,43 @@ __global__ void __launch_bounds__(256) pack_split_kernel(const float *__restrict
     }
 }
 
-cudaError_t launch_pack_split(const float *X, int64_t ld, bool kcontig, int64_t R, int64_t K, int64_t Kp,
-                              int planes, float *out, cudaStream_t s) {
-    dim3 grid((unsigned)((R + 31) / 32), (unsigned)(Kp / 32));
-    if (grid.y > 65535) return cudaErrorInvalidConfiguration;
+cudaError_t launch_pack_split2(const float *A, int64_t lda, bool a_kcontig, int64_t M, const float *B, int64_t ldb,
+                               bool b_kcontig, int64_t N, int64_t K, int64_t Kp, int planes, float *Aout, float *Bout,
+                               unsigned int *wave_ctr, cudaStream_t s) {
+    const int64_t R = M > N ? M : N;
+    const bool two = B != nullptr && N > 0;
+    dim3 grid((unsigned)((R + 31) / 32), (unsigned)(Kp / 32), two ? 2u : 1u);
+    if (grid.y > 65535 || (R + 31) / 32 > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+    PackOperand a{A, lda, M, a_kcontig ? 1 : 0, Aout};
+    PackOperand b{B, ldb, N, b_kcontig ? 1 : 0, Bout};
     cudaEvent_t ev = nullptr;
     prof_begin(s, false, &ev);
-    if (kcontig) {
-        if (planes == 2) pack_split_kernel<true, 2><<<grid, 256, 0, s>>>(X, ld, R, K, Kp, out);
-        else pack_split_kernel<true, 1><<<grid, 256, 0, s>>>(X, ld, R, K, Kp, out);
-    } else {
-        if (planes == 2) pack_split_kernel<false, 2><<<grid, 256, 0, s>>>(X, ld, R, K, Kp, out);
-        else pack_split_kernel<false, 1><<<grid, 256, 0, s>>>(X, ld, R, K, Kp, out);
-    }
+    if (planes == 2) pack_split_kernel<2><<<grid, 256, 0, s>>>(a, b, K, Kp, wave_ctr);
+    else pack_split_kernel<1><<<grid, 256, 0, s>>>(a, b, K, Kp, wave_ctr);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     prof_end(s, false, ev);
     return cudaGetLastError();
+}
+
+cudaError_t launch_pack_split(const float *X, int64_t ld, bool kcontig, int64_t R, int64_t K, int64_t Kp,
+                              int planes, float *out, cudaStream_t s) {
+    return launch_pack_split2(X, ld, kcontig, R, nullptr, 0, false, 0, K, Kp, planes, out, nullptr, nullptr, s);
+}
+
+// =====================================================================
+// KN8: split-K reduction.  C <- alpha * (P_0 + ... + P_{S-1}) + beta*C, the
+// partials summed in fixed order (deterministic).  P_s is M x N, ld = M.
+// =====================================================================
+__global__ void splitk_reduce_kernel(const float *__restrict__ P, int S, int64_t M, int64_t N, float alpha, float beta,
+                                     float *__restrict__ C, int64_t ldc) {
+    const int64_t total = M * N;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        float acc = P[e];
+        for (int sp = 1; sp < S; ++sp) acc += P[(int64_t)sp * total + e];
+        const int64_t i = e % M, j = e / M;
+        float *d = C + i + j * ldc;
+        *d = beta == 0.0f ? alpha * acc : fmaf(beta, *d, alpha * acc);
+    }
 }
 
 // =====================================================================
@@ -137,7 +173,8 @@ template <int TERMS>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
     tc_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                     int Kp, float alpha, float beta, float *__restrict__ C, int64_t ldc, int tiles_m, int tiles_n,
-                    int group_m, int kc_stages, unsigned int *__restrict__ wave_ctr) {
+                    int group_m, int kc_stages, unsigned int *__restrict__ wave_ctr, int splits,
+                    float *__restrict__ partial) {
     using Cfg = TcCfg<TERMS>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -168,7 +205,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
         n0 = tn * TC_BN;
     };
     const int nkb = Kp / TC_BK;
-    const int nchunks = (nkb + kc_stages - 1) / kc_stages;
+    // Work units: (split, tile), split-major, so that one wave of units shares
+    // operand K-slices; unit u covers K stages [kb0, kb1) of its tile.
+    const int nkb_s = (nkb + splits - 1) / splits;
+    const int total_units = total_tiles * splits;
+    auto unit = [&](int u, int &m0, int &n0, int &kb0, int &kb1, int &sp) {
+        sp = u / total_tiles;
+        tile_origin(u - sp * total_tiles, m0, n0);
+        kb0 = sp * nkb_s;
+        kb1 = min(nkb, kb0 + nkb_s);
+    };
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < Cfg::STAGES; ++s) {
@@ -199,7 +245,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
             const uint64_t pol = policy_evict_normal();
             int it = 0;
             unsigned int done_target = 0;   // CTAs that finished issuing waves 0..w-1
-            for (int t = cid, w = 0; t < total_tiles; t += nclus, ++w) {
+            for (int t = cid, w = 0; t < total_units; t += nclus, ++w) {
                 if (w > 0 && wave_ctr) {
                     // Wave lockstep: start loading wave w only when every CTA
                     // has issued all loads of wave w-1, so the ~17 operand
@@ -215,14 +261,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
                     }
                 }
                 {
-                    const int active = min(nclus, total_tiles - w * nclus);
+                    const int active = min(nclus, total_units - w * nclus);
                     done_target += 2u * (unsigned)active;
                 }
-                int m0, n0;
-                tile_origin(t, m0, n0);
+                int m0, n0, kb0, kb1, sp;
+                unit(t, m0, n0, kb0, kb1, sp);
                 const int arow = m0 + (int)rank * TC_BM;
                 const int brow = n0 + (int)rank * TC_BM;
-                for (int kb = 0; kb < nkb; ++kb, ++it) {
+                for (int kb = kb0; kb < kb1; ++kb, ++it) {
                     const int s = it % Cfg::STAGES;
                     const uint32_t ph = (uint32_t)(it / Cfg::STAGES) & 1u;
                     mbar_wait(&empty[s], ph ^ 1u);
@@ -243,10 +289,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
         if (rank == 0 && lane == 0) {
             constexpr uint32_t idesc = idesc_tf32<2 * TC_BM, TC_BN>();
             int it = 0, ch = 0;   // global stage / chunk counters (continue across tiles)
-            for (int t = cid; t < total_tiles; t += nclus) {
-                for (int kb = 0; kb < nkb; ++kb, ++it) {
-                    const bool first = (kb % kc_stages) == 0;
-                    const bool last = (kb % kc_stages) == kc_stages - 1 || kb == nkb - 1;
+            for (int t = cid; t < total_units; t += nclus) {
+                int m0, n0, kb0, kb1, sp;
+                unit(t, m0, n0, kb0, kb1, sp);
+                for (int kb = kb0; kb < kb1; ++kb, ++it) {
+                    const bool first = ((kb - kb0) % kc_stages) == 0;
+                    const bool last = ((kb - kb0) % kc_stages) == kc_stages - 1 || kb == kb1 - 1;
                     const int b = ch & 1;
                     const uint32_t dt = tmem_base + (uint32_t)(b * TC_BN);
                     if (first) {   // the epilogue has drained this buffer (both CTAs)
@@ -291,9 +339,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
         uint32_t leader_empty0;
         asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(leader_empty0) : "r"(smem_u32(&acc_empty[0])));
         int ch = 0;
-        for (int t = cid; t < total_tiles; t += nclus) {
-            int m0, n0;
-            tile_origin(t, m0, n0);
+        for (int t = cid; t < total_units; t += nclus) {
+            int m0, n0, kb0, kb1, sp;
+            unit(t, m0, n0, kb0, kb1, sp);
+            const int nchunks = (kb1 - kb0 + kc_stages - 1) / kc_stages;
             const int row = m0 + (int)rank * TC_BM + 32 * q + lane;
             float acc[128];
 #pragma unroll
@@ -318,7 +367,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
                     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(eb) : "memory");
                 }
             }
-            if (row < M) {
+            if (row < M && partial) {
+                // split-K: raw FP32 partial of split `sp` (alpha/beta in KN8)
+                const int col0 = n0 + h * 128;
+                float *pp = partial + (int64_t)sp * M * N + (int64_t)row + (int64_t)col0 * M;
+                const int jmax = min(128, N - col0);
+#pragma unroll
+                for (int j = 0; j < 128; ++j)
+                    if (j < jmax) pp[(int64_t)j * M] = acc[j];
+            } else if (row < M) {
                 const int col0 = n0 + h * 128;
                 float *cp = C + (int64_t)row + (int64_t)col0 * ldc;
                 const int jmax = min(128, N - col0);
@@ -375,9 +432,39 @@ static bool make_tmap(CUtensorMap *tm, const float *base, int64_t R, int64_t Kp,
     return r == CUDA_SUCCESS;
 }
 
+int tc_num_sms() {
+    static int num_sms = 0;
+    if (!num_sms) {
+        int dev = 0, n = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess &&
+            cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && n > 0)
+            num_sms = n;
+        else
+            return 148;   // host-only query without a device: B200
+    }
+    return num_sms;
+}
+
+// Split-K factor for sub-wave problems: enough (tile,
+// split) units to fill the CTA pairs, each split >= 4 K-stages (128 of K).
+int tc_splits(int64_t M, int64_t N, int64_t K) {
+    const int64_t tiles = ((M + 2 * TC_BM - 1) / (2 * TC_BM)) * ((N + TC_BN - 1) / TC_BN);
+    const int64_t nkb = tc_kpad(K) / TC_BK;
+    const int64_t clusters = tc_num_sms() / 2;
+    if (tiles <= 0 || tiles * 2 > clusters) return 1;
+    int64_t s = clusters / tiles;
+    if (s > nkb / 4) s = nkb / 4;
+    if (s > 16) s = 16;
+    if (s < 1) s = 1;
+    // every split must own at least one stage
+    while (s > 1 && ((nkb + s - 1) / s) * (s - 1) >= nkb) --s;
+    return (int)s;
+}
+
 template <int TERMS>
 static cudaError_t launch_tc_t(const float *Ap, const float *Bp, int64_t M, int64_t N, int64_t Kp, float alpha,
-                               float beta, float *C, int64_t ldc, unsigned int *wave_ctr, cudaStream_t s) {
+                               float beta, float *C, int64_t ldc, unsigned int *wave_ctr, int splits, float *partial,
+                               cudaStream_t s) {
     using Cfg = TcCfg<TERMS>;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
@@ -392,36 +479,38 @@ static cudaError_t launch_tc_t(const float *Ap, const float *Bp, int64_t M, int6
     const int tiles_m = (int)((M + 2 * TC_BM - 1) / (2 * TC_BM));
     const int tiles_n = (int)((N + TC_BN - 1) / TC_BN);
     const int group_m = 8;
-    static int num_sms = 0;
-    if (!num_sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-    }
-    const int64_t tiles = (int64_t)tiles_m * tiles_n;
-    if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-    const int64_t clusters = tiles < num_sms / 2 ? tiles : num_sms / 2;   // persistent: one pair per 2 SMs
+    const int64_t units = (int64_t)tiles_m * tiles_n * splits;
+    if (units > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+    const int64_t pairs = tc_num_sms() / 2;
+    const int64_t clusters = units < pairs ? units : pairs;   // persistent: one pair per 2 SMs
     const int64_t blocks = 2 * clusters;
     cudaEvent_t ev = nullptr;
     prof_begin(s, true, &ev);
     // promotion chunk: 256 of K for 3xTF32 (8 stages), none for 1xTF32
     const int kc_stages = TERMS == 3 ? 256 / TC_BK : 0x3fffffff;
     tc_sgemm_kernel<TERMS><<<(unsigned)blocks, TC_THREADS_P, Cfg::SMEM_BYTES, s>>>(
-        ta, tb, (int)M, (int)N, (int)Kp, alpha, beta, C, ldc, tiles_m, tiles_n, group_m, kc_stages, wave_ctr);
+        ta, tb, (int)M, (int)N, (int)Kp, alpha, beta, C, ldc, tiles_m, tiles_n, group_m, kc_stages, wave_ctr, splits,
+        splits > 1 ? partial : nullptr);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     prof_end(s, true, ev);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess || splits <= 1) return e;
+    const int64_t want = (M * N + 255) / 256;
+    const int blocks_r = (int)(want < (int64_t)tc_num_sms() * 8 ? want : (int64_t)tc_num_sms() * 8);
+    prof_begin(s, false, &ev);
+    splitk_reduce_kernel<<<blocks_r > 0 ? blocks_r : 1, 256, 0, s>>>(partial, splits, M, N, alpha, beta, C, ldc);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    prof_end(s, false, ev);
     return cudaGetLastError();
 }
 
 cudaError_t launch_tc_sgemm(int terms, const float *Ap, const float *Bp, int64_t M, int64_t N, int64_t Kp,
-                            float alpha, float beta, float *C, int64_t ldc, unsigned int *wave_ctr, cudaStream_t s) {
+                            float alpha, float beta, float *C, int64_t ldc, unsigned int *wave_ctr, int splits,
+                            float *partial, cudaStream_t s) {
     if (M > 0x7fffffffLL || N > 0x7fffffffLL || Kp > 0x7fffffffLL) return cudaErrorInvalidValue;
-    if (wave_ctr) {
-        cudaError_t e = cudaMemsetAsync(wave_ctr, 0, sizeof(unsigned int), s);
-        if (e != cudaSuccess) return e;
-    }
-    return terms == 3 ? launch_tc_t<3>(Ap, Bp, M, N, Kp, alpha, beta, C, ldc, wave_ctr, s)
-                      : launch_tc_t<1>(Ap, Bp, M, N, Kp, alpha, beta, C, ldc, wave_ctr, s);
+    if (splits < 1 || (splits > 1 && !partial)) return cudaErrorInvalidValue;
+    return terms == 3 ? launch_tc_t<3>(Ap, Bp, M, N, Kp, alpha, beta, C, ldc, wave_ctr, splits, partial, s)
+                      : launch_tc_t<1>(Ap, Bp, M, N, Kp, alpha, beta, C, ldc, wave_ctr, splits, partial, s);
 }
 
 }  // namespace emm

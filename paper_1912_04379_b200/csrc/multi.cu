@@ -186,9 +186,10 @@ extern "C" int emm_sgemm_multi(void *comm, char transA, char transB, int64_t M, 
         if (!tc)   // FFMA, or alpha == 0 / K == 0 (C <- beta*C)
             return emm_sgemm_ex(transA, transB, rows, nc, K, alpha, A_local, lda, bp, ldb, beta, cp, ldc, s, math,
                                 nullptr, 0);
-        cudaError_t e = launch_pack_split(bp, ldb, /*kcontig=*/bN, nc, K, Kp, planes, Bp, s);
+        cudaError_t e = launch_pack_split2(bp, ldb, /*kcontig=*/bN, nc, nullptr, 0, false, 0, K, Kp, planes, Bp,
+                                           nullptr, ctr, s);
         if (e == cudaSuccess)
-            e = launch_tc_sgemm(planes == 2 ? 3 : 1, Ap, Bp, rows, nc, Kp, alpha, beta, cp, ldc, ctr, s);
+            e = launch_tc_sgemm(planes == 2 ? 3 : 1, Ap, Bp, rows, nc, Kp, alpha, beta, cp, ldc, ctr, 1, nullptr, s);
         return cuda_st(e);
     };
 

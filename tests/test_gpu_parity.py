@@ -13,6 +13,8 @@ Bars (BASELINE.json north_star):
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -21,6 +23,11 @@ import datagen
 import oracle
 
 pytestmark = pytest.mark.gpu
+
+# The library sends latency-bound problems (2MNK <= 2^24) to the FFMA kernel;
+# these tests force every requested path at every size (EMM_SMALL_FLOPS=0),
+# and test_small_problem_default_path covers the default dispatch.
+os.environ["EMM_SMALL_FLOPS"] = "0"
 
 TOL = {"3xtf32": 1e-5, "ffma": 1e-5, "1xtf32": 5e-3}
 MATHS = ["3xtf32", "ffma", "1xtf32"]
@@ -327,6 +334,33 @@ def test_same_sign_accumulation(emm, math, K):
     Cg = case.run(emm, math)
     r = assert_close(case, Cg, R, S, T, 1e-5)
     print(f"same-sign K={K} {math}: max err/tol = {r:.3g}")
+
+
+@pytest.mark.parametrize("shape", [(64, 64, 64), (100, 100, 100), (7, 300, 5)])
+def test_small_problem_default_path(emm, monkeypatch, shape):
+    monkeypatch.delenv("EMM_SMALL_FLOPS")
+    M, N, K = shape
+    case = Case("N", "N", M, N, K, 1.0, 0.0)
+    R, S, T, _ = case.oracle()
+    for math in MATHS:
+        Cg = case.run(emm, math)
+        case.check_untouched(Cg)
+        assert_close(case, Cg, R, S, T, 1e-5)   # FFMA kernel: FP32-accurate for every mode
+
+
+@pytest.mark.parametrize("math", ["3xtf32", "1xtf32"])
+@pytest.mark.parametrize("shape", [(1531, 997, 2049), (1024, 1024, 1024), (700, 700, 700), (257, 300, 4000)])
+def test_split_k_deterministic_and_close(emm, math, shape):
+    """Sub-wave shapes take split-K (partials + fixed-order reduce): results
+    must be within tolerance and bitwise reproducible."""
+    M, N, K = shape
+    case = cached_case("N", "N", M, N, K, 0.5, -1.0, pad=(1, 2, 3))
+    R, S, T, _ = case.oracle()
+    c1 = case.run(emm, math)
+    c2 = case.run(emm, math)
+    assert torch.equal(c1, c2)
+    case.check_untouched(c1)
+    assert_close(case, c1, R, S, T, TOL[math])
 
 
 def test_torch_binding_colmajor(emm):
