@@ -13,8 +13,6 @@ Bars (BASELINE.json north_star):
 """
 from __future__ import annotations
 
-import os
-
 import numpy as np
 import pytest
 import torch
@@ -24,10 +22,14 @@ import oracle
 
 pytestmark = pytest.mark.gpu
 
-# The library sends latency-bound problems (2MNK <= 2^24) to the FFMA kernel;
-# these tests force every requested path at every size (EMM_SMALL_FLOPS=0),
-# and test_small_problem_default_path covers the default dispatch.
-os.environ["EMM_SMALL_FLOPS"] = "0"
+
+
+@pytest.fixture(autouse=True)
+def force_requested_path(monkeypatch):
+    """The library sends latency-bound problems (2MNK <= 2^24) to the FFMA
+    kernel; these tests force every requested path at every size
+    (EMM_SMALL_FLOPS=0); test_small_problem_default_path covers the default."""
+    monkeypatch.setenv("EMM_SMALL_FLOPS", "0")
 
 TOL = {"3xtf32": 1e-5, "ffma": 1e-5, "1xtf32": 5e-3}
 MATHS = ["3xtf32", "ffma", "1xtf32"]
