@@ -25,6 +25,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "emm_internal.h"
@@ -51,6 +52,7 @@ struct PackOperand {
     int64_t ld, R;
     int kcontig;      // element (r, p) at X[p + r*ld] (1) or X[r + p*ld] (0)
     float *out;       // planes x R x Kp
+    int raw_big;      // test hook (EMM_DEBUG_RAW_BIG): big = x unrounded
 };
 
 template <int PLANES>
@@ -79,7 +81,7 @@ __global__ void __launch_bounds__(256) pack_split_kernel(PackOperand opA, PackOp
         for (int i = 0; i < 4; ++i) {
             const int64_t r = r0 + ty + 8 * i, p = k0 + tx;
             if (r < R) {
-                const uint32_t big = cvt_tf32_rn(v[i]);
+                const uint32_t big = op.raw_big ? __float_as_uint(v[i]) : cvt_tf32_rn(v[i]);
                 out[r * Kp + p] = __uint_as_float(big);
                 if (PLANES == 2) out[plane + r * Kp + p] = __uint_as_float(cvt_tf32_rn(v[i] - __uint_as_float(big)));
             }
@@ -97,7 +99,7 @@ __global__ void __launch_bounds__(256) pack_split_kernel(PackOperand opA, PackOp
             const int64_t r = r0 + ty + 8 * i, p = k0 + tx;
             if (r < R) {
                 const float x = tile[tx][ty + 8 * i];
-                const uint32_t big = cvt_tf32_rn(x);
+                const uint32_t big = op.raw_big ? __float_as_uint(x) : cvt_tf32_rn(x);
                 out[r * Kp + p] = __uint_as_float(big);
                 if (PLANES == 2) out[plane + r * Kp + p] = __uint_as_float(cvt_tf32_rn(x - __uint_as_float(big)));
             }
@@ -112,8 +114,14 @@ cudaError_t launch_pack_split2(const float *A, int64_t lda, bool a_kcontig, int6
     const bool two = B != nullptr && N > 0;
     dim3 grid((unsigned)((R + 31) / 32), (unsigned)(Kp / 32), two ? 2u : 1u);
     if (grid.y > 65535 || (R + 31) / 32 > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-    PackOperand a{A, lda, M, a_kcontig ? 1 : 0, Aout};
-    PackOperand b{B, ldb, N, b_kcontig ? 1 : 0, Bout};
+    // EMM_DEBUG_RAW_BIG=1 (tests only): hand the tensor core raw FP32 bits as
+    // the "big" part, to probe its TF32 input conversion (R7).
+    static const int raw = [] {
+        const char *e = getenv("EMM_DEBUG_RAW_BIG");
+        return e && e[0] == '1' ? 1 : 0;
+    }();
+    PackOperand a{A, lda, M, a_kcontig ? 1 : 0, Aout, raw};
+    PackOperand b{B, ldb, N, b_kcontig ? 1 : 0, Bout, raw};
     cudaEvent_t ev = nullptr;
     prof_begin(s, false, &ev);
     if (planes == 2) pack_split_kernel<2><<<grid, 256, 0, s>>>(a, b, K, Kp, wave_ctr);
