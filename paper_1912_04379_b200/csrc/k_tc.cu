@@ -392,12 +392,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
                     for (int j = 0; j < 128; ++j)
                         if (j < jmax) cp[(int64_t)j * ldc] = alpha * acc[j];
                 } else {
+                    // beta != 0: issue 16 independent C loads before the 16
+                    // stores (a store could alias a later load through ldc,
+                    // so the compiler would otherwise serialise them).
 #pragma unroll
-                    for (int j = 0; j < 128; ++j)
-                        if (j < jmax) {
-                            float *d = cp + (int64_t)j * ldc;
-                            *d = fmaf(beta, *d, alpha * acc[j]);
-                        }
+                    for (int g = 0; g < 8; ++g) {
+                        float cin[16];
+                        const float *lp = cp + (int64_t)(16 * g) * ldc;
+#pragma unroll
+                        for (int j = 0; j < 16; ++j, lp += ldc) cin[j] = (16 * g + j < jmax) ? __ldcs(lp) : 0.0f;
+                        float *sp2 = cp + (int64_t)(16 * g) * ldc;
+#pragma unroll
+                        for (int j = 0; j < 16; ++j, sp2 += ldc)
+                            if (16 * g + j < jmax) __stcs(sp2, fmaf(beta, cin[j], alpha * acc[16 * g + j]));
+                    }
                 }
             }
         }
