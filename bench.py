@@ -51,7 +51,7 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="emm", choices=["emm", "reference"])
-    p.add_argument("--math", default="3xtf32", choices=["3xtf32", "ffma", "1xtf32"])
+    p.add_argument("--math", default="3xtf32", choices=["3xtf32", "ffma", "1xtf32", "tf32bf16"])
     p.add_argument("--size", type=int, default=32768)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
@@ -286,6 +286,9 @@ def main():
     tf32_burst = bf16 * TF32_PER_BF16
     if args.math == "3xtf32":
         peak, peak_b, pname = tf32_sus / 3.0, tf32_burst / 3.0, "3xTF32-effective (TF32/3)"
+    elif args.math == "tf32bf16":
+        # one TF32 MMA (K8) + one BF16 MMA (K16) per 8 of K: 2 TF32-MMA times
+        peak, peak_b, pname = tf32_sus / 2.0, tf32_burst / 2.0, "TF32+BF16-effective (TF32/2)"
     elif args.math == "1xtf32":
         peak, peak_b, pname = tf32_sus, tf32_burst, "TF32"
     else:

@@ -28,7 +28,7 @@ def peaks():
     with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
         mp = json.load(f)
     tf32 = mp["bf16_tflops"] * 1.1 / 2.25
-    return {"3xtf32": tf32 / 3, "1xtf32": tf32, "ffma": 148 * 256 * 1.965e9 / 1e12}
+    return {"3xtf32": tf32 / 3, "tf32bf16": tf32 / 2, "1xtf32": tf32, "ffma": 148 * 256 * 1.965e9 / 1e12}
 
 
 def configs():
@@ -47,7 +47,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_sweep.jsonl"))
-    ap.add_argument("--maths", default="3xtf32,1xtf32,ffma")
+    ap.add_argument("--maths", default="3xtf32,tf32bf16,1xtf32,ffma")
     ap.add_argument("--only", default="")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)

@@ -67,11 +67,17 @@ extern "C" {
  *     split x = big + small (big = rn_tf32(x), small = rn_tf32(x - big)) and
  *     C accumulates small*big + big*small + big*big in FP32 in TMEM.
  *   EMM_MATH_FFMA:   FP32 FFMA on CUDA cores (register-blocked tiles).
- *   EMM_MATH_1XTF32: one TF32 product per step (exposed lower precision). */
+ *   EMM_MATH_1XTF32: one TF32 product per step (exposed lower precision).
+ *   EMM_MATH_TF32_BF16: FP32-accurate tensor-core split with 2/3 of the
+ *     3xTF32 tensor work: big*big as one TF32 MMA per K8 and both cross terms
+ *     a_big*b_small + a_small*b_big as ONE K16 BF16 MMA on [a_big|a_small] x
+ *     [b_small;b_big] (per-product error <= ~2^-18 |ab|, inside the FP32-
+ *     accurate bound 1e-5*sum|ab|). */
 typedef enum {
     EMM_MATH_3XTF32 = 0,
     EMM_MATH_FFMA = 1,
-    EMM_MATH_1XTF32 = 2
+    EMM_MATH_1XTF32 = 2,
+    EMM_MATH_TF32_BF16 = 3
 } emm_math_t;
 
 /* C <- alpha*op(A)*op(B) + beta*C with the default FP32-accurate path

@@ -100,7 +100,12 @@ static int cuda_status(cudaError_t e) { return e == cudaSuccess ? 0 : EMM_ERR_CU
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
-static int planes_of(emm_math_t m) { return m == EMM_MATH_3XTF32 ? 2 : 1; }
+static int planes_of(emm_math_t m) { return m == EMM_MATH_3XTF32 || m == EMM_MATH_TF32_BF16 ? 2 : 1; }
+static int pack_mode(emm_math_t m) { return m == EMM_MATH_3XTF32 ? 1 : m == EMM_MATH_TF32_BF16 ? 2 : 0; }
+static int terms_of(emm_math_t m) { return m == EMM_MATH_3XTF32 ? 3 : m == EMM_MATH_TF32_BF16 ? 2 : 1; }
+static bool math_ok(emm_math_t m) {
+    return m == EMM_MATH_3XTF32 || m == EMM_MATH_FFMA || m == EMM_MATH_1XTF32 || m == EMM_MATH_TF32_BF16;
+}
 
 // Problems below this many flops are latency-bound (a few microseconds of
 // launches dominate; the paper's "overhead of setting up buffers is
@@ -152,7 +157,7 @@ extern "C" int emm_sgemm_ex(char transA, char transB, int64_t M, int64_t N, int6
                             emm_math_t math, void *workspace, size_t workspace_bytes) {
     int st = check_args(transA, transB, M, N, K, lda, ldb, ldc);
     if (st) return st;
-    if (math != EMM_MATH_3XTF32 && math != EMM_MATH_FFMA && math != EMM_MATH_1XTF32) return EMM_ERR_MATH;
+    if (!math_ok(math)) return EMM_ERR_MATH;
     // quick return (BLAS): nothing to do
     if (M == 0 || N == 0) return 0;
     const bool ab_used = !(alpha == 0.0f || K == 0);
@@ -189,17 +194,15 @@ extern "C" int emm_sgemm_ex(char transA, char transB, int64_t M, int64_t N, int6
         own = true;
     }
     const int64_t Kp = tc_kpad(K);
-    const int planes = planes_of(math);
     uint8_t *w = reinterpret_cast<uint8_t *>(ws);
     float *Ap = reinterpret_cast<float *>(w + L.a_off);
     float *Bp = reinterpret_cast<float *>(w + L.b_off);
     float *Pp = reinterpret_cast<float *>(w + L.p_off);
     unsigned int *ctr = reinterpret_cast<unsigned int *>(w + L.ctr_off);
     cudaError_t e = launch_pack_split2(A, lda, /*kcontig=*/!is_n(transA), M, B, ldb, /*kcontig=*/is_n(transB), N, K,
-                                       Kp, planes, Ap, Bp, ctr, s);
+                                       Kp, pack_mode(math), Ap, Bp, ctr, s);
     if (e == cudaSuccess)
-        e = launch_tc_sgemm(math == EMM_MATH_3XTF32 ? 3 : 1, Ap, Bp, M, N, Kp, alpha, beta, C, ldc, ctr, L.splits, Pp,
-                            s);
+        e = launch_tc_sgemm(terms_of(math), Ap, Bp, M, N, Kp, alpha, beta, C, ldc, ctr, L.splits, Pp, s);
     if (own) {
         cudaError_t e2 = cudaFreeAsync(ws, s);
         if (e == cudaSuccess) e = e2;
@@ -241,7 +244,7 @@ extern "C" int emm_sgemm_host(char transA, char transB, int64_t M, int64_t N, in
                               emm_math_t math) {
     int st = check_args(transA, transB, M, N, K, lda, ldb, ldc);
     if (st) return st;
-    if (math != EMM_MATH_3XTF32 && math != EMM_MATH_FFMA && math != EMM_MATH_1XTF32) return EMM_ERR_MATH;
+    if (!math_ok(math)) return EMM_ERR_MATH;
     if (M == 0 || N == 0) return 0;
     const bool ab_used = !(alpha == 0.0f || K == 0);
     if (!ab_used && beta == 1.0f) return 0;

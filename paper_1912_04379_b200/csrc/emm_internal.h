@@ -27,12 +27,15 @@ void prof_end(cudaStream_t s, bool is_gemm, cudaEvent_t ev0);
 // R x Kp floats (Kp = round_up(K, 32); zero-filled tail); plane 0 = big =
 // rn_tf32(x), plane 1 (if planes == 2) = small = rn_tf32(x - big).
 // kcontig: element (r, p) at X[p + r*ld]; else at X[r + p*ld].
+// mode: 0 = big plane only (1xTF32), 1 = + tf32 small plane (3xTF32),
+// 2 = + BF16 cross plane (TF32+BF16); see pack_store in k_tc.cu.
 cudaError_t launch_pack_split(const float *X, int64_t ld, bool kcontig, int64_t R, int64_t K, int64_t Kp,
-                              int planes, float *out, cudaStream_t s);
+                              int mode, float *out, cudaStream_t s);
 // Both operands in one launch (B may be NULL); also zeroes *wave_ctr.
+// first_is_b: the first operand plays the B role (cross-plane half order).
 cudaError_t launch_pack_split2(const float *A, int64_t lda, bool a_kcontig, int64_t M, const float *B, int64_t ldb,
-                               bool b_kcontig, int64_t N, int64_t K, int64_t Kp, int planes, float *Aout, float *Bout,
-                               unsigned int *wave_ctr, cudaStream_t s);
+                               bool b_kcontig, int64_t N, int64_t K, int64_t Kp, int mode, float *Aout, float *Bout,
+                               unsigned int *wave_ctr, cudaStream_t s, bool first_is_b = false);
 // C <- alpha * Ap * Bp^T + beta*C on the packed operands (tcgen05, 2-CTA,
 // persistent).  wave_ctr: 4 bytes of device scratch owned by this call, ZERO
 // when the kernel starts (launch_pack_split2 zeroes it), for the producers'

@@ -20,6 +20,7 @@
 //    of the dot product → one epilogue per tile.
 //  * N-edge special cases → predicated epilogue stores.
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
@@ -53,9 +54,33 @@ struct PackOperand {
     int kcontig;      // element (r, p) at X[p + r*ld] (1) or X[r + p*ld] (0)
     float *out;       // planes x R x Kp
     int raw_big;      // test hook (EMM_DEBUG_RAW_BIG): big = x unrounded
+    int cross_swap;   // MODE 2: per K8 group [bf16(lo) | bf16(hi)] instead of [hi | lo]
 };
 
-template <int PLANES>
+// MODE 0: plane 0 = big = rn_tf32(x).
+// MODE 1: + plane 1 = small = rn_tf32(x - big)                    (3xTF32)
+// MODE 2: + plane 1 = BF16 cross operand: for every group of 8 along K,
+//         16 bf16 = [bf16(big) x8 | bf16(x - big) x8] (A side) or the two
+//         halves swapped (B side), so that one K=16 BF16 MMA computes
+//         a_big*b_small + a_small*b_big                           (TF32+BF16)
+template <int MODE>
+__device__ __forceinline__ void pack_store(const PackOperand &op, float *__restrict__ out, int64_t plane, int64_t r,
+                                           int64_t p, int64_t Kp, float x) {
+    const uint32_t big = op.raw_big ? __float_as_uint(x) : cvt_tf32_rn(x);
+    out[r * Kp + p] = __uint_as_float(big);
+    const float lo = x - __uint_as_float(big);           // exact
+    if (MODE == 1) out[plane + r * Kp + p] = __uint_as_float(cvt_tf32_rn(lo));
+    if (MODE == 2) {
+        uint16_t *row = reinterpret_cast<uint16_t *>(out + plane + r * Kp);
+        const int64_t g = p >> 3, j = p & 7;
+        const uint16_t hb = __bfloat16_as_ushort(__float2bfloat16_rn(__uint_as_float(big)));
+        const uint16_t lb = __bfloat16_as_ushort(__float2bfloat16_rn(lo));
+        row[g * 16 + j] = op.cross_swap ? lb : hb;
+        row[g * 16 + 8 + j] = op.cross_swap ? hb : lb;
+    }
+}
+
+template <int MODE>
 __global__ void __launch_bounds__(256) pack_split_kernel(PackOperand opA, PackOperand opB, int64_t K, int64_t Kp,
                                                          unsigned int *wave_ctr) {
     __shared__ float tile[32][33];
@@ -80,11 +105,7 @@ __global__ void __launch_bounds__(256) pack_split_kernel(PackOperand opA, PackOp
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const int64_t r = r0 + ty + 8 * i, p = k0 + tx;
-            if (r < R) {
-                const uint32_t big = op.raw_big ? __float_as_uint(v[i]) : cvt_tf32_rn(v[i]);
-                out[r * Kp + p] = __uint_as_float(big);
-                if (PLANES == 2) out[plane + r * Kp + p] = __uint_as_float(cvt_tf32_rn(v[i] - __uint_as_float(big)));
-            }
+            if (r < R) pack_store<MODE>(op, out, plane, r, p, Kp, v[i]);
         }
     } else {
         // (r, p) at X[r + p*ld]: read along r, transpose through smem.
@@ -97,19 +118,14 @@ __global__ void __launch_bounds__(256) pack_split_kernel(PackOperand opA, PackOp
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const int64_t r = r0 + ty + 8 * i, p = k0 + tx;
-            if (r < R) {
-                const float x = tile[tx][ty + 8 * i];
-                const uint32_t big = op.raw_big ? __float_as_uint(x) : cvt_tf32_rn(x);
-                out[r * Kp + p] = __uint_as_float(big);
-                if (PLANES == 2) out[plane + r * Kp + p] = __uint_as_float(cvt_tf32_rn(x - __uint_as_float(big)));
-            }
+            if (r < R) pack_store<MODE>(op, out, plane, r, p, Kp, tile[tx][ty + 8 * i]);
         }
     }
 }
 
 cudaError_t launch_pack_split2(const float *A, int64_t lda, bool a_kcontig, int64_t M, const float *B, int64_t ldb,
-                               bool b_kcontig, int64_t N, int64_t K, int64_t Kp, int planes, float *Aout, float *Bout,
-                               unsigned int *wave_ctr, cudaStream_t s) {
+                               bool b_kcontig, int64_t N, int64_t K, int64_t Kp, int mode, float *Aout, float *Bout,
+                               unsigned int *wave_ctr, cudaStream_t s, bool first_is_b) {
     const int64_t R = M > N ? M : N;
     const bool two = B != nullptr && N > 0;
     dim3 grid((unsigned)((R + 31) / 32), (unsigned)(Kp / 32), two ? 2u : 1u);
@@ -120,20 +136,21 @@ cudaError_t launch_pack_split2(const float *A, int64_t lda, bool a_kcontig, int6
         const char *e = getenv("EMM_DEBUG_RAW_BIG");
         return e && e[0] == '1' ? 1 : 0;
     }();
-    PackOperand a{A, lda, M, a_kcontig ? 1 : 0, Aout, raw};
-    PackOperand b{B, ldb, N, b_kcontig ? 1 : 0, Bout, raw};
+    PackOperand a{A, lda, M, a_kcontig ? 1 : 0, Aout, raw, first_is_b ? 1 : 0};
+    PackOperand b{B, ldb, N, b_kcontig ? 1 : 0, Bout, raw, 1};
     cudaEvent_t ev = nullptr;
     prof_begin(s, false, &ev);
-    if (planes == 2) pack_split_kernel<2><<<grid, 256, 0, s>>>(a, b, K, Kp, wave_ctr);
-    else pack_split_kernel<1><<<grid, 256, 0, s>>>(a, b, K, Kp, wave_ctr);
+    if (mode == 2) pack_split_kernel<2><<<grid, 256, 0, s>>>(a, b, K, Kp, wave_ctr);
+    else if (mode == 1) pack_split_kernel<1><<<grid, 256, 0, s>>>(a, b, K, Kp, wave_ctr);
+    else pack_split_kernel<0><<<grid, 256, 0, s>>>(a, b, K, Kp, wave_ctr);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     prof_end(s, false, ev);
     return cudaGetLastError();
 }
 
 cudaError_t launch_pack_split(const float *X, int64_t ld, bool kcontig, int64_t R, int64_t K, int64_t Kp,
-                              int planes, float *out, cudaStream_t s) {
-    return launch_pack_split2(X, ld, kcontig, R, nullptr, 0, false, 0, K, Kp, planes, out, nullptr, nullptr, s);
+                              int mode, float *out, cudaStream_t s) {
+    return launch_pack_split2(X, ld, kcontig, R, nullptr, 0, false, 0, K, Kp, mode, out, nullptr, nullptr, s, false);
 }
 
 // =====================================================================
@@ -168,12 +185,15 @@ constexpr int TC_EPI_WARPS = 8;                               // 2 per TMEM lane
 constexpr int TC_THREADS_P = 64 + 32 * TC_EPI_WARPS;          // 320
 constexpr int TC_TMEM_COLS_P = 512;                           // 2 accumulator buffers
 
+// TERMS: 3 = 3xTF32 (small*big + big*small + big*big, three kind::tf32 MMAs
+// per K8), 2 = TF32+BF16 (big*big kind::tf32 + both cross terms in one K16
+// kind::f16 BF16 MMA), 1 = 1xTF32.
 template <int TERMS>
 struct TcCfg {
-    static constexpr int PLANES = TERMS == 3 ? 2 : 1;
+    static constexpr int PLANES = TERMS >= 2 ? 2 : 1;
     static constexpr int TILES_PER_STAGE = 2 * PLANES;              // A planes + B planes
     static constexpr int STAGE_BYTES = TILES_PER_STAGE * TC_TILE_BYTES;
-    static constexpr int STAGES = TERMS == 3 ? 3 : 6;
+    static constexpr int STAGES = TERMS >= 2 ? 3 : 6;
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
 
@@ -327,6 +347,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
                             // small terms first (they are the smaller magnitudes)
                             mma_tf32_2sm(dt, a_sml + koff, b_big + koff, idesc, acc0);
                             mma_tf32_2sm(dt, a_big + koff, b_sml + koff, idesc, 1u);
+                            mma_tf32_2sm(dt, a_big + koff, b_big + koff, idesc, 1u);
+                        } else if (TERMS == 2) {
+                            // cross terms (K=16 bf16 = the same 32 bytes of the row)
+                            constexpr uint32_t idesc_x = idesc_bf16<2 * TC_BM, TC_BN>();
+                            const uint64_t a_x = desc_kmajor_sw128(st + TC_TILE_BYTES);
+                            const uint64_t b_x = desc_kmajor_sw128(st + 3 * TC_TILE_BYTES);
+                            mma_f16_2sm(dt, a_x + koff, b_x + koff, idesc_x, acc0);
                             mma_tf32_2sm(dt, a_big + koff, b_big + koff, idesc, 1u);
                         } else {
                             mma_tf32_2sm(dt, a_big + koff, b_big + koff, idesc, acc0);
@@ -503,7 +530,7 @@ static cudaError_t launch_tc_t(const float *Ap, const float *Bp, int64_t M, int6
     cudaEvent_t ev = nullptr;
     prof_begin(s, true, &ev);
     // promotion chunk: 256 of K for 3xTF32 (8 stages), none for 1xTF32
-    const int kc_stages = TERMS == 3 ? 256 / TC_BK : 0x3fffffff;
+    const int kc_stages = TERMS >= 2 ? 256 / TC_BK : 0x3fffffff;
     tc_sgemm_kernel<TERMS><<<(unsigned)blocks, TC_THREADS_P, Cfg::SMEM_BYTES, s>>>(
         ta, tb, (int)M, (int)N, (int)Kp, alpha, beta, C, ldc, tiles_m, tiles_n, group_m, kc_stages, wave_ctr, splits,
         splits > 1 ? partial : nullptr);
@@ -525,8 +552,9 @@ cudaError_t launch_tc_sgemm(int terms, const float *Ap, const float *Bp, int64_t
                             float *partial, cudaStream_t s) {
     if (M > 0x7fffffffLL || N > 0x7fffffffLL || Kp > 0x7fffffffLL) return cudaErrorInvalidValue;
     if (splits < 1 || (splits > 1 && !partial)) return cudaErrorInvalidValue;
-    return terms == 3 ? launch_tc_t<3>(Ap, Bp, M, N, Kp, alpha, beta, C, ldc, wave_ctr, splits, partial, s)
-                      : launch_tc_t<1>(Ap, Bp, M, N, Kp, alpha, beta, C, ldc, wave_ctr, splits, partial, s);
+    if (terms == 3) return launch_tc_t<3>(Ap, Bp, M, N, Kp, alpha, beta, C, ldc, wave_ctr, splits, partial, s);
+    if (terms == 2) return launch_tc_t<2>(Ap, Bp, M, N, Kp, alpha, beta, C, ldc, wave_ctr, splits, partial, s);
+    return launch_tc_t<1>(Ap, Bp, M, N, Kp, alpha, beta, C, ldc, wave_ctr, splits, partial, s);
 }
 
 }  // namespace emm

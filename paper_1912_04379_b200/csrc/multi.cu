@@ -170,7 +170,9 @@ extern "C" int emm_sgemm_multi(void *comm, char transA, char transB, int64_t M, 
     float *Ap = nullptr, *Bp = nullptr;
     unsigned int *ctr = nullptr;
     const int64_t Kp = tc_kpad(K);
-    const int planes = math == EMM_MATH_3XTF32 ? 2 : 1;
+    const int planes = (math == EMM_MATH_3XTF32 || math == EMM_MATH_TF32_BF16) ? 2 : 1;
+    const int pmode = math == EMM_MATH_3XTF32 ? 1 : math == EMM_MATH_TF32_BF16 ? 2 : 0;
+    const int terms = math == EMM_MATH_3XTF32 ? 3 : math == EMM_MATH_TF32_BF16 ? 2 : 1;
     const int64_t panel = bN ? emm_multi_panel_cols(N) : N;
     if (tc && rows > 0 && N > 0) {
         const size_t a_bytes = align_up((size_t)planes * rows * Kp * 4, 1024);
@@ -179,17 +181,17 @@ extern "C" int emm_sgemm_multi(void *comm, char transA, char transB, int64_t M, 
         Ap = reinterpret_cast<float *>(ws);
         Bp = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(ws) + a_bytes);
         ctr = reinterpret_cast<unsigned int *>(reinterpret_cast<uint8_t *>(ws) + a_bytes + b_bytes);
-        st = cuda_st(launch_pack_split(A_local, lda, /*kcontig=*/!nA, rows, K, Kp, planes, Ap, s));
+        st = cuda_st(launch_pack_split(A_local, lda, /*kcontig=*/!nA, rows, K, Kp, pmode, Ap, s));
     }
     auto panel_gemm = [&](const float *bp, int64_t nc, float *cp) -> int {
         if (rows == 0 || nc == 0) return 0;
         if (!tc)   // FFMA, or alpha == 0 / K == 0 (C <- beta*C)
             return emm_sgemm_ex(transA, transB, rows, nc, K, alpha, A_local, lda, bp, ldb, beta, cp, ldc, s, math,
                                 nullptr, 0);
-        cudaError_t e = launch_pack_split2(bp, ldb, /*kcontig=*/bN, nc, nullptr, 0, false, 0, K, Kp, planes, Bp,
-                                           nullptr, ctr, s);
+        cudaError_t e = launch_pack_split2(bp, ldb, /*kcontig=*/bN, nc, nullptr, 0, false, 0, K, Kp, pmode, Bp,
+                                           nullptr, ctr, s, /*first_is_b=*/true);
         if (e == cudaSuccess)
-            e = launch_tc_sgemm(planes == 2 ? 3 : 1, Ap, Bp, rows, nc, Kp, alpha, beta, cp, ldc, ctr, 1, nullptr, s);
+            e = launch_tc_sgemm(terms, Ap, Bp, rows, nc, Kp, alpha, beta, cp, ldc, ctr, 1, nullptr, s);
         return cuda_st(e);
     };
 

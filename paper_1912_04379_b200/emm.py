@@ -14,7 +14,7 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "libemm.so")
 
-MATH = {"3xtf32": 0, "ffma": 1, "1xtf32": 2}
+MATH = {"3xtf32": 0, "ffma": 1, "1xtf32": 2, "tf32bf16": 3}
 
 
 class EmmError(RuntimeError):

@@ -31,8 +31,8 @@ def force_requested_path(monkeypatch):
     (EMM_SMALL_FLOPS=0); test_small_problem_default_path covers the default."""
     monkeypatch.setenv("EMM_SMALL_FLOPS", "0")
 
-TOL = {"3xtf32": 1e-5, "ffma": 1e-5, "1xtf32": 5e-3}
-MATHS = ["3xtf32", "ffma", "1xtf32"]
+TOL = {"3xtf32": 1e-5, "ffma": 1e-5, "1xtf32": 5e-3, "tf32bf16": 1e-5}
+MATHS = ["3xtf32", "ffma", "1xtf32", "tf32bf16"]
 SENTINEL = -12345.0
 GUARD = 4096
 
@@ -211,7 +211,7 @@ def test_c3_blas_stress(emm, math, tA, tB):
     assert_close(case, Cg, R, S, T, TOL[math], rows=rows)
 
 
-@pytest.mark.parametrize("math", ["3xtf32", "1xtf32"])
+@pytest.mark.parametrize("math", ["3xtf32", "1xtf32", "tf32bf16"])
 @pytest.mark.parametrize("shape", [(65536, 1024, 4096), (65536, 4096, 1024)])
 def test_c4_nn_layer_sampled(emm, math, shape):
     M, N, K = shape
@@ -324,7 +324,7 @@ def test_accumulate_property(emm):
     assert_close(case, c_twice, R, 2 * S, 2 * T, 1e-5)
 
 
-@pytest.mark.parametrize("math", ["3xtf32", "ffma"])
+@pytest.mark.parametrize("math", ["3xtf32", "ffma", "tf32bf16"])
 @pytest.mark.parametrize("K", [4096, 32768])
 def test_same_sign_accumulation(emm, math, K):
     """Same-sign U[0,1) data at large K (Q7): a truncating
@@ -350,7 +350,7 @@ def test_small_problem_default_path(emm, monkeypatch, shape):
         assert_close(case, Cg, R, S, T, 1e-5)   # FFMA kernel: FP32-accurate for every mode
 
 
-@pytest.mark.parametrize("math", ["3xtf32", "1xtf32"])
+@pytest.mark.parametrize("math", ["3xtf32", "1xtf32", "tf32bf16"])
 @pytest.mark.parametrize("shape", [(1531, 997, 2049), (1024, 1024, 1024), (700, 700, 700), (257, 300, 4000)])
 def test_split_k_deterministic_and_close(emm, math, shape):
     """Sub-wave shapes take split-K (partials + fixed-order reduce): results
