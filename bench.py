@@ -55,6 +55,7 @@ def parse():
     p.add_argument("--size", type=int, default=32768)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-alt", action="store_true", help="skip the other FP32-accurate tensor path")
     p.add_argument("--cpu-rows", type=int, default=0, help="oracle sample rows (0 = auto)")
     return p.parse_args()
 
@@ -233,17 +234,19 @@ def main():
     C = torch.empty((N, max(rows, 1)), dtype=torch.float32, device=dev).t()[:rows, :]
     ws = None
     if world == 1:
-        nbytes = emm.workspace_bytes("N", "N", M, N, K, args.math)
+        nbytes = max(emm.workspace_bytes("N", "N", M, N, K, m) for m in (args.math, "3xtf32", "tf32bf16"))
         ws = torch.empty(max(nbytes // 4 + 256, 1), dtype=torch.float32, device=dev) if nbytes else None
         if ws is not None and ws.data_ptr() % 1024:
             ws = ws[(1024 - ws.data_ptr() % 1024) // 4:]
     comm = emm.Comm(rank, world) if world > 1 else None
 
-    def step():
-        if world > 1:
-            emm.sgemm_multi(comm, M, N, K, A, B, C, 1.0, 0.0, math=args.math, stream=stream)
-        else:
-            emm.sgemm_ex(A, B, C, 1.0, 0.0, math=args.math, workspace=ws, stream=stream)
+    def make_step(math):
+        def step():
+            if world > 1:
+                emm.sgemm_multi(comm, M, N, K, A, B, C, 1.0, 0.0, math=math, stream=stream)
+            else:
+                emm.sgemm_ex(A, B, C, 1.0, 0.0, math=math, workspace=ws, stream=stream)
+        return step
 
     def barrier():
         torch.cuda.synchronize(dev)
@@ -251,69 +254,88 @@ def main():
             torch.distributed.barrier()
         torch.cuda.synchronize(dev)
 
-    with torch.cuda.stream(stream):
-        for _ in range(args.warmup):
-            step()
-    barrier()
-
-    clocks = ClockSampler(local)
-    clocks.start()
-    emm.profile_enable(True)
-    emm.profile_read()
-    l0 = emm.launch_count()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier()
-    ev0.record(stream)
-    with torch.cuda.stream(stream):
-        for _ in range(args.steps):
-            step()
-    ev1.record(stream)
-    barrier()
-    launches = emm.launch_count() - l0
-    ms = ev0.elapsed_time(ev1)
-    gemm_ms, gemm_n, other_ms, other_n = emm.profile_read()
-    emm.profile_enable(False)
-    clk = clocks.stop()
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
-    ms_step = ms / args.steps
-    value = flops * args.steps / (ms / 1e3) / 1e9
-
     bf16, bf16_sus, hbm, src = peaks()
     tf32_sus = bf16_sus * TF32_PER_BF16
     tf32_burst = bf16 * TF32_PER_BF16
-    if args.math == "3xtf32":
-        peak, peak_b, pname = tf32_sus / 3.0, tf32_burst / 3.0, "3xTF32-effective (TF32/3)"
-    elif args.math == "tf32bf16":
-        # one TF32 MMA (K8) + one BF16 MMA (K16) per 8 of K: 2 TF32-MMA times
-        peak, peak_b, pname = tf32_sus / 2.0, tf32_burst / 2.0, "TF32+BF16-effective (TF32/2)"
-    elif args.math == "1xtf32":
-        peak, peak_b, pname = tf32_sus, tf32_burst, "TF32"
-    else:
+
+    def path_peak(math):
+        if math == "3xtf32":
+            return tf32_sus / 3.0, tf32_burst / 3.0, "3xTF32-effective (TF32/3)"
+        if math == "tf32bf16":
+            # one TF32 MMA (K8) + one BF16 MMA (K16) per 8 of K: 2 TF32-MMA times
+            return tf32_sus / 2.0, tf32_burst / 2.0, "TF32+BF16-effective (TF32/2)"
+        if math == "1xtf32":
+            return tf32_sus, tf32_burst, "TF32"
         sm = torch.cuda.get_device_properties(dev).multi_processor_count
-        peak = peak_b = sm * 256 * 1965e6 / 1e12
-        pname = "FP32 FFMA (SMs x 256 flop/clk x 1965 MHz)"
-    flops_rank = 2.0 * rows * N * K
-    kernel_ms = gemm_ms / max(gemm_n, 1)
-    per_launch_flops = flops_rank / max(gemm_n // max(args.steps, 1), 1)
-    achieved = per_launch_flops / (kernel_ms / 1e3) / 1e12 if kernel_ms > 0 else None
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tp):
-        try:
-            with open(tp) as f:
-                traffic = json.load(f).get(f"{args.math}_{n}")
-        except Exception:
-            traffic = None
-    roofline = {"bound": "tensor" if args.math != "ffma" else "alu", "achieved": achieved, "peak": peak,
+        p = sm * 256 * 1965e6 / 1e12
+        return p, p, "FP32 FFMA (SMs x 256 flop/clk x 1965 MHz)"
+
+    def measure(math, steps, warmup):
+        """W untimed steps, then exactly `steps` timed steps bracketed by a
+        barrier + device sync; CUDA events on the launching stream; max over
+        ranks; clocks sampled during the timed region."""
+        step = make_step(math)
+        with torch.cuda.stream(stream):
+            for _ in range(warmup):
+                step()
+        barrier()
+        clocks = ClockSampler(local)
+        clocks.start()
+        emm.profile_enable(True)
+        emm.profile_read()
+        l0 = emm.launch_count()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        ev0.record(stream)
+        with torch.cuda.stream(stream):
+            for _ in range(steps):
+                step()
+        ev1.record(stream)
+        barrier()
+        launches = emm.launch_count() - l0
+        ms = ev0.elapsed_time(ev1)
+        gemm_ms, gemm_n, other_ms, other_n = emm.profile_read()
+        emm.profile_enable(False)
+        clk = clocks.stop()
+        if world > 1:
+            t = torch.tensor([ms], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ms = float(t.item())
+        peak, peak_b, pname = path_peak(math)
+        flops_rank = 2.0 * rows * N * K
+        kernel_ms = gemm_ms / max(gemm_n, 1)
+        per_launch_flops = flops_rank / max(gemm_n // max(steps, 1), 1)
+        achieved = per_launch_flops / (kernel_ms / 1e3) / 1e12 if kernel_ms > 0 else None
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tp):
+            try:
+                with open(tp) as f:
+                    traffic = json.load(f).get(f"{math}_{n}")
+            except Exception:
+                traffic = None
+        roof = {"bound": "tensor" if math != "ffma" else "alu", "achieved": achieved, "peak": peak,
                 "unit": "TFLOP/s", "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "peak_kind": f"{pname}, from {src} bf16 sustained {bf16_sus} TF x 1.1/2.25",
                 "peak_burst": peak_b, "frac_burst": (achieved / peak_b) if achieved else None,
-                "kernel": "tc_sgemm_kernel" if args.math != "ffma" else "ffma_sgemm_kernel",
+                "kernel": "tc_sgemm_kernel" if math != "ffma" else "ffma_sgemm_kernel",
                 "kernel_ms": kernel_ms, "kernel_share_of_step": (gemm_ms / ms) if ms > 0 else None,
-                "other_kernels_ms_per_step": other_ms / args.steps}
+                "other_kernels_ms_per_step": other_ms / steps}
+        return {"value": flops * steps / (ms / 1e3) / 1e9, "ms": ms, "launches": launches, "clocks": clk,
+                "roofline": roof, "peak": peak}
+
+    res = measure(args.math, args.steps, args.warmup)
+    value, ms, launches, clk, roofline, peak = (res["value"], res["ms"], res["launches"], res["clocks"],
+                                                res["roofline"], res["peak"])
+    ms_step = ms / args.steps
+    alt = {}
+    if args.math in ("3xtf32", "tf32bf16") and not args.no_alt and world == 1:
+        m2 = "tf32bf16" if args.math == "3xtf32" else "3xtf32"
+        k2 = max(3, args.steps // 2)
+        r2 = measure(m2, k2, 2)
+        alt[m2] = {"value": r2["value"], "unit": "GFLOP/s", "steps": k2, "ms_per_step": r2["ms"] / k2,
+                   "roofline": r2["roofline"], "clocks": r2["clocks"],
+                   "note": "same workload, the other FP32-accurate tensor-core split (parity-tested at 1e-5*S)"}
 
     # ---- e2e through the C-ABI host-buffer entry (copies inside the timed region)
     e2e = None
@@ -373,7 +395,7 @@ def main():
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": workload_config(n, args, world), "roofline": roofline, "cpu_baseline": cpu,
-                "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+                "e2e": e2e, "gpu_launches": launches, "clocks": clk, "alt_paths": alt or None,
                 "pct_of_roofline": 100.0 * value / 1e3 / (peak * world) if peak else None}
         print(json.dumps(line), flush=True)
     if comm is not None:
