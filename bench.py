@@ -354,7 +354,12 @@ def main():
         e2e = {"value": flops * e_steps / dt / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": 4 * (M * K + K * N),
                "d2h_bytes_per_step": 4 * M * N, "steps": e_steps,
                "api": "emm_sgemm_host (pinned host A,B -> device, C -> host, synchronous)"}
-        # spot-check the e2e result against the device result on a few entries
+        # spot-check the e2e result against a device call of the same path
+        # (deterministic: must be bitwise equal)
+        ws = None
+        with torch.cuda.stream(stream):
+            emm.sgemm(A, B, C, 1.0, 0.0, math=args.math, stream=stream)
+        stream.synchronize()
         Cd = C[:64, :64].cpu()
         hv = hC.reshape(N, M)[:64, :64].t()
         assert torch.equal(Cd, hv), "e2e result differs from device result"

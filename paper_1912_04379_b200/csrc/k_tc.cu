@@ -43,6 +43,11 @@ constexpr int TC_TILE_BYTES = 128 * TC_BK * 4;   // one 128 x 32 FP32 operand ti
 
 int64_t tc_kpad(int64_t K) { return (K + TC_BK - 1) / TC_BK * TC_BK; }
 
+// Per-call control block (zeroed by the pack launch): word 0 = wave-lockstep
+// counter, words 32.. = split-K arrival flags, one per (tile, split).
+constexpr int TC_CTRL_WORDS = 2048;
+constexpr int TC_FLAG0 = 32;
+
 // =====================================================================
 // KN4: re-buffer + split of BOTH operands in one launch (blockIdx.z = 0: A,
 // 1: B).  32x32 tiles, 256 threads.  Block (0,0,0) also zeroes the GEMM's
@@ -88,7 +93,8 @@ __global__ void __launch_bounds__(256) pack_split_kernel(PackOperand opA, PackOp
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const int64_t r0 = (int64_t)blockIdx.x * 32;
     const int64_t k0 = (int64_t)blockIdx.y * 32;
-    if (wave_ctr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0) *wave_ctr = 0u;
+    if (wave_ctr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
+        for (int i = threadIdx.x; i < TC_CTRL_WORDS; i += blockDim.x) wave_ctr[i] = 0u;
     if (r0 >= op.R) return;                               // block-uniform
     const float *__restrict__ X = op.X;
     float *__restrict__ out = op.out;
@@ -154,22 +160,6 @@ cudaError_t launch_pack_split(const float *X, int64_t ld, bool kcontig, int64_t 
 }
 
 // =====================================================================
-// KN8: split-K reduction.  C <- alpha * (P_0 + ... + P_{S-1}) + beta*C, the
-// partials summed in fixed order (deterministic).  P_s is M x N, ld = M.
-// =====================================================================
-__global__ void splitk_reduce_kernel(const float *__restrict__ P, int S, int64_t M, int64_t N, float alpha, float beta,
-                                     float *__restrict__ C, int64_t ldc) {
-    const int64_t total = M * N;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-        float acc = P[e];
-        for (int sp = 1; sp < S; ++sp) acc += P[(int64_t)sp * total + e];
-        const int64_t i = e % M, j = e / M;
-        float *d = C + i + j * ldc;
-        *d = beta == 0.0f ? alpha * acc : fmaf(beta, *d, alpha * acc);
-    }
-}
-
-// =====================================================================
 // KN1/KN2: tcgen05 GEMM on packed operands, CTA pair per 256x256 tile.
 //
 // Accumulation precision (Q7, measured on B200): the tensor core
@@ -198,7 +188,7 @@ struct TcCfg {
 };
 
 template <int TERMS>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
+__global__ void __cluster_dims__(2, 1, 1) __maxnreg__(200)   // 320 threads x 200 regs <= 64K
     tc_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                     int Kp, float alpha, float beta, float *__restrict__ C, int64_t ldc, int tiles_m, int tiles_n,
                     int group_m, int kc_stages, unsigned int *__restrict__ wave_ctr, int splits,
@@ -388,12 +378,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
                 tc_fence_after();
                 const uint32_t tb = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(b * TC_BN + h * 128);
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    uint32_t v[32];
-                    tmem_ld_32x32b_x32(tb + (uint32_t)(32 * c), v);
+                for (int c = 0; c < 8; ++c) {
+                    uint32_t v[16];
+                    tmem_ld_32x32b_x16(tb + (uint32_t)(16 * c), v);
                     tmem_ld_wait();
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) acc[32 * c + j] += __uint_as_float(v[j]);
+                    for (int j = 0; j < 16; ++j) acc[16 * c + j] += __uint_as_float(v[j]);
                 }
                 tc_fence_before();
                 __syncwarp();
@@ -402,15 +392,51 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
                     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(eb) : "memory");
                 }
             }
-            if (row < M && partial) {
-                // split-K: raw FP32 partial of split `sp` (alpha/beta in KN8)
+            if (partial && sp > 0) {
+                // split-K, split sp > 0: publish the raw FP32 partial and
+                // signal its arrival (one release per warp, 16 per unit).
                 const int col0 = n0 + h * 128;
-                float *pp = partial + (int64_t)sp * M * N + (int64_t)row + (int64_t)col0 * M;
-                const int jmax = min(128, N - col0);
+                if (row < M) {
+                    float *pp = partial + (int64_t)(sp - 1) * M * N + (int64_t)row + (int64_t)col0 * M;
+                    const int jmax = min(128, N - col0);
 #pragma unroll
-                for (int j = 0; j < 128; ++j)
-                    if (j < jmax) pp[(int64_t)j * M] = acc[j];
-            } else if (row < M) {
+                    for (int j = 0; j < 128; ++j)
+                        if (j < jmax) pp[(int64_t)j * M] = acc[j];
+                }
+                __threadfence();
+                __syncwarp();
+                if (lane == 0) {
+                    unsigned int *flag = wave_ctr + TC_FLAG0 + (t - sp * total_tiles) * splits + sp;
+                    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(flag) : "memory");
+                }
+                continue;
+            }
+            if (partial) {
+                // split 0 finishes the tile: wait for every other split of
+                // this tile (all units of a split-K launch are co-resident:
+                // units <= CTA pairs), then add their partials in FIXED order
+                // s = 1..S-1 -> deterministic.
+                const int col0 = n0 + h * 128;
+                const int jmax = min(128, N - col0);
+                for (int s2 = 1; s2 < splits; ++s2) {
+                    const unsigned int *flag = wave_ctr + TC_FLAG0 + t * splits + s2;
+                    const long long t0 = clock64();
+                    while (true) {
+                        unsigned int v;
+                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+                        if (v >= 2u * TC_EPI_WARPS) break;
+                        __nanosleep(64);
+                        if (clock64() - t0 > 40000000000LL) __trap();
+                    }
+                    if (row < M) {
+                        const float *pp = partial + (int64_t)(s2 - 1) * M * N + (int64_t)row + (int64_t)col0 * M;
+#pragma unroll
+                        for (int j = 0; j < 128; ++j)
+                            if (j < jmax) acc[j] += __ldcg(pp + (int64_t)j * M);
+                    }
+                }
+            }
+            if (row < M) {
                 const int col0 = n0 + h * 128;
                 float *cp = C + (int64_t)row + (int64_t)col0 * ldc;
                 const int jmax = min(128, N - col0);
@@ -490,6 +516,8 @@ int tc_num_sms() {
 
 // Split-K factor for sub-wave problems: enough (tile,
 // split) units to fill the CTA pairs, each split >= 4 K-stages (128 of K).
+// units = tiles * S <= CTA pairs: all units are co-resident (one wave), which
+// the in-kernel split-K fixup (split 0 waits for the others) relies on.
 int tc_splits(int64_t M, int64_t N, int64_t K) {
     const int64_t tiles = ((M + 2 * TC_BM - 1) / (2 * TC_BM)) * ((N + TC_BN - 1) / TC_BN);
     const int64_t nkb = tc_kpad(K) / TC_BK;
@@ -499,6 +527,7 @@ int tc_splits(int64_t M, int64_t N, int64_t K) {
     if (s > nkb / 4) s = nkb / 4;
     if (s > 16) s = 16;
     if (s < 1) s = 1;
+    if (tiles * s > (TC_CTRL_WORDS - TC_FLAG0)) s = (TC_CTRL_WORDS - TC_FLAG0) / tiles;
     // every split must own at least one stage
     while (s > 1 && ((nkb + s - 1) / s) * (s - 1) >= nkb) --s;
     return (int)s;
@@ -536,14 +565,6 @@ static cudaError_t launch_tc_t(const float *Ap, const float *Bp, int64_t M, int6
         splits > 1 ? partial : nullptr);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     prof_end(s, true, ev);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess || splits <= 1) return e;
-    const int64_t want = (M * N + 255) / 256;
-    const int blocks_r = (int)(want < (int64_t)tc_num_sms() * 8 ? want : (int64_t)tc_num_sms() * 8);
-    prof_begin(s, false, &ev);
-    splitk_reduce_kernel<<<blocks_r > 0 ? blocks_r : 1, 256, 0, s>>>(partial, splits, M, N, alpha, beta, C, ldc);
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-    prof_end(s, false, ev);
     return cudaGetLastError();
 }
 
@@ -551,7 +572,9 @@ cudaError_t launch_tc_sgemm(int terms, const float *Ap, const float *Bp, int64_t
                             float alpha, float beta, float *C, int64_t ldc, unsigned int *wave_ctr, int splits,
                             float *partial, cudaStream_t s) {
     if (M > 0x7fffffffLL || N > 0x7fffffffLL || Kp > 0x7fffffffLL) return cudaErrorInvalidValue;
-    if (splits < 1 || (splits > 1 && !partial)) return cudaErrorInvalidValue;
+    if (splits < 1 || (splits > 1 && (!partial || !wave_ctr))) return cudaErrorInvalidValue;
+    if (splits > 1 && ((M + 2 * TC_BM - 1) / (2 * TC_BM)) * ((N + TC_BN - 1) / TC_BN) * splits > tc_num_sms() / 2)
+        return cudaErrorInvalidValue;   // the fixup needs every unit co-resident
     if (terms == 3) return launch_tc_t<3>(Ap, Bp, M, N, Kp, alpha, beta, C, ldc, wave_ctr, splits, partial, s);
     if (terms == 2) return launch_tc_t<2>(Ap, Bp, M, N, Kp, alpha, beta, C, ldc, wave_ctr, splits, partial, s);
     return launch_tc_t<1>(Ap, Bp, M, N, Kp, alpha, beta, C, ldc, wave_ctr, splits, partial, s);
