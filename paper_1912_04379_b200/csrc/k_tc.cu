@@ -188,7 +188,7 @@ struct TcCfg {
 };
 
 template <int TERMS>
-__global__ void __cluster_dims__(2, 1, 1) __maxnreg__(200)   // 320 threads x 200 regs <= 64K
+__global__ void __cluster_dims__(2, 1, 1) __maxnreg__(192)   // 320 threads x 192 regs <= 64K
     tc_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                     int Kp, float alpha, float beta, float *__restrict__ C, int64_t ldc, int tiles_m, int tiles_n,
                     int group_m, int kc_stages, unsigned int *__restrict__ wave_ctr, int splits,
