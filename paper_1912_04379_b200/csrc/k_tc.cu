@@ -171,8 +171,11 @@ cudaError_t launch_pack_split(const float *X, int64_t ld, bool kcontig, int64_t 
 // MMAs run on the other buffer ("promotion"), bounding the truncation bias
 // to one chunk.
 // =====================================================================
-constexpr int TC_EPI_WARPS = 8;                               // 2 per TMEM lane quarter
-constexpr int TC_THREADS_P = 64 + 32 * TC_EPI_WARPS;          // 320
+// warp 0 = TMA producer, warp 1 = MMA issuer + TMEM owner, warps 2-9 = 8
+// promotion/epilogue warps (2 per TMEM lane quarter).
+constexpr int TC_EPI_WARPS = 8;
+constexpr int TC_EPI_WARP0 = 2;
+constexpr int TC_THREADS_P = 32 * (TC_EPI_WARP0 + TC_EPI_WARPS);   // 384
 constexpr int TC_TMEM_COLS_P = 512;                           // 2 accumulator buffers
 
 // TERMS: 3 = 3xTF32 (small*big + big*small + big*big, three kind::tf32 MMAs
@@ -188,7 +191,7 @@ struct TcCfg {
 };
 
 template <int TERMS>
-__global__ void __cluster_dims__(2, 1, 1) __maxnreg__(192)   // 320 threads x 192 regs <= 64K
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
     tc_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                     int Kp, float alpha, float beta, float *__restrict__ C, int64_t ldc, int tiles_m, int tiles_n,
                     int group_m, int kc_stages, unsigned int *__restrict__ wave_ctr, int splits,
@@ -357,10 +360,10 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(192)   // 320 threads x 19
                 }
             }
         }
-    } else {
+    } else if (warp >= TC_EPI_WARP0) {
         // ===== epilogue: TMEM -> FP32 registers (promotion) -> alpha/beta -> C =====
         const int q = warp & 3;                        // TMEM lane quarter of this warp
-        const int h = (warp - 2) >> 2;                 // column half (128 columns)
+        const int h = (warp - TC_EPI_WARP0) >> 2;      // column half (128 columns)
         uint32_t leader_empty0;
         asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(leader_empty0) : "r"(smem_u32(&acc_empty[0])));
         int ch = 0;
@@ -400,8 +403,8 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(192)   // 320 threads x 19
                     float *pp = partial + (int64_t)(sp - 1) * M * N + (int64_t)row + (int64_t)col0 * M;
                     const int jmax = min(128, N - col0);
 #pragma unroll
-                    for (int j = 0; j < 128; ++j)
-                        if (j < jmax) pp[(int64_t)j * M] = acc[j];
+                    for (int j = 0; j < 128; ++j, pp += M)
+                        if (j < jmax) *pp = acc[j];
                 }
                 __threadfence();
                 __syncwarp();
@@ -431,8 +434,8 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(192)   // 320 threads x 19
                     if (row < M) {
                         const float *pp = partial + (int64_t)(s2 - 1) * M * N + (int64_t)row + (int64_t)col0 * M;
 #pragma unroll
-                        for (int j = 0; j < 128; ++j)
-                            if (j < jmax) acc[j] += __ldcg(pp + (int64_t)j * M);
+                        for (int j = 0; j < 128; ++j, pp += M)
+                            if (j < jmax) acc[j] += __ldcg(pp);
                     }
                 }
             }
@@ -441,9 +444,10 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(192)   // 320 threads x 19
                 float *cp = C + (int64_t)row + (int64_t)col0 * ldc;
                 const int jmax = min(128, N - col0);
                 if (beta == 0.0f) {
+                    float *sp2 = cp;
 #pragma unroll
-                    for (int j = 0; j < 128; ++j)
-                        if (j < jmax) cp[(int64_t)j * ldc] = alpha * acc[j];
+                    for (int j = 0; j < 128; ++j, sp2 += ldc)
+                        if (j < jmax) *sp2 = alpha * acc[j];
                 } else {
                     // beta != 0: issue 16 independent C loads before the 16
                     // stores (a store could alias a later load through ldc,
