@@ -523,6 +523,14 @@ int tc_num_sms() {
 // units = tiles * S <= CTA pairs: all units are co-resident (one wave), which
 // the in-kernel split-K fixup (split 0 waits for the others) relies on.
 int tc_splits(int64_t M, int64_t N, int64_t K) {
+    if (const char *e = getenv("EMM_SPLITS")) {   // experiments: force S (clamped below)
+        const int64_t tiles0 = ((M + 2 * TC_BM - 1) / (2 * TC_BM)) * ((N + TC_BN - 1) / TC_BN);
+        int64_t s = atoi(e);
+        const int64_t nkb0 = tc_kpad(K) / TC_BK;
+        if (s < 1) s = 1;
+        while (s > 1 && (tiles0 * s > tc_num_sms() / 2 || ((nkb0 + s - 1) / s) * (s - 1) >= nkb0)) --s;
+        return (int)s;
+    }
     const int64_t tiles = ((M + 2 * TC_BM - 1) / (2 * TC_BM)) * ((N + TC_BN - 1) / TC_BN);
     const int64_t nkb = tc_kpad(K) / TC_BK;
     const int64_t clusters = tc_num_sms() / 2;
