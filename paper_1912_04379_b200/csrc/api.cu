@@ -118,8 +118,8 @@ static bool small_problem(int64_t M, int64_t N, int64_t K) {
 }
 
 // Workspace of the tensor-core paths:
-//   [Ap: planes*M*Kp | Bp: planes*N*Kp | split-K partials: (S-1)*M*N |
-//    control block: wave counter + split-K flags (8 KB)]
+//   [Ap: planes*M*Kp | Bp: planes*N*Kp | split-K partials: S*M*N |
+//    control block: wave counter (1 KB)]
 struct WsLayout {
     size_t a_off, b_off, p_off, ctr_off, total;
     int splits;
@@ -134,8 +134,8 @@ static WsLayout ws_layout(int64_t M, int64_t N, int64_t K, emm_math_t math) {
     L.a_off = 0;
     L.b_off = align_up(pl * (size_t)M * (size_t)Kp * 4, 1024);
     L.p_off = L.b_off + align_up(pl * (size_t)N * (size_t)Kp * 4, 1024);
-    L.ctr_off = L.p_off + (L.splits > 1 ? align_up((size_t)(L.splits - 1) * M * N * 4, 1024) : 0);
-    L.total = L.ctr_off + 8192;
+    L.ctr_off = L.p_off + (L.splits > 1 ? align_up((size_t)L.splits * M * N * 4, 1024) : 0);
+    L.total = L.ctr_off + 1024;
     return L;
 }
 

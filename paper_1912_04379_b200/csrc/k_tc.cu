@@ -44,9 +44,8 @@ constexpr int TC_TILE_BYTES = 128 * TC_BK * 4;   // one 128 x 32 FP32 operand ti
 int64_t tc_kpad(int64_t K) { return (K + TC_BK - 1) / TC_BK * TC_BK; }
 
 // Per-call control block (zeroed by the pack launch): word 0 = wave-lockstep
-// counter, words 32.. = split-K arrival flags, one per (tile, split).
-constexpr int TC_CTRL_WORDS = 2048;
-constexpr int TC_FLAG0 = 32;
+// counter.
+constexpr int TC_CTRL_WORDS = 32;
 
 // =====================================================================
 // KN4: re-buffer + split of BOTH operands in one launch (blockIdx.z = 0: A,
@@ -157,6 +156,25 @@ cudaError_t launch_pack_split2(const float *A, int64_t lda, bool a_kcontig, int6
 cudaError_t launch_pack_split(const float *X, int64_t ld, bool kcontig, int64_t R, int64_t K, int64_t Kp,
                               int mode, float *out, cudaStream_t s) {
     return launch_pack_split2(X, ld, kcontig, R, nullptr, 0, false, 0, K, Kp, mode, out, nullptr, nullptr, s, false);
+}
+
+// =====================================================================
+// KN8: split-K reduction.  C <- alpha * (P_0 + ... + P_{S-1}) + beta*C, the
+// partials summed in fixed order s = 0..S-1 (deterministic).  P_s is M x N
+// with ld = M.  Grid (ceil(M/256), N): thread = row, block column = j.
+// =====================================================================
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const float *__restrict__ P, int S, int64_t M, int64_t N,
+                                                            float alpha, float beta, float *__restrict__ C,
+                                                            int64_t ldc) {
+    const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
+    const int64_t j = blockIdx.y;
+    if (i >= M) return;
+    const int64_t plane = M * N;
+    const float *p = P + i + j * M;
+    float acc = p[0];
+    for (int s = 1; s < S; ++s) acc += p[(int64_t)s * plane];
+    float *d = C + i + j * ldc;
+    *d = beta == 0.0f ? alpha * acc : fmaf(beta, *d, alpha * acc);
 }
 
 // =====================================================================
@@ -395,49 +413,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
                     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(eb) : "memory");
                 }
             }
-            if (partial && sp > 0) {
-                // split-K, split sp > 0: publish the raw FP32 partial and
-                // signal its arrival (one release per warp, 16 per unit).
-                const int col0 = n0 + h * 128;
+            if (partial) {
+                // split-K: publish the raw FP32 partial of split sp; the
+                // reduce launch (KN8) sums the S partials in fixed order.
                 if (row < M) {
-                    float *pp = partial + (int64_t)(sp - 1) * M * N + (int64_t)row + (int64_t)col0 * M;
+                    const int col0 = n0 + h * 128;
+                    float *pp = partial + (int64_t)sp * M * N + (int64_t)row + (int64_t)col0 * M;
                     const int jmax = min(128, N - col0);
 #pragma unroll
                     for (int j = 0; j < 128; ++j, pp += M)
                         if (j < jmax) *pp = acc[j];
                 }
-                __threadfence();
-                __syncwarp();
-                if (lane == 0) {
-                    unsigned int *flag = wave_ctr + TC_FLAG0 + (t - sp * total_tiles) * splits + sp;
-                    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(flag) : "memory");
-                }
                 continue;
-            }
-            if (partial) {
-                // split 0 finishes the tile: wait for every other split of
-                // this tile (all units of a split-K launch are co-resident:
-                // units <= CTA pairs), then add their partials in FIXED order
-                // s = 1..S-1 -> deterministic.
-                const int col0 = n0 + h * 128;
-                const int jmax = min(128, N - col0);
-                for (int s2 = 1; s2 < splits; ++s2) {
-                    const unsigned int *flag = wave_ctr + TC_FLAG0 + t * splits + s2;
-                    const long long t0 = clock64();
-                    while (true) {
-                        unsigned int v;
-                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
-                        if (v >= 2u * TC_EPI_WARPS) break;
-                        __nanosleep(64);
-                        if (clock64() - t0 > 40000000000LL) __trap();
-                    }
-                    if (row < M) {
-                        const float *pp = partial + (int64_t)(s2 - 1) * M * N + (int64_t)row + (int64_t)col0 * M;
-#pragma unroll
-                        for (int j = 0; j < 128; ++j, pp += M)
-                            if (j < jmax) acc[j] += __ldcg(pp);
-                    }
-                }
             }
             if (row < M) {
                 const int col0 = n0 + h * 128;
@@ -520,8 +507,7 @@ int tc_num_sms() {
 
 // Split-K factor for sub-wave problems: enough (tile,
 // split) units to fill the CTA pairs, each split >= 4 K-stages (128 of K).
-// units = tiles * S <= CTA pairs: all units are co-resident (one wave), which
-// the in-kernel split-K fixup (split 0 waits for the others) relies on.
+// units = tiles * S <= CTA pairs (one wave).
 int tc_splits(int64_t M, int64_t N, int64_t K) {
     if (const char *e = getenv("EMM_SPLITS")) {   // experiments: force S (clamped below)
         const int64_t tiles0 = ((M + 2 * TC_BM - 1) / (2 * TC_BM)) * ((N + TC_BN - 1) / TC_BN);
@@ -539,7 +525,6 @@ int tc_splits(int64_t M, int64_t N, int64_t K) {
     if (s > nkb / 4) s = nkb / 4;
     if (s > 16) s = 16;
     if (s < 1) s = 1;
-    if (tiles * s > (TC_CTRL_WORDS - TC_FLAG0)) s = (TC_CTRL_WORDS - TC_FLAG0) / tiles;
     // every split must own at least one stage
     while (s > 1 && ((nkb + s - 1) / s) * (s - 1) >= nkb) --s;
     return (int)s;
@@ -577,6 +562,14 @@ static cudaError_t launch_tc_t(const float *Ap, const float *Bp, int64_t M, int6
         splits > 1 ? partial : nullptr);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     prof_end(s, true, ev);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess || splits <= 1) return e;
+    if (N > 65535) return cudaErrorInvalidConfiguration;
+    prof_begin(s, false, &ev);
+    splitk_reduce_kernel<<<dim3((unsigned)((M + 255) / 256), (unsigned)N), 256, 0, s>>>(partial, splits, M, N, alpha,
+                                                                                          beta, C, ldc);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    prof_end(s, false, ev);
     return cudaGetLastError();
 }
 
@@ -584,9 +577,7 @@ cudaError_t launch_tc_sgemm(int terms, const float *Ap, const float *Bp, int64_t
                             float alpha, float beta, float *C, int64_t ldc, unsigned int *wave_ctr, int splits,
                             float *partial, cudaStream_t s) {
     if (M > 0x7fffffffLL || N > 0x7fffffffLL || Kp > 0x7fffffffLL) return cudaErrorInvalidValue;
-    if (splits < 1 || (splits > 1 && (!partial || !wave_ctr))) return cudaErrorInvalidValue;
-    if (splits > 1 && ((M + 2 * TC_BM - 1) / (2 * TC_BM)) * ((N + TC_BN - 1) / TC_BN) * splits > tc_num_sms() / 2)
-        return cudaErrorInvalidValue;   // the fixup needs every unit co-resident
+    if (splits < 1 || (splits > 1 && !partial)) return cudaErrorInvalidValue;
     if (terms == 3) return launch_tc_t<3>(Ap, Bp, M, N, Kp, alpha, beta, C, ldc, wave_ctr, splits, partial, s);
     if (terms == 2) return launch_tc_t<2>(Ap, Bp, M, N, Kp, alpha, beta, C, ldc, wave_ctr, splits, partial, s);
     return launch_tc_t<1>(Ap, Bp, M, N, Kp, alpha, beta, C, ldc, wave_ctr, splits, partial, s);

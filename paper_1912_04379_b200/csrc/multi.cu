@@ -177,7 +177,7 @@ extern "C" int emm_sgemm_multi(void *comm, char transA, char transB, int64_t M, 
     if (tc && rows > 0 && N > 0) {
         const size_t a_bytes = align_up((size_t)planes * rows * Kp * 4, 1024);
         const size_t b_bytes = align_up((size_t)planes * panel * Kp * 4, 1024);
-        if ((st = cuda_st(cudaMallocAsync(&ws, a_bytes + b_bytes + 8192, s)))) return st;
+        if ((st = cuda_st(cudaMallocAsync(&ws, a_bytes + b_bytes + 1024, s)))) return st;
         Ap = reinterpret_cast<float *>(ws);
         Bp = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(ws) + a_bytes);
         ctr = reinterpret_cast<unsigned int *>(reinterpret_cast<uint8_t *>(ws) + a_bytes + b_bytes);

@@ -118,15 +118,15 @@ def test_row_partition_c5(emm):
 def test_workspace_bytes(emm):
     assert emm.workspace_bytes("N", "N", 64, 64, 64, "ffma") == 0
     # 3xTF32: 2 planes of M x Kp and N x Kp floats, Kp = K rounded up to 32, + counter
-    assert emm.workspace_bytes("N", "N", 2048, 1024, 33, "3xtf32") == 2 * 4 * 64 * (2048 + 1024) + 8192
-    assert emm.workspace_bytes("N", "T", 2048, 1024, 32, "1xtf32") == 4 * 32 * (2048 + 1024) + 8192
+    assert emm.workspace_bytes("N", "N", 2048, 1024, 33, "3xtf32") == 2 * 4 * 64 * (2048 + 1024) + 1024
+    assert emm.workspace_bytes("N", "T", 2048, 1024, 32, "1xtf32") == 4 * 32 * (2048 + 1024) + 1024
     # latency-bound problems (2MNK <= 2^24) take the FFMA kernel: no workspace
     assert emm.workspace_bytes("N", "N", 64, 64, 64, "3xtf32") == 0
-    # sub-wave problems add split-K partials: BJ configs[2] -> 3 splits, 2 published partials of M x N
+    # sub-wave problems add split-K partials: BJ configs[2] -> 3 partials of M x N
     M, N, K = 1531, 997, 2049
     base = 2 * 4 * 2080 * M + 2 * 4 * 2080 * N
     base = -(-2 * 4 * 2080 * M // 1024) * 1024 + -(-2 * 4 * 2080 * N // 1024) * 1024
-    assert emm.workspace_bytes("N", "N", M, N, K, "3xtf32") == base + -(-2 * M * N * 4 // 1024) * 1024 + 8192
+    assert emm.workspace_bytes("N", "N", M, N, K, "3xtf32") == base + -(-3 * M * N * 4 // 1024) * 1024 + 1024
 
 
 def test_strerror_and_version(emm):
