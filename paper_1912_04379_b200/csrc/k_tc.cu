@@ -88,6 +88,10 @@ template <int MODE>
 __global__ void __launch_bounds__(256) pack_split_kernel(PackOperand opA, PackOperand opB, int64_t K, int64_t Kp,
                                                          unsigned int *wave_ctr) {
     __shared__ float tile[32][33];
+    // Programmatic dependent launch: the GEMM may start its prologue (barrier
+    // init, TMEM alloc, descriptor prefetch) now; it waits (griddepcontrol.
+    // wait) for this grid's completion before its first operand load.
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const PackOperand &op = blockIdx.z == 0 ? opA : opB;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const int64_t r0 = (int64_t)blockIdx.x * 32;
@@ -166,6 +170,7 @@ cudaError_t launch_pack_split(const float *X, int64_t ld, bool kcontig, int64_t 
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float *__restrict__ P, int S, int64_t M, int64_t N,
                                                             float alpha, float beta, float *__restrict__ C,
                                                             int64_t ldc) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // PDL: the GEMM's partials
     const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
     const int64_t j = blockIdx.y;
     if (i >= M) return;
@@ -275,6 +280,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // PDL: everything above overlapped the previous kernel (the pack pass);
+    // from here on this grid reads its outputs (and C, wave counter).
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
     if (warp == 0) {
         // ===== TMA producer (both CTAs; each loads its half of A and B) =====
@@ -557,17 +566,42 @@ static cudaError_t launch_tc_t(const float *Ap, const float *Bp, int64_t M, int6
     prof_begin(s, true, &ev);
     // promotion chunk: 256 of K for 3xTF32 (8 stages), none for 1xTF32
     const int kc_stages = TERMS >= 2 ? 256 / TC_BK : 0x3fffffff;
-    tc_sgemm_kernel<TERMS><<<(unsigned)blocks, TC_THREADS_P, Cfg::SMEM_BYTES, s>>>(
-        ta, tb, (int)M, (int)N, (int)Kp, alpha, beta, C, ldc, tiles_m, tiles_n, group_m, kc_stages, wave_ctr, splits,
-        splits > 1 ? partial : nullptr);
+    {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((unsigned)blocks);
+        cfg.blockDim = dim3(TC_THREADS_P);
+        cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        cudaError_t le = cudaLaunchKernelEx(&cfg, tc_sgemm_kernel<TERMS>, ta, tb, (int)M, (int)N, (int)Kp, alpha, beta,
+                                            C, ldc, tiles_m, tiles_n, group_m, kc_stages, wave_ctr, splits,
+                                            splits > 1 ? partial : nullptr);
+        if (le != cudaSuccess) return le;
+    }
     g_launches.fetch_add(1, std::memory_order_relaxed);
     prof_end(s, true, ev);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || splits <= 1) return e;
     if (N > 65535) return cudaErrorInvalidConfiguration;
     prof_begin(s, false, &ev);
-    splitk_reduce_kernel<<<dim3((unsigned)((M + 255) / 256), (unsigned)N), 256, 0, s>>>(partial, splits, M, N, alpha,
-                                                                                          beta, C, ldc);
+    {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((unsigned)((M + 255) / 256), (unsigned)N);
+        cfg.blockDim = dim3(256);
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        cudaError_t le = cudaLaunchKernelEx(&cfg, splitk_reduce_kernel, (const float *)partial, splits, M, N, alpha,
+                                            beta, C, ldc);
+        if (le != cudaSuccess) return le;
+    }
     g_launches.fetch_add(1, std::memory_order_relaxed);
     prof_end(s, false, ev);
     return cudaGetLastError();
