@@ -117,29 +117,70 @@ static bool small_problem(int64_t M, int64_t N, int64_t K) {
     return 2.0 * (double)M * (double)N * (double)K <= thr;
 }
 
-// Workspace of the tensor-core paths:
-//   [Ap: planes*M*Kp | Bp: planes*N*Kp | split-K partials: S*M*N |
-//    control block: wave counter (1 KB)]
-struct WsLayout {
-    size_t a_off, b_off, p_off, ctr_off, total;
-    int splits;
+// How one tensor-core call runs:
+//  * direct (both operands TMA-legal): the GEMM reads A and B in place,
+//    K-major or MN-major per trans flag (transpose in the TMA descriptor);
+//    the split pass writes only the second plane (3xTF32: small in the
+//    operand's own layout; TF32+BF16: the K-major bf16 cross plane;
+//    1xTF32: nothing).
+//  * full (fallback, or EMM_FORCE_PACK=1): both planes re-buffered K-major.
+// Workspace: [A plane(s) | B plane(s) | split-K partials | control block],
+// 1024-byte aligned regions.  emm_sgemm_workspace_bytes returns the full
+// (larger) layout, valid for every pointer/ld.
+struct Plan {
+    bool direct = false;
+    int pack_mode = -1;      // -1: no split pass
+    int terms = 1;
+    int splits = 1;
+    size_t a_off = 0, b_off = 0, p_off = 0, ctr_off = 0, total = 0;
+    int64_t lda1 = 0, ldb1 = 0;   // second-plane leading dimensions
 };
 
-static WsLayout ws_layout(int64_t M, int64_t N, int64_t K, emm_math_t math) {
-    WsLayout L{0, 0, 0, 0, 0, 1};
-    if (math == EMM_MATH_FFMA || M == 0 || N == 0 || K == 0 || small_problem(M, N, K)) return L;
+static int64_t up4(int64_t v) { return (v + 3) / 4 * 4; }
+
+static Plan make_plan(char tA, char tB, int64_t M, int64_t N, int64_t K, emm_math_t math, bool direct) {
+    Plan P;
+    P.terms = terms_of(math);
+    P.splits = tc_splits(M, N, K);
+    P.direct = direct;
     const int64_t Kp = tc_kpad(K);
-    const size_t pl = (size_t)planes_of(math);
-    L.splits = tc_splits(M, N, K);
-    L.a_off = 0;
-    L.b_off = align_up(pl * (size_t)M * (size_t)Kp * 4, 1024);
-    L.p_off = L.b_off + align_up(pl * (size_t)N * (size_t)Kp * 4, 1024);
-    L.ctr_off = L.p_off + (L.splits > 1 ? align_up((size_t)L.splits * M * N * 4, 1024) : 0);
-    L.total = L.ctr_off + 1024;
-    return L;
+    size_t a_bytes, b_bytes;
+    if (!direct) {
+        const size_t pl = (size_t)planes_of(math);
+        P.pack_mode = math == EMM_MATH_3XTF32 ? PK_FULL3_ : math == EMM_MATH_TF32_BF16 ? PK_FULLX_ : PK_FULL1_;
+        P.lda1 = P.ldb1 = Kp;
+        a_bytes = pl * (size_t)M * Kp * 4;
+        b_bytes = pl * (size_t)N * Kp * 4;
+    } else if (math == EMM_MATH_3XTF32) {
+        P.pack_mode = PK_DSMALL_;
+        // small plane in the operand's own layout: K-major [R][up4(K)] or MN-major [K][up4(R)]
+        const bool a_mn = is_n(tA), b_mn = !is_n(tB);
+        P.lda1 = a_mn ? up4(M) : up4(K);
+        P.ldb1 = b_mn ? up4(N) : up4(K);
+        a_bytes = (size_t)(a_mn ? K : M) * P.lda1 * 4;
+        b_bytes = (size_t)(b_mn ? K : N) * P.ldb1 * 4;
+    } else if (math == EMM_MATH_TF32_BF16) {
+        P.pack_mode = PK_DCROSS_;
+        P.lda1 = P.ldb1 = Kp;
+        a_bytes = (size_t)M * Kp * 4;
+        b_bytes = (size_t)N * Kp * 4;
+    } else {
+        P.pack_mode = -1;
+        a_bytes = b_bytes = 0;
+    }
+    P.a_off = 0;
+    P.b_off = align_up(a_bytes, 1024);
+    P.p_off = P.b_off + align_up(b_bytes, 1024);
+    P.ctr_off = P.p_off + (P.splits > 1 ? align_up((size_t)P.splits * M * N * 4, 1024) : 0);
+    P.total = P.ctr_off + 1024;
+    return P;
 }
 
-static size_t ws_bytes(int64_t M, int64_t N, int64_t K, emm_math_t math) { return ws_layout(M, N, K, math).total; }
+static size_t ws_bytes(int64_t M, int64_t N, int64_t K, emm_math_t math) {
+    if (math == EMM_MATH_FFMA || M == 0 || N == 0 || K == 0 || small_problem(M, N, K)) return 0;
+    return make_plan('N', 'N', M, N, K, math, /*direct=*/false).total;
+}
+
 
 }  // namespace emm
 
@@ -182,28 +223,59 @@ extern "C" int emm_sgemm_ex(char transA, char transB, int64_t M, int64_t N, int6
         return cuda_status(
             launch_ffma_sgemm(!is_n(transA), !is_n(transB), M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, s));
 
-    // tensor-core paths: re-buffer/split both operands (one launch), then the
-    // persistent tcgen05 GEMM (+ the split-K reduce for sub-wave problems)
-    const WsLayout L = ws_layout(M, N, K, math);
+    // tensor-core paths
+    const char *fp = getenv("EMM_FORCE_PACK");   // tests / experiments: force the fallback
+    const bool force_pack = fp && fp[0] == '1';
+    const bool direct = !force_pack && tma_legal(A, lda) && tma_legal(B, ldb);
+    const Plan P = make_plan(transA, transB, M, N, K, math, direct);
     void *ws = workspace;
     bool own = false;
     if (ws) {
-        if (workspace_bytes < L.total || (reinterpret_cast<uintptr_t>(ws) & 1023u)) return EMM_ERR_WORKSPACE;
+        if (workspace_bytes < P.total || (reinterpret_cast<uintptr_t>(ws) & 1023u)) return EMM_ERR_WORKSPACE;
     } else {
-        cudaError_t e = cudaMallocAsync(&ws, L.total, s);
+        cudaError_t e = cudaMallocAsync(&ws, P.total, s);
         if (e != cudaSuccess) return cuda_status(e);
         own = true;
     }
-    const int64_t Kp = tc_kpad(K);
     uint8_t *w = reinterpret_cast<uint8_t *>(ws);
-    float *Ap = reinterpret_cast<float *>(w + L.a_off);
-    float *Bp = reinterpret_cast<float *>(w + L.b_off);
-    float *Pp = reinterpret_cast<float *>(w + L.p_off);
-    unsigned int *ctr = reinterpret_cast<unsigned int *>(w + L.ctr_off);
-    cudaError_t e = launch_pack_split2(A, lda, /*kcontig=*/!is_n(transA), M, B, ldb, /*kcontig=*/is_n(transB), N, K,
-                                       Kp, pack_mode(math), Ap, Bp, ctr, s);
-    if (e == cudaSuccess)
-        e = launch_tc_sgemm(terms_of(math), Ap, Bp, M, N, Kp, alpha, beta, C, ldc, ctr, L.splits, Pp, s);
+    float *a1 = reinterpret_cast<float *>(w + P.a_off);
+    float *b1 = reinterpret_cast<float *>(w + P.b_off);
+    float *Pp = reinterpret_cast<float *>(w + P.p_off);
+    unsigned int *ctr = reinterpret_cast<unsigned int *>(w + P.ctr_off);
+    const int64_t Kp = tc_kpad(K);
+    const bool a_kc = !is_n(transA), b_kc = is_n(transB);   // K contiguous in memory
+    TcOperands ops;
+    PackArgs pa, pb;
+    pa.X = A; pa.ld = lda; pa.R = M; pa.kcontig = a_kc; pa.b_side = false;
+    pb.X = B; pb.ld = ldb; pb.R = N; pb.kcontig = b_kc; pb.b_side = true;
+    if (P.direct) {
+        ops.a0 = TcPlane{A, lda, !a_kc, K};
+        ops.b0 = TcPlane{B, ldb, !b_kc, K};
+        if (P.pack_mode == PK_DSMALL_) {
+            ops.a1 = TcPlane{a1, P.lda1, !a_kc, K};
+            ops.b1 = TcPlane{b1, P.ldb1, !b_kc, K};
+        } else if (P.pack_mode == PK_DCROSS_) {
+            ops.a1 = TcPlane{a1, Kp, false, Kp};
+            ops.b1 = TcPlane{b1, Kp, false, Kp};
+        }
+        pa.out1 = a1; pa.ld1 = P.lda1;
+        pb.out1 = b1; pb.ld1 = P.ldb1;
+    } else {
+        // fallback: K-major planes [R][Kp]: plane 0 then plane 1 of each operand
+        const int pl = planes_of(math);
+        pa.out0 = a1; pa.ld0 = Kp; pa.out1 = a1 + (size_t)M * Kp; pa.ld1 = Kp;
+        pb.out0 = b1; pb.ld0 = Kp; pb.out1 = b1 + (size_t)N * Kp; pb.ld1 = Kp;
+        ops.a0 = TcPlane{pa.out0, Kp, false, Kp};
+        ops.b0 = TcPlane{pb.out0, Kp, false, Kp};
+        if (pl == 2) {
+            ops.a1 = TcPlane{pa.out1, Kp, false, Kp};
+            ops.b1 = TcPlane{pb.out1, Kp, false, Kp};
+        }
+    }
+    cudaError_t e = cudaSuccess;
+    if (P.pack_mode >= 0) e = launch_pack(P.pack_mode, pa, &pb, K, ctr, s);
+    else e = cudaMemsetAsync(ctr, 0, 128, s);
+    if (e == cudaSuccess) e = launch_tc_sgemm(P.terms, ops, M, N, K, alpha, beta, C, ldc, ctr, P.splits, Pp, s);
     if (own) {
         cudaError_t e2 = cudaFreeAsync(ws, s);
         if (e == cudaSuccess) e = e2;

@@ -23,27 +23,46 @@ void prof_begin(cudaStream_t s, bool is_gemm, cudaEvent_t *ev0);
 void prof_end(cudaStream_t s, bool is_gemm, cudaEvent_t ev0);
 
 // ---- tensor-core path (k_tc.cu) -----------------------------------------
-// Pack op(X) (R x K, logical) into `out` as `planes` K-major planes of
-// R x Kp floats (Kp = round_up(K, 32); zero-filled tail); plane 0 = big =
-// rn_tf32(x), plane 1 (if planes == 2) = small = rn_tf32(x - big).
-// kcontig: element (r, p) at X[p + r*ld]; else at X[r + p*ld].
-// mode: 0 = big plane only (1xTF32), 1 = + tf32 small plane (3xTF32),
-// 2 = + BF16 cross plane (TF32+BF16); see pack_store in k_tc.cu.
-cudaError_t launch_pack_split(const float *X, int64_t ld, bool kcontig, int64_t R, int64_t K, int64_t Kp,
-                              int mode, float *out, cudaStream_t s);
-// Both operands in one launch (B may be NULL); also zeroes *wave_ctr.
-// first_is_b: the first operand plays the B role (cross-plane half order).
-cudaError_t launch_pack_split2(const float *A, int64_t lda, bool a_kcontig, int64_t M, const float *B, int64_t ldb,
-                               bool b_kcontig, int64_t N, int64_t K, int64_t Kp, int mode, float *Aout, float *Bout,
-                               unsigned int *wave_ctr, cudaStream_t s, bool first_is_b = false);
-// C <- alpha * Ap * Bp^T + beta*C on the packed operands (tcgen05, 2-CTA,
-// persistent).  wave_ctr: 4 bytes of device scratch owned by this call, ZERO
-// when the kernel starts (launch_pack_split2 zeroes it), for the producers'
-// wave lockstep; NULL disables it.  splits > 1: split-K with raw partials in
+// One plane of an operand as the GEMM reads it through TMA: logical R x kext
+// (rows x K).  mn = false: K-major, element (r, p) at ptr[p + r*ld];
+// mn = true: MN-major, element (r, p) at ptr[r + p*ld].
+struct TcPlane {
+    const float *ptr = nullptr;
+    int64_t ld = 0;
+    bool mn = false;
+    int64_t kext = 0;
+};
+// plane 0 = big (the user array itself in the direct path), plane 1 = small
+// (3xTF32) or BF16 cross (TF32+BF16); plane 1 unused for 1xTF32.
+struct TcOperands {
+    TcPlane a0, a1, b0, b1;
+};
+
+// Arguments of the split pass for one operand (see the PK_* modes in k_tc.cu).
+struct PackArgs {
+    const float *X = nullptr;
+    int64_t ld = 0, R = 0;
+    bool kcontig = false;   // element (r, p) of op(X) at X[p + r*ld] (else X[r + p*ld])
+    float *out0 = nullptr;  // FULL modes: K-major big plane [R][ld0]
+    int64_t ld0 = 0;
+    float *out1 = nullptr;  // second plane
+    int64_t ld1 = 0;
+    bool b_side = false;    // B side of the cross operand (halves swapped)
+};
+enum { PK_FULL1_ = 0, PK_FULL3_ = 1, PK_FULLX_ = 2, PK_DSMALL_ = 3, PK_DCROSS_ = 4 };
+// One launch for A (and B if non-NULL); also zeroes the control block.
+cudaError_t launch_pack(int mode, const PackArgs &a, const PackArgs *b, int64_t K, unsigned int *ctrl,
+                        cudaStream_t s);
+// C <- alpha * op(A) op(B) + beta*C on the planes (tcgen05, 2-CTA,
+// persistent, PDL).  terms: 3 = 3xTF32, 2 = TF32+BF16, 1 = 1xTF32.
+// ctrl: per-call control block (word 0 = wave-lockstep counter), ZERO when
+// the kernel starts (launch_pack zeroes it; callers without a pack memset
+// it); NULL disables the lockstep.  splits > 1: split-K with raw partials in
 // `partial` (splits x M x N floats) and a fixed-order reduce launch.
-cudaError_t launch_tc_sgemm(int terms, const float *Ap, const float *Bp, int64_t M, int64_t N, int64_t Kp,
-                            float alpha, float beta, float *C, int64_t ldc, unsigned int *wave_ctr, int splits,
-                            float *partial, cudaStream_t s);
+cudaError_t launch_tc_sgemm(int terms, const TcOperands &ops, int64_t M, int64_t N, int64_t K, float alpha,
+                            float beta, float *C, int64_t ldc, unsigned int *ctrl, int splits, float *partial,
+                            cudaStream_t s);
+bool tma_legal(const void *ptr, int64_t ld);
 int64_t tc_kpad(int64_t K);
 int tc_splits(int64_t M, int64_t N, int64_t K);
 int tc_num_sms();

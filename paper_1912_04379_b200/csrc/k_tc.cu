@@ -1,15 +1,19 @@
-// k_tc.cu — the tensor-core SGEMM path for sm_100a (KN1 3xTF32, KN2 1xTF32)
-// and its operand re-buffering pass (KN4).
+// k_tc.cu — the tensor-core SGEMM path for sm_100a (KN1 3xTF32, KN2 1xTF32,
+// TF32+BF16) and its operand split pass (KN4).
 //
 // Paper → B200 mapping:
-//  * "Re-buffering: ... we deliberately buffer B' into L1 cache. By also
-//    re-ordering B to enforce optimal memory access patterns"
-//     and "padding with zeros" for K
-//    → pack_split_kernel: one pass that re-orders op(A) and op(B) into
-//    K-major, 1024-byte-friendly planes, zero-pads K to a multiple of 32 and
-//    splits each value into tf32 big/small parts (3xTF32).  Every trans /
-//    leading-dimension / alignment case becomes the same dense layout, so the
-//    main kernel has one TMA path.
+//  * The operands are read IN PLACE by TMA whenever their leading dimension
+//    is TMA-legal (16-byte strides, 16-byte aligned base): op(A) / op(B) are
+//    K-major or MN-major tiles depending on transA / transB, and the
+//    transpose lives in the TMA box + the UMMA descriptor's major mode, not
+//    in a copy.  The tensor core truncates FP32 inputs to TF32 (measured,
+//    DESIGN.md R7b), so the raw operand IS the "big" part; KN4 only writes
+//    the second plane (3xTF32: small = rn_tf32(x - trunc(x)) in the
+//    operand's own layout; TF32+BF16: the bf16 cross plane).
+//  * "Re-buffering ... re-ordering B" and "padding with
+//    zeros" for K survive as the FALLBACK for TMA-illegal
+//    leading dimensions (e.g. N = 333): KN4 re-orders both planes into
+//    K-major, 32-padded buffers.
 //  * L1 blocking + A' prefetch → TMA loads of
 //    128x32 K-major tiles into a multi-stage 128B-swizzled SMEM ring
 //    (mbarrier full/empty pairs), a producer warp running ahead.
@@ -48,36 +52,54 @@ int64_t tc_kpad(int64_t K) { return (K + TC_BK - 1) / TC_BK * TC_BK; }
 constexpr int TC_CTRL_WORDS = 32;
 
 // =====================================================================
-// KN4: re-buffer + split of BOTH operands in one launch (blockIdx.z = 0: A,
+// KN4: operand split pass, both operands in one launch (blockIdx.z = 0: A,
 // 1: B).  32x32 tiles, 256 threads.  Block (0,0,0) also zeroes the GEMM's
-// wave-lockstep counter (stream-ordered before the GEMM).
+// per-call control block (stream-ordered before the GEMM).
+//
+//   PK_FULL1  plane 0 = rn_tf32(x), K-major                (fallback 1xTF32)
+//   PK_FULL3  + plane 1 = rn_tf32(x - big), K-major       (fallback 3xTF32)
+//   PK_FULLX  + plane 1 = BF16 cross operand, K-major     (fallback TF32+BF16)
+//   PK_DSMALL plane 1 only = rn_tf32(x - trunc(x)) in the SOURCE layout
+//             (direct 3xTF32: the tensor core reads trunc(x) from the user array)
+//   PK_DCROSS plane 1 only = BF16 cross operand with big = trunc(x), K-major
+//             (direct TF32+BF16)
+// BF16 cross operand: for every group of 8 along K, 16 bf16 = [bf16(big) x8 |
+// bf16(x - big) x8] (A side) or the halves swapped (B side), so that ONE K16
+// BF16 MMA computes a_big*b_small + a_small*b_big.
+// Non-finite x: the second part is 0 (inf/NaN propagate through big*big).
 // =====================================================================
+enum { PK_FULL1 = PK_FULL1_, PK_FULL3 = PK_FULL3_, PK_FULLX = PK_FULLX_, PK_DSMALL = PK_DSMALL_, PK_DCROSS = PK_DCROSS_ };
+
 struct PackOperand {
     const float *X;
     int64_t ld, R;
     int kcontig;      // element (r, p) at X[p + r*ld] (1) or X[r + p*ld] (0)
-    float *out;       // planes x R x Kp
-    int raw_big;      // test hook (EMM_DEBUG_RAW_BIG): big = x unrounded
-    int cross_swap;   // MODE 2: per K8 group [bf16(lo) | bf16(hi)] instead of [hi | lo]
+    float *out0;      // FULL modes: big plane, K-major, row length ld0
+    int64_t ld0;
+    float *out1;      // second plane: K-major [R][ld1], or (PK_DSMALL, !kcontig) [K][ld1] MN-major
+    int64_t ld1;
+    int cross_swap;   // B side of the cross operand
+    int raw_big;      // test hook (EMM_DEBUG_RAW_BIG): FULL big = x unrounded
 };
 
-// MODE 0: plane 0 = big = rn_tf32(x).
-// MODE 1: + plane 1 = small = rn_tf32(x - big)                    (3xTF32)
-// MODE 2: + plane 1 = BF16 cross operand: for every group of 8 along K,
-//         16 bf16 = [bf16(big) x8 | bf16(x - big) x8] (A side) or the two
-//         halves swapped (B side), so that one K=16 BF16 MMA computes
-//         a_big*b_small + a_small*b_big                           (TF32+BF16)
+__device__ __forceinline__ float trunc_tf32(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+
 template <int MODE>
-__device__ __forceinline__ void pack_store(const PackOperand &op, float *__restrict__ out, int64_t plane, int64_t r,
-                                           int64_t p, int64_t Kp, float x) {
-    const uint32_t big = op.raw_big ? __float_as_uint(x) : cvt_tf32_rn(x);
-    out[r * Kp + p] = __uint_as_float(big);
-    const float lo = x - __uint_as_float(big);           // exact
-    if (MODE == 1) out[plane + r * Kp + p] = __uint_as_float(cvt_tf32_rn(lo));
-    if (MODE == 2) {
-        uint16_t *row = reinterpret_cast<uint16_t *>(out + plane + r * Kp);
+__device__ __forceinline__ void pack_store(const PackOperand &op, int64_t r, int64_t p, float x) {
+    const bool direct = MODE == PK_DSMALL || MODE == PK_DCROSS;
+    const float big = direct ? trunc_tf32(x) : (op.raw_big ? x : __uint_as_float(cvt_tf32_rn(x)));
+    const float lo = isfinite(x) ? x - big : 0.0f;                  // exact
+    if (!direct) op.out0[r * op.ld0 + p] = big;
+    if (MODE == PK_FULL3) op.out1[r * op.ld1 + p] = __uint_as_float(cvt_tf32_rn(lo));
+    if (MODE == PK_DSMALL) {
+        const float sm = __uint_as_float(cvt_tf32_rn(lo));
+        if (op.kcontig) op.out1[r * op.ld1 + p] = sm;
+        else op.out1[r + p * op.ld1] = sm;
+    }
+    if (MODE == PK_FULLX || MODE == PK_DCROSS) {
+        uint16_t *row = reinterpret_cast<uint16_t *>(op.out1 + r * op.ld1);
         const int64_t g = p >> 3, j = p & 7;
-        const uint16_t hb = __bfloat16_as_ushort(__float2bfloat16_rn(__uint_as_float(big)));
+        const uint16_t hb = __bfloat16_as_ushort(__float2bfloat16_rn(big));
         const uint16_t lb = __bfloat16_as_ushort(__float2bfloat16_rn(lo));
         row[g * 16 + j] = op.cross_swap ? lb : hb;
         row[g * 16 + 8 + j] = op.cross_swap ? hb : lb;
@@ -85,24 +107,22 @@ __device__ __forceinline__ void pack_store(const PackOperand &op, float *__restr
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(256) pack_split_kernel(PackOperand opA, PackOperand opB, int64_t K, int64_t Kp,
-                                                         unsigned int *wave_ctr) {
-    __shared__ float tile[32][33];
+__global__ void __launch_bounds__(256) pack_split_kernel(PackOperand opA, PackOperand opB, int64_t K, int64_t Kext,
+                                                         unsigned int *ctrl) {
     // Programmatic dependent launch: the GEMM may start its prologue (barrier
     // init, TMEM alloc, descriptor prefetch) now; it waits (griddepcontrol.
     // wait) for this grid's completion before its first operand load.
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    __shared__ float tile[32][33];
     const PackOperand &op = blockIdx.z == 0 ? opA : opB;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const int64_t r0 = (int64_t)blockIdx.x * 32;
     const int64_t k0 = (int64_t)blockIdx.y * 32;
-    if (wave_ctr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
-        for (int i = threadIdx.x; i < TC_CTRL_WORDS; i += blockDim.x) wave_ctr[i] = 0u;
+    if (ctrl && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
+        for (int i = threadIdx.x; i < TC_CTRL_WORDS; i += blockDim.x) ctrl[i] = 0u;
     if (r0 >= op.R) return;                               // block-uniform
     const float *__restrict__ X = op.X;
-    float *__restrict__ out = op.out;
     const int64_t R = op.R, ld = op.ld;
-    const int64_t plane = R * Kp;
     if (op.kcontig) {
         // (r, p) at X[p + r*ld]: read and write along p.
         float v[4];
@@ -114,10 +134,18 @@ __global__ void __launch_bounds__(256) pack_split_kernel(PackOperand opA, PackOp
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const int64_t r = r0 + ty + 8 * i, p = k0 + tx;
-            if (r < R) pack_store<MODE>(op, out, plane, r, p, Kp, v[i]);
+            if (r < R && p < Kext) pack_store<MODE>(op, r, p, v[i]);
+        }
+    } else if (MODE == PK_DSMALL) {
+        // (r, p) at X[r + p*ld] and the small plane in the same layout:
+        // elementwise, coalesced along r, no transpose.
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int64_t r = r0 + tx, p = k0 + ty + 8 * i;
+            if (r < R && p < K) pack_store<MODE>(op, r, p, __ldg(X + r + p * ld));
         }
     } else {
-        // (r, p) at X[r + p*ld]: read along r, transpose through smem.
+        // (r, p) at X[r + p*ld] into a K-major plane: transpose through smem.
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const int64_t r = r0 + tx, p = k0 + ty + 8 * i;
@@ -127,39 +155,44 @@ __global__ void __launch_bounds__(256) pack_split_kernel(PackOperand opA, PackOp
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const int64_t r = r0 + ty + 8 * i, p = k0 + tx;
-            if (r < R) pack_store<MODE>(op, out, plane, r, p, Kp, tile[tx][ty + 8 * i]);
+            if (r < R && p < Kext) pack_store<MODE>(op, r, p, tile[tx][ty + 8 * i]);
         }
     }
 }
 
-cudaError_t launch_pack_split2(const float *A, int64_t lda, bool a_kcontig, int64_t M, const float *B, int64_t ldb,
-                               bool b_kcontig, int64_t N, int64_t K, int64_t Kp, int mode, float *Aout, float *Bout,
-                               unsigned int *wave_ctr, cudaStream_t s, bool first_is_b) {
-    const int64_t R = M > N ? M : N;
-    const bool two = B != nullptr && N > 0;
-    dim3 grid((unsigned)((R + 31) / 32), (unsigned)(Kp / 32), two ? 2u : 1u);
-    if (grid.y > 65535 || (R + 31) / 32 > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+cudaError_t launch_pack(int mode, const PackArgs &a, const PackArgs *b, int64_t K, unsigned int *ctrl,
+                        cudaStream_t s) {
     // EMM_DEBUG_RAW_BIG=1 (tests only): hand the tensor core raw FP32 bits as
-    // the "big" part, to probe its TF32 input conversion (R7).
+    // the "big" part of the FULL modes, to probe its TF32 input conversion
+    // (R7b).
     static const int raw = [] {
         const char *e = getenv("EMM_DEBUG_RAW_BIG");
         return e && e[0] == '1' ? 1 : 0;
     }();
-    PackOperand a{A, lda, M, a_kcontig ? 1 : 0, Aout, raw, first_is_b ? 1 : 0};
-    PackOperand b{B, ldb, N, b_kcontig ? 1 : 0, Bout, raw, 1};
+    const bool dsmall = mode == PK_DSMALL;
+    const int64_t Kext = dsmall ? K : tc_kpad(K);        // FULL / cross planes are zero-padded to Kp
+    auto mk = [&](const PackArgs &x, bool b_side) {
+        PackOperand o{x.X, x.ld, x.R, x.kcontig ? 1 : 0, x.out0, x.ld0, x.out1, x.ld1, b_side ? 1 : 0, raw};
+        return o;
+    };
+    const PackOperand oa = mk(a, a.b_side);
+    const PackOperand ob = b ? mk(*b, true) : oa;
+    const int64_t R = b ? (a.R > b->R ? a.R : b->R) : a.R;
+    dim3 grid((unsigned)((R + 31) / 32), (unsigned)((Kext + 31) / 32), b ? 2u : 1u);
+    if (grid.y > 65535 || (R + 31) / 32 > 0x7fffffffLL || R <= 0 || Kext <= 0) return cudaErrorInvalidConfiguration;
     cudaEvent_t ev = nullptr;
     prof_begin(s, false, &ev);
-    if (mode == 2) pack_split_kernel<2><<<grid, 256, 0, s>>>(a, b, K, Kp, wave_ctr);
-    else if (mode == 1) pack_split_kernel<1><<<grid, 256, 0, s>>>(a, b, K, Kp, wave_ctr);
-    else pack_split_kernel<0><<<grid, 256, 0, s>>>(a, b, K, Kp, wave_ctr);
+    switch (mode) {
+        case PK_FULL1: pack_split_kernel<PK_FULL1><<<grid, 256, 0, s>>>(oa, ob, K, Kext, ctrl); break;
+        case PK_FULL3: pack_split_kernel<PK_FULL3><<<grid, 256, 0, s>>>(oa, ob, K, Kext, ctrl); break;
+        case PK_FULLX: pack_split_kernel<PK_FULLX><<<grid, 256, 0, s>>>(oa, ob, K, Kext, ctrl); break;
+        case PK_DSMALL: pack_split_kernel<PK_DSMALL><<<grid, 256, 0, s>>>(oa, ob, K, Kext, ctrl); break;
+        case PK_DCROSS: pack_split_kernel<PK_DCROSS><<<grid, 256, 0, s>>>(oa, ob, K, Kext, ctrl); break;
+        default: return cudaErrorInvalidValue;
+    }
     g_launches.fetch_add(1, std::memory_order_relaxed);
     prof_end(s, false, ev);
     return cudaGetLastError();
-}
-
-cudaError_t launch_pack_split(const float *X, int64_t ld, bool kcontig, int64_t R, int64_t K, int64_t Kp,
-                              int mode, float *out, cudaStream_t s) {
-    return launch_pack_split2(X, ld, kcontig, R, nullptr, 0, false, 0, K, Kp, mode, out, nullptr, nullptr, s, false);
 }
 
 // =====================================================================
@@ -183,7 +216,10 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float *__restr
 }
 
 // =====================================================================
-// KN1/KN2: tcgen05 GEMM on packed operands, CTA pair per 256x256 tile.
+// KN1/KN2: tcgen05 GEMM, CTA pair per 256x256 tile.  Four 2-D tensor maps:
+// A plane 0/1, B plane 0/1; plane 0 (big) and, for 3xTF32, plane 1 (small)
+// are K-major or MN-major per A_MN / B_MN; the TF32+BF16 cross plane is
+// always K-major.
 //
 // Accumulation precision (Q7, measured on B200): the tensor core
 // adds each MMA's result into the TMEM accumulator with truncation, which on
@@ -213,13 +249,16 @@ struct TcCfg {
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
 
-template <int TERMS>
+template <int TERMS, bool A_MN, bool B_MN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
-    tc_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
+    tc_sgemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
+                    const __grid_constant__ CUtensorMap tmB0, const __grid_constant__ CUtensorMap tmB1, int M, int N,
                     int Kp, float alpha, float beta, float *__restrict__ C, int64_t ldc, int tiles_m, int tiles_n,
                     int group_m, int kc_stages, unsigned int *__restrict__ wave_ctr, int splits,
                     float *__restrict__ partial) {
     using Cfg = TcCfg<TERMS>;
+    constexpr bool A1_MN = TERMS == 3 ? A_MN : false;   // cross planes are K-major
+    constexpr bool B1_MN = TERMS == 3 ? B_MN : false;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
@@ -272,8 +311,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
         fence_mbar_init();
     }
     if (warp == 0 && lane == 0) {
-        prefetch_tmap(&tmA);
-        prefetch_tmap(&tmB);
+        prefetch_tmap(&tmA0);
+        prefetch_tmap(&tmB0);
+        if (Cfg::PLANES == 2) {
+            prefetch_tmap(&tmA1);
+            prefetch_tmap(&tmB1);
+        }
     }
     if (warp == 1) tmem_alloc_2sm<TC_TMEM_COLS_P>(tmem_slot);
     tc_fence_before();
@@ -323,10 +366,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
                     const uint32_t fb = leader_full0 + (uint32_t)(s * sizeof(uint64_t));
                     if (rank == 0) mbar_arrive_expect_tx(&full[s], 2u * Cfg::STAGE_BYTES);
                     const uint32_t st = smem_u32(smem + s * Cfg::STAGE_BYTES);
+                    // a 128 (rows) x 32 (K) tile of one plane: one K-major box, or
+                    // four MN-major 32x32 boxes (transpose in the TMA box)
+                    auto load_plane = [&](const CUtensorMap *tm, uint32_t dst, int row0, bool mn) {
+                        if (mn) {
 #pragma unroll
-                    for (int p = 0; p < Cfg::PLANES; ++p) {
-                        tma_load_3d_2sm(st + p * TC_TILE_BYTES, &tmA, fb, kb * TC_BK, arow, p, pol);
-                        tma_load_3d_2sm(st + (Cfg::PLANES + p) * TC_TILE_BYTES, &tmB, fb, kb * TC_BK, brow, p, pol);
+                            for (int c = 0; c < 4; ++c)
+                                tma_load_2d_2sm(dst + c * 4096, tm, fb, row0 + 32 * c, kb * TC_BK, pol);
+                        } else {
+                            tma_load_2d_2sm(dst, tm, fb, kb * TC_BK, row0, pol);
+                        }
+                    };
+                    load_plane(&tmA0, st, arow, A_MN);
+                    load_plane(&tmB0, st + Cfg::PLANES * TC_TILE_BYTES, brow, B_MN);
+                    if (Cfg::PLANES == 2) {
+                        load_plane(&tmA1, st + TC_TILE_BYTES, arow, A1_MN);
+                        load_plane(&tmB1, st + 3 * TC_TILE_BYTES, brow, B1_MN);
                     }
                 }
                 if (wave_ctr) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(wave_ctr) : "memory");
@@ -335,7 +390,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
     } else if (warp == 1) {
         // ===== MMA issuer: one thread of the leader CTA drives the pair =====
         if (rank == 0 && lane == 0) {
-            constexpr uint32_t idesc = idesc_tf32<2 * TC_BM, TC_BN>();
+            constexpr uint32_t idesc = idesc_tf32_major<2 * TC_BM, TC_BN, A_MN, B_MN>();
+            // K8 step k of a plane: K-major advances 32 B inside the swizzle
+            // row, MN-major advances 8 K-rows = 1024 B
+            auto dsc = [](uint32_t addr, bool mn, int k) -> uint64_t {
+                return mn ? desc_mnmajor_sw128(addr + (uint32_t)(k * 1024)) : desc_kmajor_sw128(addr + (uint32_t)(k * 32));
+            };
             int it = 0, ch = 0;   // global stage / chunk counters (continue across tiles)
             for (int t = cid; t < total_units; t += nclus) {
                 int m0, n0, kb0, kb1, sp;
@@ -354,29 +414,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
                     mbar_wait(&full[s], ph);
                     tc_fence_after();
                     const uint32_t st = smem_u32(smem + s * Cfg::STAGE_BYTES);
-                    const uint64_t a_big = desc_kmajor_sw128(st);
-                    const uint64_t b_big = desc_kmajor_sw128(st + Cfg::PLANES * TC_TILE_BYTES);
+                    const uint32_t a0 = st, a1 = st + TC_TILE_BYTES;
+                    const uint32_t b0 = st + Cfg::PLANES * TC_TILE_BYTES, b1 = b0 + TC_TILE_BYTES;
 #pragma unroll
                     for (int k = 0; k < TC_BK / 8; ++k) {
-                        // advance 8 tf32 = 32 bytes along K inside the swizzle row
-                        const uint64_t koff = (uint64_t)((k * 32) >> 4);
                         const uint32_t acc0 = (first && k == 0) ? 0u : 1u;
                         if (TERMS == 3) {
-                            const uint64_t a_sml = desc_kmajor_sw128(st + TC_TILE_BYTES);
-                            const uint64_t b_sml = desc_kmajor_sw128(st + 3 * TC_TILE_BYTES);
                             // small terms first (they are the smaller magnitudes)
-                            mma_tf32_2sm(dt, a_sml + koff, b_big + koff, idesc, acc0);
-                            mma_tf32_2sm(dt, a_big + koff, b_sml + koff, idesc, 1u);
-                            mma_tf32_2sm(dt, a_big + koff, b_big + koff, idesc, 1u);
+                            mma_tf32_2sm(dt, dsc(a1, A1_MN, k), dsc(b0, B_MN, k), idesc, acc0);
+                            mma_tf32_2sm(dt, dsc(a0, A_MN, k), dsc(b1, B1_MN, k), idesc, 1u);
+                            mma_tf32_2sm(dt, dsc(a0, A_MN, k), dsc(b0, B_MN, k), idesc, 1u);
                         } else if (TERMS == 2) {
-                            // cross terms (K=16 bf16 = the same 32 bytes of the row)
+                            // cross terms: K=16 bf16 = the same 32 bytes of a K-major row
                             constexpr uint32_t idesc_x = idesc_bf16<2 * TC_BM, TC_BN>();
-                            const uint64_t a_x = desc_kmajor_sw128(st + TC_TILE_BYTES);
-                            const uint64_t b_x = desc_kmajor_sw128(st + 3 * TC_TILE_BYTES);
-                            mma_f16_2sm(dt, a_x + koff, b_x + koff, idesc_x, acc0);
-                            mma_tf32_2sm(dt, a_big + koff, b_big + koff, idesc, 1u);
+                            mma_f16_2sm(dt, dsc(a1, false, k), dsc(b1, false, k), idesc_x, acc0);
+                            mma_tf32_2sm(dt, dsc(a0, A_MN, k), dsc(b0, B_MN, k), idesc, 1u);
                         } else {
-                            mma_tf32_2sm(dt, a_big + koff, b_big + koff, idesc, acc0);
+                            mma_tf32_2sm(dt, dsc(a0, A_MN, k), dsc(b0, B_MN, k), idesc, acc0);
                         }
                     }
                     mma_commit_2sm_mc(&empty[s], (uint16_t)0x3);
@@ -486,19 +540,34 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
     return fn;
 }
 
-// planes x R x Kp FP32 (K-major), box 32 (K) x 128 (rows) x 1, 128B swizzle,
-// out-of-bounds rows read as zero.
-static bool make_tmap(CUtensorMap *tm, const float *base, int64_t R, int64_t Kp, int planes) {
+// One operand plane as a 2-D tensor map, 128B swizzle, out-of-bounds reads
+// zero (the M/N/K tails).  K-major: dims {kext, R}, box {32, 128}.
+// MN-major: dims {R, kext}, box {32, 32} (a 128-row tile is four boxes).
+static bool make_tmap(CUtensorMap *tm, const TcPlane &p, int64_t R) {
     auto enc = get_encode_fn();
-    if (!enc) return false;
-    cuuint64_t dims[3] = {(cuuint64_t)Kp, (cuuint64_t)R, (cuuint64_t)planes};
-    cuuint64_t strides[2] = {(cuuint64_t)Kp * 4, (cuuint64_t)R * (cuuint64_t)Kp * 4};
-    cuuint32_t box[3] = {(cuuint32_t)TC_BK, (cuuint32_t)TC_BM, 1};
-    cuuint32_t estr[3] = {1, 1, 1};
-    CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(base), dims, strides, box, estr,
+    if (!enc || !p.ptr) return false;
+    cuuint64_t dims[2], strides[1] = {(cuuint64_t)p.ld * 4};
+    cuuint32_t box[2], estr[2] = {1, 1};
+    if (p.mn) {
+        dims[0] = (cuuint64_t)R;
+        dims[1] = (cuuint64_t)p.kext;
+        box[0] = 32;
+        box[1] = (cuuint32_t)TC_BK;
+    } else {
+        dims[0] = (cuuint64_t)p.kext;
+        dims[1] = (cuuint64_t)R;
+        box[0] = (cuuint32_t)TC_BK;
+        box[1] = (cuuint32_t)TC_BM;
+    }
+    CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(p.ptr), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
+}
+
+bool tma_legal(const void *ptr, int64_t ld) {
+    return ptr && (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0 && ((ld * 4) & 15) == 0 && ld * 4 < (1LL << 40) &&
+           ld > 0;
 }
 
 int tc_num_sms() {
@@ -518,42 +587,42 @@ int tc_num_sms() {
 // split) units to fill the CTA pairs, each split >= 4 K-stages (128 of K).
 // units = tiles * S <= CTA pairs (one wave).
 int tc_splits(int64_t M, int64_t N, int64_t K) {
-    if (const char *e = getenv("EMM_SPLITS")) {   // experiments: force S (clamped below)
-        const int64_t tiles0 = ((M + 2 * TC_BM - 1) / (2 * TC_BM)) * ((N + TC_BN - 1) / TC_BN);
-        int64_t s = atoi(e);
-        const int64_t nkb0 = tc_kpad(K) / TC_BK;
-        if (s < 1) s = 1;
-        while (s > 1 && (tiles0 * s > tc_num_sms() / 2 || ((nkb0 + s - 1) / s) * (s - 1) >= nkb0)) --s;
-        return (int)s;
-    }
     const int64_t tiles = ((M + 2 * TC_BM - 1) / (2 * TC_BM)) * ((N + TC_BN - 1) / TC_BN);
     const int64_t nkb = tc_kpad(K) / TC_BK;
     const int64_t clusters = tc_num_sms() / 2;
-    if (tiles <= 0 || tiles * 2 > clusters) return 1;
-    int64_t s = clusters / tiles;
-    if (s > nkb / 4) s = nkb / 4;
-    if (s > 16) s = 16;
+    int64_t s;
+    if (const char *e = getenv("EMM_SPLITS")) {   // experiments: force S (clamped below)
+        s = atoi(e);
+    } else {
+        if (tiles <= 0 || tiles * 2 > clusters) return 1;
+        s = clusters / tiles;
+        if (s > nkb / 4) s = nkb / 4;
+        if (s > 16) s = 16;
+    }
     if (s < 1) s = 1;
-    // every split must own at least one stage
-    while (s > 1 && ((nkb + s - 1) / s) * (s - 1) >= nkb) --s;
+    while (s > 1 && (tiles * s > clusters || ((nkb + s - 1) / s) * (s - 1) >= nkb)) --s;
     return (int)s;
 }
 
-template <int TERMS>
-static cudaError_t launch_tc_t(const float *Ap, const float *Bp, int64_t M, int64_t N, int64_t Kp, float alpha,
-                               float beta, float *C, int64_t ldc, unsigned int *wave_ctr, int splits, float *partial,
-                               cudaStream_t s) {
+template <int TERMS, bool A_MN, bool B_MN>
+static cudaError_t launch_tc_t(const TcOperands &ops, int64_t M, int64_t N, int64_t Kp, float alpha, float beta,
+                               float *C, int64_t ldc, unsigned int *ctrl, int splits, float *partial, cudaStream_t s) {
     using Cfg = TcCfg<TERMS>;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(once, [] {
-        attr_err = cudaFuncSetAttribute(tc_sgemm_kernel<TERMS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        Cfg::SMEM_BYTES);
+        attr_err = cudaFuncSetAttribute(tc_sgemm_kernel<TERMS, A_MN, B_MN>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
     });
     if (attr_err != cudaSuccess) return attr_err;
-    CUtensorMap ta, tb;
-    if (!make_tmap(&ta, Ap, M, Kp, Cfg::PLANES) || !make_tmap(&tb, Bp, N, Kp, Cfg::PLANES))
-        return cudaErrorInvalidValue;
+    CUtensorMap ta0, ta1, tb0, tb1;
+    if (!make_tmap(&ta0, ops.a0, M) || !make_tmap(&tb0, ops.b0, N)) return cudaErrorInvalidValue;
+    if (Cfg::PLANES == 2) {
+        if (!make_tmap(&ta1, ops.a1, M) || !make_tmap(&tb1, ops.b1, N)) return cudaErrorInvalidValue;
+    } else {
+        ta1 = ta0;
+        tb1 = tb0;
+    }
     const int tiles_m = (int)((M + 2 * TC_BM - 1) / (2 * TC_BM));
     const int tiles_n = (int)((N + TC_BN - 1) / TC_BN);
     const int group_m = 8;
@@ -564,7 +633,7 @@ static cudaError_t launch_tc_t(const float *Ap, const float *Bp, int64_t M, int6
     const int64_t blocks = 2 * clusters;
     cudaEvent_t ev = nullptr;
     prof_begin(s, true, &ev);
-    // promotion chunk: 256 of K for 3xTF32 (8 stages), none for 1xTF32
+    // promotion chunk: 256 of K for the FP32-accurate splits (8 stages)
     const int kc_stages = TERMS >= 2 ? 256 / TC_BK : 0x3fffffff;
     {
         cudaLaunchConfig_t cfg{};
@@ -577,9 +646,9 @@ static cudaError_t launch_tc_t(const float *Ap, const float *Bp, int64_t M, int6
         at[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        cudaError_t le = cudaLaunchKernelEx(&cfg, tc_sgemm_kernel<TERMS>, ta, tb, (int)M, (int)N, (int)Kp, alpha, beta,
-                                            C, ldc, tiles_m, tiles_n, group_m, kc_stages, wave_ctr, splits,
-                                            splits > 1 ? partial : nullptr);
+        cudaError_t le = cudaLaunchKernelEx(&cfg, tc_sgemm_kernel<TERMS, A_MN, B_MN>, ta0, ta1, tb0, tb1, (int)M,
+                                            (int)N, (int)Kp, alpha, beta, C, ldc, tiles_m, tiles_n, group_m,
+                                            kc_stages, ctrl, splits, splits > 1 ? partial : nullptr);
         if (le != cudaSuccess) return le;
     }
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -607,14 +676,25 @@ static cudaError_t launch_tc_t(const float *Ap, const float *Bp, int64_t M, int6
     return cudaGetLastError();
 }
 
-cudaError_t launch_tc_sgemm(int terms, const float *Ap, const float *Bp, int64_t M, int64_t N, int64_t Kp,
-                            float alpha, float beta, float *C, int64_t ldc, unsigned int *wave_ctr, int splits,
-                            float *partial, cudaStream_t s) {
-    if (M > 0x7fffffffLL || N > 0x7fffffffLL || Kp > 0x7fffffffLL) return cudaErrorInvalidValue;
+template <int TERMS>
+static cudaError_t launch_tc_m(const TcOperands &ops, int64_t M, int64_t N, int64_t Kp, float alpha, float beta,
+                               float *C, int64_t ldc, unsigned int *ctrl, int splits, float *partial, cudaStream_t s) {
+    const bool am = ops.a0.mn, bm = ops.b0.mn;
+    if (!am && !bm) return launch_tc_t<TERMS, false, false>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s);
+    if (!am && bm) return launch_tc_t<TERMS, false, true>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s);
+    if (am && !bm) return launch_tc_t<TERMS, true, false>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s);
+    return launch_tc_t<TERMS, true, true>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s);
+}
+
+cudaError_t launch_tc_sgemm(int terms, const TcOperands &ops, int64_t M, int64_t N, int64_t K, float alpha,
+                            float beta, float *C, int64_t ldc, unsigned int *ctrl, int splits, float *partial,
+                            cudaStream_t s) {
+    if (M > 0x7fffffffLL || N > 0x7fffffffLL || K > 0x7fffffffLL - 32) return cudaErrorInvalidValue;
     if (splits < 1 || (splits > 1 && !partial)) return cudaErrorInvalidValue;
-    if (terms == 3) return launch_tc_t<3>(Ap, Bp, M, N, Kp, alpha, beta, C, ldc, wave_ctr, splits, partial, s);
-    if (terms == 2) return launch_tc_t<2>(Ap, Bp, M, N, Kp, alpha, beta, C, ldc, wave_ctr, splits, partial, s);
-    return launch_tc_t<1>(Ap, Bp, M, N, Kp, alpha, beta, C, ldc, wave_ctr, splits, partial, s);
+    const int64_t Kp = tc_kpad(K);
+    if (terms == 3) return launch_tc_m<3>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s);
+    if (terms == 2) return launch_tc_m<2>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s);
+    return launch_tc_m<1>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s);
 }
 
 }  // namespace emm

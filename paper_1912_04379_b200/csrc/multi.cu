@@ -159,40 +159,15 @@ extern "C" int emm_sgemm_multi(void *comm, char transA, char transB, int64_t M, 
     if (!st) st = cuda_st(cudaStreamWaitEvent(c->comm_stream, e0, 0));
     if (st) return st;
 
-    const bool nA = (transA == 'N' || transA == 'n');
     if ((st = check_args(transA, transB, rows, N, K, lda, ldb, ldc > 0 ? ldc : 1))) return st;
     if ((st = check_device())) return st;
-    const bool ab_used = !(alpha == 0.0f || K == 0);
-    const bool tc = math != EMM_MATH_FFMA && ab_used;
-    // Tensor-core paths: re-buffer/split this rank's A rows ONCE, then per
-    // B panel: wait for its broadcast, re-buffer the panel, GEMM.
-    void *ws = nullptr;
-    float *Ap = nullptr, *Bp = nullptr;
-    unsigned int *ctr = nullptr;
-    const int64_t Kp = tc_kpad(K);
-    const int planes = (math == EMM_MATH_3XTF32 || math == EMM_MATH_TF32_BF16) ? 2 : 1;
-    const int pmode = math == EMM_MATH_3XTF32 ? 1 : math == EMM_MATH_TF32_BF16 ? 2 : 0;
-    const int terms = math == EMM_MATH_3XTF32 ? 3 : math == EMM_MATH_TF32_BF16 ? 2 : 1;
     const int64_t panel = bN ? emm_multi_panel_cols(N) : N;
-    if (tc && rows > 0 && N > 0) {
-        const size_t a_bytes = align_up((size_t)planes * rows * Kp * 4, 1024);
-        const size_t b_bytes = align_up((size_t)planes * panel * Kp * 4, 1024);
-        if ((st = cuda_st(cudaMallocAsync(&ws, a_bytes + b_bytes + 1024, s)))) return st;
-        Ap = reinterpret_cast<float *>(ws);
-        Bp = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(ws) + a_bytes);
-        ctr = reinterpret_cast<unsigned int *>(reinterpret_cast<uint8_t *>(ws) + a_bytes + b_bytes);
-        st = cuda_st(launch_pack_split(A_local, lda, /*kcontig=*/!nA, rows, K, Kp, pmode, Ap, s));
-    }
+    // Each panel is one emm_sgemm_ex on the caller's stream (A read in place
+    // by TMA on the direct path; its small plane is re-derived per panel).
     auto panel_gemm = [&](const float *bp, int64_t nc, float *cp) -> int {
         if (rows == 0 || nc == 0) return 0;
-        if (!tc)   // FFMA, or alpha == 0 / K == 0 (C <- beta*C)
-            return emm_sgemm_ex(transA, transB, rows, nc, K, alpha, A_local, lda, bp, ldb, beta, cp, ldc, s, math,
-                                nullptr, 0);
-        cudaError_t e = launch_pack_split2(bp, ldb, /*kcontig=*/bN, nc, nullptr, 0, false, 0, K, Kp, pmode, Bp,
-                                           nullptr, ctr, s, /*first_is_b=*/true);
-        if (e == cudaSuccess)
-            e = launch_tc_sgemm(terms, Ap, Bp, rows, nc, Kp, alpha, beta, cp, ldc, ctr, 1, nullptr, s);
-        return cuda_st(e);
+        return emm_sgemm_ex(transA, transB, rows, nc, K, alpha, A_local, lda, bp, ldb, beta, cp, ldc, s, math, nullptr,
+                            0);
     };
 
     if (!st && bN && N > 0) {
@@ -217,10 +192,6 @@ extern "C" int emm_sgemm_multi(void *comm, char transA, char transB, int64_t M, 
         if (!st) st = cuda_st(cudaEventRecord(ev, c->comm_stream));
         if (!st) st = cuda_st(cudaStreamWaitEvent(s, ev, 0));
         if (!st) st = panel_gemm(B, N, C_local);
-    }
-    if (ws) {
-        int st2 = cuda_st(cudaFreeAsync(ws, s));
-        if (!st) st = st2;
     }
     if (st) return st;
 

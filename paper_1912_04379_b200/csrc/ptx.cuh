@@ -90,6 +90,15 @@ __device__ __forceinline__ void tma_load_3d_2sm(uint32_t smem_dst, const void *t
         "l"(reinterpret_cast<uint64_t>(tmap)), "r"(mbar_addr), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
         : "memory");
 }
+// 2-D tiled load (same completion semantics as above).
+__device__ __forceinline__ void tma_load_2d_2sm(uint32_t smem_dst, const void *tmap, uint32_t mbar_addr, int32_t c0,
+                                                int32_t c1, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_dst),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(mbar_addr), "r"(c0), "r"(c1), "l"(policy)
+        : "memory");
+}
 __device__ __forceinline__ uint64_t policy_evict_last() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
@@ -216,6 +225,30 @@ __device__ __forceinline__ uint64_t desc_kmajor_sw128(uint32_t smem_addr) {
     d |= (uint64_t)1u << 46;
     d |= (uint64_t)2u << 61;
     return d;
+}
+
+// Shared-memory matrix descriptor, MN-major, 128-byte swizzle, for a
+// 128 (MN) x 32 (K) FP32 tile stored as four 32x32 TMA boxes: each box is 32
+// K-rows of 128 B (32 MN-contiguous floats), boxes 4096 B apart.
+//   LBO (bits 16-29) = 4096 B: stride between 32-element MN chunks
+//   SBO (bits 32-45) = 1024 B: stride between 8-row K groups
+// One K8 MMA reads the 8 K-rows starting at `smem_addr` (advance 1024 B per K8).
+__device__ __forceinline__ uint64_t desc_mnmajor_sw128(uint32_t smem_addr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((smem_addr >> 4) & 0x3FFFu);
+    d |= (uint64_t)(4096u >> 4) << 16;
+    d |= (uint64_t)(1024u >> 4) << 32;
+    d |= (uint64_t)1u << 46;
+    d |= (uint64_t)2u << 61;
+    return d;
+}
+
+// Instruction descriptor, kind::tf32, FP32 accumulate, with A/B major modes
+// (bit 15 / bit 16: 0 = K-major, 1 = MN-major).
+template <int M, int N, bool A_MN, bool B_MN>
+__host__ __device__ constexpr uint32_t idesc_tf32_major() {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((A_MN ? 1u : 0u) << 15) | ((B_MN ? 1u : 0u) << 16) |
+           ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
 // Instruction descriptor, kind::tf32, FP32 accumulate, both operands K-major.

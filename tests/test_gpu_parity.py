@@ -153,6 +153,30 @@ def test_integer_exact_bitwise(emm, math, tA, tB, shape):
             f"max |diff| {np.max(np.abs(G - R))}"
 
 
+@pytest.mark.parametrize("force_pack", ["0", "1"])
+@pytest.mark.parametrize("math", ["3xtf32", "1xtf32", "tf32bf16"])
+@pytest.mark.parametrize("tA", ["N", "T"])
+@pytest.mark.parametrize("tB", ["N", "T"])
+def test_direct_and_repacked_paths(emm, monkeypatch, force_pack, math, tA, tB):
+    """TMA-legal leading dimensions take the direct path (operands read in
+    place, K- or MN-major per trans flag, transpose in the TMA box); with
+    EMM_FORCE_PACK=1 the same call takes the re-buffering fallback.  Both
+    must be bitwise exact on integer inputs and within tolerance on random
+    ones, including ragged M/N/K tails (M, N, K not multiples of 32/256)."""
+    monkeypatch.setenv("EMM_FORCE_PACK", force_pack)
+    for (M, N, K) in [(520, 388, 200), (260, 1000, 72)]:
+        case = Case(tA, tB, M, N, K, 1.0, -1.0, kind="ints", c_kind="ints", pad=(4, 8, 3))
+        R, S, T, _ = case.oracle()
+        Cg = case.run(emm, math)
+        case.check_untouched(Cg)
+        assert np.array_equal(case.logical(Cg), R.astype(np.float32).astype(np.float64))
+        case = Case(tA, tB, M, N, K, 0.75, 0.5, pad=(4, 0, 1))
+        R, S, T, _ = case.oracle()
+        Cg = case.run(emm, math)
+        case.check_untouched(Cg)
+        assert_close(case, Cg, R, S, T, TOL[math])
+
+
 def test_spec_worked_example_bitwise(emm):
     """tests/golden/spec_2x2.txt: [[1,2],[3,4]]·[[5,6],[7,8]] = [[19,22],[43,50]] (column-major)."""
     for math in MATHS:
