@@ -394,7 +394,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
             // K8 step k of a plane: K-major advances 32 B inside the swizzle
             // row, MN-major advances 8 K-rows = 1024 B
             auto dsc = [](uint32_t addr, bool mn, int k) -> uint64_t {
-                return mn ? desc_mnmajor_sw128(addr + (uint32_t)(k * 1024)) : desc_kmajor_sw128(addr + (uint32_t)(k * 32));
+                return mn ? desc_mnmajor_sw128_32b(addr + (uint32_t)(k * 1024)) : desc_kmajor_sw128(addr + (uint32_t)(k * 32));
             };
             int it = 0, ch = 0;   // global stage / chunk counters (continue across tiles)
             for (int t = cid; t < total_units; t += nclus) {
@@ -540,9 +540,10 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
     return fn;
 }
 
-// One operand plane as a 2-D tensor map, 128B swizzle, out-of-bounds reads
-// zero (the M/N/K tails).  K-major: dims {kext, R}, box {32, 128}.
-// MN-major: dims {R, kext}, box {32, 32} (a 128-row tile is four boxes).
+// One operand plane as a 2-D tensor map, out-of-bounds reads zero (the
+// M/N/K tails).  K-major: dims {kext, R}, box {32, 128}, 128B swizzle.
+// MN-major: dims {R, kext}, box {32, 32} (a 128-row tile is four boxes),
+// 128B swizzle with 32B atoms (the only MN-major TF32 UMMA layout).
 static bool make_tmap(CUtensorMap *tm, const TcPlane &p, int64_t R) {
     auto enc = get_encode_fn();
     if (!enc || !p.ptr) return false;
@@ -560,8 +561,9 @@ static bool make_tmap(CUtensorMap *tm, const TcPlane &p, int64_t R) {
         box[1] = (cuuint32_t)TC_BM;
     }
     CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(p.ptr), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                     CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     p.mn ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
 

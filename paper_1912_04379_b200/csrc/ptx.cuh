@@ -227,19 +227,22 @@ __device__ __forceinline__ uint64_t desc_kmajor_sw128(uint32_t smem_addr) {
     return d;
 }
 
-// Shared-memory matrix descriptor, MN-major, 128-byte swizzle, for a
-// 128 (MN) x 32 (K) FP32 tile stored as four 32x32 TMA boxes: each box is 32
-// K-rows of 128 B (32 MN-contiguous floats), boxes 4096 B apart.
+// Shared-memory matrix descriptor, MN-major, for a 128 (MN) x 32 (K) FP32
+// tile stored as four 32x32 TMA boxes (each 32 K-rows of 128 B = 32 MN-
+// contiguous floats, boxes 4096 B apart).  MN-major TF32 operands only exist
+// with the "128B swizzle, 32B atom" layout (layout type 1, TMA
+// CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B): 32-byte chunks XOR-swizzled inside
+// each 128-byte row, 4-row swizzle atoms.
 //   LBO (bits 16-29) = 4096 B: stride between 32-element MN chunks
-//   SBO (bits 32-45) = 1024 B: stride between 8-row K groups
+//   SBO (bits 32-45) =  512 B: stride between 4-row K groups
 // One K8 MMA reads the 8 K-rows starting at `smem_addr` (advance 1024 B per K8).
-__device__ __forceinline__ uint64_t desc_mnmajor_sw128(uint32_t smem_addr) {
+__device__ __forceinline__ uint64_t desc_mnmajor_sw128_32b(uint32_t smem_addr) {
     uint64_t d = 0;
     d |= (uint64_t)((smem_addr >> 4) & 0x3FFFu);
     d |= (uint64_t)(4096u >> 4) << 16;
-    d |= (uint64_t)(1024u >> 4) << 32;
+    d |= (uint64_t)(512u >> 4) << 32;
     d |= (uint64_t)1u << 46;
-    d |= (uint64_t)2u << 61;
+    d |= (uint64_t)1u << 61;
     return d;
 }
 
