@@ -49,6 +49,7 @@ def main():
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_sweep.jsonl"))
     ap.add_argument("--maths", default="3xtf32,tf32bf16,1xtf32,ffma")
     ap.add_argument("--only", default="")
+    ap.add_argument("--shape", default="", help="custom M,N,K,transA,transB (alpha=1, beta=0, uniform)")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
@@ -57,7 +58,12 @@ def main():
     pk = peaks()
     stream = torch.cuda.current_stream(dev)
     lines = []
-    for name, tA, tB, M, N, K, alpha, beta, pad, kind in configs():
+    cfgs = configs()
+    if args.shape:
+        m_, n_, k_, ta_, tb_ = args.shape.split(",")
+        cfgs = [(f"custom-{m_}x{n_}x{k_}-{ta_}{tb_}", ta_, tb_, int(m_), int(n_), int(k_), 1.0, 0.0, (0, 0, 0),
+                 "uniform")]
+    for name, tA, tB, M, N, K, alpha, beta, pad, kind in cfgs:
         if args.only and not name.startswith(args.only):
             continue
         ar, ac = (M, K) if tA == "N" else (K, M)
