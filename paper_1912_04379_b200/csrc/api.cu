@@ -138,6 +138,22 @@ struct Plan {
 
 static int64_t up4(int64_t v) { return (v + 3) / 4 * 4; }
 
+// Direct vs re-buffered, when both are possible (measured on
+// B200 back-to-back): the re-buffered big plane has its 13 low mantissa bits
+// zeroed, which lowers the GEMM's power draw and, under the 1 kW cap, buys
+// ~3-5% of clock on large square problems; the split pass costs
+// ~ (1/M + 1/N) of the GEMM time.  So re-buffer only when that pass is cheap.
+// EMM_FORCE_PACK=1 / EMM_FORCE_DIRECT=1 override (tests, experiments).
+static bool prefer_direct(int64_t M, int64_t N, emm_math_t math) {
+    const char *fp = getenv("EMM_FORCE_PACK");
+    if (fp && fp[0] == '1') return false;
+    const char *fd = getenv("EMM_FORCE_DIRECT");
+    if (fd && fd[0] == '1') return true;
+    const double f = 1.0 / (double)M + 1.0 / (double)N;
+    const double thr = math == EMM_MATH_1XTF32 ? 1.0e-4 : 2.9e-4;
+    return f > thr;
+}
+
 static Plan make_plan(char tA, char tB, int64_t M, int64_t N, int64_t K, emm_math_t math, bool direct) {
     Plan P;
     P.terms = terms_of(math);
@@ -224,9 +240,7 @@ extern "C" int emm_sgemm_ex(char transA, char transB, int64_t M, int64_t N, int6
             launch_ffma_sgemm(!is_n(transA), !is_n(transB), M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, s));
 
     // tensor-core paths
-    const char *fp = getenv("EMM_FORCE_PACK");   // tests / experiments: force the fallback
-    const bool force_pack = fp && fp[0] == '1';
-    const bool direct = !force_pack && tma_legal(A, lda) && tma_legal(B, ldb);
+    const bool direct = tma_legal(A, lda) && tma_legal(B, ldb) && prefer_direct(M, N, math);
     const Plan P = make_plan(transA, transB, M, N, K, math, direct);
     void *ws = workspace;
     bool own = false;

@@ -164,6 +164,7 @@ def test_direct_and_repacked_paths(emm, monkeypatch, force_pack, math, tA, tB):
     must be bitwise exact on integer inputs and within tolerance on random
     ones, including ragged M/N/K tails (M, N, K not multiples of 32/256)."""
     monkeypatch.setenv("EMM_FORCE_PACK", force_pack)
+    monkeypatch.setenv("EMM_FORCE_DIRECT", "1" if force_pack == "0" else "0")
     for (M, N, K) in [(520, 388, 200), (260, 1000, 72)]:
         case = Case(tA, tB, M, N, K, 1.0, -1.0, kind="ints", c_kind="ints", pad=(4, 8, 3))
         R, S, T, _ = case.oracle()
