@@ -40,6 +40,9 @@ def configs():
             out.append((f"c3-{tA}{tB}", tA, tB, 1531, 997, 2049, -0.75, 1.25, (13, 7, 5), "normal"))
     out.append(("c4-i", "N", "T", 65536, 1024, 4096, 1.0, 1.0, (0, 0, 0), "normal"))
     out.append(("c4-ii", "N", "T", 65536, 4096, 1024, 1.0, 1.0, (0, 0, 0), "normal"))
+    # skinny / memory-bound (not a BASELINE.json config): GB/s is the metric
+    out.append(("c6-skinny-N16", "N", "N", 65536, 16, 4096, 1.0, 0.0, (0, 0, 0), "uniform"))
+    out.append(("c6-skinny-M8", "N", "N", 8, 65536, 4096, 1.0, 0.0, (0, 0, 0), "uniform"))
     return out
 
 

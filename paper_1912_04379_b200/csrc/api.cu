@@ -138,6 +138,11 @@ struct Plan {
 
 static int64_t up4(int64_t v) { return (v + 3) / 4 * 4; }
 
+static bool env_on(const char *name) {
+    const char *e = getenv(name);
+    return e && e[0] == '1';
+}
+
 // Direct vs re-buffered, when both are possible (measured on
 // B200 back-to-back): the re-buffered big plane has its 13 low mantissa bits
 // zeroed, which lowers the GEMM's power draw and, under the 1 kW cap, buys
@@ -194,6 +199,7 @@ static Plan make_plan(char tA, char tB, int64_t M, int64_t N, int64_t K, emm_mat
 
 static size_t ws_bytes(int64_t M, int64_t N, int64_t K, emm_math_t math) {
     if (math == EMM_MATH_FFMA || M == 0 || N == 0 || K == 0 || small_problem(M, N, K)) return 0;
+    if (M <= SKINNY_MAX || N <= SKINNY_MAX) return 0;
     return make_plan('N', 'N', M, N, K, math, /*direct=*/false).total;
 }
 
@@ -234,6 +240,10 @@ extern "C" int emm_sgemm_ex(char transA, char transB, int64_t M, int64_t N, int6
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
 
     if (!ab_used) return cuda_status(launch_scale_c(M, N, beta, C, ldc, s));
+
+    if ((M <= SKINNY_MAX || N <= SKINNY_MAX) && !env_on("EMM_NO_SKINNY"))
+        return cuda_status(
+            launch_skinny_sgemm(!is_n(transA), !is_n(transB), M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, s));
 
     if (math == EMM_MATH_FFMA || small_problem(M, N, K))
         return cuda_status(

@@ -1,0 +1,165 @@
+// k_skinny.cu — KN9: skinny / memory-bound SGEMM.
+//
+// When one output dimension is tiny (N <= 16, or M <= 16 after an operand-
+// role swap C^T = op(B)^T op(A)^T), the GEMM moves 4 bytes of the long
+// operand per 2*N flops: arithmetic intensity ~N/2 flop/B, below the FP32 and
+// tensor ridge points, so HBM bandwidth is the roofline and every byte of the
+// long operand must be read exactly once.  The paper's own observation that
+// "performance is better if buffering occurs on the matrix with the largest
+// non-common dimension" becomes: keep the SMALL operand
+// (B', K x N') resident in shared memory and stream the large one through
+// registers, one row of C per thread, coalesced.
+//
+// Arithmetic: FP32 FFMA in increasing k, with the partial sums promoted into
+// a master accumulator every 256 of K (as KN3, R13), so every math
+// mode gets the FP32-accurate bound.  Deterministic (no atomics).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "emm_internal.h"
+
+namespace emm {
+
+constexpr int SK_ROWS = 256;    // rows of C' per CTA (one per thread)
+constexpr int SK_KC = 32;       // K per staged chunk
+constexpr int SK_PROMOTE = 8;   // chunks per promotion (256 of K)
+
+// C'(r, c) = alpha * sum_p A'(r, p) B'(p, c) + beta * C'(r, c),  r < Mr, c < Nc <= NC
+//   A'(r, p) at Ap[r + p*lda] (!TA) or Ap[p + r*lda] (TA)
+//   B'(p, c) at Bp[p + c*ldb] (!TB) or Bp[c + p*ldb] (TB)
+//   C'(r, c) at C[r*rs + c*cs]
+template <bool TA, bool TB, int NC>
+__global__ void __launch_bounds__(SK_ROWS) skinny_sgemm_kernel(int64_t Mr, int Nc, int64_t K, float alpha,
+                                                               const float *__restrict__ Ap, int64_t lda,
+                                                               const float *__restrict__ Bp, int64_t ldb, float beta,
+                                                               float *__restrict__ C, int64_t rs, int64_t cs) {
+    __shared__ __align__(16) float Bs[SK_KC][NC];
+    __shared__ float As[TA ? SK_ROWS : 1][TA ? SK_KC + 1 : 1];
+    const int tid = threadIdx.x;
+    const int64_t r0 = (int64_t)blockIdx.x * SK_ROWS;
+    const int64_t row = r0 + tid;
+    const bool row_ok = row < Mr;
+    float acc[NC], master[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) acc[c] = master[c] = 0.0f;
+
+    const int64_t nchunks = (K + SK_KC - 1) / SK_KC;
+    float a_next[SK_KC];
+    auto load_a = [&](int64_t k0) {
+        if (!TA) {
+            // A'(row, p) = Ap[row + p*lda]: consecutive threads, consecutive rows
+#pragma unroll
+            for (int p = 0; p < SK_KC; ++p)
+                a_next[p] = (row_ok && k0 + p < K) ? __ldcs(Ap + row + (k0 + p) * lda) : 0.0f;
+        } else {
+            // A'(r, p) = Ap[p + r*lda]: warp reads 32 consecutive p of one row
+#pragma unroll
+            for (int i = 0; i < SK_KC; ++i) {
+                const int64_t r = r0 + (tid >> 5) + 8 * i;
+                const int64_t p = k0 + (tid & 31);
+                a_next[i] = (r < Mr && p < K) ? __ldcs(Ap + p + r * lda) : 0.0f;
+            }
+        }
+    };
+    load_a(0);
+    for (int64_t ch = 0; ch < nchunks; ++ch) {
+        const int64_t k0 = ch * SK_KC;
+        __syncthreads();   // previous chunk's Bs / As reads done
+        for (int e = tid; e < SK_KC * NC; e += SK_ROWS) {
+            const int p = TB ? e / NC : e % SK_KC;
+            const int c = TB ? e % NC : e / SK_KC;
+            const int64_t kk = k0 + p;
+            Bs[p][c] = (kk < K && c < Nc) ? __ldg(TB ? Bp + c + kk * ldb : Bp + kk + (int64_t)c * ldb) : 0.0f;
+        }
+        float a_cur[SK_KC];
+        if (!TA) {
+#pragma unroll
+            for (int p = 0; p < SK_KC; ++p) a_cur[p] = a_next[p];
+        } else {
+#pragma unroll
+            for (int i = 0; i < SK_KC; ++i) As[(tid >> 5) + 8 * i][tid & 31] = a_next[i];
+        }
+        __syncthreads();
+        if (ch + 1 < nchunks) load_a(k0 + SK_KC);   // stream the next chunk while computing this one
+#pragma unroll
+        for (int p = 0; p < SK_KC; ++p) {
+            const float a = TA ? As[tid][p] : a_cur[p];
+#pragma unroll
+            for (int c = 0; c < NC; c += 4) {
+                const float4 b = *reinterpret_cast<const float4 *>(&Bs[p][c]);
+                acc[c] = fmaf(a, b.x, acc[c]);
+                acc[c + 1] = fmaf(a, b.y, acc[c + 1]);
+                acc[c + 2] = fmaf(a, b.z, acc[c + 2]);
+                acc[c + 3] = fmaf(a, b.w, acc[c + 3]);
+            }
+        }
+        if ((ch + 1) % SK_PROMOTE == 0 || ch + 1 == nchunks) {
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                master[c] += acc[c];
+                acc[c] = 0.0f;
+            }
+        }
+    }
+    if (!row_ok) return;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        if (c < Nc) {
+            float *d = C + row * rs + (int64_t)c * cs;
+            *d = beta == 0.0f ? alpha * master[c] : fmaf(beta, *d, alpha * master[c]);
+        }
+    }
+}
+
+template <bool TA, bool TB>
+static cudaError_t launch_nc(int64_t Mr, int Nc, int64_t K, float alpha, const float *Ap, int64_t lda,
+                             const float *Bp, int64_t ldb, float beta, float *C, int64_t rs, int64_t cs,
+                             cudaStream_t s) {
+    const dim3 grid((unsigned)((Mr + SK_ROWS - 1) / SK_ROWS));
+    if (Nc <= 4)
+        skinny_sgemm_kernel<TA, TB, 4><<<grid, SK_ROWS, 0, s>>>(Mr, Nc, K, alpha, Ap, lda, Bp, ldb, beta, C, rs, cs);
+    else if (Nc <= 8)
+        skinny_sgemm_kernel<TA, TB, 8><<<grid, SK_ROWS, 0, s>>>(Mr, Nc, K, alpha, Ap, lda, Bp, ldb, beta, C, rs, cs);
+    else
+        skinny_sgemm_kernel<TA, TB, 16><<<grid, SK_ROWS, 0, s>>>(Mr, Nc, K, alpha, Ap, lda, Bp, ldb, beta, C, rs, cs);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_skinny_sgemm(bool tA, bool tB, int64_t M, int64_t N, int64_t K, float alpha, const float *A,
+                                int64_t lda, const float *B, int64_t ldb, float beta, float *C, int64_t ldc,
+                                cudaStream_t s) {
+    // Roles: the long output dimension is streamed (rows of C'), the short one
+    // (<= SKINNY_MAX) is resident.  N short: C' = C, A' = op(A), B' = op(B).
+    // M short: C' = C^T = op(B)^T op(A)^T, A' = op(B)^T, B' = op(A)^T.
+    bool TA, TB;
+    int64_t Mr, lda2, ldb2, rs, cs;
+    int Nc;
+    const float *Ap, *Bp;
+    if (N <= SKINNY_MAX) {
+        Mr = M; Nc = (int)N;
+        Ap = A; lda2 = lda; TA = tA;          // op(A)(r,p): tA ? A[p + r*lda] : A[r + p*lda]
+        Bp = B; ldb2 = ldb; TB = tB;          // op(B)(p,c): tB ? B[c + p*ldb] : B[p + c*ldb]
+        rs = 1; cs = ldc;
+    } else {
+        Mr = N; Nc = (int)M;
+        // A'(r,p) = op(B)(p,r): tB ? B[r + p*ldb] (r contiguous: !TA) : B[p + r*ldb] (TA)
+        Ap = B; lda2 = ldb; TA = !tB;
+        // B'(p,c) = op(A)(c,p): tA ? A[p + c*lda] (!TB form) : A[c + p*lda] (TB form)
+        Bp = A; ldb2 = lda; TB = !tA;
+        rs = ldc; cs = 1;
+    }
+    if ((Mr + SK_ROWS - 1) / SK_ROWS > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+    cudaEvent_t ev = nullptr;
+    prof_begin(s, true, &ev);
+    cudaError_t e;
+    if (!TA && !TB) e = launch_nc<false, false>(Mr, Nc, K, alpha, Ap, lda2, Bp, ldb2, beta, C, rs, cs, s);
+    else if (!TA && TB) e = launch_nc<false, true>(Mr, Nc, K, alpha, Ap, lda2, Bp, ldb2, beta, C, rs, cs, s);
+    else if (TA && !TB) e = launch_nc<true, false>(Mr, Nc, K, alpha, Ap, lda2, Bp, ldb2, beta, C, rs, cs, s);
+    else e = launch_nc<true, true>(Mr, Nc, K, alpha, Ap, lda2, Bp, ldb2, beta, C, rs, cs, s);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    prof_end(s, true, ev);
+    return e;
+}
+
+}  // namespace emm

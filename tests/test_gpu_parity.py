@@ -178,6 +178,26 @@ def test_direct_and_repacked_paths(emm, monkeypatch, force_pack, math, tA, tB):
         assert_close(case, Cg, R, S, T, TOL[math])
 
 
+@pytest.mark.parametrize("math", MATHS)
+@pytest.mark.parametrize("tA", ["N", "T"])
+@pytest.mark.parametrize("tB", ["N", "T"])
+@pytest.mark.parametrize("shape", [(20000, 16, 700), (5003, 3, 1000), (9, 30001, 300), (16, 7000, 257)])
+def test_skinny_path(emm, math, tA, tB, shape):
+    """min(M, N) <= 16: the streaming kernel (operand-role swap when M is the
+    short side); bitwise on integers, FP32-accurate on random data for every
+    requested mode, ldc padding untouched."""
+    M, N, K = shape
+    case = cached_case(tA, tB, M, N, K, 1.0, 2.0, kind="ints", c_kind="ints", pad=(1, 2, 3))
+    R, S, T, _ = case.oracle()
+    Cg = case.run(emm, math)
+    case.check_untouched(Cg)
+    assert np.array_equal(case.logical(Cg), R.astype(np.float32).astype(np.float64))
+    case = cached_case(tA, tB, M, N, K, -0.5, 0.25, pad=(0, 1, 0))
+    R, S, T, _ = case.oracle()
+    Cg = case.run(emm, math)
+    assert_close(case, Cg, R, S, T, 1e-5)
+
+
 def test_spec_worked_example_bitwise(emm):
     """tests/golden/spec_2x2.txt: [[1,2],[3,4]]·[[5,6],[7,8]] = [[19,22],[43,50]] (column-major)."""
     for math in MATHS:
@@ -261,9 +281,11 @@ def test_k_tails(emm, math, K):
     assert_close(case, Cg, R, S, T, TOL[math])
 
 
+@pytest.mark.parametrize("no_skinny", ["0", "1"])
 @pytest.mark.parametrize("math", MATHS)
 @pytest.mark.parametrize("mn", [(1, 1), (1, 300), (300, 1), (7, 5), (127, 129), (255, 257), (256, 256)])
-def test_mn_edges(emm, math, mn):
+def test_mn_edges(emm, monkeypatch, no_skinny, math, mn):
+    monkeypatch.setenv("EMM_NO_SKINNY", no_skinny)
     M, N = mn
     for tA, tB in (("N", "N"), ("T", "T")):
         case = Case(tA, tB, M, N, 77, -0.75, 1.25, pad=(3, 0, 3))
