@@ -21,7 +21,8 @@
 
 namespace emm {
 
-constexpr int SK_ROWS = 256;    // rows of C' per CTA (one per thread)
+constexpr int SK_ROWS = 128;    // rows of C' per CTA (one per thread)
+constexpr int SK_WARPS = SK_ROWS / 32;
 constexpr int SK_KC = 32;       // K per staged chunk
 constexpr int SK_PROMOTE = 8;   // chunks per promotion (256 of K)
 
@@ -34,8 +35,10 @@ __global__ void __launch_bounds__(SK_ROWS) skinny_sgemm_kernel(int64_t Mr, int N
                                                                const float *__restrict__ Ap, int64_t lda,
                                                                const float *__restrict__ Bp, int64_t ldb, float beta,
                                                                float *__restrict__ C, int64_t rs, int64_t cs) {
-    __shared__ __align__(16) float Bs[SK_KC][NC];
-    __shared__ float As[TA ? SK_ROWS : 1][TA ? SK_KC + 1 : 1];
+    constexpr int BPT = SK_KC * NC / SK_ROWS;   // B' elements staged per thread per chunk (>= 1 when NC >= 8)
+    constexpr int BPT1 = BPT > 0 ? BPT : 1;
+    __shared__ __align__(16) float Bs[2][SK_KC][NC];
+    __shared__ float As[TA ? SK_ROWS : 1][TA ? SK_KC + 1 : 1];   // TA: single buffer (34 KB)
     const int tid = threadIdx.x;
     const int64_t r0 = (int64_t)blockIdx.x * SK_ROWS;
     const int64_t row = r0 + tid;
@@ -45,62 +48,82 @@ __global__ void __launch_bounds__(SK_ROWS) skinny_sgemm_kernel(int64_t Mr, int N
     for (int c = 0; c < NC; ++c) acc[c] = master[c] = 0.0f;
 
     const int64_t nchunks = (K + SK_KC - 1) / SK_KC;
-    float a_next[SK_KC];
-    auto load_a = [&](int64_t k0) {
+    float a_next[SK_KC], b_next[BPT1];
+    // Chunk ch of A' (this thread's row, or for TA a 32-wide slice of 32 rows)
+    // and of B' (BPT elements) into registers: the loads of chunk ch+1 are in
+    // flight while chunk ch is computed.
+    auto load = [&](int64_t k0) {
         if (!TA) {
-            // A'(row, p) = Ap[row + p*lda]: consecutive threads, consecutive rows
 #pragma unroll
             for (int p = 0; p < SK_KC; ++p)
                 a_next[p] = (row_ok && k0 + p < K) ? __ldcs(Ap + row + (k0 + p) * lda) : 0.0f;
         } else {
-            // A'(r, p) = Ap[p + r*lda]: warp reads 32 consecutive p of one row
 #pragma unroll
             for (int i = 0; i < SK_KC; ++i) {
-                const int64_t r = r0 + (tid >> 5) + 8 * i;
+                const int64_t r = r0 + (tid >> 5) + SK_WARPS * i;
                 const int64_t p = k0 + (tid & 31);
                 a_next[i] = (r < Mr && p < K) ? __ldcs(Ap + p + r * lda) : 0.0f;
             }
         }
-    };
-    load_a(0);
-    for (int64_t ch = 0; ch < nchunks; ++ch) {
-        const int64_t k0 = ch * SK_KC;
-        __syncthreads();   // previous chunk's Bs / As reads done
-        for (int e = tid; e < SK_KC * NC; e += SK_ROWS) {
+#pragma unroll
+        for (int i = 0; i < BPT1; ++i) {
+            const int e = tid + i * SK_ROWS;
             const int p = TB ? e / NC : e % SK_KC;
             const int c = TB ? e % NC : e / SK_KC;
             const int64_t kk = k0 + p;
-            Bs[p][c] = (kk < K && c < Nc) ? __ldg(TB ? Bp + c + kk * ldb : Bp + kk + (int64_t)c * ldb) : 0.0f;
+            b_next[i] = (e < SK_KC * NC && kk < K && c < Nc)
+                            ? __ldg(TB ? Bp + c + kk * ldb : Bp + kk + (int64_t)c * ldb) : 0.0f;
         }
+    };
+    auto stage = [&](int buf) {   // registers -> shared buffer `buf`
+#pragma unroll
+        for (int i = 0; i < BPT1; ++i) {
+            const int e = tid + i * SK_ROWS;
+            if (e < SK_KC * NC) {
+                const int p = TB ? e / NC : e % SK_KC;
+                const int c = TB ? e % NC : e / SK_KC;
+                Bs[buf][p][c] = b_next[i];
+            }
+        }
+        if (TA) {
+#pragma unroll
+            for (int i = 0; i < SK_KC; ++i) As[(tid >> 5) + SK_WARPS * i][tid & 31] = a_next[i];
+        }
+    };
+    load(0);
+    stage(0);
+    __syncthreads();
+    for (int64_t ch = 0; ch < nchunks; ++ch) {
+        const int buf = (int)(ch & 1);
         float a_cur[SK_KC];
         if (!TA) {
 #pragma unroll
             for (int p = 0; p < SK_KC; ++p) a_cur[p] = a_next[p];
-        } else {
-#pragma unroll
-            for (int i = 0; i < SK_KC; ++i) As[(tid >> 5) + 8 * i][tid & 31] = a_next[i];
         }
-        __syncthreads();
-        if (ch + 1 < nchunks) load_a(k0 + SK_KC);   // stream the next chunk while computing this one
+        const bool more = ch + 1 < nchunks;
+        if (more) load((ch + 1) * SK_KC);   // stream the next chunk while computing this one
 #pragma unroll
         for (int p = 0; p < SK_KC; ++p) {
             const float a = TA ? As[tid][p] : a_cur[p];
 #pragma unroll
             for (int c = 0; c < NC; c += 4) {
-                const float4 b = *reinterpret_cast<const float4 *>(&Bs[p][c]);
+                const float4 b = *reinterpret_cast<const float4 *>(&Bs[buf][p][c]);
                 acc[c] = fmaf(a, b.x, acc[c]);
                 acc[c + 1] = fmaf(a, b.y, acc[c + 1]);
                 acc[c + 2] = fmaf(a, b.z, acc[c + 2]);
                 acc[c + 3] = fmaf(a, b.w, acc[c + 3]);
             }
         }
-        if ((ch + 1) % SK_PROMOTE == 0 || ch + 1 == nchunks) {
+        if ((ch + 1) % SK_PROMOTE == 0 || !more) {
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
                 master[c] += acc[c];
                 acc[c] = 0.0f;
             }
         }
+        if (TA) __syncthreads();    // single As buffer: everyone done reading chunk ch
+        if (more) stage(buf ^ 1);   // Bs: the other buffer (last read in chunk ch-1, before the barrier)
+        __syncthreads();
     }
     if (!row_ok) return;
 #pragma unroll
