@@ -16,25 +16,25 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "emm_internal.h"
 
 namespace emm {
 
-constexpr int SK_ROWS = 128;    // rows of C' per CTA (one per thread)
-constexpr int SK_WARPS = SK_ROWS / 32;
-constexpr int SK_KC = 32;       // K per staged chunk
-constexpr int SK_PROMOTE = 8;   // chunks per promotion (256 of K)
+// ROWS: rows of C' per CTA (one per thread); KC: K per staged chunk.
 
 // C'(r, c) = alpha * sum_p A'(r, p) B'(p, c) + beta * C'(r, c),  r < Mr, c < Nc <= NC
 //   A'(r, p) at Ap[r + p*lda] (!TA) or Ap[p + r*lda] (TA)
 //   B'(p, c) at Bp[p + c*ldb] (!TB) or Bp[c + p*ldb] (TB)
 //   C'(r, c) at C[r*rs + c*cs]
-template <bool TA, bool TB, int NC>
+template <bool TA, bool TB, int NC, int SK_ROWS, int SK_KC>
 __global__ void __launch_bounds__(SK_ROWS) skinny_sgemm_kernel(int64_t Mr, int Nc, int64_t K, float alpha,
                                                                const float *__restrict__ Ap, int64_t lda,
                                                                const float *__restrict__ Bp, int64_t ldb, float beta,
                                                                float *__restrict__ C, int64_t rs, int64_t cs) {
+    constexpr int SK_WARPS = SK_ROWS / 32;
+    constexpr int SK_PROMOTE = 256 / SK_KC;     // chunks per promotion (256 of K)
     constexpr int BPT = SK_KC * NC / SK_ROWS;   // B' elements staged per thread per chunk (>= 1 when NC >= 8)
     constexpr int BPT1 = BPT > 0 ? BPT : 1;
     __shared__ __align__(16) float Bs[2][SK_KC][NC];
@@ -135,18 +135,36 @@ __global__ void __launch_bounds__(SK_ROWS) skinny_sgemm_kernel(int64_t Mr, int N
     }
 }
 
+template <bool TA, bool TB, int ROWS, int KC>
+static cudaError_t launch_cfg(int64_t Mr, int Nc, int64_t K, float alpha, const float *Ap, int64_t lda,
+                             const float *Bp, int64_t ldb, float beta, float *C, int64_t rs, int64_t cs,
+                             cudaStream_t s) {
+    const dim3 grid((unsigned)((Mr + ROWS - 1) / ROWS));
+    if (Nc <= 4)
+        skinny_sgemm_kernel<TA, TB, 4, ROWS, KC><<<grid, ROWS, 0, s>>>(Mr, Nc, K, alpha, Ap, lda, Bp, ldb, beta, C,
+                                                                        rs, cs);
+    else if (Nc <= 8)
+        skinny_sgemm_kernel<TA, TB, 8, ROWS, KC><<<grid, ROWS, 0, s>>>(Mr, Nc, K, alpha, Ap, lda, Bp, ldb, beta, C,
+                                                                        rs, cs);
+    else
+        skinny_sgemm_kernel<TA, TB, 16, ROWS, KC><<<grid, ROWS, 0, s>>>(Mr, Nc, K, alpha, Ap, lda, Bp, ldb, beta, C,
+                                                                         rs, cs);
+    return cudaGetLastError();
+}
+
 template <bool TA, bool TB>
 static cudaError_t launch_nc(int64_t Mr, int Nc, int64_t K, float alpha, const float *Ap, int64_t lda,
                              const float *Bp, int64_t ldb, float beta, float *C, int64_t rs, int64_t cs,
                              cudaStream_t s) {
-    const dim3 grid((unsigned)((Mr + SK_ROWS - 1) / SK_ROWS));
-    if (Nc <= 4)
-        skinny_sgemm_kernel<TA, TB, 4><<<grid, SK_ROWS, 0, s>>>(Mr, Nc, K, alpha, Ap, lda, Bp, ldb, beta, C, rs, cs);
-    else if (Nc <= 8)
-        skinny_sgemm_kernel<TA, TB, 8><<<grid, SK_ROWS, 0, s>>>(Mr, Nc, K, alpha, Ap, lda, Bp, ldb, beta, C, rs, cs);
-    else
-        skinny_sgemm_kernel<TA, TB, 16><<<grid, SK_ROWS, 0, s>>>(Mr, Nc, K, alpha, Ap, lda, Bp, ldb, beta, C, rs, cs);
-    return cudaGetLastError();
+    int cfg = TA ? 0 : 2;
+    if (const char *e = getenv("EMM_SKINNY_CFG")) cfg = atoi(e);   // experiments
+    if (TA) cfg = cfg == 1 ? 1 : 0;   // the TA staging needs KC == 32
+    switch (cfg) {
+        case 1: return launch_cfg<TA, TB, 128, 32>(Mr, Nc, K, alpha, Ap, lda, Bp, ldb, beta, C, rs, cs, s);
+        case 2: return launch_cfg<TA, TB, 256, 16>(Mr, Nc, K, alpha, Ap, lda, Bp, ldb, beta, C, rs, cs, s);
+        case 3: return launch_cfg<TA, TB, 128, 16>(Mr, Nc, K, alpha, Ap, lda, Bp, ldb, beta, C, rs, cs, s);
+        default: return launch_cfg<TA, TB, 256, 32>(Mr, Nc, K, alpha, Ap, lda, Bp, ldb, beta, C, rs, cs, s);
+    }
 }
 
 cudaError_t launch_skinny_sgemm(bool tA, bool tB, int64_t M, int64_t N, int64_t K, float alpha, const float *A,
@@ -172,7 +190,7 @@ cudaError_t launch_skinny_sgemm(bool tA, bool tB, int64_t M, int64_t N, int64_t 
         Bp = A; ldb2 = lda; TB = !tA;
         rs = ldc; cs = 1;
     }
-    if ((Mr + SK_ROWS - 1) / SK_ROWS > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+    if ((Mr + 127) / 128 > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
     cudaEvent_t ev = nullptr;
     prof_begin(s, true, &ev);
     cudaError_t e;
