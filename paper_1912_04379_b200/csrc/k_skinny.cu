@@ -13,12 +13,15 @@
 // Arithmetic: FP32 FFMA in increasing k, with the partial sums promoted into
 // a master accumulator every 256 of K (as KN3, R13), so every math
 // mode gets the FP32-accurate bound.  Deterministic (no atomics).
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <cstdint>
 #include <cstdlib>
 
 #include "emm_internal.h"
+#include "ptx.cuh"
 
 namespace emm {
 
@@ -167,6 +170,183 @@ static cudaError_t launch_nc(int64_t Mr, int Nc, int64_t K, float alpha, const f
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// TMA streaming variant (both operands TMA-legal).  Persistent CTAs walk
+// 256-row blocks of C'; one producer warp streams 256 x 32 tiles of A' and
+// 32 x NC tiles of B' through a 4-stage mbarrier ring; 8 compute warps (one
+// row of C' per thread) consume them.  A' tiles: !TA -> [32 p][256 rows]
+// (row-contiguous, no swizzle); TA -> [256 rows][32 p] (128B swizzle, read as
+// 16-byte chunks).  B' tiles: !TB -> [NC][32 p]; TB -> [32 p][NC].
+// ---------------------------------------------------------------------------
+namespace {
+constexpr int SKT_ROWS = 256, SKT_KC = 32, SKT_STAGES = 4;
+constexpr int SKT_THREADS = SKT_ROWS + 32;
+constexpr int SKT_A_BYTES = SKT_ROWS * SKT_KC * 4;   // 32 KB
+}  // namespace
+
+template <bool TA, bool TB, int NC>
+__global__ void __launch_bounds__(SKT_THREADS, 1)
+    skinny_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int64_t Mr,
+                      int Nc, int64_t K, float alpha, float beta, float *__restrict__ C, int64_t rs, int64_t cs) {
+    using namespace ptx;
+    constexpr int B_BYTES = SKT_KC * NC * 4;
+    constexpr int STAGE = SKT_A_BYTES + ((B_BYTES + 1023) / 1024) * 1024;
+    extern __shared__ uint8_t skt_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(skt_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + SKT_STAGES * STAGE);
+    uint64_t *empty = full + SKT_STAGES;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t nblocks = (Mr + SKT_ROWS - 1) / SKT_ROWS;
+    const int64_t nchunks = (K + SKT_KC - 1) / SKT_KC;
+    if (tid == 0) {
+        for (int s = 0; s < SKT_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], SKT_ROWS / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == SKT_ROWS / 32) {
+        // ===== producer =====
+        if (lane == 0) {
+            prefetch_tmap(&tmA);
+            prefetch_tmap(&tmB);
+            const uint64_t pa = policy_evict_first(), pb = policy_evict_last();
+            int64_t it = 0;
+            for (int64_t rb = blockIdx.x; rb < nblocks; rb += gridDim.x) {
+                for (int64_t ch = 0; ch < nchunks; ++ch, ++it) {
+                    const int s = (int)(it % SKT_STAGES);
+                    mbar_wait(&empty[s], ((uint32_t)(it / SKT_STAGES) & 1u) ^ 1u);
+                    mbar_arrive_expect_tx(&full[s], (uint32_t)(SKT_A_BYTES + B_BYTES));
+                    const uint32_t st = smem_u32(smem + s * STAGE);
+                    const int32_t r0 = (int32_t)(rb * SKT_ROWS), k0 = (int32_t)(ch * SKT_KC);
+                    if (!TA) tma_load_2d(st, &tmA, &full[s], r0, k0, pa);
+                    else tma_load_2d(st, &tmA, &full[s], k0, r0, pa);
+                    if (!TB) tma_load_2d(st + SKT_A_BYTES, &tmB, &full[s], k0, 0, pb);
+                    else tma_load_2d(st + SKT_A_BYTES, &tmB, &full[s], 0, k0, pb);
+                }
+            }
+        }
+        return;
+    }
+    // ===== compute warps: one row of C' per thread =====
+    int64_t it = 0;
+    for (int64_t rb = blockIdx.x; rb < nblocks; rb += gridDim.x) {
+        float acc[NC], master[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) acc[c] = master[c] = 0.0f;
+        for (int64_t ch = 0; ch < nchunks; ++ch, ++it) {
+            const int s = (int)(it % SKT_STAGES);
+            mbar_wait(&full[s], (uint32_t)(it / SKT_STAGES) & 1u);
+            const float *As = reinterpret_cast<const float *>(smem + s * STAGE);
+            const float *Bs = reinterpret_cast<const float *>(smem + s * STAGE + SKT_A_BYTES);
+#pragma unroll
+            for (int j = 0; j < SKT_KC / 4; ++j) {
+                float4 a;
+                if (!TA) {
+                    a.x = As[(4 * j + 0) * SKT_ROWS + tid];
+                    a.y = As[(4 * j + 1) * SKT_ROWS + tid];
+                    a.z = As[(4 * j + 2) * SKT_ROWS + tid];
+                    a.w = As[(4 * j + 3) * SKT_ROWS + tid];
+                } else {   // 128B swizzle: 16-byte chunk j of row tid sits at chunk j ^ (tid & 7)
+                    a = *reinterpret_cast<const float4 *>(As + tid * SKT_KC + 4 * (j ^ (tid & 7)));
+                }
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    float4 b;
+                    if (!TB) {
+                        b = *reinterpret_cast<const float4 *>(Bs + c * SKT_KC + 4 * j);
+                    } else {
+                        b.x = Bs[(4 * j + 0) * NC + c];
+                        b.y = Bs[(4 * j + 1) * NC + c];
+                        b.z = Bs[(4 * j + 2) * NC + c];
+                        b.w = Bs[(4 * j + 3) * NC + c];
+                    }
+                    // increasing k within the entry's sum
+                    acc[c] = fmaf(a.x, b.x, acc[c]);
+                    acc[c] = fmaf(a.y, b.y, acc[c]);
+                    acc[c] = fmaf(a.z, b.z, acc[c]);
+                    acc[c] = fmaf(a.w, b.w, acc[c]);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+            if ((ch + 1) % (256 / SKT_KC) == 0 || ch + 1 == nchunks) {
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    master[c] += acc[c];
+                    acc[c] = 0.0f;
+                }
+            }
+        }
+        const int64_t row = rb * SKT_ROWS + tid;
+        if (row < Mr) {
+#pragma unroll
+            for (int c = 0; c < NC; ++c)
+                if (c < Nc) {
+                    float *d = C + row * rs + (int64_t)c * cs;
+                    *d = beta == 0.0f ? alpha * master[c] : fmaf(beta, *d, alpha * master[c]);
+                }
+        }
+    }
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 skinny_encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        cudaDriverEntryPointQueryResult q;
+        void *p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+        return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+    }();
+    return fn;
+}
+
+static bool skinny_tmap(CUtensorMap *tm, const float *ptr, int64_t ld, uint64_t d0, uint64_t d1, uint32_t b0,
+                        uint32_t b1, bool swz) {
+    auto enc = skinny_encode_fn();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {d0, d1}, strides[1] = {(cuuint64_t)ld * 4};
+    cuuint32_t box[2] = {b0, b1}, estr[2] = {1, 1};
+    return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(ptr), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, swz ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <bool TA, bool TB, int NC>
+static cudaError_t launch_tma_nc(int64_t Mr, int Nc, int64_t K, float alpha, const float *Ap, int64_t lda,
+                                 const float *Bp, int64_t ldb, float beta, float *C, int64_t rs, int64_t cs,
+                                 cudaStream_t s) {
+    constexpr int B_BYTES = SKT_KC * NC * 4;
+    constexpr int STAGE = SKT_A_BYTES + ((B_BYTES + 1023) / 1024) * 1024;
+    constexpr int SMEM = SKT_STAGES * STAGE + 1024 + 128;
+    static cudaError_t attr = cudaFuncSetAttribute(skinny_tma_kernel<TA, TB, NC>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (attr != cudaSuccess) return attr;
+    CUtensorMap ta, tb;
+    const bool ok_a = !TA ? skinny_tmap(&ta, Ap, lda, (uint64_t)Mr, (uint64_t)K, SKT_ROWS, SKT_KC, false)
+                          : skinny_tmap(&ta, Ap, lda, (uint64_t)K, (uint64_t)Mr, SKT_KC, SKT_ROWS, true);
+    const bool ok_b = !TB ? skinny_tmap(&tb, Bp, ldb, (uint64_t)K, (uint64_t)Nc, SKT_KC, NC, false)
+                          : skinny_tmap(&tb, Bp, ldb, (uint64_t)Nc, (uint64_t)K, NC, SKT_KC, false);
+    if (!ok_a || !ok_b) return cudaErrorInvalidValue;
+    const int64_t nblocks = (Mr + SKT_ROWS - 1) / SKT_ROWS;
+    const int64_t grid = nblocks < tc_num_sms() ? nblocks : tc_num_sms();
+    skinny_tma_kernel<TA, TB, NC><<<(unsigned)grid, SKT_THREADS, SMEM, s>>>(ta, tb, Mr, Nc, K, alpha, beta, C, rs,
+                                                                             cs);
+    return cudaGetLastError();
+}
+
+template <bool TA, bool TB>
+static cudaError_t launch_tma(int64_t Mr, int Nc, int64_t K, float alpha, const float *Ap, int64_t lda,
+                              const float *Bp, int64_t ldb, float beta, float *C, int64_t rs, int64_t cs,
+                              cudaStream_t s) {
+    if (Nc <= 4) return launch_tma_nc<TA, TB, 4>(Mr, Nc, K, alpha, Ap, lda, Bp, ldb, beta, C, rs, cs, s);
+    if (Nc <= 8) return launch_tma_nc<TA, TB, 8>(Mr, Nc, K, alpha, Ap, lda, Bp, ldb, beta, C, rs, cs, s);
+    return launch_tma_nc<TA, TB, 16>(Mr, Nc, K, alpha, Ap, lda, Bp, ldb, beta, C, rs, cs, s);
+}
+
 cudaError_t launch_skinny_sgemm(bool tA, bool tB, int64_t M, int64_t N, int64_t K, float alpha, const float *A,
                                 int64_t lda, const float *B, int64_t ldb, float beta, float *C, int64_t ldc,
                                 cudaStream_t s) {
@@ -194,7 +374,13 @@ cudaError_t launch_skinny_sgemm(bool tA, bool tB, int64_t M, int64_t N, int64_t 
     cudaEvent_t ev = nullptr;
     prof_begin(s, true, &ev);
     cudaError_t e;
-    if (!TA && !TB) e = launch_nc<false, false>(Mr, Nc, K, alpha, Ap, lda2, Bp, ldb2, beta, C, rs, cs, s);
+    const bool tma = tma_legal(Ap, lda2) && tma_legal(Bp, ldb2) && !getenv("EMM_SKINNY_NO_TMA") && K > 0;
+    if (tma) {
+        if (!TA && !TB) e = launch_tma<false, false>(Mr, Nc, K, alpha, Ap, lda2, Bp, ldb2, beta, C, rs, cs, s);
+        else if (!TA && TB) e = launch_tma<false, true>(Mr, Nc, K, alpha, Ap, lda2, Bp, ldb2, beta, C, rs, cs, s);
+        else if (TA && !TB) e = launch_tma<true, false>(Mr, Nc, K, alpha, Ap, lda2, Bp, ldb2, beta, C, rs, cs, s);
+        else e = launch_tma<true, true>(Mr, Nc, K, alpha, Ap, lda2, Bp, ldb2, beta, C, rs, cs, s);
+    } else if (!TA && !TB) e = launch_nc<false, false>(Mr, Nc, K, alpha, Ap, lda2, Bp, ldb2, beta, C, rs, cs, s);
     else if (!TA && TB) e = launch_nc<false, true>(Mr, Nc, K, alpha, Ap, lda2, Bp, ldb2, beta, C, rs, cs, s);
     else if (TA && !TB) e = launch_nc<true, false>(Mr, Nc, K, alpha, Ap, lda2, Bp, ldb2, beta, C, rs, cs, s);
     else e = launch_nc<true, true>(Mr, Nc, K, alpha, Ap, lda2, Bp, ldb2, beta, C, rs, cs, s);
