@@ -180,16 +180,20 @@ static cudaError_t launch_nc(int64_t Mr, int Nc, int64_t K, float alpha, const f
 // 16-byte chunks).  B' tiles: !TB -> [NC][32 p]; TB -> [32 p][NC].
 // ---------------------------------------------------------------------------
 namespace {
-constexpr int SKT_ROWS = 256, SKT_KC = 32, SKT_STAGES = 4;
-constexpr int SKT_THREADS = SKT_ROWS + 32;
-constexpr int SKT_A_BYTES = SKT_ROWS * SKT_KC * 4;   // 32 KB
+constexpr int SKT_TPB = 256, SKT_KC = 32;        // compute threads per CTA, K per stage
+constexpr int SKT_THREADS = SKT_TPB + 32;        // + one producer warp
 }  // namespace
 
-template <bool TA, bool TB, int NC>
+// RPT rows of C' per compute thread (rows tid, tid + 256, ...): the B'
+// broadcast loads are shared by RPT rows.
+template <bool TA, bool TB, int NC, int RPT>
 __global__ void __launch_bounds__(SKT_THREADS, 1)
     skinny_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int64_t Mr,
                       int Nc, int64_t K, float alpha, float beta, float *__restrict__ C, int64_t rs, int64_t cs) {
     using namespace ptx;
+    constexpr int SKT_ROWS = SKT_TPB * RPT;
+    constexpr int SKT_STAGES = RPT == 1 ? 4 : 3;
+    constexpr int SKT_A_BYTES = SKT_ROWS * SKT_KC * 4;
     constexpr int B_BYTES = SKT_KC * NC * 4;
     constexpr int STAGE = SKT_A_BYTES + ((B_BYTES + 1023) / 1024) * 1024;
     extern __shared__ uint8_t skt_raw[];
@@ -202,12 +206,12 @@ __global__ void __launch_bounds__(SKT_THREADS, 1)
     if (tid == 0) {
         for (int s = 0; s < SKT_STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], SKT_ROWS / 32);
+            mbar_init(&empty[s], SKT_TPB / 32);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (warp == SKT_ROWS / 32) {
+    if (warp == SKT_TPB / 32) {
         // ===== producer =====
         if (lane == 0) {
             prefetch_tmap(&tmA);
@@ -221,8 +225,11 @@ __global__ void __launch_bounds__(SKT_THREADS, 1)
                     mbar_arrive_expect_tx(&full[s], (uint32_t)(SKT_A_BYTES + B_BYTES));
                     const uint32_t st = smem_u32(smem + s * STAGE);
                     const int32_t r0 = (int32_t)(rb * SKT_ROWS), k0 = (int32_t)(ch * SKT_KC);
-                    if (!TA) tma_load_2d(st, &tmA, &full[s], r0, k0, pa);
-                    else tma_load_2d(st, &tmA, &full[s], k0, r0, pa);
+#pragma unroll
+                    for (int h = 0; h < RPT; ++h) {   // 256-row boxes
+                        if (!TA) tma_load_2d(st + h * SKT_TPB * SKT_KC * 4, &tmA, &full[s], r0 + h * SKT_TPB, k0, pa);
+                        else tma_load_2d(st + h * SKT_TPB * SKT_KC * 4, &tmA, &full[s], k0, r0 + h * SKT_TPB, pa);
+                    }
                     if (!TB) tma_load_2d(st + SKT_A_BYTES, &tmB, &full[s], k0, 0, pb);
                     else tma_load_2d(st + SKT_A_BYTES, &tmB, &full[s], 0, k0, pb);
                 }
@@ -230,12 +237,14 @@ __global__ void __launch_bounds__(SKT_THREADS, 1)
         }
         return;
     }
-    // ===== compute warps: one row of C' per thread =====
+    // ===== compute warps: RPT rows of C' per thread =====
     int64_t it = 0;
     for (int64_t rb = blockIdx.x; rb < nblocks; rb += gridDim.x) {
-        float acc[NC], master[NC];
+        float acc[RPT][NC], master[RPT][NC];
 #pragma unroll
-        for (int c = 0; c < NC; ++c) acc[c] = master[c] = 0.0f;
+        for (int h = 0; h < RPT; ++h)
+#pragma unroll
+            for (int c = 0; c < NC; ++c) acc[h][c] = master[h][c] = 0.0f;
         for (int64_t ch = 0; ch < nchunks; ++ch, ++it) {
             const int s = (int)(it % SKT_STAGES);
             mbar_wait(&full[s], (uint32_t)(it / SKT_STAGES) & 1u);
@@ -243,14 +252,18 @@ __global__ void __launch_bounds__(SKT_THREADS, 1)
             const float *Bs = reinterpret_cast<const float *>(smem + s * STAGE + SKT_A_BYTES);
 #pragma unroll
             for (int j = 0; j < SKT_KC / 4; ++j) {
-                float4 a;
-                if (!TA) {
-                    a.x = As[(4 * j + 0) * SKT_ROWS + tid];
-                    a.y = As[(4 * j + 1) * SKT_ROWS + tid];
-                    a.z = As[(4 * j + 2) * SKT_ROWS + tid];
-                    a.w = As[(4 * j + 3) * SKT_ROWS + tid];
-                } else {   // 128B swizzle: 16-byte chunk j of row tid sits at chunk j ^ (tid & 7)
-                    a = *reinterpret_cast<const float4 *>(As + tid * SKT_KC + 4 * (j ^ (tid & 7)));
+                float4 a[RPT];
+#pragma unroll
+                for (int h = 0; h < RPT; ++h) {
+                    const float *Ah = As + h * SKT_TPB * SKT_KC;   // box h
+                    if (!TA) {
+                        a[h].x = Ah[(4 * j + 0) * SKT_TPB + tid];
+                        a[h].y = Ah[(4 * j + 1) * SKT_TPB + tid];
+                        a[h].z = Ah[(4 * j + 2) * SKT_TPB + tid];
+                        a[h].w = Ah[(4 * j + 3) * SKT_TPB + tid];
+                    } else {   // 128B swizzle: 16-byte chunk j of row tid sits at chunk j ^ (tid & 7)
+                        a[h] = *reinterpret_cast<const float4 *>(Ah + tid * SKT_KC + 4 * (j ^ (tid & 7)));
+                    }
                 }
 #pragma unroll
                 for (int c = 0; c < NC; ++c) {
@@ -263,31 +276,38 @@ __global__ void __launch_bounds__(SKT_THREADS, 1)
                         b.z = Bs[(4 * j + 2) * NC + c];
                         b.w = Bs[(4 * j + 3) * NC + c];
                     }
-                    // increasing k within the entry's sum
-                    acc[c] = fmaf(a.x, b.x, acc[c]);
-                    acc[c] = fmaf(a.y, b.y, acc[c]);
-                    acc[c] = fmaf(a.z, b.z, acc[c]);
-                    acc[c] = fmaf(a.w, b.w, acc[c]);
+#pragma unroll
+                    for (int h = 0; h < RPT; ++h) {   // increasing k within each entry's sum
+                        acc[h][c] = fmaf(a[h].x, b.x, acc[h][c]);
+                        acc[h][c] = fmaf(a[h].y, b.y, acc[h][c]);
+                        acc[h][c] = fmaf(a[h].z, b.z, acc[h][c]);
+                        acc[h][c] = fmaf(a[h].w, b.w, acc[h][c]);
+                    }
                 }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);
             if ((ch + 1) % (256 / SKT_KC) == 0 || ch + 1 == nchunks) {
 #pragma unroll
-                for (int c = 0; c < NC; ++c) {
-                    master[c] += acc[c];
-                    acc[c] = 0.0f;
-                }
+                for (int h = 0; h < RPT; ++h)
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) {
+                        master[h][c] += acc[h][c];
+                        acc[h][c] = 0.0f;
+                    }
             }
         }
-        const int64_t row = rb * SKT_ROWS + tid;
-        if (row < Mr) {
 #pragma unroll
-            for (int c = 0; c < NC; ++c)
-                if (c < Nc) {
-                    float *d = C + row * rs + (int64_t)c * cs;
-                    *d = beta == 0.0f ? alpha * master[c] : fmaf(beta, *d, alpha * master[c]);
-                }
+        for (int h = 0; h < RPT; ++h) {
+            const int64_t row = rb * SKT_ROWS + h * SKT_TPB + tid;
+            if (row < Mr) {
+#pragma unroll
+                for (int c = 0; c < NC; ++c)
+                    if (c < Nc) {
+                        float *d = C + row * rs + (int64_t)c * cs;
+                        *d = beta == 0.0f ? alpha * master[h][c] : fmaf(beta, *d, alpha * master[h][c]);
+                    }
+            }
         }
     }
 }
@@ -315,26 +335,28 @@ static bool skinny_tmap(CUtensorMap *tm, const float *ptr, int64_t ld, uint64_t 
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <bool TA, bool TB, int NC>
+template <bool TA, bool TB, int NC, int RPT>
 static cudaError_t launch_tma_nc(int64_t Mr, int Nc, int64_t K, float alpha, const float *Ap, int64_t lda,
                                  const float *Bp, int64_t ldb, float beta, float *C, int64_t rs, int64_t cs,
                                  cudaStream_t s) {
+    constexpr int ROWS = SKT_TPB * RPT;
+    constexpr int STAGES = RPT == 1 ? 4 : 3;
     constexpr int B_BYTES = SKT_KC * NC * 4;
-    constexpr int STAGE = SKT_A_BYTES + ((B_BYTES + 1023) / 1024) * 1024;
-    constexpr int SMEM = SKT_STAGES * STAGE + 1024 + 128;
-    static cudaError_t attr = cudaFuncSetAttribute(skinny_tma_kernel<TA, TB, NC>,
+    constexpr int STAGE = ROWS * SKT_KC * 4 + ((B_BYTES + 1023) / 1024) * 1024;
+    constexpr int SMEM = STAGES * STAGE + 1024 + 128;
+    static cudaError_t attr = cudaFuncSetAttribute(skinny_tma_kernel<TA, TB, NC, RPT>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     if (attr != cudaSuccess) return attr;
     CUtensorMap ta, tb;
-    const bool ok_a = !TA ? skinny_tmap(&ta, Ap, lda, (uint64_t)Mr, (uint64_t)K, SKT_ROWS, SKT_KC, false)
-                          : skinny_tmap(&ta, Ap, lda, (uint64_t)K, (uint64_t)Mr, SKT_KC, SKT_ROWS, true);
+    const bool ok_a = !TA ? skinny_tmap(&ta, Ap, lda, (uint64_t)Mr, (uint64_t)K, SKT_TPB, SKT_KC, false)
+                          : skinny_tmap(&ta, Ap, lda, (uint64_t)K, (uint64_t)Mr, SKT_KC, SKT_TPB, true);
     const bool ok_b = !TB ? skinny_tmap(&tb, Bp, ldb, (uint64_t)K, (uint64_t)Nc, SKT_KC, NC, false)
                           : skinny_tmap(&tb, Bp, ldb, (uint64_t)Nc, (uint64_t)K, NC, SKT_KC, false);
     if (!ok_a || !ok_b) return cudaErrorInvalidValue;
-    const int64_t nblocks = (Mr + SKT_ROWS - 1) / SKT_ROWS;
+    const int64_t nblocks = (Mr + ROWS - 1) / ROWS;
     const int64_t grid = nblocks < tc_num_sms() ? nblocks : tc_num_sms();
-    skinny_tma_kernel<TA, TB, NC><<<(unsigned)grid, SKT_THREADS, SMEM, s>>>(ta, tb, Mr, Nc, K, alpha, beta, C, rs,
-                                                                             cs);
+    skinny_tma_kernel<TA, TB, NC, RPT><<<(unsigned)grid, SKT_THREADS, SMEM, s>>>(ta, tb, Mr, Nc, K, alpha, beta, C,
+                                                                                  rs, cs);
     return cudaGetLastError();
 }
 
@@ -342,9 +364,16 @@ template <bool TA, bool TB>
 static cudaError_t launch_tma(int64_t Mr, int Nc, int64_t K, float alpha, const float *Ap, int64_t lda,
                               const float *Bp, int64_t ldb, float beta, float *C, int64_t rs, int64_t cs,
                               cudaStream_t s) {
-    if (Nc <= 4) return launch_tma_nc<TA, TB, 4>(Mr, Nc, K, alpha, Ap, lda, Bp, ldb, beta, C, rs, cs, s);
-    if (Nc <= 8) return launch_tma_nc<TA, TB, 8>(Mr, Nc, K, alpha, Ap, lda, Bp, ldb, beta, C, rs, cs, s);
-    return launch_tma_nc<TA, TB, 16>(Mr, Nc, K, alpha, Ap, lda, Bp, ldb, beta, C, rs, cs, s);
+    int rpt = 2;
+    if (const char *e = getenv("EMM_SKINNY_RPT")) rpt = atoi(e);   // experiments
+    if (rpt == 1) {
+        if (Nc <= 4) return launch_tma_nc<TA, TB, 4, 1>(Mr, Nc, K, alpha, Ap, lda, Bp, ldb, beta, C, rs, cs, s);
+        if (Nc <= 8) return launch_tma_nc<TA, TB, 8, 1>(Mr, Nc, K, alpha, Ap, lda, Bp, ldb, beta, C, rs, cs, s);
+        return launch_tma_nc<TA, TB, 16, 1>(Mr, Nc, K, alpha, Ap, lda, Bp, ldb, beta, C, rs, cs, s);
+    }
+    if (Nc <= 4) return launch_tma_nc<TA, TB, 4, 2>(Mr, Nc, K, alpha, Ap, lda, Bp, ldb, beta, C, rs, cs, s);
+    if (Nc <= 8) return launch_tma_nc<TA, TB, 8, 2>(Mr, Nc, K, alpha, Ap, lda, Bp, ldb, beta, C, rs, cs, s);
+    return launch_tma_nc<TA, TB, 16, 2>(Mr, Nc, K, alpha, Ap, lda, Bp, ldb, beta, C, rs, cs, s);
 }
 
 cudaError_t launch_skinny_sgemm(bool tA, bool tB, int64_t M, int64_t N, int64_t K, float alpha, const float *A,
