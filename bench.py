@@ -56,6 +56,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-alt", action="store_true", help="skip the other FP32-accurate tensor path")
+    p.add_argument("--force-multi", action="store_true",
+                   help="run the row-sharded emm_sgemm_multi path (NCCL) even at one rank")
     p.add_argument("--cpu-rows", type=int, default=0, help="oracle sample rows (0 = auto)")
     return p.parse_args()
 
@@ -215,8 +217,13 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    multi = world > 1 or args.force_multi
+    if multi:
         import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(world))
         dist.init_process_group("nccl", init_method="env://", device_id=dev)
     n = args.size
     M = N = K = n
@@ -224,25 +231,25 @@ def main():
     stream = torch.cuda.Stream(dev)
 
     # ---- inputs resident in HBM (generated on the device, bit-identical to host datagen)
-    r0, rows = emm.row_partition(M, world, rank) if world > 1 else (0, M)
+    r0, rows = emm.row_partition(M, world, rank) if multi else (0, M)
     A = datagen.submatrix("uniform", datagen.TAG_A, M, K, torch.arange(r0, r0 + rows), device=dev) \
-        if world > 1 else datagen.matrix("uniform", datagen.TAG_A, M, K, device=dev)
+        if multi else datagen.matrix("uniform", datagen.TAG_A, M, K, device=dev)
     if world == 1 or rank == 0:
         B = datagen.matrix("uniform", datagen.TAG_B, K, N, device=dev)
     else:
         B = torch.empty((N, K), dtype=torch.float32, device=dev).t()
     C = torch.empty((N, max(rows, 1)), dtype=torch.float32, device=dev).t()[:rows, :]
     ws = None
-    if world == 1:
+    if not multi:
         nbytes = max(emm.workspace_bytes("N", "N", M, N, K, m) for m in (args.math, "3xtf32", "tf32bf16"))
         ws = torch.empty(max(nbytes // 4 + 256, 1), dtype=torch.float32, device=dev) if nbytes else None
         if ws is not None and ws.data_ptr() % 1024:
             ws = ws[(1024 - ws.data_ptr() % 1024) // 4:]
-    comm = emm.Comm(rank, world) if world > 1 else None
+    comm = emm.Comm(rank, world) if multi else None
 
     def make_step(math):
         def step():
-            if world > 1:
+            if multi:
                 emm.sgemm_multi(comm, M, N, K, A, B, C, 1.0, 0.0, math=math, stream=stream)
             else:
                 emm.sgemm_ex(A, B, C, 1.0, 0.0, math=math, workspace=ws, stream=stream)
@@ -250,7 +257,7 @@ def main():
 
     def barrier():
         torch.cuda.synchronize(dev)
-        if world > 1:
+        if multi:
             torch.distributed.barrier()
         torch.cuda.synchronize(dev)
 
@@ -297,7 +304,7 @@ def main():
         gemm_ms, gemm_n, other_ms, other_n = emm.profile_read()
         emm.profile_enable(False)
         clk = clocks.stop()
-        if world > 1:
+        if multi:
             t = torch.tensor([ms], dtype=torch.float64, device=dev)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             ms = float(t.item())
@@ -329,7 +336,7 @@ def main():
                                                 res["roofline"], res["peak"])
     ms_step = ms / args.steps
     alt = {}
-    if args.math in ("3xtf32", "tf32bf16") and not args.no_alt and world == 1:
+    if args.math in ("3xtf32", "tf32bf16") and not args.no_alt and not multi:
         m2 = "tf32bf16" if args.math == "3xtf32" else "3xtf32"
         k2 = max(3, args.steps // 2)
         r2 = measure(m2, k2, 2)
@@ -339,7 +346,7 @@ def main():
 
     # ---- e2e through the C-ABI host-buffer entry (copies inside the timed region)
     e2e = None
-    if not args.no_e2e and world == 1:
+    if not args.no_e2e and not multi:
         del ws
         torch.cuda.empty_cache()
         hA = datagen.storage_of(A).cpu().pin_memory()
@@ -365,7 +372,7 @@ def main():
         assert torch.equal(Cd, hv), "e2e result differs from device result"
         del hA, hB, hC
         emm.release_cache()
-    elif not args.no_e2e and world > 1:
+    elif not args.no_e2e and multi:
         hA = datagen.storage_of(A).cpu().pin_memory() if rows else None
         hB = datagen.storage_of(B).cpu().pin_memory() if rank == 0 else None
         hC = torch.empty(max(rows, 1) * N, dtype=torch.float32).pin_memory()
@@ -389,7 +396,7 @@ def main():
                "api": "H2D copies + emm_sgemm_multi + D2H, per rank"}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and not multi and not args.no_cpu:
         nrows = args.cpu_rows or auto_rows(n)
         g, dt, cores = cpu_oracle_sample(n, nrows, gen_device=dev)
         cpu = {"value": g, "unit": "GFLOP/s", "cores": cores, "kind": "oracle", "seconds": dt,
@@ -399,7 +406,8 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": workload_config(n, args, world), "roofline": roofline, "cpu_baseline": cpu,
+                "config": dict(workload_config(n, args, world), **({"path": "emm_sgemm_multi (row-sharded, NCCL)"} if multi else {})),
+                "roofline": roofline, "cpu_baseline": cpu,
                 "e2e": e2e, "gpu_launches": launches, "clocks": clk, "alt_paths": alt or None,
                 "pct_of_roofline": 100.0 * value / 1e3 / (peak * world) if peak else None}
         print(json.dumps(line), flush=True)

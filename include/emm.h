@@ -126,7 +126,7 @@ void emm_release_cache(void);
 void emm_row_partition(int64_t M, int nranks, int rank, int64_t *row0, int64_t *rows);
 
 /* Width (columns) of the B column panels emm_sgemm_multi broadcasts one at a
- * time (the last panel may be narrower): ~N/8, >= 1024, multiple of 256.
+ * time (the last panel may be narrower): ~N/4, >= 1024, multiple of 256.
  * Host-only. */
 int64_t emm_multi_panel_cols(int64_t N);
 

@@ -85,8 +85,12 @@ cudaEvent_t ev_at(Comm *c, size_t i) {
 using namespace emm;
 
 extern "C" int64_t emm_multi_panel_cols(int64_t N) {
-    // ~8 panels, each >= 1024 columns and a multiple of the 256-wide tile
-    int64_t panel = (N + 7) / 8;
+    // 4 panels, each >= 1024 columns and a multiple of the 256-wide tile: the
+    // first panel's broadcast is exposed (~1/4 of B), the others hide under
+    // the previous panel's GEMM; wider panels keep each panel GEMM at many
+    // full waves (c5 at P=8: 16 x 32 = 512 tiles = 6.9 waves of 74 CTA pairs,
+    // vs 3.5 waves with 8 panels).
+    int64_t panel = (N + 3) / 4;
     if (panel < 1024) panel = 1024;
     return (panel + 255) / 256 * 256;
 }
