@@ -385,7 +385,7 @@ def main():
                     datagen.storage_of(A).copy_(hA, non_blocking=True)
                 if rank == 0:
                     datagen.storage_of(B).copy_(hB, non_blocking=True)
-                step()
+                make_step(args.math)()
                 hC[: rows * N].copy_(C.t().reshape(-1) if rows else hC[:0], non_blocking=True)
             stream.synchronize()
         barrier()
