@@ -138,6 +138,26 @@ struct Plan {
 
 static int64_t up4(int64_t v) { return (v + 3) / 4 * 4; }
 
+// emm_sgemm without a workspace takes scratch from the device's default
+// stream-ordered pool; with its default release threshold (0) every free
+// would unmap the memory at the next synchronisation and the next call would
+// map it again (tens of ms for GiB-sized scratch), so the library raises the
+// threshold once per device: freed scratch stays cached in the pool.
+static void keep_pool_memory() {
+    static std::mutex mu;
+    static bool done[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+    std::lock_guard<std::mutex> g(mu);
+    if (done[dev]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done[dev] = true;
+}
+
 static bool env_on(const char *name) {
     const char *e = getenv(name);
     return e && e[0] == '1';
@@ -257,6 +277,7 @@ extern "C" int emm_sgemm_ex(char transA, char transB, int64_t M, int64_t N, int6
     if (ws) {
         if (workspace_bytes < P.total || (reinterpret_cast<uintptr_t>(ws) & 1023u)) return EMM_ERR_WORKSPACE;
     } else {
+        keep_pool_memory();
         cudaError_t e = cudaMallocAsync(&ws, P.total, s);
         if (e != cudaSuccess) return cuda_status(e);
         own = true;

@@ -65,7 +65,20 @@ struct Comm {
     std::vector<cudaEvent_t> evs;
     float *stage = nullptr;  // all-gather staging (grown on demand)
     size_t stage_bytes = 0;
+    void *ws = nullptr;      // tensor-core workspace: A planes | B panel planes | control block
+    size_t ws_bytes = 0;
 };
+
+int grow(void **p, size_t *have, size_t need) {
+    if (*have >= need && *p) return 0;
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    *have = 0;
+    cudaError_t e = cudaMalloc(p, need);
+    if (e != cudaSuccess) return EMM_ERR_CUDA_BASE + (int)e;
+    *have = need;
+    return 0;
+}
 
 int nccl_status(ncclResult_t r) { return r == ncclSuccess ? 0 : EMM_ERR_NCCL_BASE + (int)r; }
 int cuda_st(cudaError_t e) { return e == cudaSuccess ? 0 : EMM_ERR_CUDA_BASE + (int)e; }
@@ -129,6 +142,7 @@ extern "C" int emm_comm_destroy(void *comm) {
     cudaStreamSynchronize(c->comm_stream);
     for (auto e : c->evs) cudaEventDestroy(e);
     if (c->stage) cudaFree(c->stage);
+    if (c->ws) cudaFree(c->ws);
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
     int st = 0;
     if (c->nc) st = nccl_status(nccl().commDestroy(c->nc));
@@ -166,12 +180,49 @@ extern "C" int emm_sgemm_multi(void *comm, char transA, char transB, int64_t M, 
     if ((st = check_args(transA, transB, rows, N, K, lda, ldb, ldc > 0 ? ldc : 1))) return st;
     if ((st = check_device())) return st;
     const int64_t panel = bN ? emm_multi_panel_cols(N) : N;
-    // Each panel is one emm_sgemm_ex on the caller's stream (A read in place
-    // by TMA on the direct path; its small plane is re-derived per panel).
+    // Tensor-core modes: op(A)'s rows are re-buffered ONCE per call into
+    // K-major planes in the communicator's cached workspace; each B panel is
+    // re-buffered after its broadcast and multiplied (one GEMM launch per
+    // panel).  FFMA / alpha == 0 / K == 0 / skinny: one emm_sgemm_ex per panel.
+    const bool tc = math != EMM_MATH_FFMA && !(alpha == 0.0f || K == 0) && rows > SKINNY_MAX &&
+                    N > SKINNY_MAX && 2.0 * rows * (double)N * K > (double)(1 << 24);
+    const int terms = math == EMM_MATH_3XTF32 ? 3 : math == EMM_MATH_TF32_BF16 ? 2 : 1;
+    const int planes = terms >= 2 ? 2 : 1;
+    const int pmode = math == EMM_MATH_3XTF32 ? PK_FULL3_ : math == EMM_MATH_TF32_BF16 ? PK_FULLX_ : PK_FULL1_;
+    const int64_t Kp = tc_kpad(K);
+    float *Ap = nullptr, *Bp = nullptr;
+    unsigned int *ctrl = nullptr;
+    if (tc && rows > 0 && N > 0) {
+        const size_t a_bytes = align_up((size_t)planes * rows * Kp * 4, 1024);
+        const size_t b_bytes = align_up((size_t)planes * panel * Kp * 4, 1024);
+        // stream-ordered reuse: the previous call's kernels on `s` are ordered before this one
+        if ((st = grow(&c->ws, &c->ws_bytes, a_bytes + b_bytes + 1024))) return st;
+        Ap = reinterpret_cast<float *>(c->ws);
+        Bp = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(c->ws) + a_bytes);
+        ctrl = reinterpret_cast<unsigned int *>(reinterpret_cast<uint8_t *>(c->ws) + a_bytes + b_bytes);
+        PackArgs pa;
+        pa.X = A_local; pa.ld = lda; pa.R = rows; pa.kcontig = !(transA == 'N' || transA == 'n');
+        pa.out0 = Ap; pa.ld0 = Kp; pa.out1 = Ap + (size_t)rows * Kp; pa.ld1 = Kp; pa.b_side = false;
+        st = cuda_st(launch_pack(pmode, pa, nullptr, K, nullptr, s));
+    }
     auto panel_gemm = [&](const float *bp, int64_t nc, float *cp) -> int {
         if (rows == 0 || nc == 0) return 0;
-        return emm_sgemm_ex(transA, transB, rows, nc, K, alpha, A_local, lda, bp, ldb, beta, cp, ldc, s, math, nullptr,
-                            0);
+        if (!tc)
+            return emm_sgemm_ex(transA, transB, rows, nc, K, alpha, A_local, lda, bp, ldb, beta, cp, ldc, s, math,
+                                nullptr, 0);
+        PackArgs pb;
+        pb.X = bp; pb.ld = ldb; pb.R = nc; pb.kcontig = bN;
+        pb.out0 = Bp; pb.ld0 = Kp; pb.out1 = Bp + (size_t)nc * Kp; pb.ld1 = Kp; pb.b_side = true;
+        cudaError_t e = launch_pack(pmode, pb, nullptr, K, ctrl, s);   // also zeroes the lockstep counter
+        TcOperands ops;
+        ops.a0 = TcPlane{Ap, Kp, false, Kp};
+        ops.b0 = TcPlane{Bp, Kp, false, Kp};
+        if (planes == 2) {
+            ops.a1 = TcPlane{Ap + (size_t)rows * Kp, Kp, false, Kp};
+            ops.b1 = TcPlane{Bp + (size_t)nc * Kp, Kp, false, Kp};
+        }
+        if (e == cudaSuccess) e = launch_tc_sgemm(terms, ops, rows, nc, K, alpha, beta, cp, ldc, ctrl, 1, nullptr, s);
+        return cuda_st(e);
     };
 
     if (!st && bN && N > 0) {
