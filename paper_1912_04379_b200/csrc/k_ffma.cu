@@ -6,7 +6,10 @@
 // value reused 5x) — becomes an 8x8 register tile per thread
 // (64 accumulators; each loaded A value reused 8x, each B value 8x).  The L1
 // block becomes a 128x128x16 SMEM tile, double buffered
-// through registers (the paper's alternating xmm1/xmm2 loads).
+// through registers (the paper's alternating xmm1/xmm2 loads),
+// fed by 128-bit loads along each operand's contiguous dimension (MOVAPS vs
+// MOVUPS, PAPER.md:330-331 -> LDG.128 when 16-byte aligned) and computed with
+// FFMA2 (two FP32 FMAs per issue slot on sm_100).
 // K/M/N tails are predicated loads (zero fill) and
 // predicated stores.  Any trans / leading dimension / alignment is handled by
 // the per-thread load mapping, so no packing pass is needed.
@@ -27,8 +30,64 @@ constexpr int FB_PAD = 4;
 constexpr int FB_PROMOTE = 16;
 constexpr int FB_SMEM_BYTES = (2 * FB_K * (FB_M + FB_PAD) + 2 * FB_K * (FB_N + FB_PAD) + 64 * FB_THREADS) * 4;
 
-template <bool TA, bool TB>
-__global__ void __launch_bounds__(FB_THREADS) ffma_sgemm_kernel(int64_t M, int64_t N, int64_t K, float alpha,
+// Global -> register staging of one 128 x 16 (A) or 16 x 128 (B) tile with
+// 128-bit loads along the operand's contiguous dimension when the whole
+// float4 is in bounds and 16-byte aligned (VEC), scalar loads otherwise.
+//   "MN-contiguous" (A !TA, B TB):  4 consecutive rows/cols at one k
+//   "K-contiguous"  (A TA,  B !TB): 4 consecutive k at one row/col
+struct TileLoad {
+    float v[2][4];
+};
+
+template <bool KCONT, bool VEC>
+__device__ __forceinline__ void load_tile(TileLoad &t, const float *__restrict__ X, int64_t ld, int64_t r_base,
+                                          int64_t R, int64_t k0, int64_t K, int tid) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        int rr, kk;
+        if (!KCONT) { rr = (tid & 31) * 4; kk = (tid >> 5) + 8 * h; }      // 32 float4 along rows x 16 k
+        else        { kk = (tid & 3) * 4;  rr = (tid >> 2) + 64 * h; }     // 4 float4 along k x 128 rows
+        const int64_t r = r_base + rr, p = k0 + kk;
+        if (!KCONT) {
+            const float *src = X + r + p * ld;
+            if (VEC && p < K && r + 3 < R) {
+                const float4 q = __ldg(reinterpret_cast<const float4 *>(src));
+                t.v[h][0] = q.x; t.v[h][1] = q.y; t.v[h][2] = q.z; t.v[h][3] = q.w;
+            } else {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) t.v[h][e] = (p < K && r + e < R) ? __ldg(src + e) : 0.0f;
+            }
+        } else {
+            const float *src = X + p + r * ld;
+            if (VEC && r < R && p + 3 < K) {
+                const float4 q = __ldg(reinterpret_cast<const float4 *>(src));
+                t.v[h][0] = q.x; t.v[h][1] = q.y; t.v[h][2] = q.z; t.v[h][3] = q.w;
+            } else {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) t.v[h][e] = (r < R && p + e < K) ? __ldg(src + e) : 0.0f;
+            }
+        }
+    }
+}
+
+// registers -> S[k][row] (row-contiguous smem tile, FB_PAD padded)
+template <bool KCONT>
+__device__ __forceinline__ void store_tile(const TileLoad &t, float (*S)[FB_M + FB_PAD], int tid) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        if (!KCONT) {
+            const int rr = (tid & 31) * 4, kk = (tid >> 5) + 8 * h;
+            *reinterpret_cast<float4 *>(&S[kk][rr]) = make_float4(t.v[h][0], t.v[h][1], t.v[h][2], t.v[h][3]);
+        } else {
+            const int kk = (tid & 3) * 4, rr = (tid >> 2) + 64 * h;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) S[kk + e][rr] = t.v[h][e];
+        }
+    }
+}
+
+template <bool TA, bool TB, bool VEC>
+__global__ void __launch_bounds__(FB_THREADS, 2) ffma_sgemm_kernel(int64_t M, int64_t N, int64_t K, float alpha,
                                                                 const float *__restrict__ A, int64_t lda,
                                                                 const float *__restrict__ B, int64_t ldb, float beta,
                                                                 float *__restrict__ C, int64_t ldc) {
@@ -40,64 +99,25 @@ __global__ void __launch_bounds__(FB_THREADS) ffma_sgemm_kernel(int64_t M, int64
     const int tid = threadIdx.x;
     const int64_t m0 = (int64_t)blockIdx.x * FB_M;
     const int64_t n0 = (int64_t)blockIdx.y * FB_N;
-
-    // Load mapping: consecutive threads read consecutive addresses.
-    // A (i, p): !TA -> A[i + p*lda] (i fast); TA -> A[p + i*lda] (p fast)
-    // B (p, j): !TB -> B[p + j*ldb] (p fast); TB -> B[j + p*ldb] (j fast)
-    auto load_a = [&](int64_t k0, float (&ra)[8]) {
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-            int ii, pp;
-            if (!TA) { ii = tid & 127; pp = (tid >> 7) + 2 * r; }
-            else     { pp = tid & 15;  ii = (tid >> 4) + 16 * r; }
-            const int64_t i = m0 + ii, p = k0 + pp;
-            ra[r] = (i < M && p < K) ? __ldg(TA ? A + p + i * lda : A + i + p * lda) : 0.0f;
-        }
-    };
-    auto store_a = [&](int buf, const float (&ra)[8]) {
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-            int ii, pp;
-            if (!TA) { ii = tid & 127; pp = (tid >> 7) + 2 * r; }
-            else     { pp = tid & 15;  ii = (tid >> 4) + 16 * r; }
-            As[buf][pp][ii] = ra[r];
-        }
-    };
-    auto load_b = [&](int64_t k0, float (&rb)[8]) {
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-            int jj, pp;
-            if (!TB) { pp = tid & 15;  jj = (tid >> 4) + 16 * r; }
-            else     { jj = tid & 127; pp = (tid >> 7) + 2 * r; }
-            const int64_t j = n0 + jj, p = k0 + pp;
-            rb[r] = (j < N && p < K) ? __ldg(TB ? B + j + p * ldb : B + p + j * ldb) : 0.0f;
-        }
-    };
-    auto store_b = [&](int buf, const float (&rb)[8]) {
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-            int jj, pp;
-            if (!TB) { pp = tid & 15;  jj = (tid >> 4) + 16 * r; }
-            else     { jj = tid & 127; pp = (tid >> 7) + 2 * r; }
-            Bs[buf][pp][jj] = rb[r];
-        }
-    };
+    // op(A)(i, p): !TA -> A[i + p*lda] (MN-contiguous); TA -> A[p + i*lda] (K-contiguous)
+    // op(B)(p, j): !TB -> B[p + j*ldb] (K-contiguous);  TB -> B[j + p*ldb] (MN-contiguous)
+    constexpr bool A_KC = TA, B_KC = !TB;
 
     const int tm = tid & 15, tn = tid >> 4;   // thread's 8x8 sub-tile: rows tm*4+{0..3}, 64+tm*4+{0..3}
-    float acc[8][8];
+    // FFMA2: the 8x8 accumulators as 8 x 4 pairs of adjacent columns
+    float2 acc[8][4];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = 0.0f;
-
+        for (int j = 0; j < 4; ++j) acc[i][j] = make_float2(0.0f, 0.0f);
 #pragma unroll
     for (int e = 0; e < 64; ++e) master[e * FB_THREADS + tid] = 0.0f;
 
-    float ra[8], rb[8];
-    load_a(0, ra);
-    load_b(0, rb);
-    store_a(0, ra);
-    store_b(0, rb);
+    TileLoad ta, tb;
+    load_tile<A_KC, VEC>(ta, A, lda, m0, M, 0, K, tid);
+    load_tile<B_KC, VEC>(tb, B, ldb, n0, N, 0, K, tid);
+    store_tile<A_KC>(ta, As[0], tid);
+    store_tile<B_KC>(tb, Bs[0], tid);
     __syncthreads();
 
     const int64_t nk = (K + FB_K - 1) / FB_K;
@@ -105,8 +125,8 @@ __global__ void __launch_bounds__(FB_THREADS) ffma_sgemm_kernel(int64_t M, int64
         const int buf = (int)(kt & 1);
         const bool more = kt + 1 < nk;
         if (more) {                      // prefetch the next L1 block into registers
-            load_a((kt + 1) * FB_K, ra);
-            load_b((kt + 1) * FB_K, rb);
+            load_tile<A_KC, VEC>(ta, A, lda, m0, M, (kt + 1) * FB_K, K, tid);
+            load_tile<B_KC, VEC>(tb, B, ldb, n0, N, (kt + 1) * FB_K, K, tid);
         }
 #pragma unroll
         for (int k = 0; k < FB_K; ++k) {
@@ -115,31 +135,31 @@ __global__ void __launch_bounds__(FB_THREADS) ffma_sgemm_kernel(int64_t M, int64
             const float4 b0 = *reinterpret_cast<const float4 *>(&Bs[buf][k][tn * 4]);
             const float4 b1 = *reinterpret_cast<const float4 *>(&Bs[buf][k][64 + tn * 4]);
             const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-            const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+            const float2 bv[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
+                                  make_float2(b1.z, b1.w)};
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
+            for (int i = 0; i < 8; ++i) {
+                const float2 ai = make_float2(av[i], av[i]);
 #pragma unroll
-                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+                for (int j = 0; j < 4; ++j) acc[i][j] = __ffma2_rn(ai, bv[j], acc[i][j]);
+            }
         }
         if (more) {
-            store_a(buf ^ 1, ra);
-            store_b(buf ^ 1, rb);
+            store_tile<A_KC>(ta, As[buf ^ 1], tid);
+            store_tile<B_KC>(tb, Bs[buf ^ 1], tid);
         }
         if ((kt + 1) % FB_PROMOTE == 0 || !more) {
 #pragma unroll
             for (int i = 0; i < 8; ++i)
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    master[(i * 8 + j) * FB_THREADS + tid] += acc[i][j];
-                    acc[i][j] = 0.0f;
+                for (int j = 0; j < 4; ++j) {
+                    master[(i * 8 + 2 * j) * FB_THREADS + tid] += acc[i][j].x;
+                    master[(i * 8 + 2 * j + 1) * FB_THREADS + tid] += acc[i][j].y;
+                    acc[i][j] = make_float2(0.0f, 0.0f);
                 }
         }
         __syncthreads();
     }
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = master[(i * 8 + j) * FB_THREADS + tid];
 
     // epilogue: alpha*acc + beta*C (C not read when beta == 0), predicated
 #pragma unroll
@@ -150,8 +170,9 @@ __global__ void __launch_bounds__(FB_THREADS) ffma_sgemm_kernel(int64_t M, int64
         for (int i = 0; i < 8; ++i) {
             const int64_t row = m0 + (i < 4 ? tm * 4 + i : 64 + tm * 4 + (i - 4));
             if (row < M) {
+                const float v = master[(i * 8 + j) * FB_THREADS + tid];
                 float *d = C + row + col * ldc;
-                *d = beta == 0.0f ? alpha * acc[i][j] : fmaf(beta, *d, alpha * acc[i][j]);
+                *d = beta == 0.0f ? alpha * v : fmaf(beta, *d, alpha * v);
             }
         }
     }
@@ -169,19 +190,32 @@ cudaError_t launch_ffma_sgemm(bool tA, bool tB, int64_t M, int64_t N, int64_t K,
             cudaError_t r = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, FB_SMEM_BYTES);
             if (r != cudaSuccess) e = r;
         };
-        set((const void *)ffma_sgemm_kernel<false, false>);
-        set((const void *)ffma_sgemm_kernel<false, true>);
-        set((const void *)ffma_sgemm_kernel<true, false>);
-        set((const void *)ffma_sgemm_kernel<true, true>);
+        set((const void *)ffma_sgemm_kernel<false, false, false>);
+        set((const void *)ffma_sgemm_kernel<false, true, false>);
+        set((const void *)ffma_sgemm_kernel<true, false, false>);
+        set((const void *)ffma_sgemm_kernel<true, true, false>);
+        set((const void *)ffma_sgemm_kernel<false, false, true>);
+        set((const void *)ffma_sgemm_kernel<false, true, true>);
+        set((const void *)ffma_sgemm_kernel<true, false, true>);
+        set((const void *)ffma_sgemm_kernel<true, true, true>);
         return e;
     }();
     if (attr != cudaSuccess) return attr;
+    // 128-bit loads need 16-byte aligned bases and leading dimensions
+    const bool vec = ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15u) == 0 &&
+                     (lda & 3) == 0 && (ldb & 3) == 0;
     cudaEvent_t ev = nullptr;
     prof_begin(s, true, &ev);
-    if (!tA && !tB) ffma_sgemm_kernel<false, false><<<grid, FB_THREADS, FB_SMEM_BYTES, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
-    else if (!tA && tB) ffma_sgemm_kernel<false, true><<<grid, FB_THREADS, FB_SMEM_BYTES, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
-    else if (tA && !tB) ffma_sgemm_kernel<true, false><<<grid, FB_THREADS, FB_SMEM_BYTES, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
-    else ffma_sgemm_kernel<true, true><<<grid, FB_THREADS, FB_SMEM_BYTES, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+#define EMM_FFMA_LAUNCH(TA_, TB_)                                                                                    \
+    (vec ? ffma_sgemm_kernel<TA_, TB_, true><<<grid, FB_THREADS, FB_SMEM_BYTES, s>>>(M, N, K, alpha, A, lda, B, ldb, \
+                                                                                     beta, C, ldc)                   \
+         : ffma_sgemm_kernel<TA_, TB_, false><<<grid, FB_THREADS, FB_SMEM_BYTES, s>>>(M, N, K, alpha, A, lda, B,    \
+                                                                                      ldb, beta, C, ldc))
+    if (!tA && !tB) EMM_FFMA_LAUNCH(false, false);
+    else if (!tA && tB) EMM_FFMA_LAUNCH(false, true);
+    else if (tA && !tB) EMM_FFMA_LAUNCH(true, false);
+    else EMM_FFMA_LAUNCH(true, true);
+#undef EMM_FFMA_LAUNCH
     g_launches.fetch_add(1, std::memory_order_relaxed);
     prof_end(s, true, ev);
     return cudaGetLastError();
