@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <utility>
 #include <atomic>
 #include <cstdint>
 #include <cstdio>
@@ -357,6 +358,146 @@ int ensure(void **p, size_t *have, size_t need) {
 }
 }  // namespace
 
+// Pipelined host-buffer SGEMM (tensor-core modes, M, N >= 4096): C is cut
+// into GM x GN blocks.  Stream `h2d` copies op(A) row blocks and B column
+// panels (and C blocks when beta != 0) in the order the GEMMs need them;
+// stream `comp` re-buffers each block ONCE when it lands and runs GEMM (i, j)
+// as soon as its row block and panel are packed; stream `d2h` copies each C
+// block out as soon as its GEMM is done.  PCIe traffic (both directions)
+// overlaps the tensor-core work, leaving ~one block's copy exposed.
+namespace {
+struct HostStreams {
+    cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
+    std::vector<cudaEvent_t> ev;
+    int dev = -1;
+} g_hs;
+
+cudaEvent_t hs_event(size_t i) {
+    while (g_hs.ev.size() <= i) {
+        cudaEvent_t e;
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+        g_hs.ev.push_back(e);
+    }
+    return g_hs.ev[i];
+}
+
+// rows [r0, r0+nr) of op(X) (R x K op-matrix) from host to the same place of
+// the device copy (same ld): contiguous when K is the stored column index.
+cudaError_t copy_rows(float *d, const float *h, bool rows_contig_in_col, int64_t ld, int64_t r0, int64_t nr,
+                      int64_t K, cudaStream_t s) {
+    if (rows_contig_in_col)   // stored column-major with op rows along the leading dim: 2-D copy
+        return cudaMemcpy2DAsync(d + r0, (size_t)ld * 4, h + r0, (size_t)ld * 4, (size_t)nr * 4, (size_t)K,
+                                 cudaMemcpyHostToDevice, s);
+    // op rows are stored columns: one contiguous range
+    return cudaMemcpyAsync(d + r0 * ld, h + r0 * ld, (size_t)((nr - 1) * ld + K) * 4, cudaMemcpyHostToDevice, s);
+}
+}  // namespace
+
+static int host_pipelined(char tA, char tB, int64_t M, int64_t N, int64_t K, float alpha, const float *A, int64_t lda,
+                          const float *B, int64_t ldb, float beta, float *C, int64_t ldc, emm_math_t math, float *dA,
+                          float *dB, float *dC, void *dW) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (g_hs.dev != dev) {
+        for (cudaStream_t *p : {&g_hs.h2d, &g_hs.comp, &g_hs.d2h}) {
+            if (*p) cudaStreamDestroy(*p);
+            if (cudaStreamCreateWithFlags(p, cudaStreamNonBlocking) != cudaSuccess) return EMM_ERR_NOMEM;
+        }
+        g_hs.dev = dev;
+    }
+    const int GM = 4, GN = 4;
+    const int64_t bm = (M / GM + 255) / 256 * 256, bn = (N / GN + 255) / 256 * 256;
+    const int64_t Kp = tc_kpad(K);
+    const int terms = terms_of(math), pl = planes_of(math);
+    const int pmode = math == EMM_MATH_3XTF32 ? PK_FULL3_ : math == EMM_MATH_TF32_BF16 ? PK_FULLX_ : PK_FULL1_;
+    float *Ap = reinterpret_cast<float *>(dW);
+    float *Bp = Ap + (size_t)pl * M * Kp;
+    unsigned int *ctrl = reinterpret_cast<unsigned int *>(
+        reinterpret_cast<uint8_t *>(dW) + align_up((size_t)pl * (M + N) * Kp * 4, 1024));
+    const bool a_rows_ld = is_n(tA);    // op(A) rows contiguous in a stored column
+    const bool b_rows_ld = !is_n(tB);   // op(B)^T rows (= B columns) contiguous: transB = 'T'
+    cudaStream_t h2d = g_hs.h2d, comp = g_hs.comp, d2h = g_hs.d2h;
+    cudaError_t e = cudaSuccess;
+    size_t evn = 0;
+    auto ev = [&]() { return hs_event(evn++); };
+    std::vector<cudaEvent_t> a_in(GM), b_in(GN);
+    auto rows_of = [](int64_t total, int64_t blk, int i) {
+        const int64_t r0 = i * blk, r1 = std::min(total, r0 + blk);
+        return std::make_pair(r0, r1 > r0 ? r1 - r0 : 0);
+    };
+    std::vector<cudaEvent_t> c_in(GM * GN, nullptr);
+    auto issue_c_in = [&](int i, int j) -> cudaError_t {
+        if (beta == 0.0f) return cudaSuccess;
+        auto [r0, nr] = rows_of(M, bm, i);
+        auto [c0, nc] = rows_of(N, bn, j);
+        if (nr == 0 || nc == 0) return cudaSuccess;
+        cudaError_t r = cudaMemcpy2DAsync(dC + r0 + c0 * ldc, (size_t)ldc * 4, C + r0 + c0 * ldc, (size_t)ldc * 4,
+                                          (size_t)nr * 4, (size_t)nc, cudaMemcpyHostToDevice, h2d);
+        c_in[i * GN + j] = ev();
+        if (r == cudaSuccess) r = cudaEventRecord(c_in[i * GN + j], h2d);
+        return r;
+    };
+    if (cudaMemsetAsync(ctrl, 0, 64 * 128, comp) != cudaSuccess) return EMM_ERR_NOMEM;
+    for (int i = 0; i < GM && e == cudaSuccess; ++i) {
+        auto [r0, nr] = rows_of(M, bm, i);
+        if (nr == 0) break;
+        // H2D: A row block i (then, for i == 0, the B panels interleaved)
+        e = copy_rows(dA, A, a_rows_ld, lda, r0, nr, K, h2d);
+        a_in[i] = ev();
+        if (e == cudaSuccess) e = cudaEventRecord(a_in[i], h2d);
+        for (int j = 0; j < GN && e == cudaSuccess; ++j) {
+            auto [c0, nc] = rows_of(N, bn, j);
+            if (nc == 0) break;
+            if (i == 0) {
+                e = copy_rows(dB, B, b_rows_ld, ldb, c0, nc, K, h2d);
+                b_in[j] = ev();
+                if (e == cudaSuccess) e = cudaEventRecord(b_in[j], h2d);
+            }
+            if (e == cudaSuccess) e = issue_c_in(i, j);
+        }
+        // compute: pack A block i once, then pack B panel j (first row block only) and GEMM (i, j)
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(comp, a_in[i], 0);
+        PackArgs pa;
+        pa.X = a_rows_ld ? dA + r0 : dA + r0 * lda;
+        pa.ld = lda; pa.R = nr; pa.kcontig = !a_rows_ld;
+        pa.out0 = Ap + (size_t)r0 * Kp; pa.ld0 = Kp; pa.out1 = Ap + (size_t)M * Kp + (size_t)r0 * Kp; pa.ld1 = Kp;
+        if (e == cudaSuccess) e = launch_pack(pmode, pa, nullptr, K, nullptr, comp);
+        for (int j = 0; j < GN && e == cudaSuccess; ++j) {
+            auto [c0, nc] = rows_of(N, bn, j);
+            if (nc == 0) break;
+            if (i == 0) {
+                e = cudaStreamWaitEvent(comp, b_in[j], 0);
+                PackArgs pb;
+                pb.X = b_rows_ld ? dB + c0 : dB + c0 * ldb;
+                pb.ld = ldb; pb.R = nc; pb.kcontig = !b_rows_ld; pb.b_side = true;
+                pb.out0 = Bp + (size_t)c0 * Kp; pb.ld0 = Kp; pb.out1 = Bp + (size_t)N * Kp + (size_t)c0 * Kp; pb.ld1 = Kp;
+                if (e == cudaSuccess) e = launch_pack(pmode, pb, nullptr, K, nullptr, comp);
+            }
+            if (e == cudaSuccess && c_in[i * GN + j]) e = cudaStreamWaitEvent(comp, c_in[i * GN + j], 0);
+            TcOperands ops;
+            ops.a0 = TcPlane{Ap + (size_t)r0 * Kp, Kp, false, Kp};
+            ops.b0 = TcPlane{Bp + (size_t)c0 * Kp, Kp, false, Kp};
+            if (pl == 2) {
+                ops.a1 = TcPlane{Ap + (size_t)M * Kp + (size_t)r0 * Kp, Kp, false, Kp};
+                ops.b1 = TcPlane{Bp + (size_t)N * Kp + (size_t)c0 * Kp, Kp, false, Kp};
+            }
+            if (e == cudaSuccess)
+                e = launch_tc_sgemm(terms, ops, nr, nc, K, alpha, beta, dC + r0 + c0 * ldc, ldc,
+                                    ctrl + 32 * (i * GN + j), 1, nullptr, comp);
+            // D2H of the finished block
+            cudaEvent_t done = ev();
+            if (e == cudaSuccess) e = cudaEventRecord(done, comp);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(d2h, done, 0);
+            if (e == cudaSuccess)
+                e = cudaMemcpy2DAsync(C + r0 + c0 * ldc, (size_t)ldc * 4, dC + r0 + c0 * ldc, (size_t)ldc * 4,
+                                      (size_t)nr * 4, (size_t)nc, cudaMemcpyDeviceToHost, d2h);
+        }
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(d2h);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(comp);
+    return cuda_status(e);
+}
+
 extern "C" int emm_sgemm_host(char transA, char transB, int64_t M, int64_t N, int64_t K, float alpha, const float *A,
                               int64_t lda, const float *B, int64_t ldb, float beta, float *C, int64_t ldc,
                               emm_math_t math) {
@@ -391,6 +532,14 @@ extern "C" int emm_sgemm_host(char transA, char transB, int64_t M, int64_t N, in
         return st;
     cudaStream_t s = g_hc.s;
     cudaError_t e = cudaSuccess;
+    if (ab_used && math != EMM_MATH_FFMA && M >= 4096 && N >= 4096 && K >= 256 && !env_on("EMM_HOST_NO_PIPELINE")) {
+        const int64_t Kp = tc_kpad(K);
+        const size_t pl = (size_t)planes_of(math);
+        const size_t nP = align_up(pl * (size_t)(M + N) * Kp * 4, 1024) + 64 * 128;
+        if ((st = ensure(&g_hc.dW, &g_hc.nW, nP))) return st;
+        return host_pipelined(transA, transB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, math,
+                              (float *)g_hc.dA, (float *)g_hc.dB, (float *)g_hc.dC, g_hc.dW);
+    }
     if (ab_used) {
         e = cudaMemcpyAsync(g_hc.dA, A, nA, cudaMemcpyHostToDevice, s);
         if (e == cudaSuccess) e = cudaMemcpyAsync(g_hc.dB, B, nB, cudaMemcpyHostToDevice, s);

@@ -422,6 +422,25 @@ def test_torch_binding_colmajor(emm):
     assert torch.allclose(C.double(), ref, atol=1e-4, rtol=0)
 
 
+@pytest.mark.parametrize("tA,tB", [("N", "N"), ("T", "T"), ("N", "T")])
+@pytest.mark.parametrize("beta", [0.0, 0.5])
+def test_host_buffer_pipelined(emm, tA, tB, beta):
+    """emm_sgemm_host above 4096 x 4096 runs the copy/compute pipeline (4x4
+    blocks, three streams): same bits as the device call, ldc padding intact,
+    sampled rows against the oracle."""
+    M, N, K = 4500, 4200, 300
+    case = cached_case(tA, tB, M, N, K, 1.25, beta, pad=(4, 4, 3))
+    rows = np.array([0, 1, 1023, 1151, 1152, 2999, M - 1])
+    R, S, T, _ = case.oracle(rows=rows)
+    Cf = case.Cflat.clone().pin_memory()
+    Af, Bf = case.flat(case.A).pin_memory(), case.flat(case.B).pin_memory()
+    emm.sgemm_host(tA, tB, M, N, K, 1.25, Af, case.lda, Bf, case.ldb, beta, Cf, case.ldc)
+    case.check_untouched(Cf)
+    assert_close(case, Cf, R, S, T, 1e-5, rows=rows)
+    Cd = case.run(emm, "3xtf32")
+    assert torch.equal(Cd.view(torch.int32), Cf.view(torch.int32))
+
+
 def test_host_buffer_entry(emm):
     M, N, K = 333, 257, 129
     case = Case("T", "N", M, N, K, 1.5, -0.5, pad=(1, 2, 3))
