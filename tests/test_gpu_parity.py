@@ -424,10 +424,10 @@ def test_torch_binding_colmajor(emm):
 
 @pytest.mark.parametrize("tA,tB", [("N", "N"), ("T", "T"), ("N", "T")])
 @pytest.mark.parametrize("beta", [0.0, 0.5])
-def test_host_buffer_pipelined(emm, tA, tB, beta):
+def test_host_buffer_pipelined(emm, monkeypatch, tA, tB, beta):
     """emm_sgemm_host above 4096 x 4096 runs the copy/compute pipeline (4x4
-    blocks, three streams): same bits as the device call, ldc padding intact,
-    sampled rows against the oracle."""
+    blocks, three streams, re-buffered planes): same bits as the re-buffered
+    device call, ldc padding intact, sampled rows against the oracle."""
     M, N, K = 4500, 4200, 300
     case = cached_case(tA, tB, M, N, K, 1.25, beta, pad=(4, 4, 3))
     rows = np.array([0, 1, 1023, 1151, 1152, 2999, M - 1])
@@ -437,6 +437,7 @@ def test_host_buffer_pipelined(emm, tA, tB, beta):
     emm.sgemm_host(tA, tB, M, N, K, 1.25, Af, case.lda, Bf, case.ldb, beta, Cf, case.ldc)
     case.check_untouched(Cf)
     assert_close(case, Cf, R, S, T, 1e-5, rows=rows)
+    monkeypatch.setenv("EMM_FORCE_PACK", "1")
     Cd = case.run(emm, "3xtf32")
     assert torch.equal(Cd.view(torch.int32), Cf.view(torch.int32))
 
