@@ -110,7 +110,8 @@ static bool math_ok(emm_math_t m) {
 
 // Problems below this many flops are latency-bound (a few microseconds of
 // launches dominate; the paper's "overhead of setting up buffers is
-// prohibitive" regime): one FFMA launch, which is FP32-accurate.
+// prohibitive" regime): one launch of the tiny FFMA kernel (KN10),
+// which is FP32-accurate.
 // EMM_SMALL_FLOPS (environment) overrides the threshold; 0 disables it.
 static bool small_problem(int64_t M, int64_t N, int64_t K) {
     double thr = (double)(1 << 24);
@@ -266,7 +267,10 @@ extern "C" int emm_sgemm_ex(char transA, char transB, int64_t M, int64_t N, int6
         return cuda_status(
             launch_skinny_sgemm(!is_n(transA), !is_n(transB), M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, s));
 
-    if (math == EMM_MATH_FFMA || small_problem(M, N, K))
+    if (small_problem(M, N, K))
+        return cuda_status(
+            launch_tiny_sgemm(!is_n(transA), !is_n(transB), M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, s));
+    if (math == EMM_MATH_FFMA)
         return cuda_status(
             launch_ffma_sgemm(!is_n(transA), !is_n(transB), M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, s));
 

@@ -80,6 +80,11 @@ cudaError_t launch_skinny_sgemm(bool tA, bool tB, int64_t M, int64_t N, int64_t 
                                 int64_t lda, const float *B, int64_t ldb, float beta, float *C, int64_t ldc,
                                 cudaStream_t s);
 
+// ---- latency-bound small problems (k_tiny.cu) -----------------------------
+cudaError_t launch_tiny_sgemm(bool tA, bool tB, int64_t M, int64_t N, int64_t K, float alpha, const float *A,
+                              int64_t lda, const float *B, int64_t ldb, float beta, float *C, int64_t ldc,
+                              cudaStream_t s);
+
 // ---- misc (k_misc.cu) ------------------------------------------------------
 cudaError_t launch_scale_c(int64_t M, int64_t N, float beta, float *C, int64_t ldc, cudaStream_t s);
 // dst (M x Nc column-major, ld_dst) <- src laid out as `nranks` blocks of

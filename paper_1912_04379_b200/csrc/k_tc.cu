@@ -99,7 +99,8 @@ __device__ __forceinline__ void pack_store(const PackOperand &op, int64_t r, int
     if (MODE == PK_FULLX || MODE == PK_DCROSS) {
         uint16_t *row = reinterpret_cast<uint16_t *>(op.out1 + r * op.ld1);
         const int64_t g = p >> 3, j = p & 7;
-        const uint16_t hb = __bfloat16_as_ushort(__float2bfloat16_rn(big));
+        // non-finite x: the cross terms get 0 (inf*0 would turn the big*big inf into NaN)
+        const uint16_t hb = __bfloat16_as_ushort(__float2bfloat16_rn(isfinite(x) ? big : 0.0f));
         const uint16_t lb = __bfloat16_as_ushort(__float2bfloat16_rn(lo));
         row[g * 16 + j] = op.cross_swap ? lb : hb;
         row[g * 16 + 8 + j] = op.cross_swap ? hb : lb;
