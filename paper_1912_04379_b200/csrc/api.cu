@@ -114,7 +114,7 @@ static bool math_ok(emm_math_t m) {
 // which is FP32-accurate.
 // EMM_SMALL_FLOPS (environment) overrides the threshold; 0 disables it.
 static bool small_problem(int64_t M, int64_t N, int64_t K) {
-    double thr = (double)(1 << 24);
+    double thr = (double)(1 << 27);   // measured crossover tiny vs tensor core: between 333^3 and 512^3
     if (const char *e = getenv("EMM_SMALL_FLOPS")) thr = atof(e);
     return 2.0 * (double)M * (double)N * (double)K <= thr;
 }

@@ -122,6 +122,7 @@ def test_workspace_bytes(emm):
     assert emm.workspace_bytes("N", "T", 2048, 1024, 32, "1xtf32") == 4 * 32 * (2048 + 1024) + 1024
     # latency-bound problems (2MNK <= 2^24) take the FFMA kernel: no workspace
     assert emm.workspace_bytes("N", "N", 64, 64, 64, "3xtf32") == 0
+    assert emm.workspace_bytes("N", "N", 333, 333, 333, "3xtf32") == 0   # tiny kernel (2MNK <= 2^27)
     # sub-wave problems add split-K partials: BJ configs[2] -> 3 partials of M x N
     M, N, K = 1531, 997, 2049
     base = 2 * 4 * 2080 * M + 2 * 4 * 2080 * N
