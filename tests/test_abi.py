@@ -119,7 +119,7 @@ def test_workspace_bytes(emm):
     assert emm.workspace_bytes("N", "N", 64, 64, 64, "ffma") == 0
     # 3xTF32: 2 planes of M x Kp and N x Kp floats, Kp = K rounded up to 32, + counter
     assert emm.workspace_bytes("N", "N", 2048, 1024, 33, "3xtf32") == 2 * 4 * 64 * (2048 + 1024) + 1024
-    assert emm.workspace_bytes("N", "T", 2048, 1024, 32, "1xtf32") == 4 * 32 * (2048 + 1024) + 1024
+    assert emm.workspace_bytes("N", "T", 2048, 1024, 64, "1xtf32") == 4 * 64 * (2048 + 1024) + 1024
     # latency-bound problems (2MNK <= 2^24) take the FFMA kernel: no workspace
     assert emm.workspace_bytes("N", "N", 64, 64, 64, "3xtf32") == 0
     assert emm.workspace_bytes("N", "N", 333, 333, 333, "3xtf32") == 0   # tiny kernel (2MNK <= 2^27)
