@@ -199,21 +199,43 @@ cudaError_t launch_pack(int mode, const PackArgs &a, const PackArgs *b, int64_t 
 // =====================================================================
 // KN8: split-K reduction.  C <- alpha * (P_0 + ... + P_{S-1}) + beta*C, the
 // partials summed in fixed order s = 0..S-1 (deterministic).  P_s is M x N
-// with ld = M.  Grid (ceil(M/256), N): thread = row, block column = j.
+// with ld = M.  Grid (ceil(M/1024), N): 4 rows per thread, block column = j.
 // =====================================================================
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float *__restrict__ P, int S, int64_t M, int64_t N,
                                                             float alpha, float beta, float *__restrict__ C,
                                                             int64_t ldc) {
     asm volatile("griddepcontrol.wait;" ::: "memory");   // PDL: the GEMM's partials
-    const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
+    // 4 rows per thread (stride 256): 4*(S+1) independent loads in flight
     const int64_t j = blockIdx.y;
-    if (i >= M) return;
+    const int64_t i0 = (int64_t)blockIdx.x * 1024 + threadIdx.x;
     const int64_t plane = M * N;
-    const float *p = P + i + j * M;
-    float acc = p[0];
-    for (int s = 1; s < S; ++s) acc += p[(int64_t)s * plane];
-    float *d = C + i + j * ldc;
-    *d = beta == 0.0f ? alpha * acc : fmaf(beta, *d, alpha * acc);
+    float acc[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int64_t i = i0 + 256 * r;
+        acc[r] = i < M ? __ldcg(P + i + j * M) : 0.0f;
+    }
+    for (int s = 1; s < S; ++s) {
+        float v[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int64_t i = i0 + 256 * r;
+            v[r] = i < M ? __ldcg(P + (int64_t)s * plane + i + j * M) : 0.0f;
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc[r] += v[r];
+    }
+    float cin[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int64_t i = i0 + 256 * r;
+        cin[r] = (beta != 0.0f && i < M) ? C[i + j * ldc] : 0.0f;
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int64_t i = i0 + 256 * r;
+        if (i < M) C[i + j * ldc] = beta == 0.0f ? alpha * acc[r] : fmaf(beta, cin[r], alpha * acc[r]);
+    }
 }
 
 // =====================================================================
@@ -662,7 +684,7 @@ static cudaError_t launch_tc_t(const TcOperands &ops, int64_t M, int64_t N, int6
     prof_begin(s, false, &ev);
     {
         cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3((unsigned)((M + 255) / 256), (unsigned)N);
+        cfg.gridDim = dim3((unsigned)((M + 1023) / 1024), (unsigned)N);
         cfg.blockDim = dim3(256);
         cfg.stream = s;
         cudaLaunchAttribute at[1];
