@@ -102,12 +102,40 @@ def main():
                 e1.synchronize()
                 ts.append(e0.elapsed_time(e1))
             med = statistics.median(ts)
+            b2b = None
+            if M * N * K <= 1100 ** 3:
+                # back-to-back throughput of latency-bound
+                # sizes, a CUDA Graph of 100 calls, no flush (labelled separately)
+                g = torch.cuda.CUDAGraph()
+                cs = torch.cuda.Stream(dev)
+                cs.wait_stream(stream)
+                with torch.cuda.stream(cs):
+                    call_s = cs
+                    for _ in range(2):
+                        st = emm.sgemm_ptr(tA, tB, M, N, K, alpha, dA.data_ptr(), ar + pad[0], dB.data_ptr(),
+                                           br + pad[1], beta, dC.data_ptr(), M + pad[2], call_s.cuda_stream, math,
+                                           wsp or None, nbytes)
+                    cs.synchronize()
+                    with torch.cuda.graph(g, stream=cs):
+                        for _ in range(100):
+                            emm.sgemm_ptr(tA, tB, M, N, K, alpha, dA.data_ptr(), ar + pad[0], dB.data_ptr(),
+                                          br + pad[1], beta, dC.data_ptr(), M + pad[2], cs.cuda_stream, math,
+                                          wsp or None, nbytes)
+                g.replay()
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(cs)
+                g.replay()
+                e1.record(cs)
+                e1.synchronize()
+                b2b = e0.elapsed_time(e1) / 100 * 1e3
             fl = 2.0 * M * N * K
             byt = 4.0 * (M * K + K * N + M * N + (M * N if beta != 0 else 0))
             rec = {"config": name, "math": math, "M": M, "N": N, "K": K, "transA": tA, "transB": tB,
                    "median_ms": med, "min_ms": min(ts), "gflops": fl / med / 1e6,
                    "pct_roofline": 100.0 * fl / med / 1e9 / pk[math], "gbs": byt / med / 1e6,
-                   "roofline_tflops": pk[math], "l2_flushed": True, "reps": args.reps}
+                   "roofline_tflops": pk[math], "l2_flushed": True, "reps": args.reps,
+                   "b2b_graph_us": b2b}
             print(json.dumps(rec), flush=True)
             lines.append(rec)
             del ws

@@ -6,14 +6,15 @@ import sys
 
 
 def main(sweep, bench=None):
-    print("| Config | Path | GPUs | Median time | GFLOP/s | % roofline (peak) | GB/s compulsory |")
-    print("|---|---|---|---|---|---|---|")
+    print("| Config | Path | GPUs | Median time | GFLOP/s | % roofline (peak) | GB/s compulsory | back-to-back (graph, no flush) |")
+    print("|---|---|---|---|---|---|---|---|")
     for line in open(sweep):
         r = json.loads(line)
         t = r["median_ms"] * 1e3
         ts = f"{t:.1f} µs" if t < 1000 else f"{t / 1e3:.3f} ms"
         print(f"| {r['config']} {r['M']}×{r['N']}×{r['K']} {r['transA']}{r['transB']} | {r['math']} | 1 | {ts} | "
-              f"{r['gflops']:.0f} | {r['pct_roofline']:.1f} ({r['roofline_tflops']:.0f} TF) | {r['gbs']:.0f} |")
+              f"{r['gflops']:.0f} | {r['pct_roofline']:.1f} ({r['roofline_tflops']:.0f} TF) | {r['gbs']:.0f} | "
+              + (f"{r['b2b_graph_us']:.1f} µs |" if r.get('b2b_graph_us') else "— |"))
     if bench:
         d = json.loads(open(bench).read().strip().splitlines()[-1])
         rf = d["roofline"]
