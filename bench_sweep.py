@@ -121,12 +121,13 @@ def main():
                             emm.sgemm_ptr(tA, tB, M, N, K, alpha, dA.data_ptr(), ar + pad[0], dB.data_ptr(),
                                           br + pad[1], beta, dC.data_ptr(), M + pad[2], cs.cuda_stream, math,
                                           wsp or None, nbytes)
-                g.replay()
-                torch.cuda.synchronize()
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(cs)
-                g.replay()
-                e1.record(cs)
+                with torch.cuda.stream(cs):      # replay launches on the current stream
+                    g.replay()
+                    torch.cuda.synchronize()
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(cs)
+                    g.replay()
+                    e1.record(cs)
                 e1.synchronize()
                 b2b = e0.elapsed_time(e1) / 100 * 1e3
             fl = 2.0 * M * N * K
