@@ -152,6 +152,17 @@ int emm_sgemm_multi(void *comm, char transA, char transB, int64_t M, int64_t N, 
                     float beta, float *C_local, int64_t ldc,
                     float *C_full, int64_t ldc_full, void *stream, emm_math_t math);
 
+/* Collective: register this rank's full-output buffer (M x N, ld_full; the
+ * same layout on every rank) with the communicator.  CUDA IPC handles are
+ * exchanged over NCCL and the peers' buffers mapped.  Afterwards
+ * emm_sgemm_multi(..., C_full = that buffer, ldc_full) fuses the all-gather
+ * into the GEMM: each rank's epilogue stores its C rows into every rank's
+ * C_full over NVLink (tensor-core modes), followed by a stream-ordered
+ * completion all-reduce.  The buffer must stay allocated until
+ * emm_comm_unregister_output / emm_comm_destroy. */
+int emm_comm_register_output(void *comm, float *C_full, int64_t ld_full);
+int emm_comm_unregister_output(void *comm);
+
 /* ----------------------------------------------------------------------
  * Introspection (host-only).
  * -------------------------------------------------------------------- */

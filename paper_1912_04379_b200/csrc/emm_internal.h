@@ -38,6 +38,15 @@ struct TcOperands {
     TcPlane a0, a1, b0, b1;
 };
 
+// Fused all-gather (multi-GPU): the GEMM epilogue also stores every C value
+// to each rank's full output at (row_off + row, col_off + col) through peer
+// pointers (CUDA IPC over NVLink; the own rank's buffer is base[rank]).
+struct PeerOut {
+    float *base[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    int n = 0;
+    int64_t ld = 0, row_off = 0, col_off = 0;
+};
+
 // Arguments of the split pass for one operand (see the PK_* modes in k_tc.cu).
 struct PackArgs {
     const float *X = nullptr;
@@ -61,7 +70,7 @@ cudaError_t launch_pack(int mode, const PackArgs &a, const PackArgs *b, int64_t 
 // `partial` (splits x M x N floats) and a fixed-order reduce launch.
 cudaError_t launch_tc_sgemm(int terms, const TcOperands &ops, int64_t M, int64_t N, int64_t K, float alpha,
                             float beta, float *C, int64_t ldc, unsigned int *ctrl, int splits, float *partial,
-                            cudaStream_t s);
+                            cudaStream_t s, const PeerOut *peers = nullptr);
 bool tma_legal(const void *ptr, int64_t ld);
 int64_t tc_kpad(int64_t K);
 int tc_splits(int64_t M, int64_t N, int64_t K);

@@ -278,7 +278,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
                     const __grid_constant__ CUtensorMap tmB0, const __grid_constant__ CUtensorMap tmB1, int M, int N,
                     int Kp, float alpha, float beta, float *__restrict__ C, int64_t ldc, int tiles_m, int tiles_n,
                     int group_m, int kc_stages, unsigned int *__restrict__ wave_ctr, int splits,
-                    float *__restrict__ partial) {
+                    float *__restrict__ partial, const __grid_constant__ PeerOut peers) {
     using Cfg = TcCfg<TERMS>;
     constexpr bool A1_MN = TERMS == 3 ? A_MN : false;   // cross planes are K-major
     constexpr bool B1_MN = TERMS == 3 ? B_MN : false;
@@ -519,8 +519,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
                 if (beta == 0.0f) {
                     float *sp2 = cp;
 #pragma unroll
-                    for (int j = 0; j < 128; ++j, sp2 += ldc)
-                        if (j < jmax) *sp2 = alpha * acc[j];
+                    for (int j = 0; j < 128; ++j, sp2 += ldc) {
+                        acc[j] *= alpha;
+                        if (j < jmax) *sp2 = acc[j];
+                    }
                 } else {
                     // beta != 0: issue 16 independent C loads before the 16
                     // stores (a store could alias a later load through ldc,
@@ -533,10 +535,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
                         for (int j = 0; j < 16; ++j, lp += ldc) cin[j] = (16 * g + j < jmax) ? __ldcs(lp) : 0.0f;
                         float *sp2 = cp + (int64_t)(16 * g) * ldc;
 #pragma unroll
-                        for (int j = 0; j < 16; ++j, sp2 += ldc)
-                            if (16 * g + j < jmax) __stcs(sp2, fmaf(beta, cin[j], alpha * acc[16 * g + j]));
+                        for (int j = 0; j < 16; ++j, sp2 += ldc) {
+                            acc[16 * g + j] = fmaf(beta, cin[j], alpha * acc[16 * g + j]);
+                            if (16 * g + j < jmax) __stcs(sp2, acc[16 * g + j]);
+                        }
                     }
                 }
+                // fused all-gather: the same values into every rank's full C
+                // (peer memory over NVLink)
+                for (int p = 0; p < peers.n; ++p) {
+                    float *pp = peers.base[p] + (peers.row_off + row) + (peers.col_off + col0) * peers.ld;
+#pragma unroll
+                    for (int j = 0; j < 128; ++j, pp += peers.ld)
+                        if (j < jmax) *pp = acc[j];
+                }
+                if (peers.n) __threadfence_system();
             }
         }
     }
@@ -631,7 +644,8 @@ int tc_splits(int64_t M, int64_t N, int64_t K) {
 
 template <int TERMS, bool A_MN, bool B_MN>
 static cudaError_t launch_tc_t(const TcOperands &ops, int64_t M, int64_t N, int64_t Kp, float alpha, float beta,
-                               float *C, int64_t ldc, unsigned int *ctrl, int splits, float *partial, cudaStream_t s) {
+                               float *C, int64_t ldc, unsigned int *ctrl, int splits, float *partial, cudaStream_t s,
+                               const PeerOut &peers) {
     using Cfg = TcCfg<TERMS>;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
@@ -673,7 +687,7 @@ static cudaError_t launch_tc_t(const TcOperands &ops, int64_t M, int64_t N, int6
         cfg.numAttrs = 1;
         cudaError_t le = cudaLaunchKernelEx(&cfg, tc_sgemm_kernel<TERMS, A_MN, B_MN>, ta0, ta1, tb0, tb1, (int)M,
                                             (int)N, (int)Kp, alpha, beta, C, ldc, tiles_m, tiles_n, group_m,
-                                            kc_stages, ctrl, splits, splits > 1 ? partial : nullptr);
+                                            kc_stages, ctrl, splits, splits > 1 ? partial : nullptr, peers);
         if (le != cudaSuccess) return le;
     }
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -703,23 +717,29 @@ static cudaError_t launch_tc_t(const TcOperands &ops, int64_t M, int64_t N, int6
 
 template <int TERMS>
 static cudaError_t launch_tc_m(const TcOperands &ops, int64_t M, int64_t N, int64_t Kp, float alpha, float beta,
-                               float *C, int64_t ldc, unsigned int *ctrl, int splits, float *partial, cudaStream_t s) {
+                               float *C, int64_t ldc, unsigned int *ctrl, int splits, float *partial, cudaStream_t s,
+                               const PeerOut &pe) {
     const bool am = ops.a0.mn, bm = ops.b0.mn;
-    if (!am && !bm) return launch_tc_t<TERMS, false, false>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s);
-    if (!am && bm) return launch_tc_t<TERMS, false, true>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s);
-    if (am && !bm) return launch_tc_t<TERMS, true, false>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s);
-    return launch_tc_t<TERMS, true, true>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s);
+    if (!am && !bm)
+        return launch_tc_t<TERMS, false, false>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe);
+    if (!am && bm)
+        return launch_tc_t<TERMS, false, true>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe);
+    if (am && !bm)
+        return launch_tc_t<TERMS, true, false>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe);
+    return launch_tc_t<TERMS, true, true>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe);
 }
 
 cudaError_t launch_tc_sgemm(int terms, const TcOperands &ops, int64_t M, int64_t N, int64_t K, float alpha,
                             float beta, float *C, int64_t ldc, unsigned int *ctrl, int splits, float *partial,
-                            cudaStream_t s) {
+                            cudaStream_t s, const PeerOut *peers) {
     if (M > 0x7fffffffLL || N > 0x7fffffffLL || K > 0x7fffffffLL - 32) return cudaErrorInvalidValue;
     if (splits < 1 || (splits > 1 && !partial)) return cudaErrorInvalidValue;
+    if (peers && (peers->n < 0 || peers->n > 8 || splits > 1)) return cudaErrorInvalidValue;
+    const PeerOut pe = peers ? *peers : PeerOut{};
     const int64_t Kp = tc_kpad(K);
-    if (terms == 3) return launch_tc_m<3>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s);
-    if (terms == 2) return launch_tc_m<2>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s);
-    return launch_tc_m<1>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s);
+    if (terms == 3) return launch_tc_m<3>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe);
+    if (terms == 2) return launch_tc_m<2>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe);
+    return launch_tc_m<1>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe);
 }
 
 }  // namespace emm

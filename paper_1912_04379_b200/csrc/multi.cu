@@ -13,6 +13,7 @@
 // NCCL is loaded at run time (dlopen of the process's libnccl.so.2, normally
 // the one torch already loaded), so the library has no link-time NCCL
 // dependency and the host-only entry points work on machines without it.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -36,6 +37,8 @@ struct Nccl {
     decltype(&ncclBroadcast) broadcast = nullptr;
     decltype(&ncclGroupStart) groupStart = nullptr;
     decltype(&ncclGroupEnd) groupEnd = nullptr;
+    decltype(&ncclAllGather) allGather = nullptr;
+    decltype(&ncclAllReduce) allReduce = nullptr;
 };
 
 Nccl &nccl() {
@@ -52,8 +55,10 @@ Nccl &nccl() {
         n.broadcast = (decltype(n.broadcast))dlsym(h, "ncclBroadcast");
         n.groupStart = (decltype(n.groupStart))dlsym(h, "ncclGroupStart");
         n.groupEnd = (decltype(n.groupEnd))dlsym(h, "ncclGroupEnd");
+        n.allGather = (decltype(n.allGather))dlsym(h, "ncclAllGather");
+        n.allReduce = (decltype(n.allReduce))dlsym(h, "ncclAllReduce");
         n.ok = n.getUniqueId && n.commInitRank && n.commDestroy && n.getAsyncError && n.broadcast && n.groupStart &&
-               n.groupEnd;
+               n.groupEnd && n.allGather && n.allReduce;
     });
     return n;
 }
@@ -67,6 +72,32 @@ struct Comm {
     size_t stage_bytes = 0;
     void *ws = nullptr;      // tensor-core workspace: A planes | B panel planes | control block
     size_t ws_bytes = 0;
+    // fused all-gather target (emm_comm_register_output): every rank's full C
+    float *out_local = nullptr;
+    int64_t out_ld = 0;
+    float *out_peer[8] = {};       // mapped peer buffers (own rank: out_local)
+    void *out_opened[8] = {};      // IPC mappings to close
+    int *dummy = nullptr;          // completion all-reduce operand
+};
+
+// driver cuMemGetAddressRange (allocation base of a device pointer)
+typedef CUresult (*PFN_range)(CUdeviceptr *, size_t *, CUdeviceptr);
+PFN_range range_fn() {
+    static PFN_range fn = [] {
+        cudaDriverEntryPointQueryResult q;
+        void *p = nullptr;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            return (PFN_range)p;
+        return (PFN_range) nullptr;
+    }();
+    return fn;
+}
+
+struct OutHandle {
+    cudaIpcMemHandle_t h;
+    int64_t offset;   // bytes from the allocation base to the registered pointer
+    int64_t ld;
 };
 
 int grow(void **p, size_t *have, size_t need) {
@@ -136,9 +167,77 @@ extern "C" int emm_comm_create(void **comm, const void *id128, int nranks, int r
     return 0;
 }
 
+extern "C" int emm_comm_unregister_output(void *comm) {
+    if (!comm) return EMM_ERR_COMM;
+    Comm *c = static_cast<Comm *>(comm);
+    cudaStreamSynchronize(c->comm_stream);
+    for (int r = 0; r < 8; ++r) {
+        if (c->out_opened[r]) cudaIpcCloseMemHandle(c->out_opened[r]);
+        c->out_opened[r] = nullptr;
+        c->out_peer[r] = nullptr;
+    }
+    c->out_local = nullptr;
+    c->out_ld = 0;
+    return 0;
+}
+
+// Collective: every rank registers its M x N (ld_full) full-output buffer;
+// CUDA IPC handles are all-gathered over the NCCL communicator and the
+// peers' buffers mapped, so emm_sgemm_multi can store C tiles straight into
+// them from the GEMM epilogue (NVLink peer stores, no all-gather launch).
+extern "C" int emm_comm_register_output(void *comm, float *C_full, int64_t ld_full) {
+    if (!comm || !C_full || ld_full < 1) return EMM_ERR_COMM;
+    Comm *c = static_cast<Comm *>(comm);
+    Nccl &n = nccl();
+    if (!n.ok) return EMM_ERR_COMM;
+    emm_comm_unregister_output(comm);
+    auto rf = range_fn();
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (!rf || rf(&base, &size, reinterpret_cast<CUdeviceptr>(C_full)) != CUDA_SUCCESS) return EMM_ERR_COMM;
+    OutHandle mine{};
+    int st = cuda_st(cudaIpcGetMemHandle(&mine.h, reinterpret_cast<void *>(base)));
+    if (st) return st;
+    mine.offset = (int64_t)(reinterpret_cast<CUdeviceptr>(C_full) - base);
+    mine.ld = ld_full;
+    OutHandle *dev = nullptr;
+    if ((st = cuda_st(cudaMalloc(&dev, sizeof(OutHandle) * (c->nranks + 1))))) return st;
+    std::vector<OutHandle> all(c->nranks);
+    st = cuda_st(cudaMemcpy(dev + c->nranks, &mine, sizeof mine, cudaMemcpyHostToDevice));
+    if (!st)
+        st = nccl_status(n.allGather(dev + c->nranks, dev, sizeof(OutHandle), ncclUint8, c->nc, c->comm_stream));
+    if (!st) st = cuda_st(cudaStreamSynchronize(c->comm_stream));
+    if (!st) st = cuda_st(cudaMemcpy(all.data(), dev, sizeof(OutHandle) * c->nranks, cudaMemcpyDeviceToHost));
+    cudaFree(dev);
+    if (st) return st;
+    for (int r = 0; r < c->nranks && !st; ++r) {
+        if (all[r].ld != ld_full) st = EMM_ERR_COMM;   // identical layouts required
+        if (r == c->rank) {
+            c->out_peer[r] = C_full;
+            continue;
+        }
+        void *p = nullptr;
+        if (!st) st = cuda_st(cudaIpcOpenMemHandle(&p, all[r].h, cudaIpcMemLazyEnablePeerAccess));
+        if (!st) {
+            c->out_opened[r] = p;
+            c->out_peer[r] = reinterpret_cast<float *>(static_cast<uint8_t *>(p) + all[r].offset);
+        }
+    }
+    if (!st && !c->dummy) st = cuda_st(cudaMalloc(&c->dummy, sizeof(int)));
+    if (st) {
+        emm_comm_unregister_output(comm);
+        return st;
+    }
+    c->out_local = C_full;
+    c->out_ld = ld_full;
+    return 0;
+}
+
 extern "C" int emm_comm_destroy(void *comm) {
     if (!comm) return EMM_ERR_COMM;
     Comm *c = static_cast<Comm *>(comm);
+    emm_comm_unregister_output(comm);
+    if (c->dummy) cudaFree(c->dummy);
     cudaStreamSynchronize(c->comm_stream);
     for (auto e : c->evs) cudaEventDestroy(e);
     if (c->stage) cudaFree(c->stage);
@@ -205,6 +304,9 @@ extern "C" int emm_sgemm_multi(void *comm, char transA, char transB, int64_t M, 
         pa.out0 = Ap; pa.ld0 = Kp; pa.out1 = Ap + (size_t)rows * Kp; pa.ld1 = Kp; pa.b_side = false;
         st = cuda_st(launch_pack(pmode, pa, nullptr, K, nullptr, s));
     }
+    // fused all-gather: C_full was registered -> the GEMM epilogue stores into
+    // every rank's C_full directly (tensor-core modes)
+    const bool fused = tc && C_full && C_full == c->out_local && ldc_full == c->out_ld;
     auto panel_gemm = [&](const float *bp, int64_t nc, float *cp) -> int {
         if (rows == 0 || nc == 0) return 0;
         if (!tc)
@@ -221,7 +323,17 @@ extern "C" int emm_sgemm_multi(void *comm, char transA, char transB, int64_t M, 
             ops.a1 = TcPlane{Ap + (size_t)rows * Kp, Kp, false, Kp};
             ops.b1 = TcPlane{Bp + (size_t)nc * Kp, Kp, false, Kp};
         }
-        if (e == cudaSuccess) e = launch_tc_sgemm(terms, ops, rows, nc, K, alpha, beta, cp, ldc, ctrl, 1, nullptr, s);
+        PeerOut pe;
+        if (fused) {
+            pe.n = c->nranks;
+            for (int r = 0; r < c->nranks; ++r) pe.base[r] = c->out_peer[r];
+            pe.ld = ldc_full;
+            pe.row_off = row0;
+            pe.col_off = (cp - C_local) / ldc;   // the panel's first column
+        }
+        if (e == cudaSuccess)
+            e = launch_tc_sgemm(terms, ops, rows, nc, K, alpha, beta, cp, ldc, ctrl, 1, nullptr, s,
+                                fused ? &pe : nullptr);
         return cuda_st(e);
     };
 
@@ -250,7 +362,13 @@ extern "C" int emm_sgemm_multi(void *comm, char transA, char transB, int64_t M, 
     }
     if (st) return st;
 
-    if (C_full) {
+    if (C_full && fused) {
+        // every rank's epilogue stored its rows into all C_full buffers; a
+        // stream-ordered all-reduce completes only after every rank's GEMMs
+        // (and their peer stores, fenced at system scope) have finished.
+        st = nccl_status(n.allReduce(c->dummy, c->dummy, 1, ncclInt32, ncclSum, c->nc, s));
+        if (st) return st;
+    } else if (C_full) {
         // all-gather of the row blocks: compact own block into the rank-major
         // staging buffer, P broadcasts in one NCCL group, then unpack (KN6).
         if (ldc_full < (M > 1 ? M : 1)) return -17;

@@ -61,6 +61,10 @@ def lib() -> ctypes.CDLL:
     L.emm_sgemm_multi.argtypes = [vp, ch, ch, i64, i64, i64, f32, vp, i64, vp, i64, i32, f32, vp, i64, vp, i64,
                                   vp, i32]
     L.emm_sgemm_multi.restype = i32
+    L.emm_comm_register_output.argtypes = [vp, vp, i64]
+    L.emm_comm_register_output.restype = i32
+    L.emm_comm_unregister_output.argtypes = [vp]
+    L.emm_comm_unregister_output.restype = i32
     L.emm_strerror.argtypes = [i32]
     L.emm_strerror.restype = ctypes.c_char_p
     L.emm_version.argtypes = []
@@ -221,6 +225,16 @@ class Comm:
         if st:
             raise EmmError(st, "emm_comm_create")
         self.handle, self.rank, self.nranks = h, rank, nranks
+
+    def register_output(self, C_full) -> None:
+        """Collective: map every rank's C_full so emm_sgemm_multi fuses the
+        all-gather into the GEMM epilogue (peer stores over NVLink)."""
+        st = lib().emm_comm_register_output(self.handle, C_full.data_ptr(), _ld(C_full))
+        if st:
+            raise EmmError(st, "emm_comm_register_output")
+
+    def unregister_output(self) -> None:
+        lib().emm_comm_unregister_output(self.handle)
 
     def close(self):
         if self.handle:

@@ -100,6 +100,15 @@ def nccl_multi(rank, world, M, N, K, transB, math):
     assert torch.equal(B.cpu(), datagen.storage_of(Bh)), "B not broadcast intact"
     if rows:
         assert np.array_equal(C_loc.cpu().double().numpy(), G[r0:r0 + rows]), "C_local != C_full rows"
+    # fused all-gather: register a second full output; the GEMM epilogue
+    # stores straight into every rank's copy (peer pointers); same bits
+    C_f = torch.full((N, M), float("nan"), device=dev).t()
+    comm.register_output(C_f)
+    C_loc2 = torch.full((N, max(rows, 1)), float("nan"), device=dev).t()[:rows, :]
+    emm.sgemm_multi(comm, M, N, K, A_loc, Bv, C_loc2, 1.0, 0.0, transB=transB, C_full=C_f, math=math)
+    torch.cuda.synchronize()
+    assert torch.equal(C_f.cpu(), C_full.cpu()), "fused all-gather differs from the NCCL all-gather"
+    comm.unregister_output()
     comm.close()
 
 
