@@ -56,6 +56,9 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-alt", action="store_true", help="skip the other FP32-accurate tensor path")
+    p.add_argument("--allgather", default="none", choices=["none", "nccl", "fused"],
+                   help="multi: also gather C into every rank's full M x N output (NCCL all-gather + unpack, "
+                        "or fused into the GEMM epilogue through registered peer buffers)")
     p.add_argument("--force-multi", action="store_true",
                    help="run the row-sharded emm_sgemm_multi path (NCCL) even at one rank")
     p.add_argument("--cpu-rows", type=int, default=0, help="oracle sample rows (0 = auto)")
@@ -246,11 +249,16 @@ def main():
         if ws is not None and ws.data_ptr() % 1024:
             ws = ws[(1024 - ws.data_ptr() % 1024) // 4:]
     comm = emm.Comm(rank, world) if multi else None
+    C_full = None
+    if multi and args.allgather != "none":
+        C_full = torch.empty((N, M), dtype=torch.float32, device=dev).t()
+        if args.allgather == "fused":
+            comm.register_output(C_full)
 
     def make_step(math):
         def step():
             if multi:
-                emm.sgemm_multi(comm, M, N, K, A, B, C, 1.0, 0.0, math=math, stream=stream)
+                emm.sgemm_multi(comm, M, N, K, A, B, C, 1.0, 0.0, math=math, stream=stream, C_full=C_full)
             else:
                 emm.sgemm_ex(A, B, C, 1.0, 0.0, math=math, workspace=ws, stream=stream)
         return step
@@ -406,7 +414,9 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": dict(workload_config(n, args, world), **({"path": "emm_sgemm_multi (row-sharded, NCCL)"} if multi else {})),
+                "config": dict(workload_config(n, args, world),
+                               **({"path": "emm_sgemm_multi (row-sharded, NCCL)", "allgather": args.allgather}
+                                  if multi else {})),
                 "roofline": roofline, "cpu_baseline": cpu,
                 "e2e": e2e, "gpu_launches": launches, "clocks": clk, "alt_paths": alt or None,
                 "pct_of_roofline": 100.0 * value / 1e3 / (peak * world) if peak else None}
