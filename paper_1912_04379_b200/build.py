@@ -18,7 +18,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "build")
 LIB = os.path.join(PKG, "libemm.so")
-SOURCES = ["api.cu", "k_tc.cu", "k_ffma.cu", "k_skinny.cu", "k_tiny.cu", "k_misc.cu", "multi.cu"]
+SOURCES = ["api.cu", "k_tc.cu", "k_tcl.cu", "k_ffma.cu", "k_skinny.cu", "k_tiny.cu", "k_misc.cu", "multi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -181,6 +181,20 @@ static bool prefer_direct(int64_t M, int64_t N, emm_math_t math) {
     return f > thr;
 }
 
+// 3xTF32 operand split inside the GEMM (KN11) vs a split pass + TMA GEMM.
+// EMM_SPLIT=kernel / EMM_SPLIT=pass override (tests, experiments).
+static bool prefer_inkernel_split(int64_t M, int64_t N, int64_t K) {
+    (void)K;
+    if (const char *e = getenv("EMM_SPLIT")) {
+        if (!strcmp(e, "kernel")) return true;
+        if (!strcmp(e, "pass")) return false;
+    }
+    if (env_on("EMM_FORCE_PACK") || env_on("EMM_FORCE_DIRECT")) return false;
+    (void)M;
+    (void)N;
+    return false;   // policy set from measurements
+}
+
 static Plan make_plan(char tA, char tB, int64_t M, int64_t N, int64_t K, emm_math_t math, bool direct) {
     Plan P;
     P.terms = terms_of(math);
@@ -275,6 +289,37 @@ extern "C" int emm_sgemm_ex(char transA, char transB, int64_t M, int64_t N, int6
             launch_ffma_sgemm(!is_n(transA), !is_n(transB), M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, s));
 
     // tensor-core paths
+    if (math == EMM_MATH_3XTF32 && prefer_inkernel_split(M, N, K)) {
+        // KN11: split inside the kernel (no split pass, no operand workspace)
+        const int splits = tc_splits(M, N, K);
+        const bool multiwave = tc_units(M, N, splits) > tc_num_sms() / 2;
+        const size_t p_bytes = splits > 1 ? align_up((size_t)splits * M * N * 4, 1024) : 0;
+        const size_t need = (splits > 1 || multiwave) ? p_bytes + 1024 : 0;
+        void *ws = workspace;
+        bool own = false;
+        if (need) {
+            if (ws) {
+                if (workspace_bytes < need || (reinterpret_cast<uintptr_t>(ws) & 1023u)) return EMM_ERR_WORKSPACE;
+            } else {
+                keep_pool_memory();
+                cudaError_t e = cudaMallocAsync(&ws, need, s);
+                if (e != cudaSuccess) return cuda_status(e);
+                own = true;
+            }
+        }
+        uint8_t *w = reinterpret_cast<uint8_t *>(ws);
+        float *Pp = splits > 1 ? reinterpret_cast<float *>(w) : nullptr;
+        unsigned int *ctr = multiwave ? reinterpret_cast<unsigned int *>(w + p_bytes) : nullptr;
+        cudaError_t e = ctr ? cudaMemsetAsync(ctr, 0, 128, s) : cudaSuccess;
+        if (e == cudaSuccess)
+            e = launch_tc_split_sgemm(!is_n(transA), is_n(transB), A, lda, B, ldb, M, N, K, alpha, beta, C, ldc, ctr,
+                                      splits, Pp, s);
+        if (own) {
+            cudaError_t e2 = cudaFreeAsync(ws, s);
+            if (e == cudaSuccess) e = e2;
+        }
+        return cuda_status(e);
+    }
     const bool direct = tma_legal(A, lda) && tma_legal(B, ldb) && prefer_direct(M, N, math);
     const Plan P = make_plan(transA, transB, M, N, K, math, direct);
     void *ws = workspace;

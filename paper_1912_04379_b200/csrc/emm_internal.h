@@ -71,9 +71,21 @@ cudaError_t launch_pack(int mode, const PackArgs &a, const PackArgs *b, int64_t 
 cudaError_t launch_tc_sgemm(int terms, const TcOperands &ops, int64_t M, int64_t N, int64_t K, float alpha,
                             float beta, float *C, int64_t ldc, unsigned int *ctrl, int splits, float *partial,
                             cudaStream_t s, const PeerOut *peers = nullptr);
+// Fixed-order split-K reduce (KN8): C <- alpha * sum_s P_s + beta*C.
+cudaError_t launch_splitk_reduce(const float *partial, int splits, int64_t M, int64_t N, float alpha, float beta,
+                                 float *C, int64_t ldc, cudaStream_t s);
+// KN11 (k_tcl.cu): 3xTF32 with the split in the kernel; reads the caller's
+// A and B directly (any leading dimension, 16-B vector loads when aligned).
+// a_kc / b_kc: K is the contiguous index of the stored op(A) / op(B).
+// ctrl: zeroed control block for multi-wave problems (NULL: no lockstep).
+cudaError_t launch_tc_split_sgemm(bool a_kc, bool b_kc, const float *A, int64_t lda, const float *B, int64_t ldb,
+                                  int64_t M, int64_t N, int64_t K, float alpha, float beta, float *C, int64_t ldc,
+                                  unsigned int *ctrl, int splits, float *partial, cudaStream_t s,
+                                  const PeerOut *peers = nullptr);
 bool tma_legal(const void *ptr, int64_t ld);
 int64_t tc_kpad(int64_t K);
 int tc_splits(int64_t M, int64_t N, int64_t K);
+int64_t tc_units(int64_t M, int64_t N, int splits);   // (tile, split) work units
 int tc_num_sms();
 
 // ---- CUDA-core path (k_ffma.cu) ------------------------------------------

@@ -35,15 +35,11 @@
 
 #include "emm_internal.h"
 #include "ptx.cuh"
+#include "tc_common.cuh"
 
 namespace emm {
 
 using namespace ptx;
-
-constexpr int TC_BK = 32;            // K per stage: one 128-byte swizzle row of FP32
-constexpr int TC_BM = 128;           // rows of A per CTA (UMMA M = 256 per pair)
-constexpr int TC_BN = 256;           // columns of C per pair (UMMA N)
-constexpr int TC_TILE_BYTES = 128 * TC_BK * 4;   // one 128 x 32 FP32 operand tile
 
 int64_t tc_kpad(int64_t K) { return (K + TC_BK - 1) / TC_BK * TC_BK; }
 
@@ -238,6 +234,29 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float *__restr
     }
 }
 
+cudaError_t launch_splitk_reduce(const float *partial, int splits, int64_t M, int64_t N, float alpha, float beta,
+                                 float *C, int64_t ldc, cudaStream_t s) {
+    if (N > 65535) return cudaErrorInvalidConfiguration;
+    cudaEvent_t ev = nullptr;
+    prof_begin(s, false, &ev);
+    {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((unsigned)((M + 1023) / 1024), (unsigned)N);
+        cfg.blockDim = dim3(256);
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        cudaError_t le = cudaLaunchKernelEx(&cfg, splitk_reduce_kernel, partial, splits, M, N, alpha, beta, C, ldc);
+        if (le != cudaSuccess) return le;
+    }
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    prof_end(s, false, ev);
+    return cudaGetLastError();
+}
+
 // =====================================================================
 // KN1/KN2: tcgen05 GEMM, CTA pair per 256x256 tile.  Four 2-D tensor maps:
 // A plane 0/1, B plane 0/1; plane 0 (big) and, for 3xTF32, plane 1 (small)
@@ -255,10 +274,8 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float *__restr
 // =====================================================================
 // warp 0 = TMA producer, warp 1 = MMA issuer + TMEM owner, warps 2-9 = 8
 // promotion/epilogue warps (2 per TMEM lane quarter).
-constexpr int TC_EPI_WARPS = 8;
 constexpr int TC_EPI_WARP0 = 2;
-constexpr int TC_THREADS_P = 32 * (TC_EPI_WARP0 + TC_EPI_WARPS);   // 384
-constexpr int TC_TMEM_COLS_P = 512;                           // 2 accumulator buffers
+constexpr int TC_THREADS_P = 32 * (TC_EPI_WARP0 + TC_EPI_WARPS);   // 320
 
 // TERMS: 3 = 3xTF32 (small*big + big*small + big*big, three kind::tf32 MMAs
 // per K8), 2 = TF32+BF16 (big*big kind::tf32 + both cross terms in one K16
@@ -293,34 +310,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
 
-    // ---- persistent schedule: cluster `cid` walks tiles cid, cid+nclus, ...
-    //      in grouped raster order along M (GPU-L2 analogue of the paper's L2
-    //      blocking): consecutive tile indices (one "wave"
-    //      of clusters) cover a compact group_m x ~(nclus/group_m) block.
     const int nclus = (int)(gridDim.x >> 1);
     const int cid = (int)(blockIdx.x >> 1);
-    const int total_tiles = tiles_m * tiles_n;
-    auto tile_origin = [&](int t, int &m0, int &n0) {
-        const int per_group = group_m * tiles_n;
-        const int g = t / per_group;
-        const int first_m = g * group_m;
-        const int gsize = min(tiles_m - first_m, group_m);
-        const int tm = first_m + (t % per_group) % gsize;
-        const int tn = (t % per_group) / gsize;
-        m0 = tm * (2 * TC_BM);
-        n0 = tn * TC_BN;
-    };
-    const int nkb = Kp / TC_BK;
-    // Work units: (split, tile), split-major, so that one wave of units shares
-    // operand K-slices; unit u covers K stages [kb0, kb1) of its tile.
-    const int nkb_s = (nkb + splits - 1) / splits;
-    const int total_units = total_tiles * splits;
-    auto unit = [&](int u, int &m0, int &n0, int &kb0, int &kb1, int &sp) {
-        sp = u / total_tiles;
-        tile_origin(u - sp * total_tiles, m0, n0);
-        kb0 = sp * nkb_s;
-        kb1 = min(nkb, kb0 + nkb_s);
-    };
+    const TcSched S(tiles_m, tiles_n, group_m, Kp, splits);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < Cfg::STAGES; ++s) {
@@ -341,7 +333,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
             prefetch_tmap(&tmB1);
         }
     }
-    if (warp == 1) tmem_alloc_2sm<TC_TMEM_COLS_P>(tmem_slot);
+    if (warp == 1) tmem_alloc_2sm<TC_TMEM_COLS>(tmem_slot);
     tc_fence_before();
     cluster_sync();
     tc_fence_after();
@@ -359,7 +351,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
             const uint64_t pol = policy_evict_normal();
             int it = 0;
             unsigned int done_target = 0;   // CTAs that finished issuing waves 0..w-1
-            for (int t = cid, w = 0; t < total_units; t += nclus, ++w) {
+            for (int t = cid, w = 0; t < S.total_units; t += nclus, ++w) {
                 if (w > 0 && wave_ctr) {
                     // Wave lockstep: start loading wave w only when every CTA
                     // has issued all loads of wave w-1, so the ~17 operand
@@ -375,11 +367,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
                     }
                 }
                 {
-                    const int active = min(nclus, total_units - w * nclus);
+                    const int active = min(nclus, S.total_units - w * nclus);
                     done_target += 2u * (unsigned)active;
                 }
                 int m0, n0, kb0, kb1, sp;
-                unit(t, m0, n0, kb0, kb1, sp);
+                S.unit(t, m0, n0, kb0, kb1, sp);
                 const int arow = m0 + (int)rank * TC_BM;
                 const int brow = n0 + (int)rank * TC_BM;
                 for (int kb = kb0; kb < kb1; ++kb, ++it) {
@@ -411,154 +403,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
             }
         }
     } else if (warp == 1) {
-        // ===== MMA issuer: one thread of the leader CTA drives the pair =====
-        if (rank == 0 && lane == 0) {
-            constexpr uint32_t idesc = idesc_tf32_major<2 * TC_BM, TC_BN, A_MN, B_MN>();
-            // K8 step k of a plane: K-major advances 32 B inside the swizzle
-            // row, MN-major advances 8 K-rows = 1024 B
-            auto dsc = [](uint32_t addr, bool mn, int k) -> uint64_t {
-                return mn ? desc_mnmajor_sw128_32b(addr + (uint32_t)(k * 1024)) : desc_kmajor_sw128(addr + (uint32_t)(k * 32));
-            };
-            int it = 0, ch = 0;   // global stage / chunk counters (continue across tiles)
-            for (int t = cid; t < total_units; t += nclus) {
-                int m0, n0, kb0, kb1, sp;
-                unit(t, m0, n0, kb0, kb1, sp);
-                for (int kb = kb0; kb < kb1; ++kb, ++it) {
-                    const bool first = ((kb - kb0) % kc_stages) == 0;
-                    const bool last = ((kb - kb0) % kc_stages) == kc_stages - 1 || kb == kb1 - 1;
-                    const int b = ch & 1;
-                    const uint32_t dt = tmem_base + (uint32_t)(b * TC_BN);
-                    if (first) {   // the epilogue has drained this buffer (both CTAs)
-                        mbar_wait(&acc_empty[b], (((uint32_t)ch >> 1) & 1u) ^ 1u);
-                        tc_fence_after();
-                    }
-                    const int s = it % Cfg::STAGES;
-                    const uint32_t ph = (uint32_t)(it / Cfg::STAGES) & 1u;
-                    mbar_wait(&full[s], ph);
-                    tc_fence_after();
-                    const uint32_t st = smem_u32(smem + s * Cfg::STAGE_BYTES);
-                    const uint32_t a0 = st, a1 = st + TC_TILE_BYTES;
-                    const uint32_t b0 = st + Cfg::PLANES * TC_TILE_BYTES, b1 = b0 + TC_TILE_BYTES;
-#pragma unroll
-                    for (int k = 0; k < TC_BK / 8; ++k) {
-                        const uint32_t acc0 = (first && k == 0) ? 0u : 1u;
-                        if (TERMS == 3) {
-                            // small terms first (they are the smaller magnitudes)
-                            mma_tf32_2sm(dt, dsc(a1, A1_MN, k), dsc(b0, B_MN, k), idesc, acc0);
-                            mma_tf32_2sm(dt, dsc(a0, A_MN, k), dsc(b1, B1_MN, k), idesc, 1u);
-                            mma_tf32_2sm(dt, dsc(a0, A_MN, k), dsc(b0, B_MN, k), idesc, 1u);
-                        } else if (TERMS == 2) {
-                            // cross terms: K=16 bf16 = the same 32 bytes of a K-major row
-                            constexpr uint32_t idesc_x = idesc_bf16<2 * TC_BM, TC_BN>();
-                            mma_f16_2sm(dt, dsc(a1, false, k), dsc(b1, false, k), idesc_x, acc0);
-                            mma_tf32_2sm(dt, dsc(a0, A_MN, k), dsc(b0, B_MN, k), idesc, 1u);
-                        } else {
-                            mma_tf32_2sm(dt, dsc(a0, A_MN, k), dsc(b0, B_MN, k), idesc, acc0);
-                        }
-                    }
-                    mma_commit_2sm_mc(&empty[s], (uint16_t)0x3);
-                    if (last) {
-                        mma_commit_2sm_mc(&acc_full[b], (uint16_t)0x3);
-                        ++ch;
-                    }
-                }
-            }
-        }
+        if (rank == 0 && lane == 0)
+            tc_mma_loop<TERMS, A_MN, B_MN, A1_MN, B1_MN, Cfg::PLANES, Cfg::STAGES, Cfg::STAGE_BYTES>(
+                S, cid, nclus, smem, full, empty, acc_full, acc_empty, tmem_base, kc_stages);
     } else if (warp >= TC_EPI_WARP0) {
-        // ===== epilogue: TMEM -> FP32 registers (promotion) -> alpha/beta -> C =====
-        const int q = warp & 3;                        // TMEM lane quarter of this warp
-        const int h = (warp - TC_EPI_WARP0) >> 2;      // column half (128 columns)
-        uint32_t leader_empty0;
-        asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(leader_empty0) : "r"(smem_u32(&acc_empty[0])));
-        int ch = 0;
-        for (int t = cid; t < total_units; t += nclus) {
-            int m0, n0, kb0, kb1, sp;
-            unit(t, m0, n0, kb0, kb1, sp);
-            const int nchunks = (kb1 - kb0 + kc_stages - 1) / kc_stages;
-            const int row = m0 + (int)rank * TC_BM + 32 * q + lane;
-            float acc[128];
-#pragma unroll
-            for (int j = 0; j < 128; ++j) acc[j] = 0.0f;
-            for (int c2 = 0; c2 < nchunks; ++c2, ++ch) {
-                const int b = ch & 1;
-                mbar_wait(&acc_full[b], ((uint32_t)ch >> 1) & 1u);
-                tc_fence_after();
-                const uint32_t tb = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(b * TC_BN + h * 128);
-#pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    uint32_t v[16];
-                    tmem_ld_32x32b_x16(tb + (uint32_t)(16 * c), v);
-                    tmem_ld_wait();
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) acc[16 * c + j] += __uint_as_float(v[j]);
-                }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) {
-                    const uint32_t eb = leader_empty0 + (uint32_t)(b * sizeof(uint64_t));
-                    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(eb) : "memory");
-                }
-            }
-            if (partial) {
-                // split-K: publish the raw FP32 partial of split sp; the
-                // reduce launch (KN8) sums the S partials in fixed order.
-                if (row < M) {
-                    const int col0 = n0 + h * 128;
-                    float *pp = partial + (int64_t)sp * M * N + (int64_t)row + (int64_t)col0 * M;
-                    const int jmax = min(128, N - col0);
-#pragma unroll
-                    for (int j = 0; j < 128; ++j, pp += M)
-                        if (j < jmax) *pp = acc[j];
-                }
-                continue;
-            }
-            if (row < M) {
-                const int col0 = n0 + h * 128;
-                float *cp = C + (int64_t)row + (int64_t)col0 * ldc;
-                const int jmax = min(128, N - col0);
-                if (beta == 0.0f) {
-                    float *sp2 = cp;
-#pragma unroll
-                    for (int j = 0; j < 128; ++j, sp2 += ldc) {
-                        acc[j] *= alpha;
-                        if (j < jmax) *sp2 = acc[j];
-                    }
-                } else {
-                    // beta != 0: issue 16 independent C loads before the 16
-                    // stores (a store could alias a later load through ldc,
-                    // so the compiler would otherwise serialise them).
-#pragma unroll
-                    for (int g = 0; g < 8; ++g) {
-                        float cin[16];
-                        const float *lp = cp + (int64_t)(16 * g) * ldc;
-#pragma unroll
-                        for (int j = 0; j < 16; ++j, lp += ldc) cin[j] = (16 * g + j < jmax) ? __ldcs(lp) : 0.0f;
-                        float *sp2 = cp + (int64_t)(16 * g) * ldc;
-#pragma unroll
-                        for (int j = 0; j < 16; ++j, sp2 += ldc) {
-                            acc[16 * g + j] = fmaf(beta, cin[j], alpha * acc[16 * g + j]);
-                            if (16 * g + j < jmax) __stcs(sp2, acc[16 * g + j]);
-                        }
-                    }
-                }
-                // fused all-gather: the same values into every rank's full C
-                // (peer memory over NVLink)
-                for (int p = 0; p < peers.n; ++p) {
-                    float *pp = peers.base[p] + (peers.row_off + row) + (peers.col_off + col0) * peers.ld;
-#pragma unroll
-                    for (int j = 0; j < 128; ++j, pp += peers.ld)
-                        if (j < jmax) *pp = acc[j];
-                }
-                if (peers.n) __threadfence_system();
-            }
-        }
+        tc_epilogue_loop(S, cid, nclus, rank, warp & 3, (warp - TC_EPI_WARP0) >> 2, lane, tmem_base, acc_full,
+                         acc_empty, kc_stages, M, N, alpha, beta, C, ldc, partial, peers);
     }
 
     tc_fence_before();
     cluster_sync();
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc_2sm<TC_TMEM_COLS_P>(tmem_base);
+        tmem_dealloc_2sm<TC_TMEM_COLS>(tmem_base);
     }
 }
 
@@ -642,6 +499,10 @@ int tc_splits(int64_t M, int64_t N, int64_t K) {
     return (int)s;
 }
 
+int64_t tc_units(int64_t M, int64_t N, int splits) {
+    return ((M + 2 * TC_BM - 1) / (2 * TC_BM)) * ((N + TC_BN - 1) / TC_BN) * splits;
+}
+
 template <int TERMS, bool A_MN, bool B_MN>
 static cudaError_t launch_tc_t(const TcOperands &ops, int64_t M, int64_t N, int64_t Kp, float alpha, float beta,
                                float *C, int64_t ldc, unsigned int *ctrl, int splits, float *partial, cudaStream_t s,
@@ -694,25 +555,7 @@ static cudaError_t launch_tc_t(const TcOperands &ops, int64_t M, int64_t N, int6
     prof_end(s, true, ev);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || splits <= 1) return e;
-    if (N > 65535) return cudaErrorInvalidConfiguration;
-    prof_begin(s, false, &ev);
-    {
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3((unsigned)((M + 1023) / 1024), (unsigned)N);
-        cfg.blockDim = dim3(256);
-        cfg.stream = s;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        at[0].val.programmaticStreamSerializationAllowed = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        cudaError_t le = cudaLaunchKernelEx(&cfg, splitk_reduce_kernel, (const float *)partial, splits, M, N, alpha,
-                                            beta, C, ldc);
-        if (le != cudaSuccess) return le;
-    }
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-    prof_end(s, false, ev);
-    return cudaGetLastError();
+    return launch_splitk_reduce(partial, splits, M, N, alpha, beta, C, ldc, s);
 }
 
 template <int TERMS>
