@@ -48,9 +48,10 @@ int64_t tc_kpad(int64_t K) { return (K + TC_BK - 1) / TC_BK * TC_BK; }
 constexpr int TC_CTRL_WORDS = 32;
 
 // =====================================================================
-// KN4: operand split pass, both operands in one launch (blockIdx.z = 0: A,
-// 1: B).  32x32 tiles, 256 threads.  Block (0,0,0) also zeroes the GEMM's
-// per-call control block (stream-ordered before the GEMM).
+// KN4: operand split pass, both operands in ONE launch (a flat grid: A's
+// blocks, then B's).  Block 0 also zeroes the GEMM's per-call control block
+// (stream-ordered before the GEMM).  HBM-bound: 16-byte vector loads and
+// stores wherever the layout allows.
 //
 //   PK_FULL1  plane 0 = rn_tf32(x), K-major                (fallback 1xTF32)
 //   PK_FULL3  + plane 1 = rn_tf32(x - big), K-major       (fallback 3xTF32)
@@ -63,8 +64,21 @@ constexpr int TC_CTRL_WORDS = 32;
 // bf16(x - big) x8] (A side) or the halves swapped (B side), so that ONE K16
 // BF16 MMA computes a_big*b_small + a_small*b_big.
 // Non-finite x: the second part is 0 (inf/NaN propagate through big*big).
+//
+// Two block kinds:
+//  * element-wise ("lines"): the output keeps the source orientation —
+//    K-contiguous sources (every mode) and PK_DSMALL of MN-contiguous
+//    sources.  A line is one stored column (contiguous run) of the source;
+//    a thread handles groups of 8 consecutive elements (two 16-B vectors).
+//  * transpose: MN-contiguous source -> K-major planes (the re-buffered
+//    FULL modes and PK_DCROSS): 64 (r) x 32 (p) tiles through shared memory.
 // =====================================================================
 enum { PK_FULL1 = PK_FULL1_, PK_FULL3 = PK_FULL3_, PK_FULLX = PK_FULLX_, PK_DSMALL = PK_DSMALL_, PK_DCROSS = PK_DCROSS_ };
+
+constexpr int PK_THREADS = 256;
+constexpr int PK_GROUPS = 2;                                   // 8-element groups per thread (element-wise)
+constexpr int PK_CHUNK = PK_THREADS * PK_GROUPS * 8;           // elements of a line per block
+constexpr int PK_TR = 64, PK_TP = 32;                          // transpose tile (r x p)
 
 struct PackOperand {
     const float *X;
@@ -76,15 +90,29 @@ struct PackOperand {
     int64_t ld1;
     int cross_swap;   // B side of the cross operand
     int raw_big;      // test hook (EMM_DEBUG_RAW_BIG): FULL big = x unrounded
+    // launch geometry (host-computed)
+    int transpose;    // 1: tile path, 0: element-wise lines
+    int vec;          // 16-B vector loads legal on the source (aligned base, ld % 4 == 0)
+    int64_t lines, L, Lext;   // element-wise: lines, valid / written elements per line
+    int64_t nx;       // blocks along a line (element-wise) or r-tiles (transpose)
+    int64_t nblocks;
 };
 
 __device__ __forceinline__ float trunc_tf32(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
 template <int MODE>
-__device__ __forceinline__ void pack_store(const PackOperand &op, int64_t r, int64_t p, float x) {
+__device__ __forceinline__ void split_one(const PackOperand &op, float x, float &big, float &lo) {
     const bool direct = MODE == PK_DSMALL || MODE == PK_DCROSS;
-    const float big = direct ? trunc_tf32(x) : (op.raw_big ? x : __uint_as_float(cvt_tf32_rn(x)));
-    const float lo = isfinite(x) ? x - big : 0.0f;                  // exact
+    big = direct ? trunc_tf32(x) : (op.raw_big ? x : __uint_as_float(cvt_tf32_rn(x)));
+    lo = isfinite(x) ? x - big : 0.0f;   // exact
+}
+
+// One element (r, p) of op(X) -> its output position(s) (scalar tails).
+template <int MODE>
+__device__ __forceinline__ void pack_store(const PackOperand &op, int64_t r, int64_t p, float x) {
+    float big, lo;
+    split_one<MODE>(op, x, big, lo);
+    const bool direct = MODE == PK_DSMALL || MODE == PK_DCROSS;
     if (!direct) op.out0[r * op.ld0 + p] = big;
     if (MODE == PK_FULL3) op.out1[r * op.ld1 + p] = __uint_as_float(cvt_tf32_rn(lo));
     if (MODE == PK_DSMALL) {
@@ -95,7 +123,6 @@ __device__ __forceinline__ void pack_store(const PackOperand &op, int64_t r, int
     if (MODE == PK_FULLX || MODE == PK_DCROSS) {
         uint16_t *row = reinterpret_cast<uint16_t *>(op.out1 + r * op.ld1);
         const int64_t g = p >> 3, j = p & 7;
-        // non-finite x: the cross terms get 0 (inf*0 would turn the big*big inf into NaN)
         const uint16_t hb = __bfloat16_as_ushort(__float2bfloat16_rn(isfinite(x) ? big : 0.0f));
         const uint16_t lb = __bfloat16_as_ushort(__float2bfloat16_rn(lo));
         row[g * 16 + j] = op.cross_swap ? lb : hb;
@@ -103,57 +130,154 @@ __device__ __forceinline__ void pack_store(const PackOperand &op, int64_t r, int
     }
 }
 
+// 4 consecutive output positions p0..p0+3 of line/row r (p0 % 4 == 0),
+// vector stores.  FULL/cross: K-major row r; DSMALL: the line's own layout.
 template <int MODE>
-__global__ void __launch_bounds__(256) pack_split_kernel(PackOperand opA, PackOperand opB, int64_t K, int64_t Kext,
-                                                         unsigned int *ctrl) {
+__device__ __forceinline__ void pack_store4(const PackOperand &op, float *o0, float *o1, int64_t e, const float (&x)[4]) {
+    float big[4], lo[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) split_one<MODE>(op, x[i], big[i], lo[i]);
+    if (MODE == PK_FULL1 || MODE == PK_FULL3 || MODE == PK_FULLX)
+        *reinterpret_cast<float4 *>(o0 + e) = make_float4(big[0], big[1], big[2], big[3]);
+    if (MODE == PK_FULL3 || MODE == PK_DSMALL)
+        *reinterpret_cast<float4 *>(o1 + e) =
+            make_float4(__uint_as_float(cvt_tf32_rn(lo[0])), __uint_as_float(cvt_tf32_rn(lo[1])),
+                        __uint_as_float(cvt_tf32_rn(lo[2])), __uint_as_float(cvt_tf32_rn(lo[3])));
+    if (MODE == PK_FULLX || MODE == PK_DCROSS) {
+        uint32_t hw[2], lw[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const float b0 = isfinite(x[2 * i]) ? big[2 * i] : 0.0f, b1 = isfinite(x[2 * i + 1]) ? big[2 * i + 1] : 0.0f;
+            hw[i] = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(b0)) |
+                    ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(b1)) << 16);
+            lw[i] = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(lo[2 * i])) |
+                    ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(lo[2 * i + 1])) << 16);
+        }
+        uint16_t *row = reinterpret_cast<uint16_t *>(o1);
+        const int64_t g = e >> 3, j = e & 7;   // j in {0, 4}
+        uint2 *ph = reinterpret_cast<uint2 *>(row + g * 16 + j);
+        uint2 *pl = reinterpret_cast<uint2 *>(row + g * 16 + 8 + j);
+        const uint2 H = make_uint2(hw[0], hw[1]), Lw = make_uint2(lw[0], lw[1]);
+        *ph = op.cross_swap ? Lw : H;
+        *pl = op.cross_swap ? H : Lw;
+    }
+}
+
+template <int MODE>
+__device__ __forceinline__ void pack_lines(const PackOperand &op, int64_t blk) {
+    const int64_t line = blk / op.nx;
+    const int64_t e0 = (blk - line * op.nx) * PK_CHUNK;
+    const float *__restrict__ src = op.X + line * op.ld;
+    // output line: FULL / cross planes are K-major rows; DSMALL keeps the layout
+    float *o0 = op.out0 ? op.out0 + line * op.ld0 : nullptr;
+    float *o1 = op.out1 + line * op.ld1;
+    const int64_t L = op.L, Lext = op.Lext;
+    float v[PK_GROUPS][8];
+#pragma unroll
+    for (int g = 0; g < PK_GROUPS; ++g) {
+        const int64_t e = e0 + ((int64_t)g * PK_THREADS + threadIdx.x) * 8;
+        if (op.vec && e + 8 <= L) {
+            const float4 a = __ldcs(reinterpret_cast<const float4 *>(src + e));
+            const float4 b = __ldcs(reinterpret_cast<const float4 *>(src + e + 4));
+            v[g][0] = a.x; v[g][1] = a.y; v[g][2] = a.z; v[g][3] = a.w;
+            v[g][4] = b.x; v[g][5] = b.y; v[g][6] = b.z; v[g][7] = b.w;
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[g][i] = e + i < L ? __ldcs(src + e + i) : 0.0f;
+        }
+    }
+#pragma unroll
+    for (int g = 0; g < PK_GROUPS; ++g) {
+        const int64_t e = e0 + ((int64_t)g * PK_THREADS + threadIdx.x) * 8;
+        if (e + 8 <= Lext) {
+            const float h0[4] = {v[g][0], v[g][1], v[g][2], v[g][3]};
+            const float h1[4] = {v[g][4], v[g][5], v[g][6], v[g][7]};
+            pack_store4<MODE>(op, o0, o1, e, h0);
+            pack_store4<MODE>(op, o0, o1, e + 4, h1);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                if (e + i >= Lext) break;
+                if (op.kcontig) pack_store<MODE>(op, line, e + i, v[g][i]);
+                else pack_store<MODE>(op, e + i, line, v[g][i]);   // PK_DSMALL only
+            }
+        }
+    }
+}
+
+// MN-contiguous source (r, p) at X[r + p*ld] -> K-major row r.
+template <int MODE>
+__device__ __forceinline__ void pack_transpose(const PackOperand &op, int64_t blk, int64_t K, float (*tile)[PK_TR + 1]) {
+    const int64_t tp = blk / op.nx;
+    const int64_t r0 = (blk - tp * op.nx) * PK_TR, p0 = tp * PK_TP;
+    const int64_t R = op.R, ld = op.ld;
+    // load: 32 p-rows x 16 float4 along r = 512 vectors, 2 per thread
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const int idx = threadIdx.x + i * PK_THREADS;
+        const int pp = idx >> 4, rv = (idx & 15) * 4;
+        const int64_t p = p0 + pp, r = r0 + rv;
+        float x[4] = {0.f, 0.f, 0.f, 0.f};
+        if (p < K) {
+            const float *s = op.X + r + p * ld;
+            if (op.vec && r + 4 <= R) {
+                const float4 a = __ldcs(reinterpret_cast<const float4 *>(s));
+                x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) x[j] = r + j < R ? __ldcs(s + j) : 0.0f;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) tile[pp][rv + j] = x[j];
+    }
+    __syncthreads();
+    // store: 64 rows r x 8 float4 along p, 2 per thread (8 lanes per 128-B row segment)
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const int idx = threadIdx.x + i * PK_THREADS;
+        const int rr = idx >> 3, pv = (idx & 7) * 4;
+        const int64_t r = r0 + rr;
+        if (r >= R) continue;
+        const float x[4] = {tile[pv][rr], tile[pv + 1][rr], tile[pv + 2][rr], tile[pv + 3][rr]};
+        float *o0 = op.out0 ? op.out0 + r * op.ld0 : nullptr;
+        pack_store4<MODE>(op, o0, op.out1 + r * op.ld1, p0 + pv, x);
+    }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(PK_THREADS) pack_split_kernel(PackOperand opA, PackOperand opB, int64_t K,
+                                                                unsigned int *ctrl) {
     // Programmatic dependent launch: the GEMM may start its prologue (barrier
     // init, TMEM alloc, descriptor prefetch) now; it waits (griddepcontrol.
     // wait) for this grid's completion before its first operand load.
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    __shared__ float tile[32][33];
-    const PackOperand &op = blockIdx.z == 0 ? opA : opB;
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-    const int64_t r0 = (int64_t)blockIdx.x * 32;
-    const int64_t k0 = (int64_t)blockIdx.y * 32;
-    if (ctrl && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
+    __shared__ float tile[PK_TP][PK_TR + 1];
+    if (ctrl && blockIdx.x == 0)
         for (int i = threadIdx.x; i < TC_CTRL_WORDS; i += blockDim.x) ctrl[i] = 0u;
-    if (r0 >= op.R) return;                               // block-uniform
-    const float *__restrict__ X = op.X;
-    const int64_t R = op.R, ld = op.ld;
-    if (op.kcontig) {
-        // (r, p) at X[p + r*ld]: read and write along p.
-        float v[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int64_t r = r0 + ty + 8 * i, p = k0 + tx;
-            v[i] = (r < R && p < K) ? __ldg(X + p + r * ld) : 0.0f;
-        }
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int64_t r = r0 + ty + 8 * i, p = k0 + tx;
-            if (r < R && p < Kext) pack_store<MODE>(op, r, p, v[i]);
-        }
-    } else if (MODE == PK_DSMALL) {
-        // (r, p) at X[r + p*ld] and the small plane in the same layout:
-        // elementwise, coalesced along r, no transpose.
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int64_t r = r0 + tx, p = k0 + ty + 8 * i;
-            if (r < R && p < K) pack_store<MODE>(op, r, p, __ldg(X + r + p * ld));
-        }
+    int64_t blk = blockIdx.x;
+    const bool isA = blk < opA.nblocks;
+    const PackOperand &op = isA ? opA : opB;
+    if (!isA) blk -= opA.nblocks;
+    if (op.transpose) pack_transpose<MODE>(op, blk, K, tile);   // block-uniform branch
+    else pack_lines<MODE>(op, blk);
+}
+
+static void pack_geometry(PackOperand &o, int mode, int64_t K) {
+    const bool dsmall = mode == PK_DSMALL;
+    const int64_t Kext = dsmall ? K : tc_kpad(K);        // FULL / cross planes are zero-padded to Kp
+    o.vec = ((reinterpret_cast<uintptr_t>(o.X) & 15u) == 0 && (o.ld & 3) == 0) ? 1 : 0;
+    if (o.kcontig || dsmall) {
+        o.transpose = 0;
+        o.lines = o.kcontig ? o.R : K;
+        o.L = o.kcontig ? K : o.R;
+        o.Lext = o.kcontig ? Kext : o.R;
+        o.nx = (o.Lext + PK_CHUNK - 1) / PK_CHUNK;
+        o.nblocks = o.lines * o.nx;
     } else {
-        // (r, p) at X[r + p*ld] into a K-major plane: transpose through smem.
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int64_t r = r0 + tx, p = k0 + ty + 8 * i;
-            tile[ty + 8 * i][tx] = (r < R && p < K) ? __ldg(X + r + p * ld) : 0.0f;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int64_t r = r0 + ty + 8 * i, p = k0 + tx;
-            if (r < R && p < Kext) pack_store<MODE>(op, r, p, tile[tx][ty + 8 * i]);
-        }
+        o.transpose = 1;
+        o.nx = (o.R + PK_TR - 1) / PK_TR;
+        o.nblocks = o.nx * (Kext / PK_TP);
     }
 }
 
@@ -166,25 +290,29 @@ cudaError_t launch_pack(int mode, const PackArgs &a, const PackArgs *b, int64_t 
         const char *e = getenv("EMM_DEBUG_RAW_BIG");
         return e && e[0] == '1' ? 1 : 0;
     }();
-    const bool dsmall = mode == PK_DSMALL;
-    const int64_t Kext = dsmall ? K : tc_kpad(K);        // FULL / cross planes are zero-padded to Kp
     auto mk = [&](const PackArgs &x, bool b_side) {
-        PackOperand o{x.X, x.ld, x.R, x.kcontig ? 1 : 0, x.out0, x.ld0, x.out1, x.ld1, b_side ? 1 : 0, raw};
+        PackOperand o{};
+        o.X = x.X; o.ld = x.ld; o.R = x.R; o.kcontig = x.kcontig ? 1 : 0;
+        o.out0 = x.out0; o.ld0 = x.ld0; o.out1 = x.out1; o.ld1 = x.ld1;
+        o.cross_swap = b_side ? 1 : 0; o.raw_big = raw;
+        pack_geometry(o, mode, K);
         return o;
     };
+    if (a.R <= 0 || K <= 0 || (b && b->R <= 0)) return cudaErrorInvalidConfiguration;
     const PackOperand oa = mk(a, a.b_side);
-    const PackOperand ob = b ? mk(*b, true) : oa;
-    const int64_t R = b ? (a.R > b->R ? a.R : b->R) : a.R;
-    dim3 grid((unsigned)((R + 31) / 32), (unsigned)((Kext + 31) / 32), b ? 2u : 1u);
-    if (grid.y > 65535 || (R + 31) / 32 > 0x7fffffffLL || R <= 0 || Kext <= 0) return cudaErrorInvalidConfiguration;
+    PackOperand ob = b ? mk(*b, true) : oa;
+    if (!b) ob.nblocks = 0;
+    const int64_t nblk = oa.nblocks + ob.nblocks;
+    if (nblk <= 0 || nblk > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
     cudaEvent_t ev = nullptr;
     prof_begin(s, false, &ev);
+    const dim3 grid((unsigned)nblk);
     switch (mode) {
-        case PK_FULL1: pack_split_kernel<PK_FULL1><<<grid, 256, 0, s>>>(oa, ob, K, Kext, ctrl); break;
-        case PK_FULL3: pack_split_kernel<PK_FULL3><<<grid, 256, 0, s>>>(oa, ob, K, Kext, ctrl); break;
-        case PK_FULLX: pack_split_kernel<PK_FULLX><<<grid, 256, 0, s>>>(oa, ob, K, Kext, ctrl); break;
-        case PK_DSMALL: pack_split_kernel<PK_DSMALL><<<grid, 256, 0, s>>>(oa, ob, K, Kext, ctrl); break;
-        case PK_DCROSS: pack_split_kernel<PK_DCROSS><<<grid, 256, 0, s>>>(oa, ob, K, Kext, ctrl); break;
+        case PK_FULL1: pack_split_kernel<PK_FULL1><<<grid, PK_THREADS, 0, s>>>(oa, ob, K, ctrl); break;
+        case PK_FULL3: pack_split_kernel<PK_FULL3><<<grid, PK_THREADS, 0, s>>>(oa, ob, K, ctrl); break;
+        case PK_FULLX: pack_split_kernel<PK_FULLX><<<grid, PK_THREADS, 0, s>>>(oa, ob, K, ctrl); break;
+        case PK_DSMALL: pack_split_kernel<PK_DSMALL><<<grid, PK_THREADS, 0, s>>>(oa, ob, K, ctrl); break;
+        case PK_DCROSS: pack_split_kernel<PK_DCROSS><<<grid, PK_THREADS, 0, s>>>(oa, ob, K, ctrl); break;
         default: return cudaErrorInvalidValue;
     }
     g_launches.fetch_add(1, std::memory_order_relaxed);
