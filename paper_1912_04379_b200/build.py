@@ -16,8 +16,10 @@ import sysconfig
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-OBJ = os.path.join(PKG, "build")
-LIB = os.path.join(PKG, "libemm.so")
+# EMM_TIMELINE=1: debug build with per-CTA %globaltimer stamps (tools/timeline.py)
+TIMELINE = os.environ.get("EMM_TIMELINE") == "1"
+OBJ = os.path.join(PKG, "build_tl" if TIMELINE else "build")
+LIB = os.path.join(PKG, "libemm_tl.so" if TIMELINE else "libemm.so")
 SOURCES = ["api.cu", "k_tc.cu", "k_tcl.cu", "k_ffma.cu", "k_skinny.cu", "k_tiny.cu", "k_misc.cu", "multi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -37,7 +39,8 @@ def nccl_include() -> str:
 
 def flags() -> list[str]:
     return ["-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
-            "-I", os.path.join(ROOT, "include"), "-I", nccl_include(), "--expt-relaxed-constexpr"]
+            "-I", os.path.join(ROOT, "include"), "-I", nccl_include(), "--expt-relaxed-constexpr",
+            *(["-DEMM_TIMELINE"] if TIMELINE else [])]
 
 
 def _stale(out: str, deps: list[str]) -> bool:

@@ -102,7 +102,7 @@ static int cuda_status(cudaError_t e) { return e == cudaSuccess ? 0 : EMM_ERR_CU
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 static int planes_of(emm_math_t m) { return m == EMM_MATH_3XTF32 || m == EMM_MATH_TF32_BF16 ? 2 : 1; }
-static int pack_mode(emm_math_t m) { return m == EMM_MATH_3XTF32 ? 1 : m == EMM_MATH_TF32_BF16 ? 2 : 0; }
+
 static int terms_of(emm_math_t m) { return m == EMM_MATH_3XTF32 ? 3 : m == EMM_MATH_TF32_BF16 ? 2 : 1; }
 static bool math_ok(emm_math_t m) {
     return m == EMM_MATH_3XTF32 || m == EMM_MATH_FFMA || m == EMM_MATH_1XTF32 || m == EMM_MATH_TF32_BF16;
@@ -135,6 +135,7 @@ struct Plan {
     int terms = 1;
     int splits = 1;
     size_t a_off = 0, b_off = 0, p_off = 0, ctr_off = 0, total = 0;
+    bool sk = false;          // stream-K: [flags | slots] follow the control block
     int64_t lda1 = 0, ldb1 = 0;   // second-plane leading dimensions
 };
 
@@ -229,7 +230,9 @@ static Plan make_plan(char tA, char tB, int64_t M, int64_t N, int64_t K, emm_mat
     P.b_off = align_up(a_bytes, 1024);
     P.p_off = P.b_off + align_up(b_bytes, 1024);
     P.ctr_off = P.p_off + (P.splits > 1 ? align_up((size_t)P.splits * M * N * 4, 1024) : 0);
-    P.total = P.ctr_off + 1024;
+    int dp = 0;
+    P.sk = tc_sk_plan(M, N, K, P.splits, P.terms, &dp);
+    P.total = P.ctr_off + TC_CTRL_BYTES + (P.sk ? TC_SK_FLAG_BYTES + tc_sk_slot_bytes() : 0);
     return P;
 }
 
@@ -368,9 +371,13 @@ extern "C" int emm_sgemm_ex(char transA, char transB, int64_t M, int64_t N, int6
         }
     }
     cudaError_t e = cudaSuccess;
-    if (P.pack_mode >= 0) e = launch_pack(P.pack_mode, pa, &pb, K, ctr, s);
-    else e = cudaMemsetAsync(ctr, 0, 128, s);
-    if (e == cudaSuccess) e = launch_tc_sgemm(P.terms, ops, M, N, K, alpha, beta, C, ldc, ctr, P.splits, Pp, s);
+    // zeroed before the GEMM: control block (+ stream-K flags)
+    const size_t zero_bytes = TC_CTRL_BYTES + (P.sk ? TC_SK_FLAG_BYTES : 0);
+    void *sk_ws = P.sk ? w + P.ctr_off + TC_CTRL_BYTES : nullptr;
+    if (P.pack_mode >= 0) e = launch_pack(P.pack_mode, pa, &pb, K, ctr, s, (int)(zero_bytes / 4));
+    else e = cudaMemsetAsync(ctr, 0, zero_bytes, s);
+    if (e == cudaSuccess)
+        e = launch_tc_sgemm(P.terms, ops, M, N, K, alpha, beta, C, ldc, ctr, P.splits, Pp, s, nullptr, sk_ws);
     if (own) {
         cudaError_t e2 = cudaFreeAsync(ws, s);
         if (e == cudaSuccess) e = e2;

@@ -59,9 +59,18 @@ struct PackArgs {
     bool b_side = false;    // B side of the cross operand (halves swapped)
 };
 enum { PK_FULL1_ = 0, PK_FULL3_ = 1, PK_FULLX_ = 2, PK_DSMALL_ = 3, PK_DCROSS_ = 4 };
-// One launch for A (and B if non-NULL); also zeroes the control block.
+// One launch for A (and B if non-NULL); also zeroes `ctrl_words` words at
+// ctrl (the control block, and the stream-K flags that follow it).
 cudaError_t launch_pack(int mode, const PackArgs &a, const PackArgs *b, int64_t K, unsigned int *ctrl,
-                        cudaStream_t s);
+                        cudaStream_t s, int ctrl_words = 32);
+// Per-call control block (wave-lockstep counter), and the stream-K scratch
+// that may follow it: [flags: TC_SK_FLAG_BYTES][slots: tc_sk_slot_bytes()].
+constexpr size_t TC_CTRL_BYTES = 1024;
+constexpr size_t TC_SK_FLAG_BYTES = 8192;
+size_t tc_sk_slot_bytes();
+// Stream-K for this shape?  dp_tiles: tiles of the data-
+// parallel phase; false for split-K / exact-wave / tiny-remainder shapes.
+bool tc_sk_plan(int64_t M, int64_t N, int64_t K, int splits, int terms, int *dp_tiles);
 // C <- alpha * op(A) op(B) + beta*C on the planes (tcgen05, 2-CTA,
 // persistent, PDL).  terms: 3 = 3xTF32, 2 = TF32+BF16, 1 = 1xTF32.
 // ctrl: per-call control block (word 0 = wave-lockstep counter), ZERO when
@@ -70,7 +79,7 @@ cudaError_t launch_pack(int mode, const PackArgs &a, const PackArgs *b, int64_t 
 // `partial` (splits x M x N floats) and a fixed-order reduce launch.
 cudaError_t launch_tc_sgemm(int terms, const TcOperands &ops, int64_t M, int64_t N, int64_t K, float alpha,
                             float beta, float *C, int64_t ldc, unsigned int *ctrl, int splits, float *partial,
-                            cudaStream_t s, const PeerOut *peers = nullptr);
+                            cudaStream_t s, const PeerOut *peers = nullptr, void *sk_ws = nullptr);
 // Fixed-order split-K reduce (KN8): C <- alpha * sum_s P_s + beta*C.
 cudaError_t launch_splitk_reduce(const float *partial, int splits, int64_t M, int64_t N, float alpha, float beta,
                                  float *C, int64_t ldc, cudaStream_t s);

@@ -31,6 +31,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "emm_internal.h"
@@ -43,9 +44,9 @@ using namespace ptx;
 
 int64_t tc_kpad(int64_t K) { return (K + TC_BK - 1) / TC_BK * TC_BK; }
 
-// Per-call control block (zeroed by the pack launch): word 0 = wave-lockstep
-// counter.
-constexpr int TC_CTRL_WORDS = 32;
+// Per-call control block (zeroed by the pack launch, TC_CTRL_BYTES): word 0 =
+// wave-lockstep counter.
+constexpr int TC_SK_CHUNK = 256 / TC_BK;   // stream-K granularity: 8 stages = one promotion chunk
 
 // =====================================================================
 // KN4: operand split pass, both operands in ONE launch (a flat grid: A's
@@ -172,18 +173,25 @@ __device__ __forceinline__ void pack_lines(const PackOperand &op, int64_t blk) {
     float *o0 = op.out0 ? op.out0 + line * op.ld0 : nullptr;
     float *o1 = op.out1 + line * op.ld1;
     const int64_t L = op.L, Lext = op.Lext;
+    // direct modes: the GEMM re-reads the raw operand right after this pass,
+    // so keep it in L2 (normal loads); FULL modes never read it again
+    constexpr bool keep = MODE == PK_DSMALL || MODE == PK_DCROSS;
+    auto ld4 = [](const float *p) {
+        return keep ? __ldg(reinterpret_cast<const float4 *>(p)) : __ldcs(reinterpret_cast<const float4 *>(p));
+    };
+    auto ld1 = [](const float *p) { return keep ? __ldg(p) : __ldcs(p); };
     float v[PK_GROUPS][8];
 #pragma unroll
     for (int g = 0; g < PK_GROUPS; ++g) {
         const int64_t e = e0 + ((int64_t)g * PK_THREADS + threadIdx.x) * 8;
         if (op.vec && e + 8 <= L) {
-            const float4 a = __ldcs(reinterpret_cast<const float4 *>(src + e));
-            const float4 b = __ldcs(reinterpret_cast<const float4 *>(src + e + 4));
+            const float4 a = ld4(src + e);
+            const float4 b = ld4(src + e + 4);
             v[g][0] = a.x; v[g][1] = a.y; v[g][2] = a.z; v[g][3] = a.w;
             v[g][4] = b.x; v[g][5] = b.y; v[g][6] = b.z; v[g][7] = b.w;
         } else {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) v[g][i] = e + i < L ? __ldcs(src + e + i) : 0.0f;
+            for (int i = 0; i < 8; ++i) v[g][i] = e + i < L ? ld1(src + e + i) : 0.0f;
         }
     }
 #pragma unroll
@@ -247,14 +255,14 @@ __device__ __forceinline__ void pack_transpose(const PackOperand &op, int64_t bl
 
 template <int MODE>
 __global__ void __launch_bounds__(PK_THREADS) pack_split_kernel(PackOperand opA, PackOperand opB, int64_t K,
-                                                                unsigned int *ctrl) {
+                                                                unsigned int *ctrl, int ctrl_words) {
     // Programmatic dependent launch: the GEMM may start its prologue (barrier
     // init, TMEM alloc, descriptor prefetch) now; it waits (griddepcontrol.
     // wait) for this grid's completion before its first operand load.
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     __shared__ float tile[PK_TP][PK_TR + 1];
     if (ctrl && blockIdx.x == 0)
-        for (int i = threadIdx.x; i < TC_CTRL_WORDS; i += blockDim.x) ctrl[i] = 0u;
+        for (int i = threadIdx.x; i < ctrl_words; i += blockDim.x) ctrl[i] = 0u;
     int64_t blk = blockIdx.x;
     const bool isA = blk < opA.nblocks;
     const PackOperand &op = isA ? opA : opB;
@@ -282,7 +290,7 @@ static void pack_geometry(PackOperand &o, int mode, int64_t K) {
 }
 
 cudaError_t launch_pack(int mode, const PackArgs &a, const PackArgs *b, int64_t K, unsigned int *ctrl,
-                        cudaStream_t s) {
+                        cudaStream_t s, int ctrl_words) {
     // EMM_DEBUG_RAW_BIG=1 (tests only): hand the tensor core raw FP32 bits as
     // the "big" part of the FULL modes, to probe its TF32 input conversion
     // (R7b).
@@ -308,11 +316,11 @@ cudaError_t launch_pack(int mode, const PackArgs &a, const PackArgs *b, int64_t 
     prof_begin(s, false, &ev);
     const dim3 grid((unsigned)nblk);
     switch (mode) {
-        case PK_FULL1: pack_split_kernel<PK_FULL1><<<grid, PK_THREADS, 0, s>>>(oa, ob, K, ctrl); break;
-        case PK_FULL3: pack_split_kernel<PK_FULL3><<<grid, PK_THREADS, 0, s>>>(oa, ob, K, ctrl); break;
-        case PK_FULLX: pack_split_kernel<PK_FULLX><<<grid, PK_THREADS, 0, s>>>(oa, ob, K, ctrl); break;
-        case PK_DSMALL: pack_split_kernel<PK_DSMALL><<<grid, PK_THREADS, 0, s>>>(oa, ob, K, ctrl); break;
-        case PK_DCROSS: pack_split_kernel<PK_DCROSS><<<grid, PK_THREADS, 0, s>>>(oa, ob, K, ctrl); break;
+        case PK_FULL1: pack_split_kernel<PK_FULL1><<<grid, PK_THREADS, 0, s>>>(oa, ob, K, ctrl, ctrl_words); break;
+        case PK_FULL3: pack_split_kernel<PK_FULL3><<<grid, PK_THREADS, 0, s>>>(oa, ob, K, ctrl, ctrl_words); break;
+        case PK_FULLX: pack_split_kernel<PK_FULLX><<<grid, PK_THREADS, 0, s>>>(oa, ob, K, ctrl, ctrl_words); break;
+        case PK_DSMALL: pack_split_kernel<PK_DSMALL><<<grid, PK_THREADS, 0, s>>>(oa, ob, K, ctrl, ctrl_words); break;
+        case PK_DCROSS: pack_split_kernel<PK_DCROSS><<<grid, PK_THREADS, 0, s>>>(oa, ob, K, ctrl, ctrl_words); break;
         default: return cudaErrorInvalidValue;
     }
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -423,7 +431,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
                     const __grid_constant__ CUtensorMap tmB0, const __grid_constant__ CUtensorMap tmB1, int M, int N,
                     int Kp, float alpha, float beta, float *__restrict__ C, int64_t ldc, int tiles_m, int tiles_n,
                     int group_m, int kc_stages, unsigned int *__restrict__ wave_ctr, int splits,
-                    float *__restrict__ partial, const __grid_constant__ PeerOut peers) {
+                    float *__restrict__ partial, const TcSk sk, const __grid_constant__ PeerOut peers) {
+    if (threadIdx.x == 0) EMM_TL(0);
     using Cfg = TcCfg<TERMS>;
     constexpr bool A1_MN = TERMS == 3 ? A_MN : false;   // cross planes are K-major
     constexpr bool B1_MN = TERMS == 3 ? B_MN : false;
@@ -440,7 +449,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
 
     const int nclus = (int)(gridDim.x >> 1);
     const int cid = (int)(blockIdx.x >> 1);
-    const TcSched S(tiles_m, tiles_n, group_m, Kp, splits);
+    const TcSched S(tiles_m, tiles_n, group_m, Kp, splits, sk.dp_tiles, TC_SK_CHUNK, nclus, cid);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < Cfg::STAGES; ++s) {
@@ -466,10 +475,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (threadIdx.x == 0) EMM_TL(1);
     // PDL: everything above overlapped the previous kernel (the pack pass);
     // from here on this grid reads its outputs (and C, wave counter).
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (threadIdx.x == 0) EMM_TL(2);
 
     if (warp == 0) {
         // ===== TMA producer (both CTAs; each loads its half of A and B) =====
@@ -479,27 +490,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
             const uint64_t pol = policy_evict_normal();
             int it = 0;
             unsigned int done_target = 0;   // CTAs that finished issuing waves 0..w-1
-            for (int t = cid, w = 0; t < S.total_units; t += nclus, ++w) {
-                if (w > 0 && wave_ctr) {
-                    // Wave lockstep: start loading wave w only when every CTA
-                    // has issued all loads of wave w-1, so the ~17 operand
-                    // panels a wave shares stream through L2 once (all CTAs
-                    // are co-resident: grid <= SMs, 1 CTA per SM).
-                    const long long t0 = clock64();
-                    while (true) {
-                        unsigned int v;
-                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(wave_ctr) : "memory");
-                        if (v >= done_target) break;
-                        __nanosleep(128);
-                        if (clock64() - t0 > 40000000000LL) __trap();
+            int cur_wave = 0;
+            for (int i = 0; i < S.n_items; ++i) {
+                const int w = S.wave_of(i);
+                if (w != cur_wave || i == 0) {
+                    if (w > 0 && wave_ctr) {
+                        // Wave lockstep: start loading wave w only when every CTA
+                        // has issued all loads of wave w-1, so the ~17 operand
+                        // panels a wave shares stream through L2 once (all CTAs
+                        // are co-resident: grid <= SMs, 1 CTA per SM).
+                        for (int v = cur_wave; v < w; ++v) done_target += 2u * (unsigned)S.pairs_in_wave(v);
+                        const long long t0 = clock64();
+                        while (true) {
+                            unsigned int v;
+                            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(wave_ctr) : "memory");
+                            if (v >= done_target) break;
+                            __nanosleep(128);
+                            if (clock64() - t0 > 40000000000LL) __trap();
+                        }
                     }
+                    cur_wave = w;
                 }
-                {
-                    const int active = min(nclus, S.total_units - w * nclus);
-                    done_target += 2u * (unsigned)active;
-                }
-                int m0, n0, kb0, kb1, sp;
-                S.unit(t, m0, n0, kb0, kb1, sp);
+                TcWork wk;
+                S.item(i, wk);
+                const int m0 = wk.m0, n0 = wk.n0, kb0 = wk.kb0, kb1 = wk.kb1;
                 const int arow = m0 + (int)rank * TC_BM;
                 const int brow = n0 + (int)rank * TC_BM;
                 for (int kb = kb0; kb < kb1; ++kb, ++it) {
@@ -527,16 +541,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
                         load_plane(&tmB1, st + 3 * TC_TILE_BYTES, brow, B1_MN);
                     }
                 }
-                if (wave_ctr) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(wave_ctr) : "memory");
+                // this CTA has issued every load of its current wave
+                if (wave_ctr && (i + 1 == S.n_items || S.wave_of(i + 1) != cur_wave))
+                    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(wave_ctr) : "memory");
             }
         }
     } else if (warp == 1) {
         if (rank == 0 && lane == 0)
             tc_mma_loop<TERMS, A_MN, B_MN, A1_MN, B1_MN, Cfg::PLANES, Cfg::STAGES, Cfg::STAGE_BYTES>(
-                S, cid, nclus, smem, full, empty, acc_full, acc_empty, tmem_base, kc_stages);
+                S, smem, full, empty, acc_full, acc_empty, tmem_base, kc_stages);
     } else if (warp >= TC_EPI_WARP0) {
-        tc_epilogue_loop(S, cid, nclus, rank, warp & 3, (warp - TC_EPI_WARP0) >> 2, lane, tmem_base, acc_full,
-                         acc_empty, kc_stages, M, N, alpha, beta, C, ldc, partial, peers);
+        tc_epilogue_loop(S, rank, warp & 3, (warp - TC_EPI_WARP0) >> 2, lane, tmem_base, acc_full, acc_empty,
+                         kc_stages, M, N, alpha, beta, C, ldc, partial, sk, peers);
     }
 
     tc_fence_before();
@@ -545,7 +561,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
         tc_fence_after();
         tmem_dealloc_2sm<TC_TMEM_COLS>(tmem_base);
     }
+    if (threadIdx.x == 0) EMM_TL(7);
 }
+
+#ifdef EMM_TIMELINE
+}  // namespace emm
+extern "C" int emm_debug_timeline(unsigned long long *out, int n) {
+    const int m = n < 512 * emm::TL_SLOTS ? n : 512 * emm::TL_SLOTS;
+    return (int)cudaMemcpyFromSymbol(out, emm::g_emm_timeline, (size_t)m * 8);
+}
+namespace emm {
+#endif
 
 // ---------------------------------------------------------------- host side
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
@@ -627,6 +653,73 @@ int tc_splits(int64_t M, int64_t N, int64_t K) {
     return (int)s;
 }
 
+size_t tc_sk_slot_bytes() { return (size_t)(tc_num_sms() / 2) * TC_SK_SLOT_FLOATS * sizeof(float); }
+
+// Stream-K policy (measured on B200): the remainder tiles of
+// the last, partial wave are spread over all CTA pairs only when that
+// recovers a real share of the time: >= 1 full data-parallel wave (those
+// keep the wave lockstep), a remainder <= 0.6 wave, an estimated gain
+// (idle share of the last wave / waves) >= 3%, and a split with 2-3 tensor
+// passes (1xTF32 is fill-bandwidth-bound and measured slower).  E.g. 4096^3
+// 3xTF32 (256 tiles = 3.46 waves) 553 -> 508 us; 8192^3 (13.8 waves) and
+// 3072^3 (1.95 waves) lose a few % to the piece fix-ups.  EMM_SK=0 / 1
+// forces it off / on (where legal).
+bool tc_sk_plan(int64_t M, int64_t N, int64_t K, int splits, int terms, int *dp_tiles) {
+    const char *e = getenv("EMM_SK");
+    const bool force = e && e[0] == '1';
+    if (e && e[0] == '0') return false;
+    if (splits != 1 || K <= 0) return false;
+    const int64_t tiles = ((M + 2 * TC_BM - 1) / (2 * TC_BM)) * ((N + TC_BN - 1) / TC_BN);
+    const int64_t pairs = tc_num_sms() / 2;
+    if (tiles * 2 <= pairs || tiles % pairs == 0 || tiles > 0x3fffffffLL) return false;
+    const int64_t nch = (tc_kpad(K) / TC_BK + TC_SK_CHUNK - 1) / TC_SK_CHUNK;
+    const int64_t waves = tiles / pairs, rem = tiles % pairs;
+    if (!force) {
+        const double gain = (1.0 - (double)rem / (double)pairs) / (double)(waves + 1);
+        if (terms < 2 || waves < 1 || rem > 0.6 * pairs || gain < 0.03) return false;
+    }
+    // EMM_SK_DP=minus1: stream-K over the last full wave + the remainder;
+    // default: every full wave stays data-parallel, only the remainder
+    // tiles are spread over all pairs
+    const char *dpm = getenv("EMM_SK_DP");
+    const bool minus1 = dpm && !strcmp(dpm, "minus1");
+    const int64_t dp = minus1 ? (waves >= 1 ? (waves - 1) * pairs : 0) : waves * pairs;
+    if ((tiles - dp) * nch < pairs || (tiles - dp) * nch > 0x7fffffffLL) return false;   // every range non-empty
+    *dp_tiles = (int)dp;
+    return true;
+}
+
+}  // namespace emm
+
+// Host replay of the device schedule (tests): the work items of every
+// cluster for this shape, 7 ints each (cluster, m0, n0, kb0, kb1, kind,
+// last); returns the item count (or -1 if `cap` is too small).
+extern "C" int emm_debug_schedule(int64_t M, int64_t N, int64_t K, int use_sk, int terms, int *out, int cap) {
+    using namespace emm;
+    const int splits = tc_splits(M, N, K);
+    int dp = 0x7fffffff;
+    int d = 0;
+    if (use_sk && tc_sk_plan(M, N, K, splits, terms, &d)) dp = d;
+    const int tiles_m = (int)((M + 2 * TC_BM - 1) / (2 * TC_BM)), tiles_n = (int)((N + TC_BN - 1) / TC_BN);
+    const int64_t units = tc_units(M, N, splits);
+    const int pairs = tc_num_sms() / 2;
+    const int nclus = dp < 0x7fffffff ? pairs : (int)(units < pairs ? units : pairs);
+    int n = 0;
+    for (int c = 0; c < nclus; ++c) {
+        const TcSched S(tiles_m, tiles_n, 8, (int)tc_kpad(K), splits, dp, TC_SK_CHUNK, nclus, c);
+        for (int i = 0; i < S.n_items; ++i) {
+            TcWork w;
+            S.item(i, w);
+            if (n >= cap) return -1;
+            int *o = out + 7 * n++;
+            o[0] = c; o[1] = w.m0; o[2] = w.n0; o[3] = w.kb0; o[4] = w.kb1; o[5] = w.kind; o[6] = w.last;
+        }
+    }
+    return n;
+}
+
+namespace emm {
+
 int64_t tc_units(int64_t M, int64_t N, int splits) {
     return ((M + 2 * TC_BM - 1) / (2 * TC_BM)) * ((N + TC_BN - 1) / TC_BN) * splits;
 }
@@ -634,7 +727,7 @@ int64_t tc_units(int64_t M, int64_t N, int splits) {
 template <int TERMS, bool A_MN, bool B_MN>
 static cudaError_t launch_tc_t(const TcOperands &ops, int64_t M, int64_t N, int64_t Kp, float alpha, float beta,
                                float *C, int64_t ldc, unsigned int *ctrl, int splits, float *partial, cudaStream_t s,
-                               const PeerOut &peers) {
+                               const PeerOut &peers, void *sk_ws) {
     using Cfg = TcCfg<TERMS>;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
@@ -657,7 +750,15 @@ static cudaError_t launch_tc_t(const TcOperands &ops, int64_t M, int64_t N, int6
     const int64_t units = (int64_t)tiles_m * tiles_n * splits;
     if (units > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
     const int64_t pairs = tc_num_sms() / 2;
-    const int64_t clusters = units < pairs ? units : pairs;   // persistent: one pair per 2 SMs
+    TcSk sk{0x7fffffff, nullptr, nullptr};   // dp_tiles >= tiles: stream-K off
+    int dp = 0;
+    if (sk_ws && tc_sk_plan(M, N, Kp, splits, TERMS, &dp)) {
+        sk.dp_tiles = dp;
+        sk.flags = reinterpret_cast<unsigned int *>(sk_ws);
+        sk.slots = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(sk_ws) + TC_SK_FLAG_BYTES);
+    }
+    // persistent: one pair per 2 SMs (all of them when stream-K spreads the last wave)
+    const int64_t clusters = sk.slots ? pairs : (units < pairs ? units : pairs);
     const int64_t blocks = 2 * clusters;
     cudaEvent_t ev = nullptr;
     prof_begin(s, true, &ev);
@@ -676,7 +777,7 @@ static cudaError_t launch_tc_t(const TcOperands &ops, int64_t M, int64_t N, int6
         cfg.numAttrs = 1;
         cudaError_t le = cudaLaunchKernelEx(&cfg, tc_sgemm_kernel<TERMS, A_MN, B_MN>, ta0, ta1, tb0, tb1, (int)M,
                                             (int)N, (int)Kp, alpha, beta, C, ldc, tiles_m, tiles_n, group_m,
-                                            kc_stages, ctrl, splits, splits > 1 ? partial : nullptr, peers);
+                                            kc_stages, ctrl, splits, splits > 1 ? partial : nullptr, sk, peers);
         if (le != cudaSuccess) return le;
     }
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -689,28 +790,28 @@ static cudaError_t launch_tc_t(const TcOperands &ops, int64_t M, int64_t N, int6
 template <int TERMS>
 static cudaError_t launch_tc_m(const TcOperands &ops, int64_t M, int64_t N, int64_t Kp, float alpha, float beta,
                                float *C, int64_t ldc, unsigned int *ctrl, int splits, float *partial, cudaStream_t s,
-                               const PeerOut &pe) {
+                               const PeerOut &pe, void *sk) {
     const bool am = ops.a0.mn, bm = ops.b0.mn;
     if (!am && !bm)
-        return launch_tc_t<TERMS, false, false>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe);
+        return launch_tc_t<TERMS, false, false>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe, sk);
     if (!am && bm)
-        return launch_tc_t<TERMS, false, true>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe);
+        return launch_tc_t<TERMS, false, true>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe, sk);
     if (am && !bm)
-        return launch_tc_t<TERMS, true, false>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe);
-    return launch_tc_t<TERMS, true, true>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe);
+        return launch_tc_t<TERMS, true, false>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe, sk);
+    return launch_tc_t<TERMS, true, true>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe, sk);
 }
 
 cudaError_t launch_tc_sgemm(int terms, const TcOperands &ops, int64_t M, int64_t N, int64_t K, float alpha,
                             float beta, float *C, int64_t ldc, unsigned int *ctrl, int splits, float *partial,
-                            cudaStream_t s, const PeerOut *peers) {
+                            cudaStream_t s, const PeerOut *peers, void *sk_ws) {
     if (M > 0x7fffffffLL || N > 0x7fffffffLL || K > 0x7fffffffLL - 32) return cudaErrorInvalidValue;
     if (splits < 1 || (splits > 1 && !partial)) return cudaErrorInvalidValue;
     if (peers && (peers->n < 0 || peers->n > 8 || splits > 1)) return cudaErrorInvalidValue;
     const PeerOut pe = peers ? *peers : PeerOut{};
     const int64_t Kp = tc_kpad(K);
-    if (terms == 3) return launch_tc_m<3>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe);
-    if (terms == 2) return launch_tc_m<2>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe);
-    return launch_tc_m<1>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe);
+    if (terms == 3) return launch_tc_m<3>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe, sk_ws);
+    if (terms == 2) return launch_tc_m<2>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe, sk_ws);
+    return launch_tc_m<1>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe, sk_ws);
 }
 
 }  // namespace emm

@@ -201,7 +201,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TL_THREADS, 1)
     const uint32_t rank = cluster_ctarank();
     const int nclus = (int)(gridDim.x >> 1);
     const int cid = (int)(blockIdx.x >> 1);
-    const TcSched S(tiles_m, tiles_n, group_m, Kp, splits);
+    const TcSched S(tiles_m, tiles_n, group_m, Kp, splits, 0x7fffffff /*no stream-K*/, 8, nclus, cid);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < TL_STAGES; ++s) {
@@ -227,7 +227,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TL_THREADS, 1)
         setmaxnreg_dec<TL_REGS_WG0>();
         if (warp == 0 && rank == 0 && lane == 0)
             tc_mma_loop<3, false, false, false, false, 2, TL_STAGES, TL_STAGE_BYTES>(
-                S, cid, nclus, smem, full, empty, acc_full, acc_empty, tmem_base, kc_stages);
+                S, smem, full, empty, acc_full, acc_empty, tmem_base, kc_stages);
     } else if (warp < TL_EPI_WARP0) {
         setmaxnreg_dec<TL_REGS_PROD>();
         // ===== producers: LDG -> split -> STS, both CTAs (each its 128 rows of A and of B) =====
@@ -235,7 +235,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TL_THREADS, 1)
         const uint32_t leader_full0 = mapa_leader(&full[0]);
         int it = 0;
         unsigned int done_target = 0;
-        for (int t = cid, w = 0; t < S.total_units; t += nclus, ++w) {
+        for (int i = 0; i < S.n_items; ++i) {
+            const int w = i;   // no stream-K here: item i is wave i
             if (w > 0 && wave_ctr) {
                 // wave lockstep (see k_tc.cu): every producer warp of every CTA
                 // finished loading wave w-1
@@ -251,9 +252,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TL_THREADS, 1)
                 }
                 __syncwarp();
             }
-            done_target += 2u * TL_PROD_WARPS * (unsigned)min(nclus, S.total_units - w * nclus);
-            int m0, n0, kb0, kb1, sp;
-            S.unit(t, m0, n0, kb0, kb1, sp);
+            done_target += 2u * TL_PROD_WARPS * (unsigned)S.pairs_in_wave(w);
+            TcWork wk;
+            S.item(i, wk);
+            const int m0 = wk.m0, n0 = wk.n0, kb0 = wk.kb0, kb1 = wk.kb1;
             const int arow = m0 + (int)rank * TC_BM;
             const int brow = n0 + (int)rank * TC_BM;
             for (int kb = kb0; kb < kb1; ++kb, ++it) {
@@ -275,8 +277,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TL_THREADS, 1)
         }
     } else {
         setmaxnreg_inc<TL_REGS_EPI>();
-        tc_epilogue_loop(S, cid, nclus, rank, warp & 3, (warp - TL_EPI_WARP0) >> 2, lane, tmem_base, acc_full,
-                         acc_empty, kc_stages, M, N, alpha, beta, C, ldc, partial, peers);
+        tc_epilogue_loop(S, rank, warp & 3, (warp - TL_EPI_WARP0) >> 2, lane, tmem_base, acc_full, acc_empty,
+                         kc_stages, M, N, alpha, beta, C, ldc, partial, TcSk{0x7fffffff, nullptr, nullptr}, peers);
     }
 
     tc_fence_before();
@@ -346,19 +348,19 @@ cudaError_t launch_tc_split_sgemm(bool a_kc, bool b_kc, const float *A, int64_t 
     const PeerOut pe = peers ? *peers : PeerOut{};
     const TlOperand a{A, lda, (int)M}, b{B, ldb, (int)N};
     const bool vec = tl_vec_ok(A, lda) && tl_vec_ok(B, ldb);
-#define EMM_TL(AK, BK, V) \
+#define EMM_TLX(AK, BK, V) \
     return launch_tl_t<AK, BK, V>(a, b, M, N, K, alpha, beta, C, ldc, ctrl, splits, partial, s, pe)
     if (vec) {
-        if (a_kc && b_kc) EMM_TL(true, true, true);
-        if (a_kc && !b_kc) EMM_TL(true, false, true);
-        if (!a_kc && b_kc) EMM_TL(false, true, true);
-        EMM_TL(false, false, true);
+        if (a_kc && b_kc) EMM_TLX(true, true, true);
+        if (a_kc && !b_kc) EMM_TLX(true, false, true);
+        if (!a_kc && b_kc) EMM_TLX(false, true, true);
+        EMM_TLX(false, false, true);
     }
-    if (a_kc && b_kc) EMM_TL(true, true, false);
-    if (a_kc && !b_kc) EMM_TL(true, false, false);
-    if (!a_kc && b_kc) EMM_TL(false, true, false);
-    EMM_TL(false, false, false);
-#undef EMM_TL
+    if (a_kc && b_kc) EMM_TLX(true, true, false);
+    if (a_kc && !b_kc) EMM_TLX(true, false, false);
+    if (!a_kc && b_kc) EMM_TLX(false, true, false);
+    EMM_TLX(false, false, false);
+#undef EMM_TLX
 }
 
 }  // namespace emm

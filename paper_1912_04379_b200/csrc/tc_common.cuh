@@ -18,6 +18,22 @@
 
 namespace emm {
 
+// Debug timeline (build with EMM_TIMELINE=1 -> libemm_tl.so; never in the
+// product library): %globaltimer stamps per CTA at fixed points of the
+// kernel, read back with emm_debug_timeline().
+#ifdef EMM_TIMELINE
+constexpr int TL_SLOTS = 8;
+static __device__ unsigned long long g_emm_timeline[512][TL_SLOTS];
+__device__ __forceinline__ void emm_tl_mark(int slot) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (blockIdx.x < 512) g_emm_timeline[blockIdx.x][slot] = t;
+}
+#define EMM_TL(slot) emm_tl_mark(slot)
+#else
+#define EMM_TL(slot) ((void)0)
+#endif
+
 constexpr int TC_BK = 32;            // K per stage: one 128-byte swizzle row of FP32
 constexpr int TC_BM = 128;           // rows of A per CTA (UMMA M = 256 per pair)
 constexpr int TC_BN = 256;           // columns of C per pair (UMMA N)
@@ -25,34 +41,108 @@ constexpr int TC_TILE_BYTES = 128 * TC_BK * 4;   // one 128 x 32 FP32 operand ti
 constexpr int TC_EPI_WARPS = 8;      // 2 per TMEM lane quarter, 128 columns each
 constexpr int TC_TMEM_COLS = 512;    // 2 accumulator buffers of 256 columns
 
-// Persistent schedule: cluster `cid` walks work units cid, cid + nclus, ...
-// Units are (split, tile), split-major, tiles in grouped raster order along M
+// Work item kinds.
+enum { TW_FULL = 0,     // whole tile -> C (alpha/beta epilogue)
+       TW_SPLITK = 1,   // split-K unit -> raw partial plane `sp` (fixed-order reduce launch, KN8)
+       TW_PUB = 2,      // stream-K piece not starting at k = 0 -> raw partial in slot `cid`
+       TW_OWN = 3 };    // stream-K piece starting at k = 0 -> C, after adding the partials
+                        // of the same tile published by clusters cid+1 .. last (ascending k)
+struct TcWork {
+    int m0, n0, kb0, kb1, kind, sp, last;
+};
+
+// Stream-K scratch: one partial slot per cluster (a
+// cluster publishes at most one piece: the first of its range) + one flag
+// per (slot, CTA, epilogue warp).  Slot layout [rank][warp][32 float4 groups][lane].
+constexpr int TC_SK_SLOT_FLOATS = 2 * TC_EPI_WARPS * 32 * 32 * 4;   // 256 x 256 floats
+constexpr int TC_SK_FLAGS_PER_SLOT = 2 * TC_EPI_WARPS;
+struct TcSk {
+    int dp_tiles;            // tiles of the data-parallel phase; >= tiles: stream-K off
+    float *slots;            // [nclus][TC_SK_SLOT_FLOATS]
+    unsigned int *flags;     // [nclus][TC_SK_FLAGS_PER_SLOT], zero at launch
+};
+
+// Persistent schedule.  Tiles are numbered in grouped raster order along M
 // (GPU-L2 analogue of the paper's L2 blocking): one "wave"
 // of clusters covers a compact group_m x ~(nclus / group_m) block of tiles.
+//  * split-K (splits > 1, sub-wave problems): units (split, tile), split-
+//    major; cluster cid takes units cid, cid + nclus, ...
+//  * data-parallel + stream-K: the first dp_tiles tiles (whole waves) go
+//    round-robin; the remaining tiles' K-chunks (kc stages each) are cut
+//    into nclus equal contiguous ranges, one per cluster, so the last
+//    (partial) wave keeps every SM busy.  A cluster's range is walked in
+//    ascending order: its first piece may be the tail of a tile (TW_PUB, its
+//    partial is published early), its last piece the head of another tile
+//    (TW_OWN, finished last, when the tail pieces are already published).
+//    The tile's sum is own + P(cid+1) + ... in ascending k: deterministic.
+__host__ __device__ __forceinline__ int tc_imin(int a, int b) { return a < b ? a : b; }
+
 struct TcSched {
     int tiles_m, tiles_n, group_m, nkb, splits, nkb_s, total_tiles, total_units;
-    __device__ __forceinline__ TcSched(int tm, int tn, int gm, int Kp, int sp)
-        : tiles_m(tm), tiles_n(tn), group_m(gm), nkb(Kp / TC_BK), splits(sp) {
+    int nclus, cid;
+    bool sk;
+    int dp_tiles, kc, nch, Wsk, a, b, n_dp, n_items, dp_waves;
+    __host__ __device__ __forceinline__ TcSched(int tm, int tn, int gm, int Kp, int sp, int dp, int kc_, int nclus_, int cid_)
+        : tiles_m(tm), tiles_n(tn), group_m(gm), nkb(Kp / TC_BK), splits(sp), nclus(nclus_), cid(cid_) {
         nkb_s = (nkb + splits - 1) / splits;
         total_tiles = tiles_m * tiles_n;
         total_units = total_tiles * splits;
+        sk = splits == 1 && dp < total_tiles;
+        dp_tiles = sk ? dp : total_tiles;
+        kc = kc_;
+        nch = (nkb + kc - 1) / kc;
+        Wsk = sk ? (total_tiles - dp_tiles) * nch : 0;
+        a = (int)((long long)cid * Wsk / nclus);
+        b = (int)((long long)(cid + 1) * Wsk / nclus);
+        const int dpu = sk ? dp_tiles : total_units;
+        n_dp = cid < dpu ? (dpu - cid + nclus - 1) / nclus : 0;
+        n_items = n_dp + ((sk && a < b) ? (b - 1) / nch - a / nch + 1 : 0);
+        dp_waves = dp_tiles / nclus;
     }
-    __device__ __forceinline__ void tile_origin(int t, int &m0, int &n0) const {
+    __host__ __device__ __forceinline__ void tile_origin(int t, int &m0, int &n0) const {
         const int per_group = group_m * tiles_n;
         const int g = t / per_group;
         const int first_m = g * group_m;
-        const int gsize = min(tiles_m - first_m, group_m);
+        const int gsize = tc_imin(tiles_m - first_m, group_m);
         const int tm = first_m + (t % per_group) % gsize;
         const int tn = (t % per_group) / gsize;
         m0 = tm * (2 * TC_BM);
         n0 = tn * TC_BN;
     }
-    // unit u covers K stages [kb0, kb1) of its tile, split index sp
-    __device__ __forceinline__ void unit(int u, int &m0, int &n0, int &kb0, int &kb1, int &sp) const {
-        sp = u / total_tiles;
-        tile_origin(u - sp * total_tiles, m0, n0);
-        kb0 = sp * nkb_s;
-        kb1 = min(nkb, kb0 + nkb_s);
+    __host__ __device__ __forceinline__ void item(int i, TcWork &w) const {
+        w.sp = 0;
+        w.last = 0;
+        if (i < n_dp) {
+            const int u = cid + i * nclus;
+            w.sp = u / total_tiles;
+            tile_origin(u - w.sp * total_tiles, w.m0, w.n0);
+            w.kb0 = w.sp * nkb_s;
+            w.kb1 = tc_imin(nkb, w.kb0 + nkb_s);
+            w.kind = splits > 1 ? TW_SPLITK : TW_FULL;
+            return;
+        }
+        const int j = i - n_dp;
+        const int s0 = j == 0 ? a : (a / nch + j) * nch;   // later pieces start at tile boundaries
+        const int tl = s0 / nch;
+        const int e0 = tc_imin(b, (tl + 1) * nch);
+        const int srel = s0 - tl * nch, erel = e0 - tl * nch;
+        tile_origin(dp_tiles + tl, w.m0, w.n0);
+        w.kb0 = srel * kc;
+        w.kb1 = tc_imin(nkb, erel * kc);
+        if (srel == 0 && erel == nch) {
+            w.kind = TW_FULL;
+        } else if (srel == 0) {
+            w.kind = TW_OWN;
+            const long long x = (long long)(tl + 1) * nch - 1;          // the tile's last chunk
+            w.last = (int)(((x + 1) * nclus - 1) / Wsk);                 // the cluster holding it
+        } else {
+            w.kind = TW_PUB;
+        }
+    }
+    // wave-lockstep bookkeeping (producers): wave of item i, CTA pairs in a wave
+    __host__ __device__ __forceinline__ int wave_of(int i) const { return i < n_dp ? i : dp_waves; }
+    __host__ __device__ __forceinline__ int pairs_in_wave(int w) const {
+        return sk ? nclus : tc_imin(nclus, total_units - w * nclus);
     }
 };
 
@@ -61,7 +151,7 @@ struct TcSched {
 // [A | B] (PLANES == 1).  TERMS: 3 = 3xTF32 (small*big + big*small +
 // big*big), 2 = TF32+BF16 (bf16 cross pair as one K16 MMA + big*big), 1.
 template <int TERMS, bool A_MN, bool B_MN, bool A1_MN, bool B1_MN, int PLANES, int STAGES, int STAGE_BYTES>
-__device__ __forceinline__ void tc_mma_loop(const TcSched &S, int cid, int nclus, uint8_t *smem, uint64_t *full,
+__device__ __forceinline__ void tc_mma_loop(const TcSched &S, uint8_t *smem, uint64_t *full,
                                             uint64_t *empty, uint64_t *acc_full, uint64_t *acc_empty,
                                             uint32_t tmem_base, int kc_stages) {
     using namespace ptx;
@@ -72,9 +162,10 @@ __device__ __forceinline__ void tc_mma_loop(const TcSched &S, int cid, int nclus
         return mn ? desc_mnmajor_sw128_32b(addr + (uint32_t)(k * 1024)) : desc_kmajor_sw128(addr + (uint32_t)(k * 32));
     };
     int it = 0, ch = 0;   // global stage / chunk counters (continue across tiles)
-    for (int t = cid; t < S.total_units; t += nclus) {
-        int m0, n0, kb0, kb1, sp;
-        S.unit(t, m0, n0, kb0, kb1, sp);
+    for (int i = 0; i < S.n_items; ++i) {
+        TcWork w;
+        S.item(i, w);
+        const int kb0 = w.kb0, kb1 = w.kb1;
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
             const bool first = ((kb - kb0) % kc_stages) == 0;
             const bool last = ((kb - kb0) % kc_stages) == kc_stages - 1 || kb == kb1 - 1;
@@ -88,6 +179,7 @@ __device__ __forceinline__ void tc_mma_loop(const TcSched &S, int cid, int nclus
             const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
             mbar_wait(&full[s], ph);
             tc_fence_after();
+            if (it == 0) EMM_TL(3);
             const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
             const uint32_t a0 = st, a1 = st + TC_TILE_BYTES;
             const uint32_t b0 = st + PLANES * TC_TILE_BYTES, b1 = b0 + TC_TILE_BYTES;
@@ -115,22 +207,26 @@ __device__ __forceinline__ void tc_mma_loop(const TcSched &S, int cid, int nclus
             }
         }
     }
+    EMM_TL(4);
 }
 
 // ===== epilogue: TMEM -> FP32 registers (promotion) -> alpha/beta -> C =====
 // Warp with TMEM lane quarter q (= warp % 4) and column half h.
-__device__ __forceinline__ void tc_epilogue_loop(const TcSched &S, int cid, int nclus, uint32_t rank, int q, int h,
-                                                 int lane, uint32_t tmem_base, uint64_t *acc_full,
-                                                 uint64_t *acc_empty, int kc_stages, int M, int N, float alpha,
-                                                 float beta, float *__restrict__ C, int64_t ldc,
-                                                 float *__restrict__ partial, const PeerOut &peers) {
+__device__ __forceinline__ void tc_epilogue_loop(const TcSched &S, uint32_t rank, int q, int h, int lane,
+                                                 uint32_t tmem_base, uint64_t *acc_full, uint64_t *acc_empty,
+                                                 int kc_stages, int M, int N, float alpha, float beta,
+                                                 float *__restrict__ C, int64_t ldc, float *__restrict__ partial,
+                                                 const TcSk &sk, const PeerOut &peers) {
     using namespace ptx;
     uint32_t leader_empty0;
     asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(leader_empty0) : "r"(smem_u32(&acc_empty[0])));
+    // this warp's stream-K slot part / flag index (warp id within the CTA's 8)
+    const int wslot = (int)rank * TC_EPI_WARPS + h * 4 + q;
     int ch = 0;
-    for (int t = cid; t < S.total_units; t += nclus) {
-        int m0, n0, kb0, kb1, sp;
-        S.unit(t, m0, n0, kb0, kb1, sp);
+    for (int i = 0; i < S.n_items; ++i) {
+        TcWork w;
+        S.item(i, w);
+        const int m0 = w.m0, n0 = w.n0, kb0 = w.kb0, kb1 = w.kb1, sp = w.sp;
         const int nchunks = (kb1 - kb0 + kc_stages - 1) / kc_stages;
         const int row = m0 + (int)rank * TC_BM + 32 * q + lane;
         float acc[128];
@@ -140,6 +236,7 @@ __device__ __forceinline__ void tc_epilogue_loop(const TcSched &S, int cid, int 
             const int b = ch & 1;
             mbar_wait(&acc_full[b], ((uint32_t)ch >> 1) & 1u);
             tc_fence_after();
+            if (ch == 0 && q == 0 && h == 0 && lane == 0) EMM_TL(5);
             const uint32_t tb = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(b * TC_BN + h * 128);
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
@@ -156,7 +253,52 @@ __device__ __forceinline__ void tc_epilogue_loop(const TcSched &S, int cid, int 
                 asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(eb) : "memory");
             }
         }
-        if (partial) {
+        if (w.kind == TW_PUB) {
+            // stream-K tail piece: raw partial -> slot cid (coalesced float4
+            // layout, all 256 x 256 entries), then this warp's flag (release)
+            float4 *slot = reinterpret_cast<float4 *>(sk.slots + (size_t)S.cid * TC_SK_SLOT_FLOATS) +
+                           (size_t)wslot * 32 * 32 + lane;
+#pragma unroll
+            for (int g = 0; g < 32; ++g)
+                __stcg(slot + g * 32, make_float4(acc[4 * g], acc[4 * g + 1], acc[4 * g + 2], acc[4 * g + 3]));
+            __threadfence();
+            __syncwarp();
+            if (lane == 0) {
+                unsigned int *f = sk.flags + (size_t)S.cid * TC_SK_FLAGS_PER_SLOT + wslot;
+                asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f), "r"(1u) : "memory");
+            }
+            continue;
+        }
+        if (w.kind == TW_OWN) {
+            // stream-K head piece: add the tile's other pieces in ascending k
+            for (int c = S.cid + 1; c <= w.last; ++c) {
+                const unsigned int *f = sk.flags + (size_t)c * TC_SK_FLAGS_PER_SLOT + wslot;
+                const long long t0 = clock64();
+                while (true) {
+                    unsigned int v;
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+                    if (v) break;
+                    __nanosleep(64);
+                    if (clock64() - t0 > 40000000000LL) __trap();
+                }
+                const float4 *slot = reinterpret_cast<const float4 *>(sk.slots + (size_t)c * TC_SK_SLOT_FLOATS) +
+                                     (size_t)wslot * 32 * 32 + lane;
+#pragma unroll
+                for (int g0 = 0; g0 < 32; g0 += 8) {
+                    float4 v[8];
+#pragma unroll
+                    for (int g = 0; g < 8; ++g) v[g] = __ldcg(slot + (g0 + g) * 32);
+#pragma unroll
+                    for (int g = 0; g < 8; ++g) {
+                        acc[4 * (g0 + g)] += v[g].x;
+                        acc[4 * (g0 + g) + 1] += v[g].y;
+                        acc[4 * (g0 + g) + 2] += v[g].z;
+                        acc[4 * (g0 + g) + 3] += v[g].w;
+                    }
+                }
+            }
+        }
+        if (w.kind == TW_SPLITK) {
             // split-K: publish the raw FP32 partial of split sp; the reduce
             // launch (KN8) sums the S partials in fixed order.
             if (row < M) {
@@ -209,6 +351,7 @@ __device__ __forceinline__ void tc_epilogue_loop(const TcSched &S, int cid, int 
             if (peers.n) __threadfence_system();
         }
     }
+    if (q == 0 && h == 0 && lane == 0) EMM_TL(6);
 }
 
 }  // namespace emm

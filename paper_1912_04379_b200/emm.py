@@ -12,7 +12,9 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "libemm.so")
+# EMM_LIB: alternative in-tree build of the same library (e.g. the debug
+# timeline build libemm_tl.so, tools/timeline.py)
+_LIB_PATH = os.path.join(_HERE, os.environ.get("EMM_LIB", "libemm.so"))
 
 MATH = {"3xtf32": 0, "ffma": 1, "1xtf32": 2, "tf32bf16": 3}
 
