@@ -229,7 +229,7 @@ static Plan make_plan(char tA, char tB, int64_t M, int64_t N, int64_t K, emm_mat
     P.a_off = 0;
     P.b_off = align_up(a_bytes, 1024);
     P.p_off = P.b_off + align_up(b_bytes, 1024);
-    P.ctr_off = P.p_off + (P.splits > 1 ? align_up((size_t)P.splits * M * N * 4, 1024) : 0);
+    P.ctr_off = P.p_off + align_up(tc_splitk_bytes(M, N, P.splits), 1024);
     int dp = 0;
     P.sk = tc_sk_plan(M, N, K, P.splits, P.terms, &dp);
     P.total = P.ctr_off + TC_CTRL_BYTES + (P.sk ? TC_SK_FLAG_BYTES + tc_sk_slot_bytes() : 0);
@@ -296,7 +296,7 @@ extern "C" int emm_sgemm_ex(char transA, char transB, int64_t M, int64_t N, int6
         // KN11: split inside the kernel (no split pass, no operand workspace)
         const int splits = tc_splits(M, N, K);
         const bool multiwave = tc_units(M, N, splits) > tc_num_sms() / 2;
-        const size_t p_bytes = splits > 1 ? align_up((size_t)splits * M * N * 4, 1024) : 0;
+        const size_t p_bytes = align_up(tc_splitk_bytes(M, N, splits), 1024);
         const size_t need = (splits > 1 || multiwave) ? p_bytes + 1024 : 0;
         void *ws = workspace;
         bool own = false;

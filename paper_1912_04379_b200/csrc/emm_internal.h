@@ -68,6 +68,8 @@ cudaError_t launch_pack(int mode, const PackArgs &a, const PackArgs *b, int64_t 
 constexpr size_t TC_CTRL_BYTES = 1024;
 constexpr size_t TC_SK_FLAG_BYTES = 8192;
 size_t tc_sk_slot_bytes();
+// split-K partials: one 256 x 256 FP32 slot per (split, tile) unit
+size_t tc_splitk_bytes(int64_t M, int64_t N, int splits);
 // Stream-K for this shape?  dp_tiles: tiles of the data-
 // parallel phase; false for split-K / exact-wave / tiny-remainder shapes.
 bool tc_sk_plan(int64_t M, int64_t N, int64_t K, int splits, int terms, int *dp_tiles);

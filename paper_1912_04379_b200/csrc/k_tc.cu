@@ -330,54 +330,71 @@ cudaError_t launch_pack(int mode, const PackArgs &a, const PackArgs *b, int64_t 
 
 // =====================================================================
 // KN8: split-K reduction.  C <- alpha * (P_0 + ... + P_{S-1}) + beta*C, the
-// partials summed in fixed order s = 0..S-1 (deterministic).  P_s is M x N
-// with ld = M.  Grid (ceil(M/1024), N): 4 rows per thread, block column = j.
+// partials summed in fixed order s = 0..S-1 (deterministic).  P_s of tile t
+// is the 256 x 256 slot (s*tiles + t) in the epilogue's coalesced layout
+// [rank][warp w = h*4 + q][32 float4 column groups][lane] (tc_common.cuh):
+// row = m0 + 128 rank + 32 q + lane, columns n0 + 128 h + 4g .. +3.
+// Block = one (tile, rank, warp) 32 x 128 part: 8 threads per lane-row set,
+// thread handles 4 column groups; grid (tiles * 16, 1).
 // =====================================================================
-__global__ void __launch_bounds__(256) splitk_reduce_kernel(const float *__restrict__ P, int S, int64_t M, int64_t N,
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const float *__restrict__ P, int S, int M, int N,
                                                             float alpha, float beta, float *__restrict__ C,
-                                                            int64_t ldc) {
+                                                            int64_t ldc, int tiles_m, int tiles_n, int group_m) {
     asm volatile("griddepcontrol.wait;" ::: "memory");   // PDL: the GEMM's partials
-    // 4 rows per thread (stride 256): 4*(S+1) independent loads in flight
-    const int64_t j = blockIdx.y;
-    const int64_t i0 = (int64_t)blockIdx.x * 1024 + threadIdx.x;
-    const int64_t plane = M * N;
-    float acc[4];
+    const int part = blockIdx.x & 15, t = blockIdx.x >> 4;
+    const int rank = part >> 3, wslot = part & 7, h = wslot >> 2, q = wslot & 3;
+    const int lane = threadIdx.x & 31, gq = threadIdx.x >> 5;   // 8 x 4 column groups
+    // tile origin: the same grouped raster as the GEMM's schedule
+    const int per_group = group_m * tiles_n;
+    const int gidx = t / per_group, first_m = gidx * group_m;
+    const int gsize = min(tiles_m - first_m, group_m);
+    const int m0 = (first_m + (t % per_group) % gsize) * 256, n0 = ((t % per_group) / gsize) * 256;
+    const int row = m0 + 128 * rank + 32 * q + lane;
+    const int tiles = tiles_m * tiles_n;
+    const float4 *base = reinterpret_cast<const float4 *>(P) + (size_t)t * (TC_SK_SLOT_FLOATS / 4) +
+                         (size_t)wslot * 1024 + (size_t)rank * 8 * 1024 + lane;
+    const size_t sstride = (size_t)tiles * (TC_SK_SLOT_FLOATS / 4);
+    float4 acc[4];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-        const int64_t i = i0 + 256 * r;
-        acc[r] = i < M ? __ldcg(P + i + j * M) : 0.0f;
-    }
+    for (int j = 0; j < 4; ++j) acc[j] = __ldcg(base + (4 * gq + j) * 32);
     for (int s = 1; s < S; ++s) {
-        float v[4];
+        float4 v[4];
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            const int64_t i = i0 + 256 * r;
-            v[r] = i < M ? __ldcg(P + (int64_t)s * plane + i + j * M) : 0.0f;
+        for (int j = 0; j < 4; ++j) v[j] = __ldcg(base + (size_t)s * sstride + (4 * gq + j) * 32);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            acc[j].x += v[j].x;
+            acc[j].y += v[j].y;
+            acc[j].z += v[j].z;
+            acc[j].w += v[j].w;
         }
-#pragma unroll
-        for (int r = 0; r < 4; ++r) acc[r] += v[r];
     }
-    float cin[4];
+    if (row >= M) return;
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-        const int64_t i = i0 + 256 * r;
-        cin[r] = (beta != 0.0f && i < M) ? C[i + j * ldc] : 0.0f;
-    }
+    for (int j = 0; j < 4; ++j) {
+        const float r[4] = {acc[j].x, acc[j].y, acc[j].z, acc[j].w};
+        const int c0 = n0 + 128 * h + 4 * (4 * gq + j);
+        float cin[4];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-        const int64_t i = i0 + 256 * r;
-        if (i < M) C[i + j * ldc] = beta == 0.0f ? alpha * acc[r] : fmaf(beta, cin[r], alpha * acc[r]);
+        for (int e = 0; e < 4; ++e)
+            cin[e] = (beta != 0.0f && c0 + e < N) ? C[(int64_t)row + (int64_t)(c0 + e) * ldc] : 0.0f;
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            if (c0 + e < N)
+                C[(int64_t)row + (int64_t)(c0 + e) * ldc] = beta == 0.0f ? alpha * r[e] : fmaf(beta, cin[e], alpha * r[e]);
     }
 }
 
 cudaError_t launch_splitk_reduce(const float *partial, int splits, int64_t M, int64_t N, float alpha, float beta,
                                  float *C, int64_t ldc, cudaStream_t s) {
-    if (N > 65535) return cudaErrorInvalidConfiguration;
+    const int tiles_m = (int)((M + 2 * TC_BM - 1) / (2 * TC_BM)), tiles_n = (int)((N + TC_BN - 1) / TC_BN);
+    const int64_t blocks = (int64_t)tiles_m * tiles_n * 16;
+    if (blocks > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
     cudaEvent_t ev = nullptr;
     prof_begin(s, false, &ev);
     {
         cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3((unsigned)((M + 1023) / 1024), (unsigned)N);
+        cfg.gridDim = dim3((unsigned)blocks);
         cfg.blockDim = dim3(256);
         cfg.stream = s;
         cudaLaunchAttribute at[1];
@@ -385,7 +402,8 @@ cudaError_t launch_splitk_reduce(const float *partial, int splits, int64_t M, in
         at[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        cudaError_t le = cudaLaunchKernelEx(&cfg, splitk_reduce_kernel, partial, splits, M, N, alpha, beta, C, ldc);
+        cudaError_t le = cudaLaunchKernelEx(&cfg, splitk_reduce_kernel, partial, splits, (int)M, (int)N, alpha, beta,
+                                            C, ldc, tiles_m, tiles_n, 8);
         if (le != cudaSuccess) return le;
     }
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -651,6 +669,10 @@ int tc_splits(int64_t M, int64_t N, int64_t K) {
     if (s < 1) s = 1;
     while (s > 1 && (tiles * s > clusters || ((nkb + s - 1) / s) * (s - 1) >= nkb)) --s;
     return (int)s;
+}
+
+size_t tc_splitk_bytes(int64_t M, int64_t N, int splits) {
+    return splits > 1 ? (size_t)tc_units(M, N, splits) * TC_SK_SLOT_FLOATS * sizeof(float) : 0;
 }
 
 size_t tc_sk_slot_bytes() { return (size_t)(tc_num_sms() / 2) * TC_SK_SLOT_FLOATS * sizeof(float); }

@@ -43,12 +43,12 @@ constexpr int TC_TMEM_COLS = 512;    // 2 accumulator buffers of 256 columns
 
 // Work item kinds.
 enum { TW_FULL = 0,     // whole tile -> C (alpha/beta epilogue)
-       TW_SPLITK = 1,   // split-K unit -> raw partial plane `sp` (fixed-order reduce launch, KN8)
+       TW_SPLITK = 1,   // split-K unit -> raw partial in slot (sp, tile) (fixed-order reduce launch, KN8)
        TW_PUB = 2,      // stream-K piece not starting at k = 0 -> raw partial in slot `cid`
        TW_OWN = 3 };    // stream-K piece starting at k = 0 -> C, after adding the partials
                         // of the same tile published by clusters cid+1 .. last (ascending k)
 struct TcWork {
-    int m0, n0, kb0, kb1, kind, sp, last;
+    int m0, n0, kb0, kb1, kind, sp, last, tile;
 };
 
 // Stream-K scratch: one partial slot per cluster (a
@@ -115,7 +115,8 @@ struct TcSched {
         if (i < n_dp) {
             const int u = cid + i * nclus;
             w.sp = u / total_tiles;
-            tile_origin(u - w.sp * total_tiles, w.m0, w.n0);
+            w.tile = u - w.sp * total_tiles;
+            tile_origin(w.tile, w.m0, w.n0);
             w.kb0 = w.sp * nkb_s;
             w.kb1 = tc_imin(nkb, w.kb0 + nkb_s);
             w.kind = splits > 1 ? TW_SPLITK : TW_FULL;
@@ -126,7 +127,8 @@ struct TcSched {
         const int tl = s0 / nch;
         const int e0 = tc_imin(b, (tl + 1) * nch);
         const int srel = s0 - tl * nch, erel = e0 - tl * nch;
-        tile_origin(dp_tiles + tl, w.m0, w.n0);
+        w.tile = dp_tiles + tl;
+        tile_origin(w.tile, w.m0, w.n0);
         w.kb0 = srel * kc;
         w.kb1 = tc_imin(nkb, erel * kc);
         if (srel == 0 && erel == nch) {
@@ -299,16 +301,15 @@ __device__ __forceinline__ void tc_epilogue_loop(const TcSched &S, uint32_t rank
             }
         }
         if (w.kind == TW_SPLITK) {
-            // split-K: publish the raw FP32 partial of split sp; the reduce
-            // launch (KN8) sums the S partials in fixed order.
-            if (row < M) {
-                const int col0 = n0 + h * 128;
-                float *pp = partial + (int64_t)sp * M * N + (int64_t)row + (int64_t)col0 * M;
-                const int jmax = min(128, N - col0);
+            // split-K: publish the raw FP32 partial of split sp into its slot
+            // (coalesced float4 layout, all 256 x 256 entries); the reduce
+            // launch (KN8) sums the S slots of a tile in fixed order.
+            float4 *slot = reinterpret_cast<float4 *>(partial + ((size_t)sp * S.total_tiles + w.tile) *
+                                                                   TC_SK_SLOT_FLOATS) +
+                           (size_t)wslot * 32 * 32 + lane;
 #pragma unroll
-                for (int j = 0; j < 128; ++j, pp += M)
-                    if (j < jmax) *pp = acc[j];
-            }
+            for (int g = 0; g < 32; ++g)
+                __stcg(slot + g * 32, make_float4(acc[4 * g], acc[4 * g + 1], acc[4 * g + 2], acc[4 * g + 3]));
             continue;
         }
         if (row < M) {
