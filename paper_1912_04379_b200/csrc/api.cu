@@ -461,8 +461,13 @@ static int host_pipelined(char tA, char tB, int64_t M, int64_t N, int64_t K, flo
         }
         g_hs.dev = dev;
     }
-    const int GM = 4, GN = 4;
-    const int64_t bm = (M / GM + 255) / 256 * 256, bn = (N / GN + 255) / 256 * 256;
+    // Square blocks of `blk` rows of op(A) / columns of op(B): fine enough
+    // that the first GEMM starts after ~10 ms of PCIe, at most 64 GEMMs.
+    int64_t blk = 2048;
+    if (const char *eb = getenv("EMM_HOST_BLOCK")) blk = std::max<int64_t>(256, atoll(eb) / 256 * 256);
+    blk = std::max(blk, ((std::max(M, N) + 31) / 32 + 255) / 256 * 256);
+    const int64_t bm = blk, bn = blk;
+    const int GM = (int)((M + bm - 1) / bm), GN = (int)((N + bn - 1) / bn);
     const int64_t Kp = tc_kpad(K);
     const int terms = terms_of(math), pl = planes_of(math);
     const int pmode = math == EMM_MATH_3XTF32 ? PK_FULL3_ : math == EMM_MATH_TF32_BF16 ? PK_FULLX_ : PK_FULL1_;
@@ -476,78 +481,71 @@ static int host_pipelined(char tA, char tB, int64_t M, int64_t N, int64_t K, flo
     cudaError_t e = cudaSuccess;
     size_t evn = 0;
     auto ev = [&]() { return hs_event(evn++); };
-    std::vector<cudaEvent_t> a_in(GM), b_in(GN);
-    auto rows_of = [](int64_t total, int64_t blk, int i) {
-        const int64_t r0 = i * blk, r1 = std::min(total, r0 + blk);
-        return std::make_pair(r0, r1 > r0 ? r1 - r0 : 0);
-    };
-    std::vector<cudaEvent_t> c_in(GM * GN, nullptr);
-    auto issue_c_in = [&](int i, int j) -> cudaError_t {
-        if (beta == 0.0f) return cudaSuccess;
-        auto [r0, nr] = rows_of(M, bm, i);
-        auto [c0, nc] = rows_of(N, bn, j);
-        if (nr == 0 || nc == 0) return cudaSuccess;
-        cudaError_t r = cudaMemcpy2DAsync(dC + r0 + c0 * ldc, (size_t)ldc * 4, C + r0 + c0 * ldc, (size_t)ldc * 4,
-                                          (size_t)nr * 4, (size_t)nc, cudaMemcpyHostToDevice, h2d);
-        c_in[i * GN + j] = ev();
-        if (r == cudaSuccess) r = cudaEventRecord(c_in[i * GN + j], h2d);
-        return r;
-    };
     if (cudaMemsetAsync(ctrl, 0, 64 * 128, comp) != cudaSuccess) return EMM_ERR_NOMEM;
-    for (int i = 0; i < GM && e == cudaSuccess; ++i) {
-        auto [r0, nr] = rows_of(M, bm, i);
-        if (nr == 0) break;
-        // H2D: A row block i (then, for i == 0, the B panels interleaved)
-        e = copy_rows(dA, A, a_rows_ld, lda, r0, nr, K, h2d);
-        a_in[i] = ev();
-        if (e == cudaSuccess) e = cudaEventRecord(a_in[i], h2d);
-        for (int j = 0; j < GN && e == cudaSuccess; ++j) {
-            auto [c0, nc] = rows_of(N, bn, j);
-            if (nc == 0) break;
-            if (i == 0) {
-                e = copy_rows(dB, B, b_rows_ld, ldb, c0, nc, K, h2d);
-                b_in[j] = ev();
-                if (e == cudaSuccess) e = cudaEventRecord(b_in[j], h2d);
-            }
-            if (e == cudaSuccess) e = issue_c_in(i, j);
+    // L-shaped growth (paper analogue: re-buffer each block once, PAPER.md:
+    // 133-138, then reuse it against everything already resident): land the
+    // next op(A) row block or op(B) column block — whichever keeps the
+    // resident rows and columns balanced — re-buffer it once, and at once
+    // multiply it against ALL resident blocks of the other operand with ONE
+    // GEMM; every C block is computed exactly once, when the later of its two
+    // operand blocks lands, and copied back right after.  Compute per PCIe
+    // byte grows with the resident square, so the copies hide under the
+    // tensor-core work after the first few blocks.
+    int na = 0, nb = 0, ng = 0;
+    while ((na < GM || nb < GN) && e == cudaSuccess) {
+        const int64_t rows_res = std::min(M, (int64_t)na * bm), cols_res = std::min(N, (int64_t)nb * bn);
+        const bool addA = na < GM && (nb >= GN || rows_res <= cols_res);
+        int64_t r0, nr, c0, nc;   // the GEMM's C region
+        if (addA) {
+            r0 = (int64_t)na * bm;
+            nr = std::min(bm, M - r0);
+            c0 = 0;
+            nc = cols_res;
+            e = copy_rows(dA, A, a_rows_ld, lda, r0, nr, K, h2d);
+        } else {
+            c0 = (int64_t)nb * bn;
+            nc = std::min(bn, N - c0);
+            r0 = 0;
+            nr = rows_res;
+            e = copy_rows(dB, B, b_rows_ld, ldb, c0, nc, K, h2d);
         }
-        // compute: pack A block i once, then pack B panel j (first row block only) and GEMM (i, j)
-        if (e == cudaSuccess) e = cudaStreamWaitEvent(comp, a_in[i], 0);
-        PackArgs pa;
-        pa.X = a_rows_ld ? dA + r0 : dA + r0 * lda;
-        pa.ld = lda; pa.R = nr; pa.kcontig = !a_rows_ld;
-        pa.out0 = Ap + (size_t)r0 * Kp; pa.ld0 = Kp; pa.out1 = Ap + (size_t)M * Kp + (size_t)r0 * Kp; pa.ld1 = Kp;
-        if (e == cudaSuccess) e = launch_pack(pmode, pa, nullptr, K, nullptr, comp);
-        for (int j = 0; j < GN && e == cudaSuccess; ++j) {
-            auto [c0, nc] = rows_of(N, bn, j);
-            if (nc == 0) break;
-            if (i == 0) {
-                e = cudaStreamWaitEvent(comp, b_in[j], 0);
-                PackArgs pb;
-                pb.X = b_rows_ld ? dB + c0 : dB + c0 * ldb;
-                pb.ld = ldb; pb.R = nc; pb.kcontig = !b_rows_ld; pb.b_side = true;
-                pb.out0 = Bp + (size_t)c0 * Kp; pb.ld0 = Kp; pb.out1 = Bp + (size_t)N * Kp + (size_t)c0 * Kp; pb.ld1 = Kp;
-                if (e == cudaSuccess) e = launch_pack(pmode, pb, nullptr, K, nullptr, comp);
-            }
-            if (e == cudaSuccess && c_in[i * GN + j]) e = cudaStreamWaitEvent(comp, c_in[i * GN + j], 0);
-            TcOperands ops;
-            ops.a0 = TcPlane{Ap + (size_t)r0 * Kp, Kp, false, Kp};
-            ops.b0 = TcPlane{Bp + (size_t)c0 * Kp, Kp, false, Kp};
-            if (pl == 2) {
-                ops.a1 = TcPlane{Ap + (size_t)M * Kp + (size_t)r0 * Kp, Kp, false, Kp};
-                ops.b1 = TcPlane{Bp + (size_t)N * Kp + (size_t)c0 * Kp, Kp, false, Kp};
-            }
-            if (e == cudaSuccess)
-                e = launch_tc_sgemm(terms, ops, nr, nc, K, alpha, beta, dC + r0 + c0 * ldc, ldc,
-                                    ctrl + 32 * (i * GN + j), 1, nullptr, comp);
-            // D2H of the finished block
-            cudaEvent_t done = ev();
-            if (e == cudaSuccess) e = cudaEventRecord(done, comp);
-            if (e == cudaSuccess) e = cudaStreamWaitEvent(d2h, done, 0);
-            if (e == cudaSuccess)
-                e = cudaMemcpy2DAsync(C + r0 + c0 * ldc, (size_t)ldc * 4, dC + r0 + c0 * ldc, (size_t)ldc * 4,
-                                      (size_t)nr * 4, (size_t)nc, cudaMemcpyDeviceToHost, d2h);
+        if (e == cudaSuccess && beta != 0.0f && nr > 0 && nc > 0)   // the C region this step computes
+            e = cudaMemcpy2DAsync(dC + r0 + c0 * ldc, (size_t)ldc * 4, C + r0 + c0 * ldc, (size_t)ldc * 4,
+                                  (size_t)nr * 4, (size_t)nc, cudaMemcpyHostToDevice, h2d);
+        cudaEvent_t landed = ev();
+        if (e == cudaSuccess) e = cudaEventRecord(landed, h2d);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(comp, landed, 0);
+        // re-buffer the new block once (K-major planes)
+        PackArgs pk;
+        if (addA) {
+            pk.X = a_rows_ld ? dA + r0 : dA + r0 * lda;
+            pk.ld = lda; pk.R = nr; pk.kcontig = !a_rows_ld;
+            pk.out0 = Ap + (size_t)r0 * Kp; pk.ld0 = Kp; pk.out1 = Ap + (size_t)M * Kp + (size_t)r0 * Kp; pk.ld1 = Kp;
+            ++na;
+        } else {
+            pk.X = b_rows_ld ? dB + c0 : dB + c0 * ldb;
+            pk.ld = ldb; pk.R = nc; pk.kcontig = !b_rows_ld; pk.b_side = true;
+            pk.out0 = Bp + (size_t)c0 * Kp; pk.ld0 = Kp; pk.out1 = Bp + (size_t)N * Kp + (size_t)c0 * Kp; pk.ld1 = Kp;
+            ++nb;
         }
+        if (e == cudaSuccess) e = launch_pack(pmode, pk, nullptr, K, nullptr, comp);
+        if (nr == 0 || nc == 0 || e != cudaSuccess) continue;
+        TcOperands ops;
+        ops.a0 = TcPlane{Ap + (size_t)r0 * Kp, Kp, false, Kp};
+        ops.b0 = TcPlane{Bp + (size_t)c0 * Kp, Kp, false, Kp};
+        if (pl == 2) {
+            ops.a1 = TcPlane{Ap + (size_t)M * Kp + (size_t)r0 * Kp, Kp, false, Kp};
+            ops.b1 = TcPlane{Bp + (size_t)N * Kp + (size_t)c0 * Kp, Kp, false, Kp};
+        }
+        e = launch_tc_sgemm(terms, ops, nr, nc, K, alpha, beta, dC + r0 + c0 * ldc, ldc, ctrl + 32 * (ng++ & 63), 1,
+                            nullptr, comp);
+        // D2H of the finished region
+        cudaEvent_t done = ev();
+        if (e == cudaSuccess) e = cudaEventRecord(done, comp);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(d2h, done, 0);
+        if (e == cudaSuccess)
+            e = cudaMemcpy2DAsync(C + r0 + c0 * ldc, (size_t)ldc * 4, dC + r0 + c0 * ldc, (size_t)ldc * 4,
+                                  (size_t)nr * 4, (size_t)nc, cudaMemcpyDeviceToHost, d2h);
     }
     if (e == cudaSuccess) e = cudaStreamSynchronize(d2h);
     if (e == cudaSuccess) e = cudaStreamSynchronize(comp);

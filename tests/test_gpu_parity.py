@@ -425,9 +425,11 @@ def test_torch_binding_colmajor(emm):
 @pytest.mark.parametrize("tA,tB", [("N", "N"), ("T", "T"), ("N", "T")])
 @pytest.mark.parametrize("beta", [0.0, 0.5])
 def test_host_buffer_pipelined(emm, monkeypatch, tA, tB, beta):
-    """emm_sgemm_host above 4096 x 4096 runs the copy/compute pipeline (4x4
-    blocks, three streams, re-buffered planes): same bits as the re-buffered
-    device call, ldc padding intact, sampled rows against the oracle."""
+    """emm_sgemm_host above 4096 x 4096 runs the copy/compute pipeline (L-
+    shaped growth over 2048-row/column blocks, ragged last blocks here; three
+    streams, re-buffered planes): same bits as the re-buffered device call
+    (K = 300 < 512: stream-K pieces sum like the sequential K loop), ldc
+    padding intact, sampled rows against the oracle."""
     M, N, K = 4500, 4200, 300
     case = cached_case(tA, tB, M, N, K, 1.25, beta, pad=(4, 4, 3))
     rows = np.array([0, 1, 1023, 1151, 1152, 2999, M - 1])
