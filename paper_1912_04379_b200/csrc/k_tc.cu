@@ -780,7 +780,26 @@ static cudaError_t launch_tc_t(const TcOperands &ops, int64_t M, int64_t N, int6
         sk.slots = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(sk_ws) + TC_SK_FLAG_BYTES);
     }
     // persistent: one pair per 2 SMs (all of them when stream-K spreads the last wave)
-    const int64_t clusters = sk.slots ? pairs : (units < pairs ? units : pairs);
+    int64_t clusters = sk.slots ? pairs : (units < pairs ? units : pairs);
+    // The persistent schedule (wave lockstep, stream-K flags) needs every
+    // cluster co-resident; clusters live inside one GPC, so cap the grid at
+    // what the occupancy API says fits (all 74 pairs on a B200).
+    static std::once_flag occ_once;
+    static int max_clusters = 0;
+    std::call_once(occ_once, [] {
+        cudaLaunchConfig_t oc{};
+        oc.gridDim = dim3(2 * 64);
+        oc.blockDim = dim3(TC_THREADS_P);
+        oc.dynamicSmemBytes = TcCfg<TERMS>::SMEM_BYTES;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, tc_sgemm_kernel<TERMS, A_MN, B_MN>, &oc) != cudaSuccess) n = 0;
+        max_clusters = n;
+        cudaGetLastError();
+    });
+    if (max_clusters > 0 && clusters > max_clusters) {
+        if (sk.slots) sk = TcSk{0x7fffffff, nullptr, nullptr};   // stream-K ranges assume every pair resident
+        clusters = max_clusters;
+    }
     const int64_t blocks = 2 * clusters;
     cudaEvent_t ev = nullptr;
     prof_begin(s, true, &ev);
