@@ -62,6 +62,7 @@ def parse():
     p.add_argument("--force-multi", action="store_true",
                    help="run the row-sharded emm_sgemm_multi path (NCCL) even at one rank")
     p.add_argument("--cpu-rows", type=int, default=0, help="oracle sample rows (0 = auto)")
+    p.add_argument("--no-probe", action="store_true", help="skip the MMA-only tensor-pipe ceiling probe")
     return p.parse_args()
 
 
@@ -178,6 +179,40 @@ def auto_rows(n):
     rate = 2.8e9 * cores
     r = int(15.0 * rate / (2.0 * n * n))
     return max(4, min(512, r))
+
+
+# --------------------------------------------------------------------- tensor-pipe ceiling
+def mma_probe(math, clocks_of, seconds=2.0):
+    """The GEMM's MMA stream with operands resident in SMEM (emm_debug_mma_probe,
+    k_probe.cu): burst and sustained 2MNK-equivalent TFLOP/s under the same
+    power cap, with the SM clock sampled during the sustained run."""
+    import ctypes
+    import paper_1912_04379_b200 as emm
+    terms = {"3xtf32": 3, "tf32bf16": 2, "1xtf32": 1}[math]
+    L = emm.lib()
+    L.emm_debug_mma_probe.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                                      ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_double)]
+    L.emm_debug_mma_probe.restype = ctypes.c_int
+    import torch
+    s = torch.cuda.current_stream().cuda_stream
+    stages = {3: 6000, 2: 9000, 1: 18000}[terms]      # ~5 ms per launch
+    msv, fl = ctypes.c_float(), ctypes.c_double()
+    for _ in range(3):
+        if L.emm_debug_mma_probe(terms, stages, s, ctypes.byref(msv), ctypes.byref(fl)):
+            return None
+    burst = fl.value / (msv.value * 1e-3) / 1e12
+    clocks_of.start()
+    rates = []
+    t_end = time.time() + seconds
+    while time.time() < t_end:
+        if L.emm_debug_mma_probe(terms, stages, s, ctypes.byref(msv), ctypes.byref(fl)):
+            return None
+        rates.append(fl.value / (msv.value * 1e-3) / 1e12)
+    c = clocks_of.stop()
+    return {"burst_tflops": burst, "sustained_tflops": statistics.median(rates[len(rates) // 2:]),
+            "sm_mhz": c["sm_mhz"] if c else None, "seconds": seconds,
+            "what": "the GEMM's tcgen05 MMA stream (CTA pairs, M256xN256xK8, same split) with operands resident "
+                    "in SMEM: the tensor pipe's ceiling at this power cap without TMA/L2/DRAM traffic"}
 
 
 # --------------------------------------------------------------------- reference arm
@@ -342,6 +377,13 @@ def main():
     res = measure(args.math, args.steps, args.warmup)
     value, ms, launches, clk, roofline, peak = (res["value"], res["ms"], res["launches"], res["clocks"],
                                                 res["roofline"], res["peak"])
+    if args.math != "ffma" and not args.no_probe and not multi:
+        pr = mma_probe(args.math, clocks_of=ClockSampler(local))
+        if pr and roofline.get("achieved"):
+            pr["frac"] = roofline["achieved"] / pr["sustained_tflops"]
+            if pr.get("sm_mhz") and clk and clk.get("sm_mhz"):
+                pr["frac_per_clock"] = (roofline["achieved"] / clk["sm_mhz"]) / (pr["sustained_tflops"] / pr["sm_mhz"])
+        roofline["ceiling_probe"] = pr
     ms_step = ms / args.steps
     alt = {}
     if args.math in ("3xtf32", "tf32bf16") and not args.no_alt and not multi:

@@ -177,6 +177,19 @@ void emm_profile_enable(int on);
 int emm_profile_read(double *gemm_ms, uint64_t *gemm_launches, double *other_ms,
                      uint64_t *other_launches);
 
+/* ----------------------------------------------------------------------
+ * Measurement probe (not part of the SGEMM path).  Runs the tensor-core
+ * GEMM's MMA stream (tcgen05.mma cta_group::2 M256xN256xK8 per CTA pair,
+ * terms = 3: 3xTF32, 2: TF32+BF16, 1: 1xTF32) for `stages` K-stages of 32
+ * on every CTA pair with the operands resident in shared memory — the tensor
+ * pipe's ceiling without TMA/L2/DRAM traffic (confirm the
+ * TF32 peak with a tcgen05 microbenchmark).  Synchronous: returns the
+ * CUDA-event time of the launch in *ms and, in *gemm_flops, the 2MNK a GEMM
+ * would report for the same work.  Returns 0, EMM_ERR_MATH (bad terms or
+ * stages) or 1000 + cudaError_t.
+ * -------------------------------------------------------------------- */
+int emm_debug_mma_probe(int terms, int stages, void *stream, float *ms, double *gemm_flops);
+
 #ifdef __cplusplus
 }
 #endif

@@ -116,18 +116,23 @@ def test_row_partition_c5(emm):
 
 
 def test_workspace_bytes(emm):
+    # layout: [A planes | B planes | split-K slots | ctrl 1 KB | (stream-K: flags 8 KB | slots)]
+    CTRL, FLAGS, SLOT = 1024, 8192, 256 * 256 * 4
     assert emm.workspace_bytes("N", "N", 64, 64, 64, "ffma") == 0
-    # 3xTF32: 2 planes of M x Kp and N x Kp floats, Kp = K rounded up to 32, + counter
-    assert emm.workspace_bytes("N", "N", 2048, 1024, 33, "3xtf32") == 2 * 4 * 64 * (2048 + 1024) + 1024
-    assert emm.workspace_bytes("N", "T", 2048, 1024, 64, "1xtf32") == 4 * 64 * (2048 + 1024) + 1024
-    # latency-bound problems (2MNK <= 2^24) take the FFMA kernel: no workspace
+    # 3xTF32: 2 planes of M x Kp and N x Kp floats, Kp = K rounded up to 32
+    assert emm.workspace_bytes("N", "N", 2048, 1024, 33, "3xtf32") == 2 * 4 * 64 * (2048 + 1024) + CTRL
+    assert emm.workspace_bytes("N", "T", 2048, 1024, 64, "1xtf32") == 4 * 64 * (2048 + 1024) + CTRL
+    # latency-bound problems (2MNK <= 2^27) take the tiny FFMA kernel: no workspace
     assert emm.workspace_bytes("N", "N", 64, 64, 64, "3xtf32") == 0
-    assert emm.workspace_bytes("N", "N", 333, 333, 333, "3xtf32") == 0   # tiny kernel (2MNK <= 2^27)
-    # sub-wave problems add split-K partials: BJ configs[2] -> 3 partials of M x N
+    assert emm.workspace_bytes("N", "N", 333, 333, 333, "3xtf32") == 0
+    # sub-wave problems add split-K slots: BJ configs[2] -> 24 tiles x 3 splits of 256 x 256 floats
     M, N, K = 1531, 997, 2049
-    base = 2 * 4 * 2080 * M + 2 * 4 * 2080 * N
     base = -(-2 * 4 * 2080 * M // 1024) * 1024 + -(-2 * 4 * 2080 * N // 1024) * 1024
-    assert emm.workspace_bytes("N", "N", M, N, K, "3xtf32") == base + -(-3 * M * N * 4 // 1024) * 1024 + 1024
+    assert emm.workspace_bytes("N", "N", M, N, K, "3xtf32") == base + 24 * 3 * SLOT + CTRL
+    # stream-K shapes add one slot per CTA pair (4096^3 3xTF32: 256 tiles = 3.46 waves)
+    base = 2 * 2 * 4 * 4096 * 4096
+    assert emm.workspace_bytes("N", "N", 4096, 4096, 4096, "3xtf32") == base + CTRL + FLAGS + 74 * SLOT
+    assert emm.workspace_bytes("N", "N", 4096, 4096, 4096, "1xtf32") == base // 2 + CTRL
 
 
 def test_strerror_and_version(emm):
