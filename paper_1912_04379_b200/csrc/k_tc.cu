@@ -45,7 +45,9 @@ using namespace ptx;
 int64_t tc_kpad(int64_t K) { return (K + TC_BK - 1) / TC_BK * TC_BK; }
 
 // Per-call control block (zeroed by the pack launch, TC_CTRL_BYTES): word 0 =
-// wave-lockstep counter.
+// wave-lockstep counter.  A lockstep wait longer than this many SM cycles
+// (~1 ms) means the grid is not fully resident: the CTA stops waiting.
+constexpr long long TC_LOCKSTEP_TIMEOUT = 2000000LL;
 constexpr int TC_SK_CHUNK = 256 / TC_BK;   // stream-K granularity: 8 stages = one promotion chunk
 
 // =====================================================================
@@ -509,14 +511,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
             int it = 0;
             unsigned int done_target = 0;   // CTAs that finished issuing waves 0..w-1
             int cur_wave = 0;
+            bool lockstep = wave_ctr != nullptr;
             for (int i = 0; i < S.n_items; ++i) {
                 const int w = S.wave_of(i);
                 if (w != cur_wave || i == 0) {
-                    if (w > 0 && wave_ctr) {
+                    if (w > 0 && lockstep) {
                         // Wave lockstep: start loading wave w only when every CTA
                         // has issued all loads of wave w-1, so the ~17 operand
-                        // panels a wave shares stream through L2 once (all CTAs
-                        // are co-resident: grid <= SMs, 1 CTA per SM).
+                        // panels a wave shares stream through L2 once.  It is an
+                        // L2 optimisation, not a correctness barrier: when the
+                        // grid is not fully co-resident (another kernel holds
+                        // SMs, e.g. concurrent GEMMs on other streams) the wait
+                        // gives up after ~1 ms and this CTA drops the lockstep
+                        // for the rest of the launch (no cross-kernel deadlock).
                         for (int v = cur_wave; v < w; ++v) done_target += 2u * (unsigned)S.pairs_in_wave(v);
                         const long long t0 = clock64();
                         while (true) {
@@ -524,7 +531,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
                             asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(wave_ctr) : "memory");
                             if (v >= done_target) break;
                             __nanosleep(128);
-                            if (clock64() - t0 > 40000000000LL) __trap();
+                            if (clock64() - t0 > TC_LOCKSTEP_TIMEOUT) {
+                                lockstep = false;
+                                break;
+                            }
                         }
                     }
                     cur_wave = w;
