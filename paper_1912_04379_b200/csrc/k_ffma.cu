@@ -87,7 +87,9 @@ __device__ __forceinline__ void store_tile(const TileLoad &t, float (*S)[FB_M + 
 }
 
 template <bool TA, bool TB, bool VEC>
-__global__ void __launch_bounds__(FB_THREADS, 2) ffma_sgemm_kernel(int64_t M, int64_t N, int64_t K, float alpha,
+// One CTA per SM: the 128-register cap of two CTAs spilled the prefetch
+// registers (up to 332 B); without it: equal at 4096-8192, c3 281 -> 228 us.
+__global__ void __launch_bounds__(FB_THREADS, 1) ffma_sgemm_kernel(int64_t M, int64_t N, int64_t K, float alpha,
                                                                 const float *__restrict__ A, int64_t lda,
                                                                 const float *__restrict__ B, int64_t ldb, float beta,
                                                                 float *__restrict__ C, int64_t ldc) {
