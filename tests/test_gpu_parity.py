@@ -453,3 +453,25 @@ def test_host_buffer_entry(emm):
                    case.ldc)
     case.check_untouched(Cf)
     assert_close(case, Cf, R, S, T, 1e-5)
+
+
+@pytest.mark.parametrize("math", ["3xtf32", "tf32bf16", "ffma"])
+@pytest.mark.parametrize("shape,tA,tB", [((1 << 20, 256, 64), "N", "N"),      # 4096 tile rows, multi-wave
+                                         ((256, 256, 1 << 20), "T", "N"),      # K = 2^20: split-K x16, 2048 stages each
+                                         ((300, 1 << 18, 96), "N", "T")])      # 1024 tile columns
+def test_extreme_extents(emm, math, shape, tA, tB):
+    """Maximum-extent cases: very long M, N or K (tile counts, split-K
+    ranges and 64-bit offsets far from the tested mid sizes).  Integer-exact
+    data (|sums| < 2^24 except for K = 2^20, checked with the tolerance)."""
+    M, N, K = shape
+    exact = K < (1 << 16)
+    case = cached_case(tA, tB, M, N, K, 1.0, 0.0, kind="ints" if exact else "uniform")
+    rows = np.unique(np.r_[0:4, M // 2:M // 2 + 4, M - 4:M])
+    R, S, T, _ = case.oracle(rows=rows)
+    Cg = case.run(emm, math)
+    case.check_untouched(Cg)
+    G = case.logical(Cg)[rows]
+    if exact:
+        assert np.array_equal(G, R.astype(np.float32).astype(np.float64))
+    else:
+        assert_close(case, Cg, R, S, T, TOL[math], rows=rows)
