@@ -21,14 +21,22 @@
 
 namespace emm {
 
-constexpr int FB_M = 128, FB_N = 128, FB_K = 16, FB_THREADS = 256;
-constexpr int FB_PAD = 4;
+// K-tile 32 (one CTA per SM leaves the registers for it): the per-tile
+// staging, barrier and address work is amortised over 2x the FFMA2s of the
+// earlier K-tile 16.
+constexpr int FB_M = 128, FB_N = 128, FB_K = 32, FB_THREADS = 256;
+constexpr int FB_H = FB_K / 8;   // float4 staged per thread per operand tile
 // Promotion: every FB_PROMOTE K-tiles (256 of K) the 64 register partial sums
 // are added (round-to-nearest) into a per-thread master copy in SMEM and
 // restarted, so sequential FP32 rounding error grows with 256 + K/256 terms
 // instead of K (same-sign data at K = 32768 otherwise exceeds 1e-5 * S).
-constexpr int FB_PROMOTE = 16;
-constexpr int FB_SMEM_BYTES = (2 * FB_K * (FB_M + FB_PAD) + 2 * FB_K * (FB_N + FB_PAD) + 64 * FB_THREADS) * 4;
+constexpr int FB_PROMOTE = 256 / FB_K;
+constexpr int FB_SMEM_BYTES = (2 * FB_K * FB_M + 2 * FB_K * FB_N + 64 * FB_THREADS) * 4;
+// SMEM tiles S[k][row] (row-contiguous, unpadded) with the 16-byte groups of
+// row k XOR-swizzled by (k / 4) % 8: the transposing scalar stores of a
+// K-contiguous operand (8 k x 4 rows per warp instruction) hit 32 distinct
+// banks, and every float4 read stays a contiguous float4.
+__device__ __forceinline__ int fb_swz(int k, int r) { return r ^ (((k >> 2) & 7) << 2); }
 
 // Global -> register staging of one 128 x 16 (A) or 16 x 128 (B) tile with
 // 128-bit loads along the operand's contiguous dimension when the whole
@@ -36,17 +44,17 @@ constexpr int FB_SMEM_BYTES = (2 * FB_K * (FB_M + FB_PAD) + 2 * FB_K * (FB_N + F
 //   "MN-contiguous" (A !TA, B TB):  4 consecutive rows/cols at one k
 //   "K-contiguous"  (A TA,  B !TB): 4 consecutive k at one row/col
 struct TileLoad {
-    float v[2][4];
+    float v[FB_H][4];
 };
 
 template <bool KCONT, bool VEC>
 __device__ __forceinline__ void load_tile(TileLoad &t, const float *__restrict__ X, int64_t ld, int64_t r_base,
                                           int64_t R, int64_t k0, int64_t K, int tid) {
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < FB_H; ++h) {
         int rr, kk;
-        if (!KCONT) { rr = (tid & 31) * 4; kk = (tid >> 5) + 8 * h; }      // 32 float4 along rows x 16 k
-        else        { kk = (tid & 3) * 4;  rr = (tid >> 2) + 64 * h; }     // 4 float4 along k x 128 rows
+        if (!KCONT) { rr = (tid & 31) * 4; kk = (tid >> 5) + 8 * h; }      // 32 float4 along rows x 32 k
+        else        { kk = (tid & 7) * 4;  rr = (tid >> 3) + 32 * h; }     // 8 float4 along k x 128 rows
         const int64_t r = r_base + rr, p = k0 + kk;
         if (!KCONT) {
             const float *src = X + r + p * ld;
@@ -70,18 +78,19 @@ __device__ __forceinline__ void load_tile(TileLoad &t, const float *__restrict__
     }
 }
 
-// registers -> S[k][row] (row-contiguous smem tile, FB_PAD padded)
+// registers -> S[k][row] (row-contiguous smem tile, fb_swz-swizzled)
 template <bool KCONT>
-__device__ __forceinline__ void store_tile(const TileLoad &t, float (*S)[FB_M + FB_PAD], int tid) {
+__device__ __forceinline__ void store_tile(const TileLoad &t, float (*S)[FB_M], int tid) {
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < FB_H; ++h) {
         if (!KCONT) {
             const int rr = (tid & 31) * 4, kk = (tid >> 5) + 8 * h;
-            *reinterpret_cast<float4 *>(&S[kk][rr]) = make_float4(t.v[h][0], t.v[h][1], t.v[h][2], t.v[h][3]);
+            *reinterpret_cast<float4 *>(&S[kk][fb_swz(kk, rr)]) =
+                make_float4(t.v[h][0], t.v[h][1], t.v[h][2], t.v[h][3]);
         } else {
-            const int kk = (tid & 3) * 4, rr = (tid >> 2) + 64 * h;
+            const int kk = (tid & 7) * 4, rr = (tid >> 3) + 32 * h;
 #pragma unroll
-            for (int e = 0; e < 4; ++e) S[kk + e][rr] = t.v[h][e];
+            for (int e = 0; e < 4; ++e) S[kk + e][fb_swz(kk + e, rr)] = t.v[h][e];
         }
     }
 }
@@ -94,10 +103,9 @@ __global__ void __launch_bounds__(FB_THREADS, 1) ffma_sgemm_kernel(int64_t M, in
                                                                 const float *__restrict__ B, int64_t ldb, float beta,
                                                                 float *__restrict__ C, int64_t ldc) {
     extern __shared__ __align__(16) float fb_smem[];
-    float(*As)[FB_K][FB_M + FB_PAD] = reinterpret_cast<float(*)[FB_K][FB_M + FB_PAD]>(fb_smem);
-    float(*Bs)[FB_K][FB_N + FB_PAD] =
-        reinterpret_cast<float(*)[FB_K][FB_N + FB_PAD]>(fb_smem + 2 * FB_K * (FB_M + FB_PAD));
-    float *master = fb_smem + 2 * FB_K * (FB_M + FB_PAD) + 2 * FB_K * (FB_N + FB_PAD);   // [64][256]
+    float(*As)[FB_K][FB_M] = reinterpret_cast<float(*)[FB_K][FB_M]>(fb_smem);
+    float(*Bs)[FB_K][FB_N] = reinterpret_cast<float(*)[FB_K][FB_N]>(fb_smem + 2 * FB_K * FB_M);
+    float *master = fb_smem + 2 * FB_K * FB_M + 2 * FB_K * FB_N;   // [64][256]
     const int tid = threadIdx.x;
     const int64_t m0 = (int64_t)blockIdx.x * FB_M;
     const int64_t n0 = (int64_t)blockIdx.y * FB_N;
@@ -132,10 +140,10 @@ __global__ void __launch_bounds__(FB_THREADS, 1) ffma_sgemm_kernel(int64_t M, in
         }
 #pragma unroll
         for (int k = 0; k < FB_K; ++k) {
-            const float4 a0 = *reinterpret_cast<const float4 *>(&As[buf][k][tm * 4]);
-            const float4 a1 = *reinterpret_cast<const float4 *>(&As[buf][k][64 + tm * 4]);
-            const float4 b0 = *reinterpret_cast<const float4 *>(&Bs[buf][k][tn * 4]);
-            const float4 b1 = *reinterpret_cast<const float4 *>(&Bs[buf][k][64 + tn * 4]);
+            const float4 a0 = *reinterpret_cast<const float4 *>(&As[buf][k][fb_swz(k, tm * 4)]);
+            const float4 a1 = *reinterpret_cast<const float4 *>(&As[buf][k][fb_swz(k, 64 + tm * 4)]);
+            const float4 b0 = *reinterpret_cast<const float4 *>(&Bs[buf][k][fb_swz(k, tn * 4)]);
+            const float4 b1 = *reinterpret_cast<const float4 *>(&Bs[buf][k][fb_swz(k, 64 + tn * 4)]);
             const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
             const float2 bv[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
                                   make_float2(b1.z, b1.w)};
