@@ -9,7 +9,7 @@ import os
 import statistics
 import sys
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))   # tests/ helper (uses the oracle)
 sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
