@@ -101,10 +101,14 @@ int emm_sgemm_ex(char transA, char transB, int64_t M, int64_t N, int64_t K,
 size_t emm_sgemm_workspace_bytes(char transA, char transB, int64_t M, int64_t N,
                                  int64_t K, emm_math_t math);
 
-/* End-to-end form: A, B, C are HOST pointers (pinned or pageable, same
- * layouts as above).  Copies A, B (and C when beta != 0) to device buffers
- * cached by the library, runs emm_sgemm_ex on an internal stream, copies C
- * back and synchronises.  Returns when C holds the result. */
+/* End-to-end form: A, B, C are HOST pointers (pinned or pageable; pinned
+ * for full PCIe speed; same layouts as above).  Copies A, B (and C when
+ * beta != 0) to device buffers cached by the library and copies C back;
+ * returns when C holds the result (synchronous).  Tensor-core modes with
+ * M, N >= 4096 pipeline it over 2048-row / 2048-column blocks on three
+ * internal streams (copies in both directions overlap the GEMMs, DESIGN.md
+ * §6b); other calls copy, run emm_sgemm_ex on an internal stream, and copy
+ * back.  Not reentrant with itself (serialised by a library mutex). */
 int emm_sgemm_host(char transA, char transB, int64_t M, int64_t N, int64_t K,
                    float alpha, const float *A, int64_t lda,
                    const float *B, int64_t ldb,

@@ -414,13 +414,13 @@ int ensure(void **p, size_t *have, size_t need) {
 }
 }  // namespace
 
-// Pipelined host-buffer SGEMM (tensor-core modes, M, N >= 4096): C is cut
-// into GM x GN blocks.  Stream `h2d` copies op(A) row blocks and B column
-// panels (and C blocks when beta != 0) in the order the GEMMs need them;
-// stream `comp` re-buffers each block ONCE when it lands and runs GEMM (i, j)
-// as soon as its row block and panel are packed; stream `d2h` copies each C
-// block out as soon as its GEMM is done.  PCIe traffic (both directions)
-// overlaps the tensor-core work, leaving ~one block's copy exposed.
+// Pipelined host-buffer SGEMM (tensor-core modes, M, N >= 4096): three
+// streams over op(A) row blocks and op(B) column blocks (host_pipelined: L-
+// shaped growth — each landed block is re-buffered once on `comp` and
+// multiplied against every resident block of the other operand in one GEMM;
+// `h2d` copies blocks (and the C regions when beta != 0) in that order, `d2h`
+// copies each C region out as soon as its GEMM is done).  PCIe traffic in both
+// directions overlaps the tensor-core work after the first few blocks.
 namespace {
 struct HostStreams {
     cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
