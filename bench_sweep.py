@@ -14,6 +14,7 @@ import json
 import os
 import statistics
 import sys
+import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -53,6 +54,9 @@ def main():
     ap.add_argument("--maths", default="3xtf32,tf32bf16,1xtf32,ffma")
     ap.add_argument("--only", default="")
     ap.add_argument("--shape", default="", help="custom M,N,K,transA,transB (alpha=1, beta=0, uniform)")
+    ap.add_argument("--cooldown", type=float, default=2.0,
+                    help="idle seconds before each (config, path) row: the power-capped B200's clock depends on "
+                         "the preceding load, so rows are measured from the same thermal state")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
@@ -90,6 +94,8 @@ def main():
                                    beta, dC.data_ptr(), M + pad[2], stream.cuda_stream, math,
                                    wsp or None, nbytes)
                 assert st == 0, emm.strerror(st)
+            torch.cuda.synchronize()
+            time.sleep(args.cooldown)
             for _ in range(3):
                 call()
             ts = []
@@ -135,7 +141,7 @@ def main():
             rec = {"config": name, "math": math, "M": M, "N": N, "K": K, "transA": tA, "transB": tB,
                    "median_ms": med, "min_ms": min(ts), "gflops": fl / med / 1e6,
                    "pct_roofline": 100.0 * fl / med / 1e9 / pk[math], "gbs": byt / med / 1e6,
-                   "roofline_tflops": pk[math], "l2_flushed": True, "reps": args.reps,
+                   "roofline_tflops": pk[math], "l2_flushed": True, "reps": args.reps, "cooldown_s": args.cooldown,
                    "b2b_graph_us": b2b}
             print(json.dumps(rec), flush=True)
             lines.append(rec)

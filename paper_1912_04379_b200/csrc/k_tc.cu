@@ -779,6 +779,10 @@ static cudaError_t launch_tc_t(const TcOperands &ops, int64_t M, int64_t N, int6
     const int tiles_m = (int)((M + 2 * TC_BM - 1) / (2 * TC_BM));
     const int tiles_n = (int)((N + TC_BN - 1) / TC_BN);
     const int group_m = 8;
+    // 1xTF32 is operand-fill-bound: the wave lockstep's boundary stalls cost
+    // more than its L2 reuse buys (c4-ii +4.7%, c4-i +2.4% without it;
+    // 3xTF32 -1%, profiles/r01_ab_1x_lockstep_group.txt)
+    if (TERMS == 1) ctrl = nullptr;
     const int64_t units = (int64_t)tiles_m * tiles_n * splits;
     if (units > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
     const int64_t pairs = tc_num_sms() / 2;
