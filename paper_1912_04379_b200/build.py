@@ -20,7 +20,7 @@ CSRC = os.path.join(PKG, "csrc")
 TIMELINE = os.environ.get("EMM_TIMELINE") == "1"
 OBJ = os.path.join(PKG, "build_tl" if TIMELINE else "build")
 LIB = os.path.join(PKG, "libemm_tl.so" if TIMELINE else "libemm.so")
-SOURCES = ["api.cu", "k_tc.cu", "k_tcl.cu", "k_ffma.cu", "k_skinny.cu", "k_tiny.cu", "k_misc.cu", "multi.cu", "k_probe.cu"]
+SOURCES = ["api.cu", "k_tc.cu", "k_tcl.cu", "k_ffma.cu", "k_ffma_tma.cu", "k_skinny.cu", "k_tiny.cu", "k_misc.cu", "multi.cu", "k_probe.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

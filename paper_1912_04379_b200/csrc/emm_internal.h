@@ -94,6 +94,8 @@ cudaError_t launch_tc_split_sgemm(bool a_kc, bool b_kc, const float *A, int64_t 
                                   unsigned int *ctrl, int splits, float *partial, cudaStream_t s,
                                   const PeerOut *peers = nullptr);
 bool tma_legal(const void *ptr, int64_t ld);
+bool encode_tmap_f32_2d(CUtensorMap *tm, const float *ptr, int64_t d0, int64_t d1, int64_t ld, int box0, int box1,
+                        CUtensorMapSwizzle swz);
 int64_t tc_kpad(int64_t K);
 int tc_splits(int64_t M, int64_t N, int64_t K);
 int64_t tc_units(int64_t M, int64_t N, int splits);   // (tile, split) work units
@@ -103,6 +105,14 @@ int tc_num_sms();
 cudaError_t launch_ffma_sgemm(bool tA, bool tB, int64_t M, int64_t N, int64_t K, float alpha, const float *A,
                               int64_t lda, const float *B, int64_t ldb, float beta, float *C, int64_t ldc,
                               cudaStream_t s);
+
+// KN3b (k_ffma_tma.cu): warp-specialised FFMA SGEMM, TMA-fed SMEM ring.
+// Returns false (nothing launched) when the shape / layout is not covered
+// (both operands K-contiguous, or not TMA-legal); the caller then runs KN3.
+bool ffma_tma_eligible(bool tA, bool tB, const float *A, int64_t lda, const float *B, int64_t ldb);
+cudaError_t launch_ffma_tma_sgemm(bool tA, bool tB, int64_t M, int64_t N, int64_t K, float alpha, const float *A,
+                                  int64_t lda, const float *B, int64_t ldb, float beta, float *C, int64_t ldc,
+                                  cudaStream_t s);
 
 // ---- skinny / memory-bound path (k_skinny.cu) ----------------------------
 // min(M, N) <= SKINNY_MAX: stream the long operand once, FP32 FFMA with

@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "emm_internal.h"
 
@@ -147,12 +148,11 @@ __global__ void __launch_bounds__(FB_THREADS, 1) ffma_sgemm_kernel(int64_t M, in
             const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
             const float2 bv[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
                                   make_float2(b1.z, b1.w)};
+            // b pair fixed over 8 FFMA2s (operand reuse), scalar a varies
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const float2 ai = make_float2(av[i], av[i]);
+            for (int j = 0; j < 4; ++j)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) acc[i][j] = __ffma2_rn(ai, bv[j], acc[i][j]);
-            }
+                for (int i = 0; i < 8; ++i) acc[i][j] = __ffma2_rn(make_float2(av[i], av[i]), bv[j], acc[i][j]);
         }
         if (more) {
             store_tile<A_KC>(ta, As[buf ^ 1], tid);
@@ -191,6 +191,12 @@ __global__ void __launch_bounds__(FB_THREADS, 1) ffma_sgemm_kernel(int64_t M, in
 cudaError_t launch_ffma_sgemm(bool tA, bool tB, int64_t M, int64_t N, int64_t K, float alpha, const float *A,
                               int64_t lda, const float *B, int64_t ldb, float beta, float *C, int64_t ldc,
                               cudaStream_t s) {
+    // KN3b (TMA-fed, warp-specialised) whenever it covers the layout;
+    // EMM_FFMA_CLASSIC=1 keeps KN3 (A/B comparisons, tests)
+    const char *cv = getenv("EMM_FFMA_CLASSIC");
+    const bool classic = cv && *cv && *cv != '0';
+    if (!classic && ffma_tma_eligible(tA, tB, A, lda, B, ldb))
+        return launch_ffma_tma_sgemm(tA, tB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, s);
     const int64_t gx = (M + FB_M - 1) / FB_M, gy = (N + FB_N - 1) / FB_N;
     if (gx > 0x7fffffffLL || gy > 65535) return cudaErrorInvalidConfiguration;
     dim3 grid((unsigned)gx, (unsigned)gy);

@@ -1,0 +1,284 @@
+// k_ffma_tma.cu — KN3b: warp-specialised FP32 FFMA SGEMM (EMM_MATH_FFMA).
+//
+// Same arithmetic as KN3 (k_ffma.cu): an 8x8 register tile per thread (the
+// paper's L0 register blocking), FFMA2 (two FP32 FMAs per
+// issue slot), sequential FP32 accumulation along K with promotion into a
+// master copy every 256 of K.  What changes is the operand staging, the part
+// KN3 spends its non-FMA issue slots and barriers on:
+//   * one producer warp streams the 128 x 32 A and B tiles of each K-stage
+//     into a 4-stage SMEM ring with TMA (cp.async.bulk.tensor, OOB = zero,
+//     the paper's zero-padded K tail PAPER.md:449-451), full/empty mbarriers;
+//   * 8 consumer warps never stage through registers or meet at
+//     __syncthreads: they wait on the stage's full barrier, run 32 x 32
+//     FFMA2 per thread from SMEM, and release the stage.
+// SMEM tiles keep each operand's own majorness (no transpose anywhere):
+//   MN-contiguous (A transA=N, B transB=T): four [32 k][32 mn] TMA boxes,
+//     128B swizzle; a thread reads float4 along mn (rows 4t..4t+3, 64+4t..).
+//   K-contiguous  (A transA=T, B transB=N): one [128 rows][32 k] box, 128B
+//     swizzle; a thread owns rows t, t+16, ..., t+112 and reads float4
+//     along k (4 k-steps per load).
+// FFMA2 pairs two accumulators that share one operand value: adjacent
+// columns when B is MN-contiguous, else adjacent rows (A MN-contiguous).
+// The TN case (both K-contiguous) and non-TMA-legal layouts stay on KN3.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "emm_internal.h"
+#include "ptx.cuh"
+
+namespace emm {
+
+using namespace ptx;
+
+namespace {
+constexpr int FT_M = 128, FT_N = 128, FT_K = 32, FT_STAGES = 4;
+constexpr int FT_TILE_FLOATS = 128 * FT_K;                  // one operand tile: 16 KB
+constexpr int FT_STAGE_BYTES = 2 * FT_TILE_FLOATS * 4;      // A + B: 32 KB
+constexpr int FT_CONSUMERS = 256, FT_THREADS = FT_CONSUMERS + 32;
+constexpr int FT_PROMOTE = 256 / FT_K;                      // stages per promotion (256 of K)
+constexpr int FT_MASTER_FLOATS = 64 * FT_CONSUMERS;
+constexpr int FT_SMEM = FT_STAGES * FT_STAGE_BYTES + FT_MASTER_FLOATS * 4 + 1024 /*align*/ + 128 /*barriers*/;
+constexpr int FT_GROUP_M = 16;                              // raster: 16 tile-rows per group (L2 reuse of B)
+// Dedicated producer warp (default).  -DEMM_FT_SEP=0 instead lets consumer
+// thread 0 issue the loads (256 threads, up to 255 registers): measured
+// slower, c2-8192 54.7 vs 57.7 TFLOP/s — thread 0 waits for the slowest warp
+// to free a slot and holds back warp 0.
+#ifndef EMM_FT_SEP
+#define EMM_FT_SEP 1
+#endif
+constexpr bool FT_SEP = EMM_FT_SEP != 0;
+constexpr int FT_BLOCK = FT_SEP ? FT_THREADS : FT_CONSUMERS;
+
+// float index of the float4 holding (mn = 4q..4q+3, k) in an MN-contiguous tile
+__device__ __forceinline__ int mn_idx(int q, int k) { return (q >> 3) * 1024 + k * 32 + (((q & 7) ^ (k & 7)) << 2); }
+// float index of the float4 holding (row r, k = 4g..4g+3) in a K-contiguous tile
+__device__ __forceinline__ int kc_idx(int r, int g) { return r * 32 + ((g ^ (r & 7)) << 2); }
+
+// The 8 operand values of one thread for 4 consecutive k (k = 4g + kk):
+// v[kk][e], e = the thread's row (A) / column (B) slot.
+//   MN-contiguous: slot e -> mn = 4t + e (e < 4), 64 + 4t + (e - 4)
+//   K-contiguous:  slot e -> row t + 16 e
+template <bool MN>
+__device__ __forceinline__ void load_group(const float *__restrict__ T, int t, int g, float (&v)[4][8]) {
+    if (MN) {
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+            const float4 x0 = *reinterpret_cast<const float4 *>(T + mn_idx(t, 4 * g + kk));
+            const float4 x1 = *reinterpret_cast<const float4 *>(T + mn_idx(16 + t, 4 * g + kk));
+            v[kk][0] = x0.x; v[kk][1] = x0.y; v[kk][2] = x0.z; v[kk][3] = x0.w;
+            v[kk][4] = x1.x; v[kk][5] = x1.y; v[kk][6] = x1.z; v[kk][7] = x1.w;
+        }
+    } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const float4 x = *reinterpret_cast<const float4 *>(T + kc_idx(t + 16 * e, g));
+            v[0][e] = x.x; v[1][e] = x.y; v[2][e] = x.z; v[3][e] = x.w;
+        }
+    }
+}
+__device__ __forceinline__ int slot_pos(bool mn, int t, int e) { return mn ? (e < 4 ? 4 * t + e : 60 + 4 * t + e) : t + 16 * e; }
+}  // namespace
+
+// PAIR_J (B MN-contiguous): acc[i*4 + j/2] holds (i, j), (i, j+1);
+// else (A MN-contiguous):   acc[(i/2)*8 + j] holds (i, j), (i+1, j).
+template <bool A_MN, bool B_MN, bool SEP>
+__global__ void __launch_bounds__(SEP ? FT_THREADS : FT_CONSUMERS, 1)
+    ffma_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
+                    int K, float alpha, float beta, float *__restrict__ C, int64_t ldc, int tiles_m, int tiles_n) {
+    static_assert(A_MN || B_MN, "TN (both K-contiguous) runs on KN3");
+    constexpr bool PAIR_J = B_MN;
+    extern __shared__ __align__(1024) uint8_t ft_raw[];
+    // 1024-B aligned base for the 128B-swizzled TMA boxes; offset arithmetic
+    // on the shared array (not via an integer cast) keeps the reads LDS
+    uint8_t *smem = ft_raw + ((1024u - (smem_u32(ft_raw) & 1023u)) & 1023u);
+    float *master = reinterpret_cast<float *>(smem + FT_STAGES * FT_STAGE_BYTES);
+    uint64_t *full = reinterpret_cast<uint64_t *>(master + FT_MASTER_FLOATS);
+    uint64_t *empty = full + FT_STAGES;
+
+    // grouped raster: FT_GROUP_M tile-rows share each B panel while it is in L2
+    const int bid = (int)blockIdx.x;
+    const int per_group = FT_GROUP_M * tiles_n;
+    const int first_m = (bid / per_group) * FT_GROUP_M;
+    const int gsize = min(tiles_m - first_m, FT_GROUP_M);
+    const int m0 = (first_m + (bid % per_group) % gsize) * FT_M;
+    const int n0 = ((bid % per_group) / gsize) * FT_N;
+    const int nk = (K + FT_K - 1) / FT_K;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < FT_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], FT_CONSUMERS / 32);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    const uint64_t pol = policy_evict_normal();
+    // loads of K-stage kt into ring slot kt % FT_STAGES (one thread)
+    auto issue = [&](int kt) {
+        const int s = kt % FT_STAGES;
+        mbar_wait(&empty[s], ((uint32_t)(kt / FT_STAGES) & 1u) ^ 1u);
+        mbar_arrive_expect_tx(&full[s], FT_STAGE_BYTES);
+        const uint32_t st = smem_u32(smem + s * FT_STAGE_BYTES);
+        const uint32_t sb = st + FT_TILE_FLOATS * 4;
+        const int k0 = kt * FT_K;
+        if (A_MN) {
+#pragma unroll
+            for (int b = 0; b < 4; ++b) tma_load_2d(st + b * 4096, &tmA, &full[s], m0 + 32 * b, k0, pol);
+        } else {
+            tma_load_2d(st, &tmA, &full[s], k0, m0, pol);
+        }
+        if (B_MN) {
+#pragma unroll
+            for (int b = 0; b < 4; ++b) tma_load_2d(sb + b * 4096, &tmB, &full[s], n0 + 32 * b, k0, pol);
+        } else {
+            tma_load_2d(sb, &tmB, &full[s], k0, n0, pol);
+        }
+    };
+    if (SEP) {
+        if (warp == FT_CONSUMERS / 32) {
+            // ===== producer warp: one lane issues the TMA loads =====
+            if (lane == 0) {
+                prefetch_tmap(&tmA);
+                prefetch_tmap(&tmB);
+                for (int kt = 0; kt < nk; ++kt) issue(kt);
+            }
+            return;
+        }
+    } else if (threadIdx.x == 0) {
+        // no producer warp (all 64K registers to the 8 FFMA warps): thread 0
+        // fills the first FT_STAGES - 1 slots here and one more per K-stage
+        for (int kt = 0; kt < FT_STAGES - 1 && kt < nk; ++kt) issue(kt);
+    }
+
+    // ===== consumers =====
+    const int c = threadIdx.x;
+    const int tm = c & 15, tn = c >> 4;
+    float2 acc[32];
+#pragma unroll
+    for (int e = 0; e < 32; ++e) acc[e] = make_float2(0.0f, 0.0f);
+#pragma unroll
+    for (int e = 0; e < 64; ++e) master[e * FT_CONSUMERS + c] = 0.0f;
+
+    for (int kt = 0; kt < nk; ++kt) {
+        const int s = kt % FT_STAGES;
+        // slot of stage kt-1: free once every warp has finished kt-1
+        if (!SEP && c == 0 && kt + FT_STAGES - 1 < nk) issue(kt + FT_STAGES - 1);
+        mbar_wait(&full[s], (uint32_t)(kt / FT_STAGES) & 1u);
+        const float *As = reinterpret_cast<const float *>(smem + s * FT_STAGE_BYTES);
+        const float *Bs = As + FT_TILE_FLOATS;
+#pragma unroll
+        for (int g = 0; g < FT_K / 4; ++g) {
+            float av[4][8], bv[4][8];
+            load_group<A_MN>(As, tm, g, av);
+            load_group<B_MN>(Bs, tn, g, bv);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+                // the pair operand stays fixed over 8 consecutive FFMA2s (operand
+                // reuse cache) while the broadcast scalar varies: 125 vs 108
+                // FMA/clk/SM for the other order (tools/ffma2_probe.cu)
+                if (PAIR_J) {
+#pragma unroll
+                    for (int jp = 0; jp < 4; ++jp)
+#pragma unroll
+                        for (int i = 0; i < 8; ++i)
+                            acc[i * 4 + jp] = __ffma2_rn(make_float2(av[kk][i], av[kk][i]),
+                                                         make_float2(bv[kk][2 * jp], bv[kk][2 * jp + 1]), acc[i * 4 + jp]);
+                } else {
+#pragma unroll
+                    for (int ip = 0; ip < 4; ++ip)
+#pragma unroll
+                        for (int j = 0; j < 8; ++j)
+                            acc[ip * 8 + j] = __ffma2_rn(make_float2(av[kk][2 * ip], av[kk][2 * ip + 1]),
+                                                         make_float2(bv[kk][j], bv[kk][j]), acc[ip * 8 + j]);
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if ((kt + 1) % FT_PROMOTE == 0 || kt + 1 == nk) {
+            // promotion: master (SMEM, per-thread column) += register partials
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const float2 &p = PAIR_J ? acc[i * 4 + (j >> 1)] : acc[(i >> 1) * 8 + j];
+                    const float v = PAIR_J ? ((j & 1) ? p.y : p.x) : ((i & 1) ? p.y : p.x);
+                    master[(i * 8 + j) * FT_CONSUMERS + c] += v;
+                }
+#pragma unroll
+            for (int e = 0; e < 32; ++e) acc[e] = make_float2(0.0f, 0.0f);
+        }
+    }
+
+    // epilogue: alpha*acc + beta*C (C not read when beta == 0), predicated
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const int col = n0 + slot_pos(B_MN, tn, j);
+        if (col >= N) continue;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int row = m0 + slot_pos(A_MN, tm, i);
+            if (row < M) {
+                const float v = master[(i * 8 + j) * FT_CONSUMERS + c];
+                float *d = C + row + (int64_t)col * ldc;
+                *d = beta == 0.0f ? alpha * v : fmaf(beta, *d, alpha * v);
+            }
+        }
+    }
+}
+
+bool ffma_tma_eligible(bool tA, bool tB, const float *A, int64_t lda, const float *B, int64_t ldb) {
+    // KN3b needs one MN-contiguous operand (not TN) and TMA-legal layouts
+    return !(tA && !tB) && tma_legal(A, lda) && tma_legal(B, ldb);
+}
+
+cudaError_t launch_ffma_tma_sgemm(bool tA, bool tB, int64_t M, int64_t N, int64_t K, float alpha, const float *A,
+                                  int64_t lda, const float *B, int64_t ldb, float beta, float *C, int64_t ldc,
+                                  cudaStream_t s) {
+    const bool a_mn = !tA, b_mn = tB;
+    if (!a_mn && !b_mn) return cudaErrorInvalidValue;
+    if (M > 0x7fffff00LL || N > 0x7fffff00LL || K > 0x7fffff00LL) return cudaErrorInvalidValue;
+    const int64_t tiles_m = (M + FT_M - 1) / FT_M, tiles_n = (N + FT_N - 1) / FT_N;
+    if (tiles_m * tiles_n > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+    // A: transA=N stored M x K (MN-contiguous), T stored K x M; B: transB=N
+    // stored K x N (K-contiguous), T stored N x K.
+    CUtensorMap ta, tb;
+    const bool ok_a = a_mn ? encode_tmap_f32_2d(&ta, A, M, K, lda, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B)
+                           : encode_tmap_f32_2d(&ta, A, K, M, lda, 32, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+    const bool ok_b = b_mn ? encode_tmap_f32_2d(&tb, B, N, K, ldb, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B)
+                           : encode_tmap_f32_2d(&tb, B, K, N, ldb, 32, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (!ok_a || !ok_b) return cudaErrorInvalidValue;
+    static cudaError_t attr = [] {
+        cudaError_t e = cudaSuccess;
+        auto set = [&](const void *f) {
+            cudaError_t r = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, FT_SMEM);
+            if (r != cudaSuccess) e = r;
+        };
+        set((const void *)ffma_tma_kernel<true, false, FT_SEP>);
+        set((const void *)ffma_tma_kernel<true, true, FT_SEP>);
+        set((const void *)ffma_tma_kernel<false, true, FT_SEP>);
+        return e;
+    }();
+    if (attr != cudaSuccess) return attr;
+    const unsigned grid = (unsigned)(tiles_m * tiles_n);
+    cudaEvent_t ev = nullptr;
+    prof_begin(s, true, &ev);
+    if (a_mn && !b_mn)
+        ffma_tma_kernel<true, false, FT_SEP><<<grid, FT_BLOCK, FT_SMEM, s>>>(ta, tb, (int)M, (int)N, (int)K, alpha, beta, C,
+                                                                       ldc, (int)tiles_m, (int)tiles_n);
+    else if (a_mn)
+        ffma_tma_kernel<true, true, FT_SEP><<<grid, FT_BLOCK, FT_SMEM, s>>>(ta, tb, (int)M, (int)N, (int)K, alpha, beta, C,
+                                                                      ldc, (int)tiles_m, (int)tiles_n);
+    else
+        ffma_tma_kernel<false, true, FT_SEP><<<grid, FT_BLOCK, FT_SMEM, s>>>(ta, tb, (int)M, (int)N, (int)K, alpha, beta, C,
+                                                                       ldc, (int)tiles_m, (int)tiles_n);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    prof_end(s, true, ev);
+    return cudaGetLastError();
+}
+
+}  // namespace emm

@@ -615,6 +615,20 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
     return fn;
 }
 
+// Plain 2-D FP32 tensor map (column-major array: dims {d0 = contiguous,
+// d1}, row stride ld elements), out-of-bounds reads zero; used by the
+// TMA-fed FFMA kernel (k_ffma_tma.cu).
+bool encode_tmap_f32_2d(CUtensorMap *tm, const float *ptr, int64_t d0, int64_t d1, int64_t ld, int box0, int box1,
+                        CUtensorMapSwizzle swz) {
+    auto enc = get_encode_fn();
+    if (!enc || !ptr) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)d0, (cuuint64_t)d1}, strides[1] = {(cuuint64_t)ld * 4};
+    cuuint32_t box[2] = {(cuuint32_t)box0, (cuuint32_t)box1}, estr[2] = {1, 1};
+    return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(ptr), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // One operand plane as a 2-D tensor map, out-of-bounds reads zero (the
 // M/N/K tails).  K-major: dims {kext, R}, box {32, 128}, 128B swizzle.
 // MN-major: dims {R, kext}, box {32, 32} (a 128-row tile is four boxes),
