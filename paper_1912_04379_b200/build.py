@@ -18,8 +18,13 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 # EMM_TIMELINE=1: debug build with per-CTA %globaltimer stamps (tools/timeline.py)
 TIMELINE = os.environ.get("EMM_TIMELINE") == "1"
-OBJ = os.path.join(PKG, "build_tl" if TIMELINE else "build")
-LIB = os.path.join(PKG, "libemm_tl.so" if TIMELINE else "libemm.so")
+# EMM_VARIANT=<tag> with EMM_VARIANT_FLAGS="-DX=1 ...": an A/B build of the
+# same sources into build_<tag>/libemm_<tag>.so (loaded with EMM_LIB)
+VARIANT = os.environ.get("EMM_VARIANT", "")
+VARIANT_FLAGS = os.environ.get("EMM_VARIANT_FLAGS", "").split() if VARIANT else []
+_TAG = "tl" if TIMELINE else VARIANT
+OBJ = os.path.join(PKG, f"build_{_TAG}" if _TAG else "build")
+LIB = os.path.join(PKG, f"libemm_{_TAG}.so" if _TAG else "libemm.so")
 SOURCES = ["api.cu", "k_tc.cu", "k_tcl.cu", "k_ffma.cu", "k_ffma_tma.cu", "k_skinny.cu", "k_tiny.cu", "k_misc.cu", "multi.cu", "k_probe.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -40,7 +45,7 @@ def nccl_include() -> str:
 def flags() -> list[str]:
     return ["-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
             "-I", os.path.join(ROOT, "include"), "-I", nccl_include(), "--expt-relaxed-constexpr",
-            *(["-DEMM_TIMELINE"] if TIMELINE else [])]
+            *(["-DEMM_TIMELINE"] if TIMELINE else []), *VARIANT_FLAGS]
 
 
 def _stale(out: str, deps: list[str]) -> bool:

@@ -50,31 +50,42 @@ constexpr int FT_GROUP_M = 16;                              // raster: 16 tile-r
 #endif
 constexpr bool FT_SEP = EMM_FT_SEP != 0;
 constexpr int FT_BLOCK = FT_SEP ? FT_THREADS : FT_CONSUMERS;
+#ifndef EMM_FT_GK
+#define EMM_FT_GK 2
+#endif
+constexpr int FT_GK = EMM_FT_GK;                            // k per operand group (2 or 4)
 
 // float index of the float4 holding (mn = 4q..4q+3, k) in an MN-contiguous tile
 __device__ __forceinline__ int mn_idx(int q, int k) { return (q >> 3) * 1024 + k * 32 + (((q & 7) ^ (k & 7)) << 2); }
-// float index of the float4 holding (row r, k = 4g..4g+3) in a K-contiguous tile
-__device__ __forceinline__ int kc_idx(int r, int g) { return r * 32 + ((g ^ (r & 7)) << 2); }
+// float index of (row r, k) in a K-contiguous tile (k % GK == 0: the start
+// of an aligned float2 / float4 along k)
+__device__ __forceinline__ int kc_idx(int r, int k) { return r * 32 + (((k >> 2) ^ (r & 7)) << 2) + (k & 3); }
 
-// The 8 operand values of one thread for 4 consecutive k (k = 4g + kk):
+// The 8 operand values of one thread for GK consecutive k (k = GK*g + kk):
 // v[kk][e], e = the thread's row (A) / column (B) slot.
 //   MN-contiguous: slot e -> mn = 4t + e (e < 4), 64 + 4t + (e - 4)
-//   K-contiguous:  slot e -> row t + 16 e
-template <bool MN>
-__device__ __forceinline__ void load_group(const float *__restrict__ T, int t, int g, float (&v)[4][8]) {
+//   K-contiguous:  slot e -> row t + 16 e (one float2 / float4 along k)
+template <bool MN, int GK>
+__device__ __forceinline__ void load_group(const float *__restrict__ T, int t, int g, float (&v)[GK][8]) {
     if (MN) {
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-            const float4 x0 = *reinterpret_cast<const float4 *>(T + mn_idx(t, 4 * g + kk));
-            const float4 x1 = *reinterpret_cast<const float4 *>(T + mn_idx(16 + t, 4 * g + kk));
+        for (int kk = 0; kk < GK; ++kk) {
+            const float4 x0 = *reinterpret_cast<const float4 *>(T + mn_idx(t, GK * g + kk));
+            const float4 x1 = *reinterpret_cast<const float4 *>(T + mn_idx(16 + t, GK * g + kk));
             v[kk][0] = x0.x; v[kk][1] = x0.y; v[kk][2] = x0.z; v[kk][3] = x0.w;
             v[kk][4] = x1.x; v[kk][5] = x1.y; v[kk][6] = x1.z; v[kk][7] = x1.w;
+        }
+    } else if (GK == 4) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const float4 x = *reinterpret_cast<const float4 *>(T + kc_idx(t + 16 * e, 4 * g));
+            v[0][e] = x.x; v[1 % GK][e] = x.y; v[2 % GK][e] = x.z; v[3 % GK][e] = x.w;
         }
     } else {
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-            const float4 x = *reinterpret_cast<const float4 *>(T + kc_idx(t + 16 * e, g));
-            v[0][e] = x.x; v[1][e] = x.y; v[2][e] = x.z; v[3][e] = x.w;
+            const float2 x = *reinterpret_cast<const float2 *>(T + kc_idx(t + 16 * e, GK * g));
+            v[0][e] = x.x; v[1 % GK][e] = x.y;
         }
     }
 }
@@ -170,13 +181,20 @@ __global__ void __launch_bounds__(SEP ? FT_THREADS : FT_CONSUMERS, 1)
         mbar_wait(&full[s], (uint32_t)(kt / FT_STAGES) & 1u);
         const float *As = reinterpret_cast<const float *>(smem + s * FT_STAGE_BYTES);
         const float *Bs = As + FT_TILE_FLOATS;
+        // operand groups double-buffered: group g+1 is read from SMEM while
+        // group g's FFMA2s run
+        float av[2][FT_GK][8], bv[2][FT_GK][8];
+        load_group<A_MN, FT_GK>(As, tm, 0, av[0]);
+        load_group<B_MN, FT_GK>(Bs, tn, 0, bv[0]);
 #pragma unroll
-        for (int g = 0; g < FT_K / 4; ++g) {
-            float av[4][8], bv[4][8];
-            load_group<A_MN>(As, tm, g, av);
-            load_group<B_MN>(Bs, tn, g, bv);
+        for (int g = 0; g < FT_K / FT_GK; ++g) {
+            if (g + 1 < FT_K / FT_GK) {
+                load_group<A_MN, FT_GK>(As, tm, g + 1, av[(g + 1) & 1]);
+                load_group<B_MN, FT_GK>(Bs, tn, g + 1, bv[(g + 1) & 1]);
+            }
+            const int u = g & 1;
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
+            for (int kk = 0; kk < FT_GK; ++kk) {
                 // the pair operand stays fixed over 8 consecutive FFMA2s (operand
                 // reuse cache) while the broadcast scalar varies: 125 vs 108
                 // FMA/clk/SM for the other order (tools/ffma2_probe.cu)
@@ -185,15 +203,16 @@ __global__ void __launch_bounds__(SEP ? FT_THREADS : FT_CONSUMERS, 1)
                     for (int jp = 0; jp < 4; ++jp)
 #pragma unroll
                         for (int i = 0; i < 8; ++i)
-                            acc[i * 4 + jp] = __ffma2_rn(make_float2(av[kk][i], av[kk][i]),
-                                                         make_float2(bv[kk][2 * jp], bv[kk][2 * jp + 1]), acc[i * 4 + jp]);
+                            acc[i * 4 + jp] = __ffma2_rn(make_float2(av[u][kk][i], av[u][kk][i]),
+                                                         make_float2(bv[u][kk][2 * jp], bv[u][kk][2 * jp + 1]),
+                                                         acc[i * 4 + jp]);
                 } else {
 #pragma unroll
                     for (int ip = 0; ip < 4; ++ip)
 #pragma unroll
                         for (int j = 0; j < 8; ++j)
-                            acc[ip * 8 + j] = __ffma2_rn(make_float2(av[kk][2 * ip], av[kk][2 * ip + 1]),
-                                                         make_float2(bv[kk][j], bv[kk][j]), acc[ip * 8 + j]);
+                            acc[ip * 8 + j] = __ffma2_rn(make_float2(av[u][kk][2 * ip], av[u][kk][2 * ip + 1]),
+                                                         make_float2(bv[u][kk][j], bv[u][kk][j]), acc[ip * 8 + j]);
                 }
             }
         }
