@@ -94,6 +94,15 @@ cudaError_t launch_tc_split_sgemm(bool a_kc, bool b_kc, const float *A, int64_t 
                                   unsigned int *ctrl, int splits, float *partial, cudaStream_t s,
                                   const PeerOut *peers = nullptr);
 bool tma_legal(const void *ptr, int64_t ld);
+// A plane as the tcgen05 kernels' 2-D tensor map (K-major box {32, 128},
+// MN-major box {32, 32} with the 32B-atom 128B swizzle), OOB reads zero.
+bool tc_make_tmap(CUtensorMap *tm, const TcPlane &p, int64_t R);
+// KN2w (k_tc1w.cu): 1xTF32 with a 256 x 512 tile per CTA pair (the whole
+// 512-column TMEM as one accumulator) — 25% fewer operand bytes per flop
+// than the 256 x 256 tile.  Full tiles only (no split-K / stream-K / peers).
+bool tc1w_wanted(int64_t M, int64_t N, int64_t K);
+cudaError_t launch_tc1w_sgemm(const TcOperands &ops, int64_t M, int64_t N, int64_t K, float alpha, float beta,
+                              float *C, int64_t ldc, cudaStream_t s);
 bool encode_tmap_f32_2d(CUtensorMap *tm, const float *ptr, int64_t d0, int64_t d1, int64_t ld, int box0, int box1,
                         CUtensorMapSwizzle swz);
 int64_t tc_kpad(int64_t K);

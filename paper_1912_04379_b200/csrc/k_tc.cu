@@ -633,7 +633,7 @@ bool encode_tmap_f32_2d(CUtensorMap *tm, const float *ptr, int64_t d0, int64_t d
 // M/N/K tails).  K-major: dims {kext, R}, box {32, 128}, 128B swizzle.
 // MN-major: dims {R, kext}, box {32, 32} (a 128-row tile is four boxes),
 // 128B swizzle with 32B atoms (the only MN-major TF32 UMMA layout).
-static bool make_tmap(CUtensorMap *tm, const TcPlane &p, int64_t R) {
+bool tc_make_tmap(CUtensorMap *tm, const TcPlane &p, int64_t R) {
     auto enc = get_encode_fn();
     if (!enc || !p.ptr) return false;
     cuuint64_t dims[2], strides[1] = {(cuuint64_t)p.ld * 4};
@@ -783,9 +783,9 @@ static cudaError_t launch_tc_t(const TcOperands &ops, int64_t M, int64_t N, int6
     });
     if (attr_err != cudaSuccess) return attr_err;
     CUtensorMap ta0, ta1, tb0, tb1;
-    if (!make_tmap(&ta0, ops.a0, M) || !make_tmap(&tb0, ops.b0, N)) return cudaErrorInvalidValue;
+    if (!tc_make_tmap(&ta0, ops.a0, M) || !tc_make_tmap(&tb0, ops.b0, N)) return cudaErrorInvalidValue;
     if (Cfg::PLANES == 2) {
-        if (!make_tmap(&ta1, ops.a1, M) || !make_tmap(&tb1, ops.b1, N)) return cudaErrorInvalidValue;
+        if (!tc_make_tmap(&ta1, ops.a1, M) || !tc_make_tmap(&tb1, ops.b1, N)) return cudaErrorInvalidValue;
     } else {
         ta1 = ta0;
         tb1 = tb0;
@@ -877,6 +877,8 @@ cudaError_t launch_tc_sgemm(int terms, const TcOperands &ops, int64_t M, int64_t
     if (splits < 1 || (splits > 1 && !partial)) return cudaErrorInvalidValue;
     if (peers && (peers->n < 0 || peers->n > 8 || splits > 1)) return cudaErrorInvalidValue;
     const PeerOut pe = peers ? *peers : PeerOut{};
+    if (terms == 1 && splits == 1 && pe.n == 0 && tc1w_wanted(M, N, K))
+        return launch_tc1w_sgemm(ops, M, N, K, alpha, beta, C, ldc, s);
     const int64_t Kp = tc_kpad(K);
     if (terms == 3) return launch_tc_m<3>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe, sk_ws);
     if (terms == 2) return launch_tc_m<2>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe, sk_ws);
