@@ -52,7 +52,9 @@ def _check(case, dC):
 @pytest.mark.parametrize("shape,math", [((8192, 4096, 512), "3xtf32"),     # 512 tiles: 6.9 waves, lockstep
                                         ((4096, 4096, 1024), "3xtf32"),    # 3.46 waves: stream-K remainder
                                         ((8192, 4096, 512), "tf32bf16"),
-                                        ((8192, 4096, 512), "1xtf32")])
+                                        ((8192, 4096, 512), "1xtf32"),
+                                        ((8192, 4096, 2048), "1xtf32"),    # KN2w (256x512 tiles)
+                                        ((4096, 2048, 512), "ffma")])      # KN3b
 def test_concurrent_streams(emm, shape, math):
     M, N, K = shape
     cases = [Case("N", "T" if i % 2 else "N", M, N, K, 1.0, 1.0, kind="ints", c_kind="ints", seed=i)

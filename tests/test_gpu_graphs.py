@@ -32,6 +32,8 @@ def emm():
     ((1024, 1024, 1024), "3xtf32", False),    # emm_sgemm-style: scratch from the stream-ordered pool
     ((333, 333, 333), "3xtf32", True),        # tiny kernel
     ((20000, 16, 700), "3xtf32", True),       # skinny kernel
+    ((4096, 4096, 2048), "1xtf32", True),     # KN2w: 256x512 tiles
+    ((2048, 1536, 512), "ffma", True),        # KN3b: TMA-fed FFMA
 ])
 def test_graph_replay_bitwise(emm, shape, math, with_ws):
     M, N, K = shape
