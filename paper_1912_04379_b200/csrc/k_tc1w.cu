@@ -13,9 +13,13 @@
 // panel" at the L1 level, applied to the SMEM ring).
 //
 // Without a second TMEM buffer the epilogue cannot run under the next
-// tile's MMAs wholesale; instead it drains the N-half 0 columns first and
-// releases them, and the MMA issuer starts the next tile with the half-0
-// MMAs of the first W_STAGES stages (already in SMEM) while half 1 drains.
+// tile's MMAs wholesale; instead it moves the N-half 0 columns to registers
+// and releases them at once (then scales and stores them), and the MMA
+// issuer starts the next tile with the half-0 MMAs of the first W_STAGES
+// stages (already in SMEM) while half 1 drains.  (Prefetching the tile's C_in
+// into L2 while its MMAs run was measured: c4-ii 1.030 -> 1.016 ms but c4-i
+// 0.764 -> 0.782 ms — the prefetched C crowds the wave's operand panels out
+// of L2 — so it is not done.)
 // Warp roles as in KN1/KN2: warp 0 TMA producer, warp 1 MMA issuer (leader
 // CTA), warps 2-9 epilogue (lane quarter q = warp % 4, column half).
 #include <cuda.h>
@@ -186,40 +190,46 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (TC_EPI_WARPS +
             for (int h = 0; h < 2; ++h) {
                 const int col0 = n0 + h * 256 + hh * 128;
                 const uint32_t tb = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(h * 256 + hh * 128);
-                float *cp = C + (int64_t)row + (int64_t)col0 * ldc;
-                const int jmax = min(128, N - col0);
-#pragma unroll 1
-                for (int c = 0; c < 4; ++c) {   // 4 x 32 columns
-                    uint32_t v0[16], v1[16];
-                    tmem_ld_32x32b_x16(tb + (uint32_t)(32 * c), v0);
-                    tmem_ld_32x32b_x16(tb + (uint32_t)(32 * c + 16), v1);
-                    tmem_ld_wait();
-                    if (row < M) {
-                        float o[32];
+                // this warp's 32 rows x 128 columns of half h -> registers, then
+                // release the half at once: the next tile's MMAs may start on it
+                // while the values are scaled and stored
+                float acc[128];
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) {
-                            o[j] = alpha * __uint_as_float(v0[j]);
-                            o[16 + j] = alpha * __uint_as_float(v1[j]);
-                        }
-                        float *p = cp + (int64_t)(32 * c) * ldc;
-                        if (beta != 0.0f) {
-                            float cin[32];
+                for (int c = 0; c < 8; ++c) {
+                    uint32_t v[16];
+                    tmem_ld_32x32b_x16(tb + (uint32_t)(16 * c), v);
 #pragma unroll
-                            for (int j = 0; j < 32; ++j) cin[j] = (32 * c + j < jmax) ? __ldcs(p + (int64_t)j * ldc) : 0.0f;
-#pragma unroll
-                            for (int j = 0; j < 32; ++j) o[j] = fmaf(beta, cin[j], o[j]);
-                        }
-#pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            if (32 * c + j < jmax) __stcs(p + (int64_t)j * ldc, o[j]);
-                    }
+                    for (int j = 0; j < 16; ++j) acc[16 * c + j] = __uint_as_float(v[j]);
                 }
-                // this warp's part of half h is in registers / stored: release it
+                tmem_ld_wait();
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) {
                     const uint32_t eb = leader_empty0 + (uint32_t)(h * sizeof(uint64_t));
                     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(eb) : "memory");
+                }
+                if (row >= M) continue;
+                float *cp = C + (int64_t)row + (int64_t)col0 * ldc;
+                const int jmax = min(128, N - col0);
+                if (beta == 0.0f) {
+                    float *sp = cp;
+#pragma unroll
+                    for (int j = 0; j < 128; ++j, sp += ldc)
+                        if (j < jmax) __stcs(sp, alpha * acc[j]);
+                } else {
+                    // 16 independent C loads before the 16 stores of a group
+                    // (a store may alias a later load through ldc)
+#pragma unroll
+                    for (int g = 0; g < 8; ++g) {
+                        float cin[16];
+                        const float *lp = cp + (int64_t)(16 * g) * ldc;
+#pragma unroll
+                        for (int j = 0; j < 16; ++j, lp += ldc) cin[j] = (16 * g + j < jmax) ? __ldcs(lp) : 0.0f;
+                        float *sp = cp + (int64_t)(16 * g) * ldc;
+#pragma unroll
+                        for (int j = 0; j < 16; ++j, sp += ldc)
+                            if (16 * g + j < jmax) __stcs(sp, fmaf(beta, cin[j], alpha * acc[16 * g + j]));
+                    }
                 }
             }
         }
