@@ -461,13 +461,28 @@ static int host_pipelined(char tA, char tB, int64_t M, int64_t N, int64_t K, flo
         }
         g_hs.dev = dev;
     }
-    // Square blocks of `blk` rows of op(A) / columns of op(B): fine enough
-    // that the first GEMM starts after ~10 ms of PCIe, at most 64 GEMMs.
+    // Blocks of op(A) rows / op(B) columns: 2048 (EMM_HOST_BLOCK; at most 64
+    // blocks per operand); EMM_HOST_FIRST sizes the first two of each operand
+    // and EMM_HOST_CHUNK splits each GEMM region into pieces with their own
+    // copy-back.  Both default off: at 32768^3 first = 1024 starts the first
+    // GEMM 4.9 ms earlier but the smaller GEMMs cost more (307 vs 304 ms), and
+    // 8192-wide pieces cut the copy-back tail 5 -> 1.5 ms but fall off whole
+    // waves (316 ms; profiles/r01_e2e_timeline.txt).
     int64_t blk = 2048;
     if (const char *eb = getenv("EMM_HOST_BLOCK")) blk = std::max<int64_t>(256, atoll(eb) / 256 * 256);
     blk = std::max(blk, ((std::max(M, N) + 31) / 32 + 255) / 256 * 256);
-    const int64_t bm = blk, bn = blk;
-    const int GM = (int)((M + bm - 1) / bm), GN = (int)((N + bn - 1) / bn);
+    int64_t first = blk;
+    if (const char *ef = getenv("EMM_HOST_FIRST")) first = std::max<int64_t>(256, atoll(ef) / 256 * 256);
+    first = std::min(first, blk);
+    auto bounds = [&](int64_t R) {   // block starts, R appended
+        std::vector<int64_t> b{0};
+        while (b.back() < R) b.push_back(std::min(R, b.back() + (b.size() <= 2 ? first : blk)));
+        return b;
+    };
+    const std::vector<int64_t> ra = bounds(M), cb = bounds(N);
+    const int GM = (int)ra.size() - 1, GN = (int)cb.size() - 1;
+    int64_t chunk = INT64_MAX;
+    if (const char *ec = getenv("EMM_HOST_CHUNK")) chunk = std::max<int64_t>(512, atoll(ec) / 256 * 256);
     const int64_t Kp = tc_kpad(K);
     const int terms = terms_of(math), pl = planes_of(math);
     const int pmode = math == EMM_MATH_3XTF32 ? PK_FULL3_ : math == EMM_MATH_TF32_BF16 ? PK_FULLX_ : PK_FULL1_;
@@ -493,18 +508,18 @@ static int host_pipelined(char tA, char tB, int64_t M, int64_t N, int64_t K, flo
     // tensor-core work after the first few blocks.
     int na = 0, nb = 0, ng = 0;
     while ((na < GM || nb < GN) && e == cudaSuccess) {
-        const int64_t rows_res = std::min(M, (int64_t)na * bm), cols_res = std::min(N, (int64_t)nb * bn);
+        const int64_t rows_res = ra[na], cols_res = cb[nb];
         const bool addA = na < GM && (nb >= GN || rows_res <= cols_res);
         int64_t r0, nr, c0, nc;   // the GEMM's C region
         if (addA) {
-            r0 = (int64_t)na * bm;
-            nr = std::min(bm, M - r0);
+            r0 = ra[na];
+            nr = ra[na + 1] - r0;
             c0 = 0;
             nc = cols_res;
             e = copy_rows(dA, A, a_rows_ld, lda, r0, nr, K, h2d);
         } else {
-            c0 = (int64_t)nb * bn;
-            nc = std::min(bn, N - c0);
+            c0 = cb[nb];
+            nc = cb[nb + 1] - c0;
             r0 = 0;
             nr = rows_res;
             e = copy_rows(dB, B, b_rows_ld, ldb, c0, nc, K, h2d);
@@ -530,22 +545,31 @@ static int host_pipelined(char tA, char tB, int64_t M, int64_t N, int64_t K, flo
         }
         if (e == cudaSuccess) e = launch_pack(pmode, pk, nullptr, K, nullptr, comp);
         if (nr == 0 || nc == 0 || e != cudaSuccess) continue;
-        TcOperands ops;
-        ops.a0 = TcPlane{Ap + (size_t)r0 * Kp, Kp, false, Kp};
-        ops.b0 = TcPlane{Bp + (size_t)c0 * Kp, Kp, false, Kp};
-        if (pl == 2) {
-            ops.a1 = TcPlane{Ap + (size_t)M * Kp + (size_t)r0 * Kp, Kp, false, Kp};
-            ops.b1 = TcPlane{Bp + (size_t)N * Kp + (size_t)c0 * Kp, Kp, false, Kp};
+        // the region in pieces along its long side: GEMM, then D2H of the piece
+        const bool split_cols = nc >= nr;
+        const int64_t len = split_cols ? nc : nr;
+        for (int64_t o = 0; o < len && e == cudaSuccess; o += chunk) {
+            const int64_t pr0 = split_cols ? r0 : r0 + o, pnr = split_cols ? nr : std::min(chunk, nr - o);
+            const int64_t pc0 = split_cols ? c0 + o : c0, pnc = split_cols ? std::min(chunk, nc - o) : nc;
+            TcOperands ops;
+            ops.a0 = TcPlane{Ap + (size_t)pr0 * Kp, Kp, false, Kp};
+            ops.b0 = TcPlane{Bp + (size_t)pc0 * Kp, Kp, false, Kp};
+            if (pl == 2) {
+                ops.a1 = TcPlane{Ap + (size_t)M * Kp + (size_t)pr0 * Kp, Kp, false, Kp};
+                ops.b1 = TcPlane{Bp + (size_t)N * Kp + (size_t)pc0 * Kp, Kp, false, Kp};
+            }
+            unsigned int *cw = ctrl + 32 * (ng & 63);   // zeroed once for the first 64 GEMMs
+            if (ng++ >= 64) e = cudaMemsetAsync(cw, 0, 128, comp);
+            if (e == cudaSuccess)
+                e = launch_tc_sgemm(terms, ops, pnr, pnc, K, alpha, beta, dC + pr0 + pc0 * ldc, ldc, cw, 1, nullptr,
+                                    comp);
+            cudaEvent_t done = ev();
+            if (e == cudaSuccess) e = cudaEventRecord(done, comp);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(d2h, done, 0);
+            if (e == cudaSuccess)
+                e = cudaMemcpy2DAsync(C + pr0 + pc0 * ldc, (size_t)ldc * 4, dC + pr0 + pc0 * ldc, (size_t)ldc * 4,
+                                      (size_t)pnr * 4, (size_t)pnc, cudaMemcpyDeviceToHost, d2h);
         }
-        e = launch_tc_sgemm(terms, ops, nr, nc, K, alpha, beta, dC + r0 + c0 * ldc, ldc, ctrl + 32 * (ng++ & 63), 1,
-                            nullptr, comp);
-        // D2H of the finished region
-        cudaEvent_t done = ev();
-        if (e == cudaSuccess) e = cudaEventRecord(done, comp);
-        if (e == cudaSuccess) e = cudaStreamWaitEvent(d2h, done, 0);
-        if (e == cudaSuccess)
-            e = cudaMemcpy2DAsync(C + r0 + c0 * ldc, (size_t)ldc * 4, dC + r0 + c0 * ldc, (size_t)ldc * 4,
-                                  (size_t)nr * 4, (size_t)nc, cudaMemcpyDeviceToHost, d2h);
     }
     if (e == cudaSuccess) e = cudaStreamSynchronize(d2h);
     if (e == cudaSuccess) e = cudaStreamSynchronize(comp);
