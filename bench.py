@@ -368,7 +368,8 @@ def main():
                 "unit": "TFLOP/s", "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "peak_kind": f"{pname}, from {src} bf16 sustained {bf16_sus} TF x 1.1/2.25",
                 "peak_burst": peak_b, "frac_burst": (achieved / peak_b) if achieved else None,
-                "kernel": "tc_sgemm_kernel" if math != "ffma" else "ffma_sgemm_kernel",
+                "kernel": {"ffma": "ffma_tma_kernel (KN3b)", "1xtf32": "tc1w_kernel (KN2w, 256x512 tiles)"}.get(
+                    math, "tc_sgemm_kernel"),
                 "kernel_ms": kernel_ms, "kernel_share_of_step": (gemm_ms / ms) if ms > 0 else None,
                 "other_kernels_ms_per_step": other_ms / steps}
         return {"value": flops * steps / (ms / 1e3) / 1e9, "ms": ms, "launches": launches, "clocks": clk,
