@@ -33,23 +33,33 @@ namespace emm {
 using namespace ptx;
 
 namespace {
-constexpr int FT_M = 128, FT_N = 128, FT_K = 32, FT_STAGES = 4;
+constexpr int FT_M = 128, FT_N = 128, FT_K = 32;
 constexpr int FT_TILE_FLOATS = 128 * FT_K;                  // one operand tile: 16 KB
 constexpr int FT_STAGE_BYTES = 2 * FT_TILE_FLOATS * 4;      // A + B: 32 KB
 constexpr int FT_CONSUMERS = 256, FT_THREADS = FT_CONSUMERS + 32;
 constexpr int FT_PROMOTE = 256 / FT_K;                      // stages per promotion (256 of K)
 constexpr int FT_MASTER_FLOATS = 64 * FT_CONSUMERS;
-constexpr int FT_SMEM = FT_STAGES * FT_STAGE_BYTES + FT_MASTER_FLOATS * 4 + 1024 /*align*/ + 128 /*barriers*/;
 constexpr int FT_GROUP_M = 16;                              // raster: 16 tile-rows per group (L2 reuse of B)
-// Dedicated producer warp (default).  -DEMM_FT_SEP=0 instead lets consumer
-// thread 0 issue the loads (256 threads, up to 255 registers): measured
-// slower, c2-8192 54.7 vs 57.7 TFLOP/s — thread 0 waits for the slowest warp
-// to free a slot and holds back warp 0.
+// Two ways to feed the ring:
+//  SEP = true:  a dedicated producer warp (288 threads -> 168 registers per
+//               thread), 4 stages, promotion master in SMEM;
+//  SEP = false: no producer warp — the LAST warp to finish a stage refills
+//               its slot (a shared counter per slot, nobody waits for it) —
+//               256 threads, up to 255 registers, master in registers,
+//               6 stages.  Measured slower (c2-8192 19.79 vs 19.06 ms, c4-i
+//               9.42 vs 8.98; profiles/r01_ab_ffma_kn3b_noprodwarp2.jsonl):
+//               the extra registers buy nothing and the refilling warp
+//               stalls; an earlier "thread 0 refills" form was slower still.
+template <bool SEP>
+struct FtCfg {
+    static constexpr int STAGES = SEP ? 4 : 6;
+    static constexpr int BLOCK = SEP ? FT_THREADS : FT_CONSUMERS;
+    static constexpr int SMEM = STAGES * FT_STAGE_BYTES + (SEP ? FT_MASTER_FLOATS * 4 : 0) + 1024 + 256;
+};
 #ifndef EMM_FT_SEP
 #define EMM_FT_SEP 1
 #endif
 constexpr bool FT_SEP = EMM_FT_SEP != 0;
-constexpr int FT_BLOCK = FT_SEP ? FT_THREADS : FT_CONSUMERS;
 #ifndef EMM_FT_GK
 #define EMM_FT_GK 2
 #endif
@@ -95,18 +105,20 @@ __device__ __forceinline__ int slot_pos(bool mn, int t, int e) { return mn ? (e 
 // PAIR_J (B MN-contiguous): acc[i*4 + j/2] holds (i, j), (i, j+1);
 // else (A MN-contiguous):   acc[(i/2)*8 + j] holds (i, j), (i+1, j).
 template <bool A_MN, bool B_MN, bool SEP>
-__global__ void __launch_bounds__(SEP ? FT_THREADS : FT_CONSUMERS, 1)
+__global__ void __launch_bounds__(FtCfg<SEP>::BLOCK, 1)
     ffma_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                     int K, float alpha, float beta, float *__restrict__ C, int64_t ldc, int tiles_m, int tiles_n) {
     static_assert(A_MN || B_MN, "TN (both K-contiguous) runs on KN3");
     constexpr bool PAIR_J = B_MN;
+    constexpr int STAGES = FtCfg<SEP>::STAGES;
     extern __shared__ __align__(1024) uint8_t ft_raw[];
     // 1024-B aligned base for the 128B-swizzled TMA boxes; offset arithmetic
     // on the shared array (not via an integer cast) keeps the reads LDS
     uint8_t *smem = ft_raw + ((1024u - (smem_u32(ft_raw) & 1023u)) & 1023u);
-    float *master = reinterpret_cast<float *>(smem + FT_STAGES * FT_STAGE_BYTES);
-    uint64_t *full = reinterpret_cast<uint64_t *>(master + FT_MASTER_FLOATS);
-    uint64_t *empty = full + FT_STAGES;
+    float *master_s = reinterpret_cast<float *>(smem + STAGES * FT_STAGE_BYTES);   // SEP only
+    uint64_t *full = reinterpret_cast<uint64_t *>(master_s + (SEP ? FT_MASTER_FLOATS : 0));
+    uint64_t *empty = full + STAGES;                                               // SEP only
+    unsigned int *done_cnt = reinterpret_cast<unsigned int *>(empty + STAGES);    // !SEP only
 
     // grouped raster: FT_GROUP_M tile-rows share each B panel while it is in L2
     const int bid = (int)blockIdx.x;
@@ -119,19 +131,20 @@ __global__ void __launch_bounds__(SEP ? FT_THREADS : FT_CONSUMERS, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < FT_STAGES; ++s) {
+        for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], FT_CONSUMERS / 32);
+            done_cnt[s] = 0;
         }
         fence_mbar_init();
     }
     __syncthreads();
 
     const uint64_t pol = policy_evict_normal();
-    // loads of K-stage kt into ring slot kt % FT_STAGES (one thread)
+    // loads of K-stage kt into ring slot kt % STAGES (one thread; the slot
+    // is known to be free)
     auto issue = [&](int kt) {
-        const int s = kt % FT_STAGES;
-        mbar_wait(&empty[s], ((uint32_t)(kt / FT_STAGES) & 1u) ^ 1u);
+        const int s = kt % STAGES;
         mbar_arrive_expect_tx(&full[s], FT_STAGE_BYTES);
         const uint32_t st = smem_u32(smem + s * FT_STAGE_BYTES);
         const uint32_t sb = st + FT_TILE_FLOATS * 4;
@@ -155,14 +168,15 @@ __global__ void __launch_bounds__(SEP ? FT_THREADS : FT_CONSUMERS, 1)
             if (lane == 0) {
                 prefetch_tmap(&tmA);
                 prefetch_tmap(&tmB);
-                for (int kt = 0; kt < nk; ++kt) issue(kt);
+                for (int kt = 0; kt < nk; ++kt) {
+                    mbar_wait(&empty[kt % STAGES], ((uint32_t)(kt / STAGES) & 1u) ^ 1u);
+                    issue(kt);
+                }
             }
             return;
         }
     } else if (threadIdx.x == 0) {
-        // no producer warp (all 64K registers to the 8 FFMA warps): thread 0
-        // fills the first FT_STAGES - 1 slots here and one more per K-stage
-        for (int kt = 0; kt < FT_STAGES - 1 && kt < nk; ++kt) issue(kt);
+        for (int kt = 0; kt < STAGES && kt < nk; ++kt) issue(kt);   // fill the ring
     }
 
     // ===== consumers =====
@@ -171,14 +185,17 @@ __global__ void __launch_bounds__(SEP ? FT_THREADS : FT_CONSUMERS, 1)
     float2 acc[32];
 #pragma unroll
     for (int e = 0; e < 32; ++e) acc[e] = make_float2(0.0f, 0.0f);
+    float master_r[SEP ? 1 : 64];   // !SEP: promotion master in registers
 #pragma unroll
-    for (int e = 0; e < 64; ++e) master[e * FT_CONSUMERS + c] = 0.0f;
+    for (int e = 0; e < (SEP ? 1 : 64); ++e) master_r[e] = 0.0f;
+    if (SEP) {
+#pragma unroll
+        for (int e = 0; e < 64; ++e) master_s[e * FT_CONSUMERS + c] = 0.0f;
+    }
 
     for (int kt = 0; kt < nk; ++kt) {
-        const int s = kt % FT_STAGES;
-        // slot of stage kt-1: free once every warp has finished kt-1
-        if (!SEP && c == 0 && kt + FT_STAGES - 1 < nk) issue(kt + FT_STAGES - 1);
-        mbar_wait(&full[s], (uint32_t)(kt / FT_STAGES) & 1u);
+        const int s = kt % STAGES;
+        mbar_wait(&full[s], (uint32_t)(kt / STAGES) & 1u);
         const float *As = reinterpret_cast<const float *>(smem + s * FT_STAGE_BYTES);
         const float *Bs = As + FT_TILE_FLOATS;
         // operand groups double-buffered: group g+1 is read from SMEM while
@@ -217,16 +234,31 @@ __global__ void __launch_bounds__(SEP ? FT_THREADS : FT_CONSUMERS, 1)
             }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
+        if (SEP) {
+            if (lane == 0) mbar_arrive(&empty[s]);
+        } else if (lane == 0) {
+            // the last of the 8 warps to finish this stage refills its slot
+            unsigned int old;
+            asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                         : "=r"(old) : "r"(smem_u32(&done_cnt[s])) : "memory");
+            if (old == FT_CONSUMERS / 32 - 1) {
+                done_cnt[s] = 0;
+                fence_proxy_async_smem();   // generic reads of the slot before the async-proxy overwrite
+                if (kt + STAGES < nk) issue(kt + STAGES);
+            }
+        }
         if ((kt + 1) % FT_PROMOTE == 0 || kt + 1 == nk) {
-            // promotion: master (SMEM, per-thread column) += register partials
+            // promotion: master += register partials (round-to-nearest adds)
 #pragma unroll
             for (int i = 0; i < 8; ++i)
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     const float2 &p = PAIR_J ? acc[i * 4 + (j >> 1)] : acc[(i >> 1) * 8 + j];
                     const float v = PAIR_J ? ((j & 1) ? p.y : p.x) : ((i & 1) ? p.y : p.x);
-                    master[(i * 8 + j) * FT_CONSUMERS + c] += v;
+                    if (SEP)
+                        master_s[(i * 8 + j) * FT_CONSUMERS + c] += v;
+                    else
+                        master_r[(i * 8 + j) % (SEP ? 1 : 64)] += v;
                 }
 #pragma unroll
             for (int e = 0; e < 32; ++e) acc[e] = make_float2(0.0f, 0.0f);
@@ -242,7 +274,7 @@ __global__ void __launch_bounds__(SEP ? FT_THREADS : FT_CONSUMERS, 1)
         for (int i = 0; i < 8; ++i) {
             const int row = m0 + slot_pos(A_MN, tm, i);
             if (row < M) {
-                const float v = master[(i * 8 + j) * FT_CONSUMERS + c];
+                const float v = SEP ? master_s[(i * 8 + j) * FT_CONSUMERS + c] : master_r[(i * 8 + j) % (SEP ? 1 : 64)];
                 float *d = C + row + (int64_t)col * ldc;
                 *d = beta == 0.0f ? alpha * v : fmaf(beta, *d, alpha * v);
             }
@@ -274,7 +306,7 @@ cudaError_t launch_ffma_tma_sgemm(bool tA, bool tB, int64_t M, int64_t N, int64_
     static cudaError_t attr = [] {
         cudaError_t e = cudaSuccess;
         auto set = [&](const void *f) {
-            cudaError_t r = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, FT_SMEM);
+            cudaError_t r = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, FtCfg<FT_SEP>::SMEM);
             if (r != cudaSuccess) e = r;
         };
         set((const void *)ffma_tma_kernel<true, false, FT_SEP>);
@@ -287,13 +319,13 @@ cudaError_t launch_ffma_tma_sgemm(bool tA, bool tB, int64_t M, int64_t N, int64_
     cudaEvent_t ev = nullptr;
     prof_begin(s, true, &ev);
     if (a_mn && !b_mn)
-        ffma_tma_kernel<true, false, FT_SEP><<<grid, FT_BLOCK, FT_SMEM, s>>>(ta, tb, (int)M, (int)N, (int)K, alpha, beta, C,
+        ffma_tma_kernel<true, false, FT_SEP><<<grid, FtCfg<FT_SEP>::BLOCK, FtCfg<FT_SEP>::SMEM, s>>>(ta, tb, (int)M, (int)N, (int)K, alpha, beta, C,
                                                                        ldc, (int)tiles_m, (int)tiles_n);
     else if (a_mn)
-        ffma_tma_kernel<true, true, FT_SEP><<<grid, FT_BLOCK, FT_SMEM, s>>>(ta, tb, (int)M, (int)N, (int)K, alpha, beta, C,
+        ffma_tma_kernel<true, true, FT_SEP><<<grid, FtCfg<FT_SEP>::BLOCK, FtCfg<FT_SEP>::SMEM, s>>>(ta, tb, (int)M, (int)N, (int)K, alpha, beta, C,
                                                                       ldc, (int)tiles_m, (int)tiles_n);
     else
-        ffma_tma_kernel<false, true, FT_SEP><<<grid, FT_BLOCK, FT_SMEM, s>>>(ta, tb, (int)M, (int)N, (int)K, alpha, beta, C,
+        ffma_tma_kernel<false, true, FT_SEP><<<grid, FtCfg<FT_SEP>::BLOCK, FtCfg<FT_SEP>::SMEM, s>>>(ta, tb, (int)M, (int)N, (int)K, alpha, beta, C,
                                                                        ldc, (int)tiles_m, (int)tiles_n);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     prof_end(s, true, ev);
