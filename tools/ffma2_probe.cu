@@ -140,6 +140,9 @@ __global__ void __launch_bounds__(256, 1) probe_smem(float *out, long long *clk)
             const int u = DBUF ? (g & 1) : 0;
             if (DBUF) {
                 if (g + 1 < 8) load(g + 1, av[(g + 1) & 1], bv[(g + 1) & 1]);
+                // keep the next group's LDS ahead of this group's FFMA2 block
+                // (the block then runs without LDS in between)
+                asm volatile("" ::: "memory");
             } else if (g > 0) {
                 load(g, av[0], bv[0]);
             }
