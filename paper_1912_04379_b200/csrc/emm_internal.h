@@ -97,6 +97,7 @@ bool tma_legal(const void *ptr, int64_t ld);
 // A plane as the tcgen05 kernels' 2-D tensor map (K-major box {32, 128},
 // MN-major box {32, 32} with the 32B-atom 128B swizzle), OOB reads zero.
 bool tc_make_tmap(CUtensorMap *tm, const TcPlane &p, int64_t R);
+bool tc_make_tmap_rows(CUtensorMap *tm, const TcPlane &p, int64_t R, int box_rows);
 // KN2w (k_tc1w.cu): 1xTF32 with a 256 x 512 tile per CTA pair (the whole
 // 512-column TMEM as one accumulator) — 25% fewer operand bytes per flop
 // than the 256 x 256 tile.  Full tiles only (no split-K / stream-K / peers).

@@ -428,23 +428,6 @@ cudaError_t launch_splitk_reduce(const float *partial, int splits, int64_t M, in
 // MMAs run on the other buffer ("promotion"), bounding the truncation bias
 // to one chunk.
 // =====================================================================
-// warp 0 = TMA producer, warp 1 = MMA issuer + TMEM owner, warps 2-9 = 8
-// promotion/epilogue warps (2 per TMEM lane quarter).
-constexpr int TC_EPI_WARP0 = 2;
-constexpr int TC_THREADS_P = 32 * (TC_EPI_WARP0 + TC_EPI_WARPS);   // 320
-
-// TERMS: 3 = 3xTF32 (small*big + big*small + big*big, three kind::tf32 MMAs
-// per K8), 2 = TF32+BF16 (big*big kind::tf32 + both cross terms in one K16
-// kind::f16 BF16 MMA), 1 = 1xTF32.
-template <int TERMS>
-struct TcCfg {
-    static constexpr int PLANES = TERMS >= 2 ? 2 : 1;
-    static constexpr int TILES_PER_STAGE = 2 * PLANES;              // A planes + B planes
-    static constexpr int STAGE_BYTES = TILES_PER_STAGE * TC_TILE_BYTES;
-    static constexpr int STAGES = TERMS >= 2 ? 3 : 6;
-    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-};
-
 template <int TERMS, bool A_MN, bool B_MN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
     tc_sgemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
@@ -633,7 +616,10 @@ bool encode_tmap_f32_2d(CUtensorMap *tm, const float *ptr, int64_t d0, int64_t d
 // M/N/K tails).  K-major: dims {kext, R}, box {32, 128}, 128B swizzle.
 // MN-major: dims {R, kext}, box {32, 32} (a 128-row tile is four boxes),
 // 128B swizzle with 32B atoms (the only MN-major TF32 UMMA layout).
-bool tc_make_tmap(CUtensorMap *tm, const TcPlane &p, int64_t R) {
+bool tc_make_tmap(CUtensorMap *tm, const TcPlane &p, int64_t R) { return tc_make_tmap_rows(tm, p, R, TC_BM); }
+
+// Same with `box_rows` rows per K-major box (MN-major planes: 32x32 boxes).
+bool tc_make_tmap_rows(CUtensorMap *tm, const TcPlane &p, int64_t R, int box_rows) {
     auto enc = get_encode_fn();
     if (!enc || !p.ptr) return false;
     cuuint64_t dims[2], strides[1] = {(cuuint64_t)p.ld * 4};
@@ -647,7 +633,7 @@ bool tc_make_tmap(CUtensorMap *tm, const TcPlane &p, int64_t R) {
         dims[0] = (cuuint64_t)p.kext;
         dims[1] = (cuuint64_t)R;
         box[0] = (cuuint32_t)TC_BK;
-        box[1] = (cuuint32_t)TC_BM;
+        box[1] = (cuuint32_t)box_rows;
     }
     CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(p.ptr), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE,

@@ -41,6 +41,23 @@ constexpr int TC_TILE_BYTES = 128 * TC_BK * 4;   // one 128 x 32 FP32 operand ti
 constexpr int TC_EPI_WARPS = 8;      // 2 per TMEM lane quarter, 128 columns each
 constexpr int TC_TMEM_COLS = 512;    // 2 accumulator buffers of 256 columns
 
+// warp 0 = TMA producer, warp 1 = MMA issuer + TMEM owner, warps 2-9 = 8
+// promotion/epilogue warps (2 per TMEM lane quarter).
+constexpr int TC_EPI_WARP0 = 2;
+constexpr int TC_THREADS_P = 32 * (TC_EPI_WARP0 + TC_EPI_WARPS);   // 320
+
+// TERMS: 3 = 3xTF32 (small*big + big*small + big*big, three kind::tf32 MMAs
+// per K8), 2 = TF32+BF16 (big*big kind::tf32 + both cross terms in one K16
+// kind::f16 BF16 MMA), 1 = 1xTF32.
+template <int TERMS>
+struct TcCfg {
+    static constexpr int PLANES = TERMS >= 2 ? 2 : 1;
+    static constexpr int TILES_PER_STAGE = 2 * PLANES;              // A planes + B planes
+    static constexpr int STAGE_BYTES = TILES_PER_STAGE * TC_TILE_BYTES;
+    static constexpr int STAGES = TERMS >= 2 ? 3 : 6;
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
+
 // Work item kinds.
 enum { TW_FULL = 0,     // whole tile -> C (alpha/beta epilogue)
        TW_SPLITK = 1,   // split-K unit -> raw partial in slot (sp, tile) (fixed-order reduce launch, KN8)
