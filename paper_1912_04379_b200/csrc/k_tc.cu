@@ -428,10 +428,14 @@ cudaError_t launch_splitk_reduce(const float *partial, int splits, int64_t M, in
 // MMAs run on the other buffer ("promotion"), bounding the truncation bias
 // to one chunk.
 // =====================================================================
-template <int TERMS, bool A_MN, bool B_MN>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
+// Cluster size from the launch (2, or a preferred 4 = two CTA pairs sharing
+// B by TMA multicast for data-parallel launches); tmB0h/tmB1h:
+// the K-major B planes with 64-row boxes for the multicast half-loads.
+template <int TERMS, bool A_MN, bool B_MN, bool MC>
+__global__ void __launch_bounds__(TC_THREADS_P, 1)
     tc_sgemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
-                    const __grid_constant__ CUtensorMap tmB0, const __grid_constant__ CUtensorMap tmB1, int M, int N,
+                    const __grid_constant__ CUtensorMap tmB0, const __grid_constant__ CUtensorMap tmB1,
+                    const __grid_constant__ CUtensorMap tmB0h, const __grid_constant__ CUtensorMap tmB1h, int M, int N,
                     int Kp, float alpha, float beta, float *__restrict__ C, int64_t ldc, int tiles_m, int tiles_n,
                     int group_m, int kc_stages, unsigned int *__restrict__ wave_ctr, int splits,
                     float *__restrict__ partial, const TcSk sk, const __grid_constant__ PeerOut peers) {
@@ -448,16 +452,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t rank = cluster_ctarank();
+    const uint32_t crank = cluster_ctarank();
+    const int cl = MC ? (int)cluster_nctarank() : 2;   // 2, or 4 (two pairs; MC launches only)
+    const uint32_t rank = crank & 1u;                // rank in the CTA pair
+    const uint32_t leader = crank & ~1u;             // the pair leader's cluster rank
+    const int pair = (int)(crank >> 1);              // pair in the cluster
 
-    const int nclus = (int)(gridDim.x >> 1);
+    const int nclus = (int)(gridDim.x >> 1);         // CTA pairs
     const int cid = (int)(blockIdx.x >> 1);
     const TcSched S(tiles_m, tiles_n, group_m, Kp, splits, sk.dp_tiles, TC_SK_CHUNK, nclus, cid);
+    const int n_it = tc_n_items(S, cl);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < Cfg::STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], (uint32_t)(cl / 2));   // one stage-release commit per pair
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&acc_full[b], 1);
@@ -489,13 +498,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
         // ===== TMA producer (both CTAs; each loads its half of A and B) =====
         if (lane == 0) {
             uint32_t leader_full0;
-            asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(leader_full0) : "r"(smem_u32(&full[0])));
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                         : "=r"(leader_full0)
+                         : "r"(smem_u32(&full[0])), "r"(leader));
             const uint64_t pol = policy_evict_normal();
             int it = 0;
             unsigned int done_target = 0;   // CTAs that finished issuing waves 0..w-1
             int cur_wave = 0;
             bool lockstep = wave_ctr != nullptr;
-            for (int i = 0; i < S.n_items; ++i) {
+            for (int i = 0; i < n_it; ++i) {
                 const int w = S.wave_of(i);
                 if (w != cur_wave || i == 0) {
                     if (w > 0 && lockstep) {
@@ -522,8 +533,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
                     }
                     cur_wave = w;
                 }
-                TcWork wk;
-                S.item(i, wk);
+                TcItem ti;
+                tc_get_item(S, cl, i, ti);
+                const TcWork &wk = ti.w;
                 const int m0 = wk.m0, n0 = wk.n0, kb0 = wk.kb0, kb1 = wk.kb1;
                 const int arow = m0 + (int)rank * TC_BM;
                 const int brow = n0 + (int)rank * TC_BM;
@@ -545,25 +557,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS_P, 1)
                             tma_load_2d_2sm(dst, tm, fb, kb * TC_BK, row0, pol);
                         }
                     };
+                    // multicast (4-cluster, shared B): half of this CTA's B
+                    // half-tile, to the same-rank CTA of both pairs; completion on
+                    // each destination pair leader's barrier at this offset
+                    const uint32_t fbm = smem_u32(&full[s]) & 0xFEFFFFFFu;
+                    const uint16_t mask = (uint16_t)((1u << rank) | (1u << (2 + rank)));
+                    auto load_b = [&](const CUtensorMap *tm, const CUtensorMap *tmh, uint32_t dst, bool mn) {
+                        if (!ti.mc) {
+                            load_plane(tm, dst, brow, mn);
+                        } else if (mn) {
+#pragma unroll
+                            for (int c = 2 * pair; c < 2 * pair + 2; ++c)
+                                tma_load_2d_2sm_mc(dst + c * 4096, tm, fbm, brow + 32 * c, kb * TC_BK, mask, pol);
+                        } else {
+                            tma_load_2d_2sm_mc(dst + pair * 8192, tmh, fbm, kb * TC_BK, brow + 64 * pair, mask, pol);
+                        }
+                    };
                     load_plane(&tmA0, st, arow, A_MN);
-                    load_plane(&tmB0, st + Cfg::PLANES * TC_TILE_BYTES, brow, B_MN);
+                    load_b(&tmB0, &tmB0h, st + Cfg::PLANES * TC_TILE_BYTES, B_MN);
                     if (Cfg::PLANES == 2) {
                         load_plane(&tmA1, st + TC_TILE_BYTES, arow, A1_MN);
-                        load_plane(&tmB1, st + 3 * TC_TILE_BYTES, brow, B1_MN);
+                        load_b(&tmB1, &tmB1h, st + 3 * TC_TILE_BYTES, B1_MN);
                     }
                 }
                 // this CTA has issued every load of its current wave
-                if (wave_ctr && (i + 1 == S.n_items || S.wave_of(i + 1) != cur_wave))
+                if (wave_ctr && (i + 1 == n_it || S.wave_of(i + 1) != cur_wave))
                     asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(wave_ctr) : "memory");
             }
         }
     } else if (warp == 1) {
         if (rank == 0 && lane == 0)
-            tc_mma_loop<TERMS, A_MN, B_MN, A1_MN, B1_MN, Cfg::PLANES, Cfg::STAGES, Cfg::STAGE_BYTES>(
-                S, smem, full, empty, acc_full, acc_empty, tmem_base, kc_stages);
+            tc_mma_loop<TERMS, A_MN, B_MN, A1_MN, B1_MN, Cfg::PLANES, Cfg::STAGES, Cfg::STAGE_BYTES, MC>(
+                S, smem, full, empty, acc_full, acc_empty, tmem_base, kc_stages, cl, pair);
     } else if (warp >= TC_EPI_WARP0) {
-        tc_epilogue_loop(S, rank, warp & 3, (warp - TC_EPI_WARP0) >> 2, lane, tmem_base, acc_full, acc_empty,
-                         kc_stages, M, N, alpha, beta, C, ldc, partial, sk, peers);
+        tc_epilogue_loop<MC>(S, rank, warp & 3, (warp - TC_EPI_WARP0) >> 2, lane, tmem_base, acc_full, acc_empty,
+                         kc_stages, M, N, alpha, beta, C, ldc, partial, sk, peers, cl, leader);
     }
 
     tc_fence_before();
@@ -756,6 +784,18 @@ int64_t tc_units(int64_t M, int64_t N, int splits) {
     return ((M + 2 * TC_BM - 1) / (2 * TC_BM)) * ((N + TC_BN - 1) / TC_BN) * splits;
 }
 
+// Preferred clusters of 4 (B multicast between two CTA pairs) for the
+// data-parallel 3xTF32 / TF32+BF16 schedule at K >= 4096 (measured, one
+// B200: c5 260.0 -> 262.3 / 263.6 TFLOP/s, c2-8192 +0.6% (3x) / +1.2%
+// (TF32+BF16); c4-ii, K = 1024, -5%: profiles/r01_ab_pref4.txt).
+// EMM_PREF4=0 / 1 forces.
+static bool tc_pref4_wanted(int terms, int64_t K) {
+    const char *e = getenv("EMM_PREF4");
+    if (e && e[0] == '0') return false;
+    if (e && e[0] == '1') return true;
+    return terms >= 2 && K >= 4096;
+}
+
 template <int TERMS, bool A_MN, bool B_MN>
 static cudaError_t launch_tc_t(const TcOperands &ops, int64_t M, int64_t N, int64_t Kp, float alpha, float beta,
                                float *C, int64_t ldc, unsigned int *ctrl, int splits, float *partial, cudaStream_t s,
@@ -764,11 +804,17 @@ static cudaError_t launch_tc_t(const TcOperands &ops, int64_t M, int64_t N, int6
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(once, [] {
-        attr_err = cudaFuncSetAttribute(tc_sgemm_kernel<TERMS, A_MN, B_MN>,
+        attr_err = cudaFuncSetAttribute(tc_sgemm_kernel<TERMS, A_MN, B_MN, false>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+        if (attr_err == cudaSuccess && TERMS >= 2)
+            attr_err = cudaFuncSetAttribute(tc_sgemm_kernel<TERMS, A_MN, B_MN, TERMS >= 2>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+        if (attr_err == cudaSuccess && TERMS >= 2)
+            attr_err = cudaFuncSetAttribute(tc_sgemm_kernel<TERMS, A_MN, B_MN, TERMS >= 2>,
+                                            cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     });
     if (attr_err != cudaSuccess) return attr_err;
-    CUtensorMap ta0, ta1, tb0, tb1;
+    CUtensorMap ta0, ta1, tb0, tb1, tb0h, tb1h;
     if (!tc_make_tmap(&ta0, ops.a0, M) || !tc_make_tmap(&tb0, ops.b0, N)) return cudaErrorInvalidValue;
     if (Cfg::PLANES == 2) {
         if (!tc_make_tmap(&ta1, ops.a1, M) || !tc_make_tmap(&tb1, ops.b1, N)) return cudaErrorInvalidValue;
@@ -776,6 +822,10 @@ static cudaError_t launch_tc_t(const TcOperands &ops, int64_t M, int64_t N, int6
         ta1 = ta0;
         tb1 = tb0;
     }
+    // K-major B planes with 64-row boxes: the multicast half-loads of 4-clusters
+    if (!tc_make_tmap_rows(&tb0h, ops.b0, N, TC_BM / 2) ||
+        !tc_make_tmap_rows(&tb1h, Cfg::PLANES == 2 ? ops.b1 : ops.b0, N, TC_BM / 2))
+        return cudaErrorInvalidValue;
     const int tiles_m = (int)((M + 2 * TC_BM - 1) / (2 * TC_BM));
     const int tiles_n = (int)((N + TC_BN - 1) / TC_BN);
     const int group_m = 8;
@@ -805,8 +855,15 @@ static cudaError_t launch_tc_t(const TcOperands &ops, int64_t M, int64_t N, int6
         oc.gridDim = dim3(2 * 64);
         oc.blockDim = dim3(TC_THREADS_P);
         oc.dynamicSmemBytes = TcCfg<TERMS>::SMEM_BYTES;
+        cudaLaunchAttribute ca[1];
+        ca[0].id = cudaLaunchAttributeClusterDimension;
+        ca[0].val.clusterDim.x = 2;
+        ca[0].val.clusterDim.y = 1;
+        ca[0].val.clusterDim.z = 1;
+        oc.attrs = ca;
+        oc.numAttrs = 1;
         int n = 0;
-        if (cudaOccupancyMaxActiveClusters(&n, tc_sgemm_kernel<TERMS, A_MN, B_MN>, &oc) != cudaSuccess) n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, tc_sgemm_kernel<TERMS, A_MN, B_MN, false>, &oc) != cudaSuccess) n = 0;
         max_clusters = n;
         cudaGetLastError();
     });
@@ -825,12 +882,25 @@ static cudaError_t launch_tc_t(const TcOperands &ops, int64_t M, int64_t N, int6
         cfg.blockDim = dim3(TC_THREADS_P);
         cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
         cfg.stream = s;
-        cudaLaunchAttribute at[1];
+        // clusters of one CTA pair; for data-parallel schedules a PREFERRED
+        // size of 4 (two pairs sharing B by multicast; the B200 forms as many
+        // 4-clusters as its GPCs hold and pairs on the remaining SMs)
+        cudaLaunchAttribute at[3];
         at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         at[0].val.programmaticStreamSerializationAllowed = 1;
+        at[1].id = cudaLaunchAttributeClusterDimension;
+        at[1].val.clusterDim.x = 2;
+        at[1].val.clusterDim.y = 1;
+        at[1].val.clusterDim.z = 1;
+        at[2].id = cudaLaunchAttributePreferredClusterDimension;
+        at[2].val.preferredClusterDim.x = 4;
+        at[2].val.preferredClusterDim.y = 1;
+        at[2].val.preferredClusterDim.z = 1;
         cfg.attrs = at;
-        cfg.numAttrs = 1;
-        cudaError_t le = cudaLaunchKernelEx(&cfg, tc_sgemm_kernel<TERMS, A_MN, B_MN>, ta0, ta1, tb0, tb1, (int)M,
+        const bool mc = TERMS >= 2 && tc_pref4_wanted(TERMS, Kp) && splits == 1 && !sk.slots && blocks % 4 == 0;
+        cfg.numAttrs = mc ? 3 : 2;
+        auto kern = mc ? tc_sgemm_kernel<TERMS, A_MN, B_MN, TERMS >= 2> : tc_sgemm_kernel<TERMS, A_MN, B_MN, false>;
+        cudaError_t le = cudaLaunchKernelEx(&cfg, kern, ta0, ta1, tb0, tb1, tb0h, tb1h, (int)M,
                                             (int)N, (int)Kp, alpha, beta, C, ldc, tiles_m, tiles_n, group_m,
                                             kc_stages, ctrl, splits, splits > 1 ? partial : nullptr, sk, peers);
         if (le != cudaSuccess) return le;

@@ -18,6 +18,12 @@ __device__ __forceinline__ uint32_t cluster_ctarank() {
     return r;
 }
 
+__device__ __forceinline__ uint32_t cluster_nctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+    return r;
+}
+
 __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n"
                  "barrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -139,6 +145,18 @@ __device__ __forceinline__ void tma_load_2d_2sm(uint32_t smem_dst, const void *t
         "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
         " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_dst),
         "l"(reinterpret_cast<uint64_t>(tmap)), "r"(mbar_addr), "r"(c0), "r"(c1), "l"(policy)
+        : "memory");
+}
+// 2-D tiled load multicast to the CTAs of `cta_mask` (same smem offset in
+// each); completion bytes are signalled on the mbarrier at the same offset in
+// each destination CTA's pair leader (cta_group::2).  `mbar_addr` is this
+// CTA's barrier address with the pair-peer bit cleared (CuTe convention).
+__device__ __forceinline__ void tma_load_2d_2sm_mc(uint32_t smem_dst, const void *tmap, uint32_t mbar_addr, int32_t c0,
+                                                   int32_t c1, uint16_t cta_mask, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5, %6;" ::"r"(smem_dst),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(mbar_addr), "r"(c0), "r"(c1), "h"(cta_mask), "l"(policy)
         : "memory");
 }
 // 2-D tiled load into this CTA's smem, completion on this CTA's mbarrier.

@@ -158,6 +158,21 @@ struct TcSched {
             w.kind = TW_PUB;
         }
     }
+    // data-parallel schedule (no stream-K) of another pair `c` (the partner
+    // pair of a 4-cluster): its item count and its item i
+    __host__ __device__ __forceinline__ int n_items_of(int c) const {
+        return c < total_units ? (total_units - c + nclus - 1) / nclus : 0;
+    }
+    __host__ __device__ __forceinline__ void item_of(int c, int i, TcWork &w) const {
+        const int u = c + i * nclus;
+        w.sp = u / total_tiles;
+        w.tile = u - w.sp * total_tiles;
+        tile_origin(w.tile, w.m0, w.n0);
+        w.kb0 = w.sp * nkb_s;
+        w.kb1 = tc_imin(nkb, w.kb0 + nkb_s);
+        w.kind = splits > 1 ? TW_SPLITK : TW_FULL;
+        w.last = 0;
+    }
     // wave-lockstep bookkeeping (producers): wave of item i, CTA pairs in a wave
     __host__ __device__ __forceinline__ int wave_of(int i) const { return i < n_dp ? i : dp_waves; }
     __host__ __device__ __forceinline__ int pairs_in_wave(int w) const {
@@ -165,14 +180,46 @@ struct TcSched {
     }
 };
 
+// Clusters of two CTA pairs (launched with a PREFERRED cluster size of 4,
+// DESIGN.md §3): pair cid and its partner cid ^ 1 walk the same schedule
+// positions, and with the grouped raster their data-parallel tiles at the
+// same position are vertically adjacent (same B tile), so B is multicast.
+// When the partner has fewer items (last, partial wave) this pair mirrors
+// the partner's item as a dummy (computed, never stored) so both pairs run
+// the same stage sequence — each stage slot is released by both pairs'
+// MMAs.  A cluster of 2 (cl == 2) is the plain schedule.
+struct TcItem {
+    TcWork w;
+    bool dummy;   // mirror of the partner's item: no epilogue stores
+    bool mc;      // B shared with the partner pair (multicast loads)
+};
+// cl == 4 only for data-parallel launches (no stream-K, no split-K)
+__host__ __device__ __forceinline__ int tc_n_items(const TcSched &S, int cl) {
+    if (cl != 4) return S.n_items;
+    const int pn = S.n_items_of(S.cid ^ 1);
+    return pn > S.n_items ? pn : S.n_items;
+}
+__host__ __device__ __forceinline__ void tc_get_item(const TcSched &S, int cl, int i, TcItem &it) {
+    const bool have = i < S.n_items, phave = cl == 4 && i < S.n_items_of(S.cid ^ 1);
+    TcWork pw;
+    if (have) S.item(i, it.w);
+    if (phave) S.item_of(S.cid ^ 1, i, pw);
+    it.dummy = !have;
+    if (!have) it.w = pw;
+    if (!phave) pw = it.w;
+    it.mc = cl == 4 && it.w.kind == TW_FULL && pw.kind == TW_FULL && pw.n0 == it.w.n0 && pw.kb0 == it.w.kb0 &&
+            pw.kb1 == it.w.kb1;
+}
+
 // ===== MMA issuer: one thread of the leader CTA drives the pair =====
 // Stage s holds [A plane0 | A plane1 | B plane0 | B plane1] (PLANES == 2) or
 // [A | B] (PLANES == 1).  TERMS: 3 = 3xTF32 (small*big + big*small +
 // big*big), 2 = TF32+BF16 (bf16 cross pair as one K16 MMA + big*big), 1.
-template <int TERMS, bool A_MN, bool B_MN, bool A1_MN, bool B1_MN, int PLANES, int STAGES, int STAGE_BYTES>
+template <int TERMS, bool A_MN, bool B_MN, bool A1_MN, bool B1_MN, int PLANES, int STAGES, int STAGE_BYTES,
+          bool MC = false>
 __device__ __forceinline__ void tc_mma_loop(const TcSched &S, uint8_t *smem, uint64_t *full,
                                             uint64_t *empty, uint64_t *acc_full, uint64_t *acc_empty,
-                                            uint32_t tmem_base, int kc_stages) {
+                                            uint32_t tmem_base, int kc_stages, int cl = 2, int pair = 0) {
     using namespace ptx;
     constexpr uint32_t idesc = idesc_tf32_major<2 * TC_BM, TC_BN, A_MN, B_MN>();
     // K8 step k of a plane: K-major advances 32 B inside the swizzle row,
@@ -181,9 +228,16 @@ __device__ __forceinline__ void tc_mma_loop(const TcSched &S, uint8_t *smem, uin
         return mn ? desc_mnmajor_sw128_32b(addr + (uint32_t)(k * 1024)) : desc_kmajor_sw128(addr + (uint32_t)(k * 32));
     };
     int it = 0, ch = 0;   // global stage / chunk counters (continue across tiles)
-    for (int i = 0; i < S.n_items; ++i) {
-        TcWork w;
-        S.item(i, w);
+    // stage slots are released to both pairs of a 4-cluster (each slot
+    // receives the partner's multicast B); the accumulator only to this pair
+    if (!MC) cl = 2, pair = 0;   // compile-time plain schedule
+    const uint16_t rel_mask = (uint16_t)(cl == 4 ? 0xF : 0x3);
+    const uint16_t acc_mask = (uint16_t)(0x3u << (2 * pair));
+    const int n_it = tc_n_items(S, cl);
+    for (int i = 0; i < n_it; ++i) {
+        TcItem ti;
+        tc_get_item(S, cl, i, ti);
+        const TcWork &w = ti.w;
         const int kb0 = w.kb0, kb1 = w.kb1;
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
             const bool first = ((kb - kb0) % kc_stages) == 0;
@@ -219,9 +273,9 @@ __device__ __forceinline__ void tc_mma_loop(const TcSched &S, uint8_t *smem, uin
                     mma_tf32_2sm(dt, dsc(a0, A_MN, k), dsc(b0, B_MN, k), idesc, acc0);
                 }
             }
-            mma_commit_2sm_mc(&empty[s], (uint16_t)0x3);
+            mma_commit_2sm_mc(&empty[s], rel_mask);
             if (last) {
-                mma_commit_2sm_mc(&acc_full[b], (uint16_t)0x3);
+                mma_commit_2sm_mc(&acc_full[b], acc_mask);
                 ++ch;
             }
         }
@@ -231,20 +285,27 @@ __device__ __forceinline__ void tc_mma_loop(const TcSched &S, uint8_t *smem, uin
 
 // ===== epilogue: TMEM -> FP32 registers (promotion) -> alpha/beta -> C =====
 // Warp with TMEM lane quarter q (= warp % 4) and column half h.
+template <bool MC = false>
 __device__ __forceinline__ void tc_epilogue_loop(const TcSched &S, uint32_t rank, int q, int h, int lane,
                                                  uint32_t tmem_base, uint64_t *acc_full, uint64_t *acc_empty,
                                                  int kc_stages, int M, int N, float alpha, float beta,
                                                  float *__restrict__ C, int64_t ldc, float *__restrict__ partial,
-                                                 const TcSk &sk, const PeerOut &peers) {
+                                                 const TcSk &sk, const PeerOut &peers, int cl = 2,
+                                                 uint32_t leader = 0) {
     using namespace ptx;
-    uint32_t leader_empty0;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(leader_empty0) : "r"(smem_u32(&acc_empty[0])));
+    if (!MC) cl = 2, leader = 0;   // compile-time plain schedule
+    uint32_t leader_empty0;   // the pair leader's acc_empty[0]
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                 : "=r"(leader_empty0)
+                 : "r"(smem_u32(&acc_empty[0])), "r"(leader));
     // this warp's stream-K slot part / flag index (warp id within the CTA's 8)
     const int wslot = (int)rank * TC_EPI_WARPS + h * 4 + q;
     int ch = 0;
-    for (int i = 0; i < S.n_items; ++i) {
-        TcWork w;
-        S.item(i, w);
+    const int n_it = tc_n_items(S, cl);
+    for (int i = 0; i < n_it; ++i) {
+        TcItem ti;
+        tc_get_item(S, cl, i, ti);
+        const TcWork &w = ti.w;
         const int m0 = w.m0, n0 = w.n0, kb0 = w.kb0, kb1 = w.kb1, sp = w.sp;
         const int nchunks = (kb1 - kb0 + kc_stages - 1) / kc_stages;
         const int row = m0 + (int)rank * TC_BM + 32 * q + lane;
@@ -272,6 +333,7 @@ __device__ __forceinline__ void tc_epilogue_loop(const TcSched &S, uint32_t rank
                 asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(eb) : "memory");
             }
         }
+        if (ti.dummy) continue;   // mirrored partner item: drained, never stored
         if (w.kind == TW_PUB) {
             // stream-K tail piece: raw partial -> slot cid (coalesced float4
             // layout, all 256 x 256 entries), then this warp's flag (release)
@@ -329,7 +391,7 @@ __device__ __forceinline__ void tc_epilogue_loop(const TcSched &S, uint32_t rank
                 __stcg(slot + g * 32, make_float4(acc[4 * g], acc[4 * g + 1], acc[4 * g + 2], acc[4 * g + 3]));
             continue;
         }
-        if (row < M) {
+        if (row < M && !ti.dummy) {
             const int col0 = n0 + h * 128;
             float *cp = C + (int64_t)row + (int64_t)col0 * ldc;
             const int jmax = min(128, N - col0);

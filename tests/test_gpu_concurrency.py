@@ -54,6 +54,7 @@ def _check(case, dC):
                                         ((8192, 4096, 512), "tf32bf16"),
                                         ((8192, 4096, 512), "1xtf32"),
                                         ((8192, 4096, 2048), "1xtf32"),    # KN2w (256x512 tiles)
+                                        ((8192, 4096, 4096), "3xtf32"),    # preferred clusters of 4
                                         ((4096, 2048, 512), "ffma")])      # KN3b
 def test_concurrent_streams(emm, shape, math):
     M, N, K = shape

@@ -29,6 +29,7 @@ def emm():
     ((4096, 4096, 1024), "3xtf32", True),     # stream-K remainder (flags + slots)
     ((8192, 4096, 512), "3xtf32", True),      # multi-wave lockstep
     ((8192, 4096, 512), "tf32bf16", True),
+    ((8192, 4096, 4096), "3xtf32", True),     # preferred clusters of 4 (B multicast) + lockstep
     ((1024, 1024, 1024), "3xtf32", False),    # emm_sgemm-style: scratch from the stream-ordered pool
     ((333, 333, 333), "3xtf32", True),        # tiny kernel
     ((20000, 16, 700), "3xtf32", True),       # skinny kernel
