@@ -199,6 +199,13 @@ __host__ __device__ __forceinline__ int tc_n_items(const TcSched &S, int cl) {
     const int pn = S.n_items_of(S.cid ^ 1);
     return pn > S.n_items ? pn : S.n_items;
 }
+// MMA issuer / epilogue: the item only (its own, or the partner's mirrored)
+__host__ __device__ __forceinline__ void tc_get_work(const TcSched &S, int cl, int i, TcWork &w, bool &dummy) {
+    dummy = cl == 4 && i >= S.n_items;
+    if (dummy) S.item_of(S.cid ^ 1, i, w);
+    else S.item(i, w);
+}
+// producer: also whether B is shared with the partner pair (multicast)
 __host__ __device__ __forceinline__ void tc_get_item(const TcSched &S, int cl, int i, TcItem &it) {
     const bool have = i < S.n_items, phave = cl == 4 && i < S.n_items_of(S.cid ^ 1);
     TcWork pw;
@@ -235,9 +242,9 @@ __device__ __forceinline__ void tc_mma_loop(const TcSched &S, uint8_t *smem, uin
     const uint16_t acc_mask = (uint16_t)(0x3u << (2 * pair));
     const int n_it = tc_n_items(S, cl);
     for (int i = 0; i < n_it; ++i) {
-        TcItem ti;
-        tc_get_item(S, cl, i, ti);
-        const TcWork &w = ti.w;
+        TcWork w;
+        bool dummy;
+        tc_get_work(S, cl, i, w, dummy);
         const int kb0 = w.kb0, kb1 = w.kb1;
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
             const bool first = ((kb - kb0) % kc_stages) == 0;
@@ -303,9 +310,9 @@ __device__ __forceinline__ void tc_epilogue_loop(const TcSched &S, uint32_t rank
     int ch = 0;
     const int n_it = tc_n_items(S, cl);
     for (int i = 0; i < n_it; ++i) {
-        TcItem ti;
-        tc_get_item(S, cl, i, ti);
-        const TcWork &w = ti.w;
+        TcWork w;
+        bool dummy;
+        tc_get_work(S, cl, i, w, dummy);
         const int m0 = w.m0, n0 = w.n0, kb0 = w.kb0, kb1 = w.kb1, sp = w.sp;
         const int nchunks = (kb1 - kb0 + kc_stages - 1) / kc_stages;
         const int row = m0 + (int)rank * TC_BM + 32 * q + lane;
@@ -333,7 +340,7 @@ __device__ __forceinline__ void tc_epilogue_loop(const TcSched &S, uint32_t rank
                 asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(eb) : "memory");
             }
         }
-        if (ti.dummy) continue;   // mirrored partner item: drained, never stored
+        if (dummy) continue;   // mirrored partner item: drained, never stored
         if (w.kind == TW_PUB) {
             // stream-K tail piece: raw partial -> slot cid (coalesced float4
             // layout, all 256 x 256 entries), then this warp's flag (release)
@@ -391,7 +398,7 @@ __device__ __forceinline__ void tc_epilogue_loop(const TcSched &S, uint32_t rank
                 __stcg(slot + g * 32, make_float4(acc[4 * g], acc[4 * g + 1], acc[4 * g + 2], acc[4 * g + 3]));
             continue;
         }
-        if (row < M && !ti.dummy) {
+        if (row < M) {
             const int col0 = n0 + h * 128;
             float *cp = C + (int64_t)row + (int64_t)col0 * ldc;
             const int jmax = min(128, N - col0);
