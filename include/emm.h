@@ -194,6 +194,16 @@ int emm_profile_read(double *gemm_ms, uint64_t *gemm_launches, double *other_ms,
  * -------------------------------------------------------------------- */
 int emm_debug_mma_probe(int terms, int stages, void *stream, float *ms, double *gemm_flops);
 
+/* Host replays of the tcgen05 GEMM's persistent schedule (host-only, no GPU;
+ * they run the same __host__ __device__ scheduling code as the kernel, for
+ * tests).  emm_debug_schedule: the work items of every CTA pair of a launch,
+ * 7 ints each (pair, m0, n0, kb0, kb1, kind, last).  emm_debug_pair_schedule:
+ * the items every pair runs on preferred clusters of 4 (data-parallel
+ * schedule), 8 ints each (pair, i, m0, n0, kb0, kb1, dummy, multicast).
+ * Both return the item count, or -1 when `cap` items do not fit in `out`. */
+int emm_debug_schedule(int64_t M, int64_t N, int64_t K, int use_sk, int terms, int *out, int cap);
+int emm_debug_pair_schedule(int64_t M, int64_t N, int64_t K, int *out, int cap);
+
 #ifdef __cplusplus
 }
 #endif

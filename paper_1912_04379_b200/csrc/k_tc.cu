@@ -778,6 +778,33 @@ extern "C" int emm_debug_schedule(int64_t M, int64_t N, int64_t K, int use_sk, i
     return n;
 }
 
+// Host replay of the 4-cluster pairing (preferred clusters, data-parallel
+// schedule): for every CTA pair, the items it runs under cl = 4 — its own
+// and the partner's mirrored ones — 8 ints each (pair, i, m0, n0, kb0, kb1,
+// dummy, multicast); returns the count (-1 if `cap` is too small).
+extern "C" int emm_debug_pair_schedule(int64_t M, int64_t N, int64_t K, int *out, int cap) {
+    using namespace emm;
+    const int tiles_m = (int)((M + 2 * TC_BM - 1) / (2 * TC_BM)), tiles_n = (int)((N + TC_BN - 1) / TC_BN);
+    const int64_t units = (int64_t)tiles_m * tiles_n;
+    const int pairs = tc_num_sms() / 2;
+    const int nclus = (int)(units < pairs ? units : pairs);
+    int n = 0;
+    for (int c = 0; c < nclus; ++c) {
+        const TcSched S(tiles_m, tiles_n, 8, (int)tc_kpad(K), 1, 0x7fffffff, TC_SK_CHUNK, nclus, c);
+        const int cl = (c ^ 1) < nclus ? 4 : 2;   // an odd last pair has no partner
+        const int n_it = tc_n_items(S, cl);
+        for (int i = 0; i < n_it; ++i) {
+            TcItem it;
+            tc_get_item(S, cl, i, it);
+            if (n >= cap) return -1;
+            int *o = out + 8 * n++;
+            o[0] = c; o[1] = i; o[2] = it.w.m0; o[3] = it.w.n0; o[4] = it.w.kb0; o[5] = it.w.kb1;
+            o[6] = it.dummy ? 1 : 0; o[7] = it.mc ? 1 : 0;
+        }
+    }
+    return n;
+}
+
 namespace emm {
 
 int64_t tc_units(int64_t M, int64_t N, int splits) {

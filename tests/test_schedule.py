@@ -122,3 +122,65 @@ def test_stream_k_policy(monkeypatch):
     # exact waves -> never stream-K; sub-half-wave -> split-K
     assert check(256 * 74, 512, 1024)[0] == {TW_FULL}
     assert check(1024, 1024, 1024)[0] == {TW_SPLITK}
+
+
+# ---- preferred clusters of 4 (B multicast between the two pairs of a cluster)
+def pair_schedule(M, N, K):
+    L = emm.lib()
+    L.emm_debug_pair_schedule.argtypes = [ctypes.c_int64] * 3 + [ctypes.c_void_p, ctypes.c_int]
+    L.emm_debug_pair_schedule.restype = ctypes.c_int
+    cap = 1 << 17
+    out = np.zeros(8 * cap, dtype=np.int32)
+    n = L.emm_debug_pair_schedule(M, N, K, out.ctypes.data, cap)
+    assert n >= 0
+    return out[: 8 * n].reshape(n, 8)
+
+
+def check_pairs(M, N, K):
+    """Both pairs of a 4-cluster run the same number of items with equal K
+    ranges (each stage slot is released by both pairs' MMAs); a dummy item is
+    the partner's item; a multicast item's partner holds the vertically
+    adjacent tile of the same column (same B tile); the non-dummy items cover
+    every tile exactly once."""
+    it = pair_schedule(M, N, K)
+    tm, tn = -(-M // 256), -(-N // 256)
+    by = {}
+    for c, i, m0, n0, kb0, kb1, dummy, mc in it.tolist():
+        by.setdefault(c, []).append((m0, n0, kb0, kb1, dummy, mc))
+    cover = {}
+    for c, lst in by.items():
+        for m0, n0, kb0, kb1, dummy, mc in lst:
+            if not dummy:
+                cover[(m0, n0)] = cover.get((m0, n0), 0) + 1
+        p = c ^ 1
+        if p not in by:
+            assert not any(x[5] for x in lst)
+            continue
+        other = by[p]
+        assert len(other) == len(lst), f"pairs {c},{p}: item counts differ"
+        for a, b in zip(lst, other):
+            assert (a[2], a[3]) == (b[2], b[3]), "K ranges differ"
+            assert a[5] == b[5], "multicast decision not symmetric"
+            if a[4]:
+                assert not b[4] and (a[0], a[1]) == (b[0], b[1]), "dummy is not the partner's item"
+            if a[5] and not a[4] and not b[4]:
+                assert a[1] == b[1] and abs(a[0] - b[0]) == 256, "multicast partner not the adjacent tile"
+    assert len(cover) == tm * tn and all(v == 1 for v in cover.values())
+    return it
+
+
+@pytest.mark.parametrize("shape", [(32768, 32768, 32768), (8192, 8192, 8192), (65536, 4096, 1024), (65536, 1024, 4096),
+                                   (4096, 4096, 4096), (3000, 2000, 700), (2816, 3072, 2049), (1800, 5000, 300),
+                                   (256, 65536, 512), (12345, 6789, 1000)])
+def test_pair_schedule(shape):
+    it = check_pairs(*shape)
+    assert len(it)
+
+
+def test_pair_schedule_random():
+    rng = random.Random(7)
+    for _ in range(300):
+        M, N = rng.randint(1, 40000), rng.randint(1, 40000)
+        if (-(-M // 256)) * (-(-N // 256)) > 200000:
+            continue
+        check_pairs(M, N, rng.randint(1, 5000))
