@@ -3,7 +3,7 @@ structured cases): random M, N, K (log-uniform, 1..3000 / 1..5000), trans,
 leading-dimension padding, alpha / beta (including 0), math mode, data
 distribution and the policy switches (tiny-kernel threshold, re-buffered vs
 direct operands, stream-K forced / off, skinny path off, 1xTF32 256x512 tiles
-forced, the FFMA kernel without TMA).  Each case checks
+forced, the FFMA kernel without TMA, preferred clusters of 4 forced / off).  Each case checks
 the tolerance predicate against the oracle (every entry, or sampled rows for
 large cases), that ldc padding and the guard region keep their sentinel, and
 that A and B are not written.
@@ -52,7 +52,8 @@ def _cases():
             kind=rng.choice(["uniform", "normal"]),
             env={"EMM_SMALL_FLOPS": rng.choice([None, "0"]), "EMM_FORCE_PACK": rng.choice([None, None, "1"]),
                  "EMM_SK": rng.choice([None, None, "0", "1"]), "EMM_NO_SKINNY": rng.choice([None, None, "1"]),
-                 "EMM_WIDE": rng.choice([None, None, "1"]), "EMM_FFMA_CLASSIC": rng.choice([None, None, "1"])}))
+                 "EMM_WIDE": rng.choice([None, None, "1"]), "EMM_FFMA_CLASSIC": rng.choice([None, None, "1"]),
+                 "EMM_PREF4": rng.choice([None, "1", "1", "0"])}))
     return out
 
 
