@@ -185,6 +185,77 @@ void run_smem() {
            fma_per_block / (double)c0, 2.0 * fma_per_block * sms / (ms * 1e-3) / 1e12);
 }
 
+// SMEM-fed 16x8 register tile (PAIR_I: A MN-contiguous pairs along rows, B
+// K-contiguous scalars): per k 4 LDS.128 of A, 8 B quads per 4 k.
+__global__ void __launch_bounds__(256, 1) probe_smem16(float *out, long long *clk) {
+    __shared__ __align__(16) float As[16][256];
+    __shared__ __align__(16) float Bs[128][20];
+    __shared__ int zero_s;
+    if (threadIdx.x == 0) zero_s = 0;
+    for (int i = threadIdx.x; i < 16 * 256; i += blockDim.x) As[i / 256][i % 256] = (float)(i & 7) * 0.5f;
+    for (int i = threadIdx.x; i < 128 * 20; i += blockDim.x) Bs[i / 20][i % 20] = (float)(i & 3) * 0.25f;
+    __syncthreads();
+    const int tm = threadIdx.x & 15, tn = threadIdx.x >> 4;
+    float2 acc[64];
+#pragma unroll
+    for (int e = 0; e < 64; ++e) acc[e] = make_float2(0.f, 0.f);
+    const long long t0 = clock64();
+    for (int it = 0; it < ITERS / 32; ++it) {
+        const int z = *(volatile int *)&zero_s;
+        const float *Ab = &As[0][0] + z, *Bb = &Bs[0][0] + z;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+            float bq[4][8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const float4 x = *reinterpret_cast<const float4 *>(Bb + (tn + 16 * e) * 20 + 4 * g);
+                bq[0][e] = x.x; bq[1][e] = x.y; bq[2][e] = x.z; bq[3][e] = x.w;
+            }
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+                float a[16];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float4 x = *reinterpret_cast<const float4 *>(Ab + (4 * g + kk) * 256 + 64 * q + 4 * tm);
+                    a[4 * q] = x.x; a[4 * q + 1] = x.y; a[4 * q + 2] = x.z; a[4 * q + 3] = x.w;
+                }
+#pragma unroll
+                for (int ip = 0; ip < 8; ++ip)
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        acc[ip * 8 + j] = __ffma2_rn(make_float2(a[2 * ip], a[2 * ip + 1]),
+                                                     make_float2(bq[kk][j], bq[kk][j]), acc[ip * 8 + j]);
+            }
+        }
+    }
+    const long long t1 = clock64();
+    float sum = 0.f;
+#pragma unroll
+    for (int e = 0; e < 64; ++e) sum += acc[e].x + acc[e].y;
+    out[blockIdx.x * blockDim.x + threadIdx.x] = sum;
+    if (threadIdx.x == 0) clk[blockIdx.x] = t1 - t0;
+}
+
+void run_smem16() {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    float *out; long long *clk;
+    cudaMalloc(&out, (size_t)sms * 256 * 4);
+    cudaMalloc(&clk, sms * 8);
+    probe_smem16<<<sms, 256>>>(out, clk);
+    cudaDeviceSynchronize();
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    probe_smem16<<<sms, 256>>>(out, clk);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    long long c0; cudaMemcpy(&c0, clk, 8, cudaMemcpyDeviceToHost);
+    const double fma_per_block = 256.0 * 128.0 * (ITERS / 32) * 16;
+    printf("%-34s threads 256: %.1f FMA/clk/SM (block 0 clock), %.1f TFLOP/s (event)\n", "16x8 loop from SMEM",
+           fma_per_block / (double)c0, 2.0 * fma_per_block * sms / (ms * 1e-3) / 1e12);
+}
+
 int main() {
     run<0>("ffma2 a-scalar x b-pair (i outer)", 1);
     run<1>("ffma2 a-scalar x b-pair (j outer)", 1);
@@ -195,5 +266,6 @@ int main() {
     run<4>("ffma2 16x8 (j outer), 2 warps/SMSP", 1, 256);
     run_smem<false>();
     run_smem<true>();
+    run_smem16();
     return 0;
 }
