@@ -395,8 +395,8 @@ extern "C" int emm_sgemm(char transA, char transB, int64_t M, int64_t N, int64_t
 namespace {
 std::mutex g_host_mu;
 struct HostCache {
-    void *dA = nullptr, *dB = nullptr, *dC = nullptr, *dW = nullptr;
-    size_t nA = 0, nB = 0, nC = 0, nW = 0;
+    void *dA = nullptr, *dB = nullptr, *dC = nullptr, *dW = nullptr, *dR = nullptr;
+    size_t nA = 0, nB = 0, nC = 0, nW = 0, nR = 0;
     cudaStream_t s = nullptr;
     int dev = -1;
 } g_hc;
@@ -440,18 +440,25 @@ cudaEvent_t hs_event(size_t i) {
 // rows [r0, r0+nr) of op(X) (R x K op-matrix) from host to the same place of
 // the device copy (same ld): contiguous when K is the stored column index.
 cudaError_t copy_rows(float *d, const float *h, bool rows_contig_in_col, int64_t ld, int64_t r0, int64_t nr,
-                      int64_t K, cudaStream_t s) {
-    if (rows_contig_in_col)   // stored column-major with op rows along the leading dim: 2-D copy
-        return cudaMemcpy2DAsync(d + r0, (size_t)ld * 4, h + r0, (size_t)ld * 4, (size_t)nr * 4, (size_t)K,
+                      int64_t k0, int64_t nk, int64_t K, cudaStream_t s) {
+    if (rows_contig_in_col) {   // stored column-major with op rows along the leading dim: 2-D copy
+        const int64_t o = r0 + k0 * ld;
+        return cudaMemcpy2DAsync(d + o, (size_t)ld * 4, h + o, (size_t)ld * 4, (size_t)nr * 4, (size_t)nk,
                                  cudaMemcpyHostToDevice, s);
-    // op rows are stored columns: one contiguous range
-    return cudaMemcpyAsync(d + r0 * ld, h + r0 * ld, (size_t)((nr - 1) * ld + K) * 4, cudaMemcpyHostToDevice, s);
+    }
+    // op rows are stored columns: one contiguous range for all of K, else a
+    // 2-D copy of the K sub-range of each row
+    if (k0 == 0 && nk == K)
+        return cudaMemcpyAsync(d + r0 * ld, h + r0 * ld, (size_t)((nr - 1) * ld + K) * 4, cudaMemcpyHostToDevice, s);
+    const int64_t o = k0 + r0 * ld;
+    return cudaMemcpy2DAsync(d + o, (size_t)ld * 4, h + o, (size_t)ld * 4, (size_t)nk * 4, (size_t)nr,
+                             cudaMemcpyHostToDevice, s);
 }
 }  // namespace
 
 static int host_pipelined(char tA, char tB, int64_t M, int64_t N, int64_t K, float alpha, const float *A, int64_t lda,
                           const float *B, int64_t ldb, float beta, float *C, int64_t ldc, emm_math_t math, float *dA,
-                          float *dB, float *dC, void *dW) {
+                          float *dB, float *dC, void *dW, float *dR) {
     int dev = 0;
     cudaGetDevice(&dev);
     if (g_hs.dev != dev) {
@@ -506,69 +513,94 @@ static int host_pipelined(char tA, char tB, int64_t M, int64_t N, int64_t K, flo
     // operand blocks lands, and copied back right after.  Compute per PCIe
     // byte grows with the resident square, so the copies hide under the
     // tensor-core work after the first few blocks.
-    int na = 0, nb = 0, ng = 0;
-    while ((na < GM || nb < GN) && e == cudaSuccess) {
-        const int64_t rows_res = ra[na], cols_res = cb[nb];
-        const bool addA = na < GM && (nb >= GN || rows_res <= cols_res);
-        int64_t r0, nr, c0, nc;   // the GEMM's C region
-        if (addA) {
-            r0 = ra[na];
-            nr = ra[na + 1] - r0;
-            c0 = 0;
-            nc = cols_res;
-            e = copy_rows(dA, A, a_rows_ld, lda, r0, nr, K, h2d);
-        } else {
-            c0 = cb[nb];
-            nc = cb[nb + 1] - c0;
-            r0 = 0;
-            nr = rows_res;
-            e = copy_rows(dB, B, b_rows_ld, ldb, c0, nc, K, h2d);
-        }
-        if (e == cudaSuccess && beta != 0.0f && nr > 0 && nc > 0)   // the C region this step computes
-            e = cudaMemcpy2DAsync(dC + r0 + c0 * ldc, (size_t)ldc * 4, C + r0 + c0 * ldc, (size_t)ldc * 4,
-                                  (size_t)nr * 4, (size_t)nc, cudaMemcpyHostToDevice, h2d);
-        cudaEvent_t landed = ev();
-        if (e == cudaSuccess) e = cudaEventRecord(landed, h2d);
-        if (e == cudaSuccess) e = cudaStreamWaitEvent(comp, landed, 0);
-        // re-buffer the new block once (K-major planes)
-        PackArgs pk;
-        if (addA) {
-            pk.X = a_rows_ld ? dA + r0 : dA + r0 * lda;
-            pk.ld = lda; pk.R = nr; pk.kcontig = !a_rows_ld;
-            pk.out0 = Ap + (size_t)r0 * Kp; pk.ld0 = Kp; pk.out1 = Ap + (size_t)M * Kp + (size_t)r0 * Kp; pk.ld1 = Kp;
-            ++na;
-        } else {
-            pk.X = b_rows_ld ? dB + c0 : dB + c0 * ldb;
-            pk.ld = ldb; pk.R = nc; pk.kcontig = !b_rows_ld; pk.b_side = true;
-            pk.out0 = Bp + (size_t)c0 * Kp; pk.ld0 = Kp; pk.out1 = Bp + (size_t)N * Kp + (size_t)c0 * Kp; pk.ld1 = Kp;
-            ++nb;
-        }
-        if (e == cudaSuccess) e = launch_pack(pmode, pk, nullptr, K, nullptr, comp);
-        if (nr == 0 || nc == 0 || e != cudaSuccess) continue;
-        // the region in pieces along its long side: GEMM, then D2H of the piece
-        const bool split_cols = nc >= nr;
-        const int64_t len = split_cols ? nc : nr;
-        for (int64_t o = 0; o < len && e == cudaSuccess; o += chunk) {
-            const int64_t pr0 = split_cols ? r0 : r0 + o, pnr = split_cols ? nr : std::min(chunk, nr - o);
-            const int64_t pc0 = split_cols ? c0 + o : c0, pnc = split_cols ? std::min(chunk, nc - o) : nc;
-            TcOperands ops;
-            ops.a0 = TcPlane{Ap + (size_t)pr0 * Kp, Kp, false, Kp};
-            ops.b0 = TcPlane{Bp + (size_t)pc0 * Kp, Kp, false, Kp};
-            if (pl == 2) {
-                ops.a1 = TcPlane{Ap + (size_t)M * Kp + (size_t)pr0 * Kp, Kp, false, Kp};
-                ops.b1 = TcPlane{Bp + (size_t)N * Kp + (size_t)pc0 * Kp, Kp, false, Kp};
+    // K phases (dR != nullptr): the first half of K for every block first
+    // (half the bytes per block, so the tensor cores are fed ~2x sooner while
+    // the resident square grows), raw partials into dR; then the second half,
+    // each GEMM continuing the promotion chain from dR (acc_init) — the same
+    // additions in the same order as one pass over K, so the result is bit-
+    // identical to the device call.  K1 ends on a 256-of-K promotion boundary.
+    int nphase = dR ? 2 : 1;
+    if (const char *ep = getenv("EMM_HOST_KPHASES")) nphase = dR ? std::max(2, std::min(8, atoi(ep))) : 1;
+    // phase boundaries on 256-of-K promotion boundaries
+    auto kb = [&](int p) { return p >= nphase ? K : (K * p / nphase) / 256 * 256; };
+    int ng = 0;
+    for (int ph = 0; ph < nphase && e == cudaSuccess; ++ph) {
+        const int64_t k0 = kb(ph), nk = kb(ph + 1) - kb(ph);
+        const bool last_phase = ph == nphase - 1;
+        if (nk <= 0) continue;
+        int na = 0, nb = 0;
+        while ((na < GM || nb < GN) && e == cudaSuccess) {
+            const int64_t rows_res = ra[na], cols_res = cb[nb];
+            const bool addA = na < GM && (nb >= GN || rows_res <= cols_res);
+            int64_t r0, nr, c0, nc;   // the GEMM's C region
+            if (addA) {
+                r0 = ra[na];
+                nr = ra[na + 1] - r0;
+                c0 = 0;
+                nc = cols_res;
+                e = copy_rows(dA, A, a_rows_ld, lda, r0, nr, k0, nk, K, h2d);
+            } else {
+                c0 = cb[nb];
+                nc = cb[nb + 1] - c0;
+                r0 = 0;
+                nr = rows_res;
+                e = copy_rows(dB, B, b_rows_ld, ldb, c0, nc, k0, nk, K, h2d);
             }
-            unsigned int *cw = ctrl + 32 * (ng & 63);   // zeroed once for the first 64 GEMMs
-            if (ng++ >= 64) e = cudaMemsetAsync(cw, 0, 128, comp);
-            if (e == cudaSuccess)
-                e = launch_tc_sgemm(terms, ops, pnr, pnc, K, alpha, beta, dC + pr0 + pc0 * ldc, ldc, cw, 1, nullptr,
-                                    comp);
-            cudaEvent_t done = ev();
-            if (e == cudaSuccess) e = cudaEventRecord(done, comp);
-            if (e == cudaSuccess) e = cudaStreamWaitEvent(d2h, done, 0);
-            if (e == cudaSuccess)
-                e = cudaMemcpy2DAsync(C + pr0 + pc0 * ldc, (size_t)ldc * 4, dC + pr0 + pc0 * ldc, (size_t)ldc * 4,
-                                      (size_t)pnr * 4, (size_t)pnc, cudaMemcpyDeviceToHost, d2h);
+            if (e == cudaSuccess && beta != 0.0f && nr > 0 && nc > 0 && last_phase)   // the C region this step computes
+                e = cudaMemcpy2DAsync(dC + r0 + c0 * ldc, (size_t)ldc * 4, C + r0 + c0 * ldc, (size_t)ldc * 4,
+                                      (size_t)nr * 4, (size_t)nc, cudaMemcpyHostToDevice, h2d);
+            cudaEvent_t landed = ev();
+            if (e == cudaSuccess) e = cudaEventRecord(landed, h2d);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(comp, landed, 0);
+            // re-buffer the new block once (K-major planes)
+            PackArgs pk;
+            if (addA) {
+                pk.X = a_rows_ld ? dA + r0 + k0 * lda : dA + r0 * lda + k0;
+                pk.ld = lda; pk.R = nr; pk.kcontig = !a_rows_ld;
+                pk.out0 = Ap + (size_t)r0 * Kp + k0; pk.ld0 = Kp;
+                pk.out1 = Ap + (size_t)M * Kp + (size_t)r0 * Kp + k0; pk.ld1 = Kp;
+                ++na;
+            } else {
+                pk.X = b_rows_ld ? dB + c0 + k0 * ldb : dB + c0 * ldb + k0;
+                pk.ld = ldb; pk.R = nc; pk.kcontig = !b_rows_ld; pk.b_side = true;
+                pk.out0 = Bp + (size_t)c0 * Kp + k0; pk.ld0 = Kp;
+                pk.out1 = Bp + (size_t)N * Kp + (size_t)c0 * Kp + k0; pk.ld1 = Kp;
+                ++nb;
+            }
+            if (e == cudaSuccess) e = launch_pack(pmode, pk, nullptr, nk, nullptr, comp);
+            if (nr == 0 || nc == 0 || e != cudaSuccess) continue;
+            // the region in pieces along its long side: GEMM, then D2H of the piece
+            const bool split_cols = nc >= nr;
+            const int64_t len = split_cols ? nc : nr;
+            for (int64_t o = 0; o < len && e == cudaSuccess; o += chunk) {
+                const int64_t pr0 = split_cols ? r0 : r0 + o, pnr = split_cols ? nr : std::min(chunk, nr - o);
+                const int64_t pc0 = split_cols ? c0 + o : c0, pnc = split_cols ? std::min(chunk, nc - o) : nc;
+                TcOperands ops;
+                const int64_t kext = tc_kpad(nk);   // this phase's K columns of the planes (zero padded)
+                ops.a0 = TcPlane{Ap + (size_t)pr0 * Kp + k0, Kp, false, kext};
+                ops.b0 = TcPlane{Bp + (size_t)pc0 * Kp + k0, Kp, false, kext};
+                if (pl == 2) {
+                    ops.a1 = TcPlane{Ap + (size_t)M * Kp + (size_t)pr0 * Kp + k0, Kp, false, kext};
+                    ops.b1 = TcPlane{Bp + (size_t)N * Kp + (size_t)pc0 * Kp + k0, Kp, false, kext};
+                }
+                unsigned int *cw = ctrl + 32 * (ng & 63);   // zeroed once for the first 64 GEMMs
+                if (ng++ >= 64) e = cudaMemsetAsync(cw, 0, 128, comp);
+                if (e == cudaSuccess) {
+                    if (!last_phase)   // raw partial of the K prefix (continuing the previous phases')
+                        e = launch_tc_sgemm(terms, ops, pnr, pnc, nk, 1.0f, 0.0f, dR + pr0 + pc0 * M, M, cw, 1, nullptr,
+                                            comp, nullptr, nullptr, ph > 0 ? dR + pr0 + pc0 * M : nullptr, M);
+                    else
+                        e = launch_tc_sgemm(terms, ops, pnr, pnc, nk, alpha, beta, dC + pr0 + pc0 * ldc, ldc, cw, 1,
+                                            nullptr, comp, nullptr, nullptr, dR ? dR + pr0 + pc0 * M : nullptr, M);
+                }
+                if (!last_phase) continue;
+                cudaEvent_t done = ev();
+                if (e == cudaSuccess) e = cudaEventRecord(done, comp);
+                if (e == cudaSuccess) e = cudaStreamWaitEvent(d2h, done, 0);
+                if (e == cudaSuccess)
+                    e = cudaMemcpy2DAsync(C + pr0 + pc0 * ldc, (size_t)ldc * 4, dC + pr0 + pc0 * ldc, (size_t)ldc * 4,
+                                          (size_t)pnr * 4, (size_t)pnc, cudaMemcpyDeviceToHost, d2h);
+            }
         }
     }
     if (e == cudaSuccess) e = cudaStreamSynchronize(d2h);
@@ -615,8 +647,13 @@ extern "C" int emm_sgemm_host(char transA, char transB, int64_t M, int64_t N, in
         const size_t pl = (size_t)planes_of(math);
         const size_t nP = align_up(pl * (size_t)(M + N) * Kp * 4, 1024) + 64 * 128;
         if ((st = ensure(&g_hc.dW, &g_hc.nW, nP))) return st;
+        // K phases for the FP32-accurate splits at large K (EMM_HOST_KSPLIT=0/1)
+        const char *ek = getenv("EMM_HOST_KSPLIT");
+        const bool ksplit = math != EMM_MATH_1XTF32 && (ek ? ek[0] == '1' : K >= 8192) && K >= 512;
+        if (ksplit && (st = ensure(&g_hc.dR, &g_hc.nR, (size_t)M * N * 4))) return st;
         return host_pipelined(transA, transB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, math,
-                              (float *)g_hc.dA, (float *)g_hc.dB, (float *)g_hc.dC, g_hc.dW);
+                              (float *)g_hc.dA, (float *)g_hc.dB, (float *)g_hc.dC, g_hc.dW,
+                              ksplit ? (float *)g_hc.dR : nullptr);
     }
     if (ab_used) {
         e = cudaMemcpyAsync(g_hc.dA, A, nA, cudaMemcpyHostToDevice, s);
@@ -644,6 +681,7 @@ extern "C" void emm_release_cache(void) {
     if (g_hc.dB) cudaFree(g_hc.dB);
     if (g_hc.dC) cudaFree(g_hc.dC);
     if (g_hc.dW) cudaFree(g_hc.dW);
+    if (g_hc.dR) cudaFree(g_hc.dR);
     if (g_hc.s) cudaStreamDestroy(g_hc.s);
     g_hc = HostCache{};
 }

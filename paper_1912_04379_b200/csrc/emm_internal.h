@@ -81,7 +81,13 @@ bool tc_sk_plan(int64_t M, int64_t N, int64_t K, int splits, int terms, int *dp_
 // `partial` (splits x M x N floats) and a fixed-order reduce launch.
 cudaError_t launch_tc_sgemm(int terms, const TcOperands &ops, int64_t M, int64_t N, int64_t K, float alpha,
                             float beta, float *C, int64_t ldc, unsigned int *ctrl, int splits, float *partial,
-                            cudaStream_t s, const PeerOut *peers = nullptr, void *sk_ws = nullptr);
+                            cudaStream_t s, const PeerOut *peers = nullptr, void *sk_ws = nullptr,
+                            const float *acc_init = nullptr, int64_t ld_init = 0);
+// acc_init (3xTF32 / TF32+BF16, whole tiles): the FP32 promotion chain of
+// every output starts from acc_init[r + c*ld_init] (the raw partial, alpha = 1
+// and beta = 0, of an earlier call over a K prefix that ends on a 256-of-K
+// boundary) — together the calls add the same numbers in the same order as
+// one call over all of K (K-phased host pipeline).
 // Fixed-order split-K reduce (KN8): C <- alpha * sum_s P_s + beta*C.
 cudaError_t launch_splitk_reduce(const float *partial, int splits, int64_t M, int64_t N, float alpha, float beta,
                                  float *C, int64_t ldc, cudaStream_t s);

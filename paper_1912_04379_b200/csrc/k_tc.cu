@@ -438,7 +438,8 @@ __global__ void __launch_bounds__(TC_THREADS_P, 1)
                     const __grid_constant__ CUtensorMap tmB0h, const __grid_constant__ CUtensorMap tmB1h, int M, int N,
                     int Kp, float alpha, float beta, float *__restrict__ C, int64_t ldc, int tiles_m, int tiles_n,
                     int group_m, int kc_stages, unsigned int *__restrict__ wave_ctr, int splits,
-                    float *__restrict__ partial, const TcSk sk, const __grid_constant__ PeerOut peers) {
+                    float *__restrict__ partial, const TcSk sk, const __grid_constant__ PeerOut peers,
+                    const float *__restrict__ acc_init, int64_t ld_init) {
     if (threadIdx.x == 0) EMM_TL(0);
     using Cfg = TcCfg<TERMS>;
     constexpr bool A1_MN = TERMS == 3 ? A_MN : false;   // cross planes are K-major
@@ -591,7 +592,8 @@ __global__ void __launch_bounds__(TC_THREADS_P, 1)
                 S, smem, full, empty, acc_full, acc_empty, tmem_base, kc_stages, cl, pair);
     } else if (warp >= TC_EPI_WARP0) {
         tc_epilogue_loop<MC>(S, rank, warp & 3, (warp - TC_EPI_WARP0) >> 2, lane, tmem_base, acc_full, acc_empty,
-                         kc_stages, M, N, alpha, beta, C, ldc, partial, sk, peers, cl, leader);
+                         kc_stages, M, N, alpha, beta, C, ldc, partial, sk, peers, cl, leader, acc_init,
+                              ld_init);
     }
 
     tc_fence_before();
@@ -826,7 +828,9 @@ static bool tc_pref4_wanted(int terms, int64_t K) {
 template <int TERMS, bool A_MN, bool B_MN>
 static cudaError_t launch_tc_t(const TcOperands &ops, int64_t M, int64_t N, int64_t Kp, float alpha, float beta,
                                float *C, int64_t ldc, unsigned int *ctrl, int splits, float *partial, cudaStream_t s,
-                               const PeerOut &peers, void *sk_ws) {
+                               const PeerOut &peers, void *sk_ws, const float *acc_init, int64_t ld_init) {
+    if (acc_init && splits != 1) return cudaErrorInvalidValue;
+    if (acc_init) sk_ws = nullptr;   // whole tiles only
     using Cfg = TcCfg<TERMS>;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
@@ -929,7 +933,8 @@ static cudaError_t launch_tc_t(const TcOperands &ops, int64_t M, int64_t N, int6
         auto kern = mc ? tc_sgemm_kernel<TERMS, A_MN, B_MN, TERMS >= 2> : tc_sgemm_kernel<TERMS, A_MN, B_MN, false>;
         cudaError_t le = cudaLaunchKernelEx(&cfg, kern, ta0, ta1, tb0, tb1, tb0h, tb1h, (int)M,
                                             (int)N, (int)Kp, alpha, beta, C, ldc, tiles_m, tiles_n, group_m,
-                                            kc_stages, ctrl, splits, splits > 1 ? partial : nullptr, sk, peers);
+                                            kc_stages, ctrl, splits, splits > 1 ? partial : nullptr, sk, peers,
+                                            acc_init, ld_init);
         if (le != cudaSuccess) return le;
     }
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -942,30 +947,37 @@ static cudaError_t launch_tc_t(const TcOperands &ops, int64_t M, int64_t N, int6
 template <int TERMS>
 static cudaError_t launch_tc_m(const TcOperands &ops, int64_t M, int64_t N, int64_t Kp, float alpha, float beta,
                                float *C, int64_t ldc, unsigned int *ctrl, int splits, float *partial, cudaStream_t s,
-                               const PeerOut &pe, void *sk) {
+                               const PeerOut &pe, void *sk, const float *ai, int64_t ldi) {
     const bool am = ops.a0.mn, bm = ops.b0.mn;
     if (!am && !bm)
-        return launch_tc_t<TERMS, false, false>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe, sk);
+        return launch_tc_t<TERMS, false, false>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe, sk,
+                                                ai, ldi);
     if (!am && bm)
-        return launch_tc_t<TERMS, false, true>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe, sk);
+        return launch_tc_t<TERMS, false, true>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe, sk,
+                                               ai, ldi);
     if (am && !bm)
-        return launch_tc_t<TERMS, true, false>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe, sk);
-    return launch_tc_t<TERMS, true, true>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe, sk);
+        return launch_tc_t<TERMS, true, false>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe, sk,
+                                               ai, ldi);
+    return launch_tc_t<TERMS, true, true>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe, sk, ai,
+                                          ldi);
 }
 
 cudaError_t launch_tc_sgemm(int terms, const TcOperands &ops, int64_t M, int64_t N, int64_t K, float alpha,
                             float beta, float *C, int64_t ldc, unsigned int *ctrl, int splits, float *partial,
-                            cudaStream_t s, const PeerOut *peers, void *sk_ws) {
+                            cudaStream_t s, const PeerOut *peers, void *sk_ws, const float *acc_init,
+                            int64_t ld_init) {
     if (M > 0x7fffffffLL || N > 0x7fffffffLL || K > 0x7fffffffLL - 32) return cudaErrorInvalidValue;
     if (splits < 1 || (splits > 1 && !partial)) return cudaErrorInvalidValue;
     if (peers && (peers->n < 0 || peers->n > 8 || splits > 1)) return cudaErrorInvalidValue;
     const PeerOut pe = peers ? *peers : PeerOut{};
-    if (terms == 1 && splits == 1 && pe.n == 0 && tc1w_wanted(M, N, K))
+    if (terms == 1 && splits == 1 && pe.n == 0 && !acc_init && tc1w_wanted(M, N, K))
         return launch_tc1w_sgemm(ops, M, N, K, alpha, beta, C, ldc, s);
     const int64_t Kp = tc_kpad(K);
-    if (terms == 3) return launch_tc_m<3>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe, sk_ws);
-    if (terms == 2) return launch_tc_m<2>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe, sk_ws);
-    return launch_tc_m<1>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe, sk_ws);
+    if (terms == 3)
+        return launch_tc_m<3>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe, sk_ws, acc_init, ld_init);
+    if (terms == 2)
+        return launch_tc_m<2>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe, sk_ws, acc_init, ld_init);
+    return launch_tc_m<1>(ops, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe, sk_ws, acc_init, ld_init);
 }
 
 }  // namespace emm

@@ -298,7 +298,8 @@ __device__ __forceinline__ void tc_epilogue_loop(const TcSched &S, uint32_t rank
                                                  int kc_stages, int M, int N, float alpha, float beta,
                                                  float *__restrict__ C, int64_t ldc, float *__restrict__ partial,
                                                  const TcSk &sk, const PeerOut &peers, int cl = 2,
-                                                 uint32_t leader = 0) {
+                                                 uint32_t leader = 0, const float *__restrict__ acc_init = nullptr,
+                                                 int64_t ld_init = 0) {
     using namespace ptx;
     if (!MC) cl = 2, leader = 0;   // compile-time plain schedule
     uint32_t leader_empty0;   // the pair leader's acc_empty[0]
@@ -317,8 +318,19 @@ __device__ __forceinline__ void tc_epilogue_loop(const TcSched &S, uint32_t rank
         const int nchunks = (kb1 - kb0 + kc_stages - 1) / kc_stages;
         const int row = m0 + (int)rank * TC_BM + 32 * q + lane;
         float acc[128];
+        if (acc_init && row < M) {
+            // K-phased call (host pipeline): continue the FP32 promotion chain
+            // from the raw partial of the earlier K range (same additions in
+            // the same order as one call over all of K)
+            const int col0 = n0 + h * 128;
+            const float *ip = acc_init + (int64_t)row + (int64_t)col0 * ld_init;
+            const int jmax = min(128, N - col0);
 #pragma unroll
-        for (int j = 0; j < 128; ++j) acc[j] = 0.0f;
+            for (int j = 0; j < 128; ++j) acc[j] = j < jmax ? __ldcs(ip + (int64_t)j * ld_init) : 0.0f;
+        } else {
+#pragma unroll
+            for (int j = 0; j < 128; ++j) acc[j] = 0.0f;
+        }
         for (int c2 = 0; c2 < nchunks; ++c2, ++ch) {
             const int b = ch & 1;
             mbar_wait(&acc_full[b], ((uint32_t)ch >> 1) & 1u);

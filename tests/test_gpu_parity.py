@@ -424,7 +424,7 @@ def test_torch_binding_colmajor(emm):
 
 @pytest.mark.parametrize("tA,tB", [("N", "N"), ("T", "T"), ("N", "T")])
 @pytest.mark.parametrize("beta", [0.0, 0.5])
-@pytest.mark.parametrize("blocks", [None, (256, 512)], ids=["default", "first256-chunk512"])
+@pytest.mark.parametrize("blocks", [None, (256, 512), "ksplit"], ids=["default", "first256-chunk512", "ksplit"])
 def test_host_buffer_pipelined(emm, monkeypatch, tA, tB, beta, blocks):
     """emm_sgemm_host above 4096 x 4096 runs the copy/compute pipeline (L-
     shaped growth over 2048-row/column blocks, the first two 1024, ragged
@@ -432,10 +432,17 @@ def test_host_buffer_pipelined(emm, monkeypatch, tA, tB, beta, blocks):
     pieces with its own copy-back): same bits as the re-buffered device call
     (K = 300 < 512: stream-K pieces sum like the sequential K loop), ldc
     padding intact, sampled rows against the oracle."""
-    if blocks:
+    M, N, K = 4500, 4200, 300
+    if blocks == "ksplit":
+        # two K phases (K1 = 512, a promotion boundary), the second continuing
+        # from the first's raw partials: still the device call's bits (stream-K
+        # off there: its piece sums are not the sequential K loop above 512)
+        monkeypatch.setenv("EMM_HOST_KSPLIT", "1")
+        monkeypatch.setenv("EMM_SK", "0")
+        K = 1300
+    elif blocks:
         monkeypatch.setenv("EMM_HOST_FIRST", str(blocks[0]))
         monkeypatch.setenv("EMM_HOST_CHUNK", str(blocks[1]))
-    M, N, K = 4500, 4200, 300
     case = cached_case(tA, tB, M, N, K, 1.25, beta, pad=(4, 4, 3))
     rows = np.array([0, 1, 1023, 1151, 1152, 2999, M - 1])
     R, S, T, _ = case.oracle(rows=rows)
