@@ -23,6 +23,12 @@
 //    elected thread issues.  "shuffling and write back" deferred to the end
 //    of the dot product → one epilogue per tile.
 //  * N-edge special cases → predicated epilogue stores.
+//  * B200-specific: persistent CTA pairs with a wave lockstep (L2 reuse of
+//    the wave's panels), split-K / hybrid stream-K for partial waves, and for
+//    data-parallel launches at K >= 4096 a PREFERRED cluster size of 4 (two
+//    pairs on vertically adjacent tiles share B by TMA multicast; MC
+//    template); `acc_init` lets a later call over the rest of K continue the
+//    FP32 promotion chains of an earlier one (K-phased host pipeline).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
