@@ -424,7 +424,8 @@ def test_torch_binding_colmajor(emm):
 
 @pytest.mark.parametrize("tA,tB", [("N", "N"), ("T", "T"), ("N", "T")])
 @pytest.mark.parametrize("beta", [0.0, 0.5])
-@pytest.mark.parametrize("blocks", [None, (256, 512), "ksplit"], ids=["default", "first256-chunk512", "ksplit"])
+@pytest.mark.parametrize("blocks", [None, (256, 512), "ksplit", "ksplit3"],
+                         ids=["default", "first256-chunk512", "ksplit", "ksplit3"])
 def test_host_buffer_pipelined(emm, monkeypatch, tA, tB, beta, blocks):
     """emm_sgemm_host above 4096 x 4096 runs the copy/compute pipeline (L-
     shaped growth over 2048-row/column blocks, the first two 1024, ragged
@@ -433,13 +434,15 @@ def test_host_buffer_pipelined(emm, monkeypatch, tA, tB, beta, blocks):
     (K = 300 < 512: stream-K pieces sum like the sequential K loop), ldc
     padding intact, sampled rows against the oracle."""
     M, N, K = 4500, 4200, 300
-    if blocks == "ksplit":
+    if blocks == "ksplit3":   # three K phases (the middle one both reads and writes the partials)
+        monkeypatch.setenv("EMM_HOST_KPHASES", "3")
+    if blocks in ("ksplit", "ksplit3"):
         # two K phases (K1 = 512, a promotion boundary), the second continuing
         # from the first's raw partials: still the device call's bits (stream-K
         # off there: its piece sums are not the sequential K loop above 512)
         monkeypatch.setenv("EMM_HOST_KSPLIT", "1")
         monkeypatch.setenv("EMM_SK", "0")
-        K = 1300
+        K = 1300 if blocks == "ksplit" else 2000
     elif blocks:
         monkeypatch.setenv("EMM_HOST_FIRST", str(blocks[0]))
         monkeypatch.setenv("EMM_HOST_CHUNK", str(blocks[1]))
