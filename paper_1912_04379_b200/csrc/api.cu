@@ -738,7 +738,7 @@ extern "C" const char *emm_strerror(int status) {
     return "unknown status";
 }
 
-extern "C" const char *emm_version(void) { return "emm 0.1 (sm_100a: tcgen05 3xTF32/1xTF32, FFMA)"; }
+extern "C" const char *emm_version(void) { return "emm 0.2 (sm_100a: tcgen05 3xTF32 / TF32+BF16 / 1xTF32, TMA-fed FFMA)"; }
 
 extern "C" uint64_t emm_launch_count(void) { return g_launches.load(); }
 
