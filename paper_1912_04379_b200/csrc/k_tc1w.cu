@@ -39,23 +39,38 @@ using namespace ptx;
 
 namespace {
 constexpr int W_BN = 512;                              // C columns per pair
-constexpr int W_STAGES = 4;
 constexpr int W_STAGE_BYTES = 3 * TC_TILE_BYTES;      // A | B half 0 | B half 1 (per CTA)
-constexpr int W_SMEM = W_STAGES * W_STAGE_BYTES + 1024 + 256;
+// beta != 0 with a TMA-legal C (TMAC): the epilogue reads C_in through TMA
+// into a ring of 4 x (128 rows x 16 columns) buffers per column group — many
+// more bytes in flight than per-thread loads (the beta = 1 epilogue was
+// load-latency-bound: c4-ii 1.03 ms vs 0.79 ms at beta = 0) — so the operand
+// ring shrinks to 3 stages.
+constexpr int W_CB_COLS = 16, W_CB_N = 4;
+constexpr int W_CB_BYTES = 128 * W_CB_COLS * 4;       // 8 KB
+template <bool TMAC>
+struct WCfg {
+    static constexpr int STAGES = TMAC ? 3 : 4;
+    static constexpr int CBUF = TMAC ? 2 * W_CB_N * W_CB_BYTES : 0;   // two column groups
+    static constexpr int SMEM = STAGES * W_STAGE_BYTES + CBUF + 1024 + 512;
+};
 constexpr int W_GROUP_M = 8;
 }  // namespace
 
-template <bool A_MN, bool B_MN>
+template <bool A_MN, bool B_MN, bool TMAC>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (TC_EPI_WARPS + 2), 1)
-    tc1w_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-                int Kp, float alpha, float beta, float *__restrict__ C, int64_t ldc, int tiles_m, int tiles_n) {
+    tc1w_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ CUtensorMap tmC, int M, int N, int Kp, float alpha, float beta,
+                float *__restrict__ C, int64_t ldc, int tiles_m, int tiles_n) {
+    constexpr int W_STAGES = WCfg<TMAC>::STAGES;
     extern __shared__ __align__(1024) uint8_t w_raw[];
     uint8_t *smem = w_raw + ((1024u - (smem_u32(w_raw) & 1023u)) & 1023u);
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + W_STAGES * W_STAGE_BYTES);
+    float *cbuf = reinterpret_cast<float *>(smem + W_STAGES * W_STAGE_BYTES);   // TMAC: [2 groups][W_CB_N][16][128]
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + W_STAGES * W_STAGE_BYTES + WCfg<TMAC>::CBUF);
     uint64_t *empty = full + W_STAGES;
     uint64_t *acc_full = empty + W_STAGES;   // [1]
     uint64_t *acc_empty = acc_full + 1;      // [2]: N-half 0 / 1 drained (both CTAs' epilogue warps)
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 2);
+    uint64_t *cfull = acc_empty + 2;         // TMAC: [2 groups][W_CB_N] C-chunk landed
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(cfull + 2 * W_CB_N);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
@@ -78,11 +93,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (TC_EPI_WARPS +
         mbar_init(&acc_full[0], 1);
         mbar_init(&acc_empty[0], 2 * TC_EPI_WARPS);
         mbar_init(&acc_empty[1], 2 * TC_EPI_WARPS);
+        for (int i = 0; i < 2 * W_CB_N; ++i) mbar_init(&cfull[i], 1);
         fence_mbar_init();
     }
     if (warp == 0 && lane == 0) {
         prefetch_tmap(&tmA);
         prefetch_tmap(&tmB);
+        if (TMAC) prefetch_tmap(&tmC);
     }
     if (warp == 1) tmem_alloc_2sm<TC_TMEM_COLS>(tmem_slot);
     tc_fence_before();
@@ -179,7 +196,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (TC_EPI_WARPS +
         const int q = warp & 3, hh = (warp - 2) >> 2;   // lane quarter, 128-column part of each half
         uint32_t leader_empty0;
         asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(leader_empty0) : "r"(smem_u32(&acc_empty[0])));
-        int tl = 0;
+        int tl = 0, cph = 0;   // tile counter, C-chunk counter (TMAC ring phases)
         for (int t = cid; t < tiles; t += nclus, ++tl) {
             int m0, n0;
             origin(t, m0, n0);
@@ -208,9 +225,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (TC_EPI_WARPS +
                     const uint32_t eb = leader_empty0 + (uint32_t)(h * sizeof(uint64_t));
                     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(eb) : "memory");
                 }
-                if (row >= M) continue;
                 float *cp = C + (int64_t)row + (int64_t)col0 * ldc;
                 const int jmax = min(128, N - col0);
+                if (TMAC) {
+                    // C_in chunks of 16 columns x this group's 128 rows through
+                    // TMA into a 4-deep ring; stores stay per thread (coalesced)
+                    const int rl = 32 * q + lane;                      // row within the CTA's 128
+                    float *gb = cbuf + hh * (W_CB_N * W_CB_BYTES / 4);
+                    uint64_t *gf = cfull + hh * W_CB_N;
+                    const bool leader_t = q == (TC_EPI_WARP0 & 3) && lane == 0;   // first warp of the group
+                    const int crow = m0 + (int)rank * TC_BM;
+                    auto issue = [&](int c) {
+                        const int b = c % W_CB_N;
+                        mbar_arrive_expect_tx(&gf[b], W_CB_BYTES);
+                        tma_load_2d(smem_u32(gb + b * (W_CB_BYTES / 4)), &tmC, &gf[b], crow, col0 + W_CB_COLS * c,
+                                    policy_evict_first());
+                    };
+                    if (leader_t)
+                        for (int c = 0; c < W_CB_N; ++c) issue(c);
+#pragma unroll
+                    for (int c = 0; c < 128 / W_CB_COLS; ++c, ++cph) {
+                        const int b = c % W_CB_N;
+                        mbar_wait(&gf[b], (uint32_t)((cph / W_CB_N) & 1));
+                        const float *bp = gb + b * (W_CB_BYTES / 4) + rl;
+                        float *sp = cp + (int64_t)(W_CB_COLS * c) * ldc;
+#pragma unroll
+                        for (int j = 0; j < W_CB_COLS; ++j, sp += ldc) {
+                            const int jj = W_CB_COLS * c + j;
+                            if (row < M && jj < jmax) __stcs(sp, fmaf(beta, bp[j * 128], alpha * acc[jj]));
+                        }
+                        // the group's 128 threads are done with buffer b
+                        if (hh == 0)
+                            asm volatile("bar.sync 1, 128;" ::: "memory");
+                        else
+                            asm volatile("bar.sync 2, 128;" ::: "memory");
+                        if (leader_t && c + W_CB_N < 128 / W_CB_COLS) issue(c + W_CB_N);
+                    }
+                    continue;
+                }
+                if (row >= M) continue;
                 if (beta == 0.0f) {
                     float *sp = cp;
 #pragma unroll
@@ -244,41 +297,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (TC_EPI_WARPS +
 }
 
 // Policy: 1xTF32 problems of at least one full wave of 256 x 512 tiles
-// (smaller ones keep KN2's split-K / finer tiles) and K >= 2048, where the
-// epilogue that no longer hides fully under the next tile's MMAs is a small
-// share of a tile (measured: 8192^3 1.72 -> 1.34 ms, 4096^3 0.256 -> 0.186,
-// c4-i 0.93 -> 0.76; c4-ii, K = 1024 with beta = 1, 1.01 -> 1.03 ms:
-// profiles/r01_ab_1x_wide.txt).  EMM_WIDE=0 / 1 forces.
+// (smaller ones keep KN2's split-K / finer tiles) and K >= 1024 (measured:
+// 8192^3 1.72 -> 1.34 ms, 4096^3 0.256 -> 0.186, c4-i 0.95 -> 0.77; c4-ii,
+// K = 1024 with beta = 1, 1.03 -> 0.94 ms once C_in comes through TMA, and
+// 0.96 -> 0.79 ms at beta = 0: profiles/r01_ab_1x_wide*.txt).
+// EMM_WIDE=0 / 1 forces.
 bool tc1w_wanted(int64_t M, int64_t N, int64_t K) {
     const char *e = getenv("EMM_WIDE");
     if (e && e[0] == '0') return false;
     const int64_t tiles = ((M + 255) / 256) * ((N + W_BN - 1) / W_BN);
     if (e && e[0] == '1') return tiles <= 0x7fffffffLL;
-    return N > 256 && K >= 2048 && tiles >= tc_num_sms() / 2 && tiles <= 0x7fffffffLL;
+    return N > 256 && K >= 1024 && tiles >= tc_num_sms() / 2 && tiles <= 0x7fffffffLL;
 }
 
-template <bool A_MN, bool B_MN>
+template <bool A_MN, bool B_MN, bool TMAC>
 static cudaError_t launch_w(const TcOperands &ops, int64_t M, int64_t N, int64_t Kp, float alpha, float beta,
                             float *C, int64_t ldc, cudaStream_t s) {
+    constexpr int SMEM = WCfg<TMAC>::SMEM;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     static int max_clusters = 0;
     std::call_once(once, [] {
-        attr_err = cudaFuncSetAttribute(tc1w_kernel<A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize, W_SMEM);
+        attr_err = cudaFuncSetAttribute(tc1w_kernel<A_MN, B_MN, TMAC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        SMEM);
         cudaLaunchConfig_t oc{};
         oc.gridDim = dim3(2 * 64);
         oc.blockDim = dim3(32 * (TC_EPI_WARPS + 2));
-        oc.dynamicSmemBytes = W_SMEM;
+        oc.dynamicSmemBytes = SMEM;
         int n = 0;
         if (attr_err == cudaSuccess &&
-            cudaOccupancyMaxActiveClusters(&n, tc1w_kernel<A_MN, B_MN>, &oc) != cudaSuccess)
+            cudaOccupancyMaxActiveClusters(&n, tc1w_kernel<A_MN, B_MN, TMAC>, &oc) != cudaSuccess)
             n = 0;
         max_clusters = n;
         cudaGetLastError();
     });
     if (attr_err != cudaSuccess) return attr_err;
-    CUtensorMap ta, tb;
+    CUtensorMap ta, tb, tc;
     if (!tc_make_tmap(&ta, ops.a0, M) || !tc_make_tmap(&tb, ops.b0, N)) return cudaErrorInvalidValue;
+    if (TMAC) {   // C_in tiles of 128 rows x 16 columns, no swizzle
+        if (!encode_tmap_f32_2d(&tc, C, M, N, ldc, 128, W_CB_COLS, CU_TENSOR_MAP_SWIZZLE_NONE))
+            return cudaErrorInvalidValue;
+    } else {
+        tc = ta;
+    }
     const int tiles_m = (int)((M + 255) / 256), tiles_n = (int)((N + W_BN - 1) / W_BN);
     const int64_t tiles = (int64_t)tiles_m * tiles_n;
     int64_t clusters = tc_num_sms() / 2;
@@ -289,19 +350,28 @@ static cudaError_t launch_w(const TcOperands &ops, int64_t M, int64_t N, int64_t
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)(2 * clusters));
     cfg.blockDim = dim3(32 * (TC_EPI_WARPS + 2));
-    cfg.dynamicSmemBytes = W_SMEM;
+    cfg.dynamicSmemBytes = SMEM;
     cfg.stream = s;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    cudaError_t le = cudaLaunchKernelEx(&cfg, tc1w_kernel<A_MN, B_MN>, ta, tb, (int)M, (int)N, (int)Kp, alpha, beta,
-                                        C, ldc, tiles_m, tiles_n);
+    cudaError_t le = cudaLaunchKernelEx(&cfg, tc1w_kernel<A_MN, B_MN, TMAC>, ta, tb, tc, (int)M, (int)N, (int)Kp,
+                                        alpha, beta, C, ldc, tiles_m, tiles_n);
     if (le != cudaSuccess) return le;
     g_launches.fetch_add(1, std::memory_order_relaxed);
     prof_end(s, true, ev);
     return cudaGetLastError();
+}
+
+template <bool A_MN, bool B_MN>
+static cudaError_t launch_w2(const TcOperands &ops, int64_t M, int64_t N, int64_t Kp, float alpha, float beta,
+                             float *C, int64_t ldc, cudaStream_t s) {
+    const char *e = getenv("EMM_WIDE_TMAC");
+    const bool tmac = beta != 0.0f && tma_legal(C, ldc) && !(e && e[0] == '0');
+    return tmac ? launch_w<A_MN, B_MN, true>(ops, M, N, Kp, alpha, beta, C, ldc, s)
+                : launch_w<A_MN, B_MN, false>(ops, M, N, Kp, alpha, beta, C, ldc, s);
 }
 
 cudaError_t launch_tc1w_sgemm(const TcOperands &ops, int64_t M, int64_t N, int64_t K, float alpha, float beta,
@@ -309,10 +379,10 @@ cudaError_t launch_tc1w_sgemm(const TcOperands &ops, int64_t M, int64_t N, int64
     if (M > 0x7fffffffLL || N > 0x7fffffffLL || K > 0x7fffffffLL - 32) return cudaErrorInvalidValue;
     const int64_t Kp = tc_kpad(K);
     const bool am = ops.a0.mn, bm = ops.b0.mn;
-    if (!am && !bm) return launch_w<false, false>(ops, M, N, Kp, alpha, beta, C, ldc, s);
-    if (!am && bm) return launch_w<false, true>(ops, M, N, Kp, alpha, beta, C, ldc, s);
-    if (am && !bm) return launch_w<true, false>(ops, M, N, Kp, alpha, beta, C, ldc, s);
-    return launch_w<true, true>(ops, M, N, Kp, alpha, beta, C, ldc, s);
+    if (!am && !bm) return launch_w2<false, false>(ops, M, N, Kp, alpha, beta, C, ldc, s);
+    if (!am && bm) return launch_w2<false, true>(ops, M, N, Kp, alpha, beta, C, ldc, s);
+    if (am && !bm) return launch_w2<true, false>(ops, M, N, Kp, alpha, beta, C, ldc, s);
+    return launch_w2<true, true>(ops, M, N, Kp, alpha, beta, C, ldc, s);
 }
 
 }  // namespace emm
