@@ -17,6 +17,7 @@ run c2-8192_1xtf32  tc1w            --only c2-8192 --maths 1xtf32
 run c2-8192_ffma    ffma            --only c2-8192 --maths ffma
 run c4-i_1xtf32     tc1w            --only c4-i    --maths 1xtf32
 run c2-4096_ffma    ffma            --only c2-4096 --maths ffma
+run c4-ii_1xtf32    tc1w            --only c4-ii   --maths 1xtf32
 run c4-i_3xtf32     tc_sgemm        --only c4-i    --maths 3xtf32
 run c4-i_pack       pack_split      --only c4-i    --maths 3xtf32
 run c4-ii_3xtf32    tc_sgemm        --only c4-ii   --maths 3xtf32
