@@ -88,6 +88,16 @@ cudaError_t launch_tc_sgemm(int terms, const TcOperands &ops, int64_t M, int64_t
 // and beta = 0, of an earlier call over a K prefix that ends on a 256-of-K
 // boundary) — together the calls add the same numbers in the same order as
 // one call over all of K (K-phased host pipeline).
+// Per-split launchers (k_tc_t{1,2,3}.cu, Kp = the padded K).
+#define EMM_TC_TERMS_DECL(T)                                                                                        \
+    cudaError_t launch_tc_terms##T(const TcOperands &ops, int64_t M, int64_t N, int64_t Kp, float alpha, float beta, \
+                                   float *C, int64_t ldc, unsigned int *ctrl, int splits, float *partial,             \
+                                   cudaStream_t s, const PeerOut &pe, void *sk_ws, const float *acc_init,             \
+                                   int64_t ld_init);
+EMM_TC_TERMS_DECL(1)
+EMM_TC_TERMS_DECL(2)
+EMM_TC_TERMS_DECL(3)
+#undef EMM_TC_TERMS_DECL
 // Fixed-order split-K reduce (KN8): C <- alpha * sum_s P_s + beta*C.
 cudaError_t launch_splitk_reduce(const float *partial, int splits, int64_t M, int64_t N, float alpha, float beta,
                                  float *C, int64_t ldc, cudaStream_t s);

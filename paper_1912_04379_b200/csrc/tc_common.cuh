@@ -58,6 +58,12 @@ struct TcCfg {
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
 
+// Per-call control block (zeroed by the pack launch, TC_CTRL_BYTES): word 0 =
+// wave-lockstep counter.  A lockstep wait longer than this many SM cycles
+// (~1 ms) means the grid is not fully resident: the CTA stops waiting.
+constexpr long long TC_LOCKSTEP_TIMEOUT = 2000000LL;
+constexpr int TC_SK_CHUNK = 256 / TC_BK;   // stream-K granularity: 8 stages = one promotion chunk
+
 // Work item kinds.
 enum { TW_FULL = 0,     // whole tile -> C (alpha/beta epilogue)
        TW_SPLITK = 1,   // split-K unit -> raw partial in slot (sp, tile) (fixed-order reduce launch, KN8)
@@ -292,14 +298,26 @@ __device__ __forceinline__ void tc_mma_loop(const TcSched &S, uint8_t *smem, uin
 
 // ===== epilogue: TMEM -> FP32 registers (promotion) -> alpha/beta -> C =====
 // Warp with TMEM lane quarter q (= warp % 4) and column half h.
-template <bool MC = false>
+// beta != 0 with a TMA-legal C (TMAC): C_in comes through TMA in chunks of
+// 128 rows x 16 columns into a 2-deep ring per column half (group of 4
+// warps); the first two chunks of a tile are requested while its last K
+// chunk is still in the tensor pipe.
+constexpr int TC_CB_COLS = 16, TC_CB_N = 2;
+constexpr int TC_CB_BYTES = 128 * TC_CB_COLS * 4;          // 8 KB
+constexpr int TC_CBUF_BYTES = 2 * TC_CB_N * TC_CB_BYTES;    // both halves: 32 KB
+struct TcCin {
+    const CUtensorMap *tm = nullptr;   // C as a 2-D tensor map, box {128 rows, 16 cols}
+    float *buf = nullptr;              // [2 halves][TC_CB_N][16][128]
+    uint64_t *full = nullptr;          // [2 halves][TC_CB_N]
+};
+template <bool MC = false, bool TMAC = false>
 __device__ __forceinline__ void tc_epilogue_loop(const TcSched &S, uint32_t rank, int q, int h, int lane,
                                                  uint32_t tmem_base, uint64_t *acc_full, uint64_t *acc_empty,
                                                  int kc_stages, int M, int N, float alpha, float beta,
                                                  float *__restrict__ C, int64_t ldc, float *__restrict__ partial,
                                                  const TcSk &sk, const PeerOut &peers, int cl = 2,
                                                  uint32_t leader = 0, const float *__restrict__ acc_init = nullptr,
-                                                 int64_t ld_init = 0) {
+                                                 int64_t ld_init = 0, const TcCin cin_tma = TcCin{}) {
     using namespace ptx;
     if (!MC) cl = 2, leader = 0;   // compile-time plain schedule
     uint32_t leader_empty0;   // the pair leader's acc_empty[0]
@@ -308,7 +326,11 @@ __device__ __forceinline__ void tc_epilogue_loop(const TcSched &S, uint32_t rank
                  : "r"(smem_u32(&acc_empty[0])), "r"(leader));
     // this warp's stream-K slot part / flag index (warp id within the CTA's 8)
     const int wslot = (int)rank * TC_EPI_WARPS + h * 4 + q;
-    int ch = 0;
+    int ch = 0, cph = 0;   // TMEM chunk counter, C_in chunk counter (TMAC ring phases)
+    const bool tmac = TMAC && beta != 0.0f;
+    const bool cleader = q == (TC_EPI_WARP0 & 3) && lane == 0;   // first warp of this column half
+    float *gbuf = TMAC ? cin_tma.buf + h * (TC_CB_N * TC_CB_BYTES / 4) : nullptr;
+    uint64_t *gfull = TMAC ? cin_tma.full + h * TC_CB_N : nullptr;
     const int n_it = tc_n_items(S, cl);
     for (int i = 0; i < n_it; ++i) {
         TcWork w;
@@ -331,8 +353,18 @@ __device__ __forceinline__ void tc_epilogue_loop(const TcSched &S, uint32_t rank
 #pragma unroll
             for (int j = 0; j < 128; ++j) acc[j] = 0.0f;
         }
+        const bool stores = !dummy && (w.kind == TW_FULL || w.kind == TW_OWN);
+        const int crow = m0 + (int)rank * TC_BM, ccol0 = n0 + h * 128;
+        auto cissue = [&](int c) {   // C_in chunk c of this item into ring slot c % TC_CB_N
+            const int bb = c % TC_CB_N;
+            mbar_arrive_expect_tx(&gfull[bb], TC_CB_BYTES);
+            tma_load_2d(smem_u32(gbuf + bb * (TC_CB_BYTES / 4)), cin_tma.tm, &gfull[bb], crow,
+                        ccol0 + TC_CB_COLS * c, policy_evict_first());
+        };
         for (int c2 = 0; c2 < nchunks; ++c2, ++ch) {
             const int b = ch & 1;
+            if (TMAC && tmac && stores && cleader && c2 == nchunks - 1)
+                for (int c = 0; c < TC_CB_N; ++c) cissue(c);
             mbar_wait(&acc_full[b], ((uint32_t)ch >> 1) & 1u);
             tc_fence_after();
             if (ch == 0 && q == 0 && h == 0 && lane == 0) EMM_TL(5);
@@ -410,11 +442,38 @@ __device__ __forceinline__ void tc_epilogue_loop(const TcSched &S, uint32_t rank
                 __stcg(slot + g * 32, make_float4(acc[4 * g], acc[4 * g + 1], acc[4 * g + 2], acc[4 * g + 3]));
             continue;
         }
+        if (TMAC && tmac) {
+            // the 4 warps of this column half walk the 8 C_in chunks together
+            const int col0 = n0 + h * 128;
+            float *cp = C + (int64_t)row + (int64_t)col0 * ldc;
+            const int jmax = min(128, N - col0);
+            const int rl = 32 * q + lane;
+#pragma unroll
+            for (int c = 0; c < 128 / TC_CB_COLS; ++c, ++cph) {
+                const int bb = c % TC_CB_N;
+                mbar_wait(&gfull[bb], (uint32_t)((cph / TC_CB_N) & 1));
+                const float *bp = gbuf + bb * (TC_CB_BYTES / 4) + rl;
+                float *sp2 = cp + (int64_t)(TC_CB_COLS * c) * ldc;
+#pragma unroll
+                for (int j = 0; j < TC_CB_COLS; ++j, sp2 += ldc) {
+                    const int jj = TC_CB_COLS * c + j;
+                    acc[jj] = fmaf(beta, bp[j * 128], alpha * acc[jj]);
+                    if (row < M && jj < jmax) __stcs(sp2, acc[jj]);
+                }
+                if (h == 0)
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
+                else
+                    asm volatile("bar.sync 2, 128;" ::: "memory");
+                if (cleader && c + TC_CB_N < 128 / TC_CB_COLS) cissue(c + TC_CB_N);
+            }
+        }
         if (row < M) {
             const int col0 = n0 + h * 128;
             float *cp = C + (int64_t)row + (int64_t)col0 * ldc;
             const int jmax = min(128, N - col0);
-            if (beta == 0.0f) {
+            if (TMAC && tmac) {
+                // stored above
+            } else if (beta == 0.0f) {
                 float *sp2 = cp;
 #pragma unroll
                 for (int j = 0; j < 128; ++j, sp2 += ldc) {

@@ -1,0 +1,54 @@
+"""beta != 0 epilogues that read C_in through TMA (KN1 3xTF32 / TF32+BF16,
+`EMM_TMAC`): the same fmaf(beta, c, alpha * acc) per entry as the per-thread
+load path, so the results must be bitwise identical (EMM_TMAC=1 vs 0) on any
+inputs — with stream-K owners, preferred clusters of 4, partial waves and
+ragged M / N; plus oracle parity on sampled rows."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from test_gpu_parity import TOL, Case, assert_close
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def emm():
+    from paper_1912_04379_b200 import build
+    build.build()
+    import paper_1912_04379_b200 as e
+    torch.cuda.set_device(0)
+    return e
+
+
+@pytest.fixture(autouse=True)
+def no_small_paths(monkeypatch):
+    monkeypatch.setenv("EMM_SMALL_FLOPS", "0")
+    monkeypatch.setenv("EMM_NO_SKINNY", "1")
+
+
+@pytest.mark.parametrize("math", ["3xtf32", "tf32bf16"])
+@pytest.mark.parametrize("shape,trans,env", [
+    ((8192, 2048, 1024), "NT", {}),                       # data-parallel, several waves
+    ((4096, 4096, 1024), "NN", {"EMM_SK": "1"}),          # stream-K owners add published partials first
+    ((3000, 2000, 700), "TT", {}),                        # split-K (reduce launch) + ragged edges
+    ((8192, 4096, 4096), "NN", {"EMM_PREF4": "1"}),       # preferred clusters of 4 (dummies in the last wave)
+    ((2820, 4100, 2049), "TN", {}),                       # ragged M / N (TMA clips the C boxes)
+], ids=lambda v: "x".join(map(str, v)) if isinstance(v, tuple) else (v if isinstance(v, str) else "-".join(v) or "default"))
+def test_tmac_bitwise(emm, monkeypatch, math, shape, trans, env):
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    M, N, K = shape
+    case = Case(trans[0], trans[1], M, N, K, -0.75, 1.25, kind="normal", sigma=1.0 / np.sqrt(K))
+    monkeypatch.setenv("EMM_TMAC", "1")
+    G1 = case.run(emm, math)
+    monkeypatch.setenv("EMM_TMAC", "0")
+    G0 = case.run(emm, math)
+    assert torch.equal(G1.view(torch.int32), G0.view(torch.int32)), "TMA-fed C_in epilogue differs"
+    case.check_untouched(G1)
+    rows = np.unique(np.r_[0:3, 127:130, M // 2:M // 2 + 2, M - 3:M])
+    R, S, T, st = case.oracle(rows=rows)
+    assert st == 0
+    assert_close(case, G1, R, S, T, TOL[math], rows=rows)
