@@ -52,3 +52,24 @@ def test_tmac_bitwise(emm, monkeypatch, math, shape, trans, env):
     R, S, T, st = case.oracle(rows=rows)
     assert st == 0
     assert_close(case, G1, R, S, T, TOL[math], rows=rows)
+
+
+def test_tmac_with_k_phases(emm, monkeypatch):
+    """Host-buffer entry in two K phases, the second phase continuing the
+    promotion chains (acc_init) with a TMA-fed C_in epilogue (aligned ldc):
+    bitwise equal to the device call."""
+    monkeypatch.setenv("EMM_HOST_KSPLIT", "1")
+    monkeypatch.setenv("EMM_SK", "0")
+    M, N, K = 4608, 4224, 1300
+    case = Case("N", "T", M, N, K, 1.25, 0.5, kind="normal", sigma=1.0 / np.sqrt(K))
+    assert (case.ldc * 4) % 16 == 0
+    Cf = case.Cflat.clone().pin_memory()
+    Af, Bf = case.flat(case.A).pin_memory(), case.flat(case.B).pin_memory()
+    emm.sgemm_host("N", "T", M, N, K, 1.25, Af, case.lda, Bf, case.ldb, 0.5, Cf, case.ldc)
+    case.check_untouched(Cf)
+    monkeypatch.setenv("EMM_FORCE_PACK", "1")
+    Cd = case.run(emm, "3xtf32")
+    assert torch.equal(Cd.view(torch.int32), Cf.view(torch.int32))
+    rows = np.array([0, 1, 2047, 2048, M - 1])
+    R, S, T, st = case.oracle(rows=rows)
+    assert_close(case, Cf, R, S, T, TOL["3xtf32"], rows=rows)
