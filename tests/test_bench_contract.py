@@ -1,0 +1,63 @@
+"""bench.py's JSON contract (no GPU): the committed final bench line carries
+every key the driver and the judge read, with sane types and values, and the
+reference arm (`--impl reference`, the oracle on the host cores) prints a
+well-formed line on a small size."""
+from __future__ import annotations
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+FINAL = os.path.join(ROOT, "profiles", "r01_bench_v12.jsonl")
+
+
+def last_line(path):
+    with open(path) as f:
+        return json.loads(f.read().strip().splitlines()[-1])
+
+
+def check_common(d):
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config"):
+        assert k in d, k
+    assert d["unit"] == "GFLOP/s" and d["higher_is_better"] is True and d["scaling"] in ("strong", "weak")
+    assert d["value"] > 0 and d["ms_per_step"] > 0 and d["steps"] >= 1
+    assert d["config"].get("workload")
+    assert d["vs_baseline"] is None   # BASELINE.md holds no published number for this metric/workload
+
+
+@pytest.mark.skipif(not os.path.exists(FINAL), reason="no committed bench line")
+def test_final_bench_line_has_the_contract():
+    d = last_line(FINAL)
+    check_common(d)
+    assert d["n_gpus"] == 1 and d["warmup"] >= 3 and d["dtype"] == "f32" and d["data"] == "synthetic"
+    assert "32768" in d["config"]["workload"]
+    r = d["roofline"]
+    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+        assert k in r, k
+    assert r["bound"] == "tensor" and r["unit"] == "TFLOP/s"
+    assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    assert r["traffic"] and r["traffic"] > 1e9
+    c = d["cpu_baseline"]
+    assert c["kind"] == "oracle" and c["cores"] >= 1 and c["value"] > 0 and c["sample"]
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] == 2 * 4 * 32768 ** 2 and e["d2h_bytes_per_step"] == 4 * 32768 ** 2
+    assert d["gpu_launches"] >= d["steps"]   # the library's own kernels ran inside the timed region
+    cl = d["clocks"]
+    assert cl["sm_mhz"] > 0 and cl["sm_max_mhz"] >= cl["sm_mhz"]
+    assert not set(cl["reasons"]) & {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+
+
+def test_reference_arm_small():
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--size", "512",
+                          "--steps", "1", "--warmup", "0"], capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = json.loads(out.stdout.strip().splitlines()[-1])
+    check_common(d)
+    assert d["impl"] == "reference"
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] == d["value"]
+    assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
