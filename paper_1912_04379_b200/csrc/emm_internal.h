@@ -22,7 +22,7 @@ extern std::atomic<uint64_t> g_launches;
 void prof_begin(cudaStream_t s, bool is_gemm, cudaEvent_t *ev0);
 void prof_end(cudaStream_t s, bool is_gemm, cudaEvent_t ev0);
 
-// ---- tensor-core path (k_tc.cu) -----------------------------------------
+// ---- tensor-core path (k_tc.cu host side, tc_kernel.cuh + k_tc_t{1,2,3}.cu kernels)
 // One plane of an operand as the GEMM reads it through TMA: logical R x kext
 // (rows x K).  mn = false: K-major, element (r, p) at ptr[p + r*ld];
 // mn = true: MN-major, element (r, p) at ptr[r + p*ld].

@@ -1,5 +1,7 @@
 // k_tc.cu — the tensor-core SGEMM path for sm_100a (KN1 3xTF32, KN2 1xTF32,
-// TF32+BF16) and its operand split pass (KN4).
+// TF32+BF16): its operand split pass (KN4), the split-K reduce (KN8), tensor
+// maps, schedules and the launch dispatch; the GEMM kernel itself is in
+// tc_kernel.cuh, compiled per split in k_tc_t{1,2,3}.cu.
 //
 // Paper → B200 mapping:
 //  * The operands are read IN PLACE by TMA whenever their leading dimension

@@ -239,7 +239,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TL_THREADS, 1)
         for (int i = 0; i < S.n_items; ++i) {
             const int w = i;   // no stream-K here: item i is wave i
             if (w > 0 && lockstep) {
-                // wave lockstep (see k_tc.cu): every producer warp of every CTA
+                // wave lockstep (see tc_kernel.cuh): every producer warp of every CTA
                 // finished loading wave w-1; bounded (~1 ms), then dropped
                 int stop = 0;
                 if (lane == 0) {

@@ -1,6 +1,7 @@
 // tc_common.cuh — pieces shared by the two tcgen05 GEMM kernels:
-//   * k_tc.cu  tc_sgemm_kernel      operands staged by TMA (planes prepared
-//                                   in global memory by the split pass)
+//   * tc_kernel.cuh (k_tc_t{1,2,3}.cu) tc_sgemm_kernel   operands staged by
+//                                   TMA (user arrays in place, or planes
+//                                   prepared by the split pass in k_tc.cu)
 //   * k_tcl.cu tc_split_sgemm_kernel operands loaded with LDG by producer
 //                                   warps that split them in registers
 //                                   (in-kernel 3xTF32 split)
