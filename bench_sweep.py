@@ -47,6 +47,54 @@ def configs():
     return out
 
 
+class NvmlSampler:
+    """SM clock, board power and throttle reasons polled every 2 ms while a
+    row's timed reps run (SURVEY.md §8(d) step 6); None without NVML.  NVML's
+    power reading is a trailing average, so rows shorter than ~1 s report
+    mostly the idle power before them; their clock is the burst clock (the
+    power limiter's time constant is longer than such rows)."""
+
+    def __init__(self, index):
+        self.index, self.samples, self.reasons, self.stop_flag, self.t = index, [], 0, False, None
+
+    def start(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+        except Exception:
+            return
+
+        rsn = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            getattr(pynvml, "nvmlDeviceGetCurrentClocksThrottleReasons", None)
+
+        def run():
+            while not self.stop_flag:
+                try:
+                    self.samples.append((pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+                                         pynvml.nvmlDeviceGetPowerUsage(h) / 1000.0))
+                    if rsn:
+                        self.reasons |= rsn(h)
+                except Exception:
+                    break
+                time.sleep(0.002)
+        import threading
+        self.t = threading.Thread(target=run, daemon=True)
+        self.t.start()
+
+    def stop(self):
+        if not self.t:
+            return None
+        self.stop_flag = True
+        self.t.join(timeout=1)
+        if not self.samples:
+            return None
+        names = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap"}
+        return {"sm_mhz": statistics.median(c for c, _ in self.samples),
+                "power_w": statistics.median(p for _, p in self.samples), "samples": len(self.samples),
+                "reasons": sorted(v for k, v in names.items() if self.reasons & k)}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=20)
@@ -99,6 +147,8 @@ def main():
             for _ in range(3):
                 call()
             ts = []
+            smp = NvmlSampler(dev.index or 0)
+            smp.start()
             for _ in range(args.reps):
                 flush.zero_()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -107,6 +157,7 @@ def main():
                 e1.record(stream)
                 e1.synchronize()
                 ts.append(e0.elapsed_time(e1))
+            clk = smp.stop()
             med = statistics.median(ts)
             b2b = None
             if M * N * K <= 1100 ** 3:
@@ -142,7 +193,7 @@ def main():
                    "median_ms": med, "min_ms": min(ts), "gflops": fl / med / 1e6,
                    "pct_roofline": 100.0 * fl / med / 1e9 / pk[math], "gbs": byt / med / 1e6,
                    "roofline_tflops": pk[math], "l2_flushed": True, "reps": args.reps, "cooldown_s": args.cooldown,
-                   "b2b_graph_us": b2b}
+                   "b2b_graph_us": b2b, "clocks": clk}
             print(json.dumps(rec), flush=True)
             lines.append(rec)
             del ws
