@@ -7,7 +7,9 @@ package ``paper_1912_04379_b200``.  It shares no code with the CUDA path.
 Parity pins (tests/test_oracle.py): brute force with exact rationals on tiny
 sizes, the (AB)^T = B^T A^T invariant, closed forms (identity, all-ones,
 alpha = 0, beta = 0 with NaN C, K = 0, K = 1), the worked 2x2 example
-(tests/golden/), a correctly-rounded fsum bound and float64 numpy matmul.
+(tests/golden/), a correctly-rounded fsum bound and float64 numpy matmul; the
+drop-in oracle_sgemm against exact float64 results rounded to float32 with
+ldc-padding sentinels.
 """
 from __future__ import annotations
 

@@ -349,3 +349,48 @@ def test_datagen_splitmix_matches_python_and_grid():
     assert I.min() == -8 and I.max() == 8
     Nn = datagen.matrix("normal", datagen.TAG_B, 4096, 16, sigma=0.5)
     assert abs(float(Nn.double().std()) - 0.5) < 0.01 and abs(float(Nn.double().mean())) < 0.01
+
+
+# --------------------------------------------------------------------------
+# the drop-in form oracle_sgemm (C <- (float)R through ldc)
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("tA,tB", [("N", "N"), ("N", "T"), ("T", "N"), ("T", "T")])
+@pytest.mark.parametrize("beta", [0.0, 1.25])
+def test_dropin_sgemm_exact_rounding_and_ldc_padding(tA, tB, beta):
+    """oracle_sgemm on a ragged shape with ldc padding: every logical entry
+    equals the float32 round-to-nearest of the exact result, computed here by
+    numpy float64 matmul on integer-valued inputs (every product and partial
+    sum is an integer < 2^53, so the float64 result is exact), while the
+    magnitudes (|entries| up to 4096, K = 19) put the results above 2^24 so the
+    float32 rounding is exercised.  ldc padding (a NaN-payload sentinel) is
+    never written; with beta = 0 a NaN-filled C is never read."""
+    rng = np.random.default_rng(31)
+    M, N, K = 37, 23, 19
+    alpha = -0.75
+    ar, ac = stored_shape(tA, M, K)
+    br, bc = stored_shape(tB, K, N)
+    lda, ldb, ldc = ar + 3, br + 2, M + 5
+    A = rng.integers(-4096, 4097, size=lda * ac).astype(np.float32)
+    B = rng.integers(-4096, 4097, size=ldb * bc).astype(np.float32)
+    sentinel = np.frombuffer(np.uint32(0x7FC0BEEF).tobytes(), dtype=np.float32)[0]
+    C = np.full(ldc * N, sentinel, dtype=np.float32)
+    cin = rng.integers(-(1 << 20), 1 << 20, size=(M, N)).astype(np.float32)
+    if beta != 0.0:
+        C.reshape(N, ldc)[:, :M] = cin.T
+    C0 = C.copy()
+    exact = alpha * (logical(A, tA, M, K, lda).astype(np.float64) @ logical(B, tB, K, N, ldb).astype(np.float64))
+    if beta != 0.0:
+        exact = exact + beta * cin.astype(np.float64)
+    assert np.all(np.abs(exact) < 2.0 ** 52) and np.max(np.abs(exact)) > 2.0 ** 24
+    assert oracle.sgemm(tA, tB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc) == 0
+    got = C.reshape(N, ldc)[:, :M].T
+    assert np.array_equal(got, exact.astype(np.float32))
+    pad = C.reshape(N, ldc)[:, M:]
+    assert np.array_equal(pad.view(np.uint32), C0.reshape(N, ldc)[:, M:].view(np.uint32))
+
+
+def test_dropin_sgemm_argument_error_leaves_C():
+    C = np.full(12, 3.0, np.float32)
+    assert oracle.sgemm("N", "N", 4, 3, 2, 1.0, np.ones(8, np.float32), 3, np.ones(6, np.float32), 2,
+                        0.0, C, 4) == -8
+    assert np.all(C == 3.0)
