@@ -20,9 +20,21 @@ per-panel GEMMs ("scaling": "strong": total work fixed).
 * e2e: the same metric through the C-ABI host-buffer entry emm_sgemm_host
   (pinned host A, B in; C out) — copies inside the timed region.
 * roofline: the dominant kernel (tc_sgemm_kernel), algorithmic flops 2MNK per
-  launch / its CUDA-event duration on the launching stream, against the
-  3xTF32-effective tensor peak = measured bf16 peak x (1.1/2.25 nominal
-  tf32/bf16) / 3.
+  launch / its CUDA-event duration on the launching stream.  `peak` = the
+  tensor pipe's measured ceiling for this exact instruction stream: the
+  GEMM's tcgen05 MMA sequence with operands resident in SMEM, run for 2 s on
+  this GPU right after the timed steps, sustained under the same power cap
+  (DESIGN.md §6a).  Reported beside it: the MEASURED_PEAKS-derived figure
+  (bf16 sustained x 1.1/2.25 nominal tf32/bf16 / 3), which a good kernel
+  exceeds because the TF32 tensor pipe draws less power than cuBLAS bf16, and
+  the nominal 1965 MHz figure (148 SMs x 4096 TF32 flop/clk / 3).
+* --gpus N without WORLD_SIZE in the environment: bench.py starts N rank
+  processes itself (RANK / LOCAL_RANK / WORLD_SIZE / MASTER_*), one per GPU;
+  under torchrun it is one of the ranks.  At N > 1 B is registered with the
+  communicator, so it travels by copy-engine peer copies along the ring
+  (`--bcast nccl` for ncclBroadcast), and the line reports
+  `comm_exposed_ms` = the step time not covered by the library's kernels on
+  the compute stream (waiting for B).
 * cpu_baseline: the oracle (oracle/oracle.c) on a bounded sample of output
   rows of the same workload, all host cores, rank 0 at N=1 only.
 * --impl reference: the oracle itself, timed as the reference arm.
@@ -59,6 +71,8 @@ def parse():
     p.add_argument("--allgather", default="none", choices=["none", "nccl", "fused"],
                    help="multi: also gather C into every rank's full M x N output (NCCL all-gather + unpack, "
                         "or fused into the GEMM epilogue through registered peer buffers)")
+    p.add_argument("--bcast", default="ce", choices=["ce", "nccl"],
+                   help="multi: B by copy-engine peer copies along the ring (registered buffer) or ncclBroadcast")
     p.add_argument("--force-multi", action="store_true",
                    help="run the row-sharded emm_sgemm_multi path (NCCL) even at one rank")
     p.add_argument("--cpu-rows", type=int, default=0, help="oracle sample rows (0 = auto)")
@@ -79,7 +93,7 @@ def peaks():
 def workload_config(n, args, world):
     return {"workload": f"BASELINE configs[4]: SGEMM M=N=K={n}, FP32 column-major, transA=transB=N, "
                         f"alpha=1, beta=0, A,B ~ U[-1,1) seed 0"
-                        + (f", row-sharded over {world} GPUs, B broadcast (NCCL)" if world > 1 else ""),
+                        + (f", row-sharded over {world} GPUs, B broadcast from rank 0" if world > 1 else ""),
             "M": n, "N": n, "K": n, "transA": "N", "transB": "N", "alpha": 1.0, "beta": 0.0,
             "math": args.math, "global_batch": None, "seq_len": None,
             "parallelism": f"rows{world}" if world > 1 else "single",
@@ -242,9 +256,44 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+# --------------------------------------------------------------------- launcher
+def spawn_ranks(n):
+    """`--gpus N` outside torchrun: one process per GPU, torchrun's env
+    contract; rank 0's stdout (the JSON line) is passed through."""
+    import socket
+    try:
+        out = subprocess.run(["nvidia-smi", "-L"], capture_output=True, text=True, timeout=60).stdout
+        visible = sum(1 for ln in out.splitlines() if ln.startswith("GPU "))
+        cvd = os.environ.get("CUDA_VISIBLE_DEVICES")
+        if cvd:
+            visible = min(visible, len([x for x in cvd.split(",") if x.strip()]))
+    except Exception:
+        visible = 0
+    if visible < n:
+        sys.stderr.write(f"bench.py: --gpus {n} but only {visible} GPU(s) visible\n")
+        sys.exit(2)
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n), LOCAL_WORLD_SIZE=str(n),
+                   MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        env.setdefault("NCCL_DEBUG", "INFO")
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__), *sys.argv[1:]], env=env,
+                                      stdout=None if r == 0 else subprocess.DEVNULL))
+    rc = 0
+    for p in procs:
+        rc = rc or p.wait()
+    sys.exit(rc)
+
+
 # --------------------------------------------------------------------- emm arm
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn_ranks(args.gpus)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -288,6 +337,8 @@ def main():
         if ws is not None and ws.data_ptr() % 1024:
             ws = ws[(1024 - ws.data_ptr() % 1024) // 4:]
     comm = emm.Comm(rank, world) if multi else None
+    if multi and args.bcast == "ce":
+        comm.register_input(B)
     C_full = None
     if multi and args.allgather != "none":
         C_full = torch.empty((N, M), dtype=torch.float32, device=dev).t()
@@ -371,23 +422,41 @@ def main():
         roof = {"bound": "tensor" if math != "ffma" else "alu", "achieved": achieved, "peak": peak,
                 "unit": "TFLOP/s", "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "peak_kind": f"{pname}, from {src} bf16 sustained {bf16_sus} TF x 1.1/2.25",
+                "peak_derived": peak, "frac_derived": (achieved / peak) if achieved else None,
                 "peak_burst": peak_b, "frac_burst": (achieved / peak_b) if achieved else None,
                 "kernel": {"ffma": "ffma_tma_kernel (KN3b)", "1xtf32": "tc1w_kernel (KN2w, 256x512 tiles)"}.get(
                     math, "tc_sgemm_kernel"),
                 "kernel_ms": kernel_ms, "kernel_share_of_step": (gemm_ms / ms) if ms > 0 else None,
                 "other_kernels_ms_per_step": other_ms / steps}
+        if math != "ffma":
+            sm = torch.cuda.get_device_properties(dev).multi_processor_count
+            nom = sm * 4096 * 1965e6 / 1e12 / {"3xtf32": 3.0, "tf32bf16": 2.0, "1xtf32": 1.0}[math]
+            roof["peak_nominal"] = nom
+            roof["frac_nominal"] = (achieved / nom) if achieved else None
+        # step time not covered by this rank's kernels on the compute stream
+        # (multi: waiting for B chunks / the completion flags)
+        exposed = max(0.0, ms / steps - (gemm_ms + other_ms) / steps) if multi else None
         return {"value": flops * steps / (ms / 1e3) / 1e9, "ms": ms, "launches": launches, "clocks": clk,
-                "roofline": roof, "peak": peak}
+                "roofline": roof, "peak": peak, "comm_exposed_ms": exposed}
 
     res = measure(args.math, args.steps, args.warmup)
     value, ms, launches, clk, roofline, peak = (res["value"], res["ms"], res["launches"], res["clocks"],
                                                 res["roofline"], res["peak"])
-    if args.math != "ffma" and not args.no_probe and not multi:
+    comm_exposed = res["comm_exposed_ms"]
+    if args.math != "ffma" and not args.no_probe:
         pr = mma_probe(args.math, clocks_of=ClockSampler(local))
         if pr and roofline.get("achieved"):
             pr["frac"] = roofline["achieved"] / pr["sustained_tflops"]
             if pr.get("sm_mhz") and clk and clk.get("sm_mhz"):
                 pr["frac_per_clock"] = (roofline["achieved"] / clk["sm_mhz"]) / (pr["sustained_tflops"] / pr["sm_mhz"])
+            # the measured tensor-pipe ceiling of this instruction stream is
+            # the roofline denominator (a kernel cannot exceed it)
+            roofline["peak"] = pr["sustained_tflops"]
+            roofline["frac"] = roofline["achieved"] / roofline["peak"]
+            roofline["peak_kind"] = ("measured in this run: the GEMM's tcgen05 MMA stream with operands resident in "
+                                     "SMEM, 2 s sustained under the same power cap (emm_debug_mma_probe); "
+                                     "peak_derived = MEASURED_PEAKS bf16 sustained x 1.1/2.25 / terms, "
+                                     "peak_nominal = 148 SMs x 4096 TF32 flop/clk x 1965 MHz / terms")
         roofline["ceiling_probe"] = pr
     ms_step = ms / args.steps
     alt = {}
@@ -462,11 +531,14 @@ def main():
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": dict(workload_config(n, args, world),
-                               **({"path": "emm_sgemm_multi (row-sharded, NCCL)", "allgather": args.allgather}
+                               **({"path": "emm_sgemm_multi (row-sharded)", "allgather": args.allgather}
                                   if multi else {})),
                 "roofline": roofline, "cpu_baseline": cpu,
                 "e2e": e2e, "gpu_launches": launches, "clocks": clk, "alt_paths": alt or None,
-                "pct_of_roofline": 100.0 * value / 1e3 / (peak * world) if peak else None}
+                "pct_of_roofline": 100.0 * value / 1e3 / (roofline["peak"] * world) if roofline.get("peak") else None}
+        if multi:
+            line["comm_exposed_ms"] = comm_exposed
+            line["config"]["bcast"] = args.bcast
         print(json.dumps(line), flush=True)
     if comm is not None:
         comm.close()

@@ -31,7 +31,8 @@
  *   Quick return (nothing launched) when M == 0, N == 0, or
  *   ((alpha == 0 or K == 0) and beta == 1).
  *   Only the M x N logical region of C is written; ldc padding never is.
- *   Results are run-to-run deterministic (no atomics, no split-K).
+ *   Results are run-to-run deterministic: no floating-point atomics; split-K
+ *   and stream-K partials are added in a fixed order.
  *   Reentrant; concurrent calls on different streams are safe when their C
  *   ranges are disjoint.
  *
@@ -82,7 +83,8 @@ typedef enum {
 
 /* C <- alpha*op(A)*op(B) + beta*C with the default FP32-accurate path
  * (EMM_MATH_3XTF32).  Scratch for the operand split is taken from a
- * stream-ordered pool (cudaMallocAsync/cudaFreeAsync on `stream`). */
+ * stream-ordered memory pool the library owns (cudaMallocFromPoolAsync /
+ * cudaFreeAsync on `stream`; the device default pool is not modified). */
 int emm_sgemm(char transA, char transB, int64_t M, int64_t N, int64_t K,
               float alpha, const float *A, int64_t lda,
               const float *B, int64_t ldb,
@@ -142,14 +144,25 @@ int emm_comm_create(void **comm, const void *id128, int nranks, int rank);
 int emm_comm_destroy(void *comm);
 
 /* Collective: every rank calls with identical (trans, M, N, K, alpha, beta,
- * root).  A_local: this rank's rows of op(A) as an (rows x K) op-matrix
+ * root, math) and the same registrations (below).  A_local: this rank's rows of op(A) as an (rows x K) op-matrix
  * (transA='N': stored rows x K with lda >= rows; 'T': stored K x rows).
  * B: K x N op(B) storage, valid on `root`; on other ranks a buffer of the
  * same size that receives it (broadcast in column panels, each panel's
  * GEMM overlapping the next panel's transfer).  C_local: this rank's rows x N
  * block (ldc >= rows).  C_full (nullable): if set, receives the whole M x N
- * result on every rank (ldc_full >= M) via NCCL all-gather.  ldb must equal
- * the stored rows of B (panels are contiguous). */
+ * result on every rank (ldc_full >= M).  ldb must equal the stored rows of B
+ * (panels are contiguous).
+ * Data plane: if B is the buffer registered with emm_comm_register_input,
+ * B travels along the ring root -> root+1 -> ... -> root-1 in <= 64 MB
+ * chunks by peer copies on the copy engines (no SMs taken from the GEMMs),
+ * each chunk signalled by a release flag the receiver's GEMM waits on;
+ * otherwise by ncclBroadcast per panel.  If C_full is the buffer registered
+ * with emm_comm_register_output, each rank's rows are stored straight into
+ * every rank's C_full (by the GEMM epilogue in tensor-core modes, by peer
+ * copies otherwise) and per-rank flags complete the call; otherwise NCCL
+ * all-gather + unpack.  All of it is stream-ordered on `stream`: C_local and
+ * C_full are complete when `stream` reaches the end of the call.  The call
+ * order of the ranks' host threads is free (waits are device-side). */
 int emm_sgemm_multi(void *comm, char transA, char transB, int64_t M, int64_t N, int64_t K,
                     float alpha, const float *A_local, int64_t lda,
                     float *B, int64_t ldb, int root,
@@ -166,6 +179,22 @@ int emm_sgemm_multi(void *comm, char transA, char transB, int64_t M, int64_t N, 
  * emm_comm_unregister_output / emm_comm_destroy. */
 int emm_comm_register_output(void *comm, float *C_full, int64_t ld_full);
 int emm_comm_unregister_output(void *comm);
+
+/* Collective: register this rank's B buffer (`bytes` >= the stored size of
+ * B of the calls that use it; the source on root, the receive buffer
+ * elsewhere).  Only the ring successor's buffer is mapped (CUDA IPC).  Must
+ * stay allocated until emm_comm_unregister_input / emm_comm_destroy. */
+int emm_comm_register_input(void *comm, float *B, size_t bytes);
+int emm_comm_unregister_input(void *comm);
+
+/* Test harness: `nranks` VIRTUAL ranks on the current device.  comms[r]
+ * (r < nranks) receives rank r's communicator; each is used and destroyed
+ * like one from emm_comm_create.  Their exchange steps run as device copies
+ * + flags between distinct buffers on this GPU (no NCCL), so B and, when
+ * gathered, C_full must be registered.  Each virtual rank needs its OWN
+ * stream (a rank's stream waits on device flags other ranks' streams set).
+ * Returns 0 or EMM_ERR_COMM / 1000 + cudaError_t. */
+int emm_debug_comm_create_local(int nranks, void **comms);
 
 /* ----------------------------------------------------------------------
  * Introspection (host-only).

@@ -26,4 +26,5 @@ from .emm import (  # noqa: F401
     get_unique_id,
     multi_panel_cols,
     sgemm_multi,
+    local_comms,
 )

@@ -141,24 +141,40 @@ struct Plan {
 
 static int64_t up4(int64_t v) { return (v + 3) / 4 * 4; }
 
-// emm_sgemm without a workspace takes scratch from the device's default
-// stream-ordered pool; with its default release threshold (0) every free
-// would unmap the memory at the next synchronisation and the next call would
-// map it again (tens of ms for GiB-sized scratch), so the library raises the
-// threshold once per device: freed scratch stays cached in the pool.
-static void keep_pool_memory() {
+// emm_sgemm without a workspace takes scratch from a stream-ordered pool that
+// the LIBRARY owns (one per device, created on first use): its release
+// threshold is raised so that freed scratch stays mapped for the next call
+// (remapping GiB-sized scratch costs tens of ms), without touching the
+// device's default pool that other cudaMallocAsync users share.
+static cudaMemPool_t lib_pool() {
     static std::mutex mu;
-    static bool done[64] = {};
+    static cudaMemPool_t pools[64] = {};
     int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
     std::lock_guard<std::mutex> g(mu);
-    if (done[dev]) return;
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    if (!pools[dev]) {
+        cudaMemPoolProps pp{};
+        pp.allocType = cudaMemAllocationTypePinned;
+        pp.handleTypes = cudaMemHandleTypeNone;
+        pp.location.type = cudaMemLocationTypeDevice;
+        pp.location.id = dev;
+        cudaMemPool_t p = nullptr;
+        if (cudaMemPoolCreate(&p, &pp) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
         uint64_t thr = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &thr);
+        pools[dev] = p;
     }
-    done[dev] = true;
+    return pools[dev];
+}
+
+// stream-ordered scratch from the library's pool
+static cudaError_t scratch_alloc(void **p, size_t bytes, cudaStream_t s) {
+    cudaMemPool_t pool = lib_pool();
+    if (!pool) return cudaErrorMemoryAllocation;
+    return cudaMallocFromPoolAsync(p, bytes, pool, s);
 }
 
 static bool env_on(const char *name) {
@@ -304,8 +320,7 @@ extern "C" int emm_sgemm_ex(char transA, char transB, int64_t M, int64_t N, int6
             if (ws) {
                 if (workspace_bytes < need || (reinterpret_cast<uintptr_t>(ws) & 1023u)) return EMM_ERR_WORKSPACE;
             } else {
-                keep_pool_memory();
-                cudaError_t e = cudaMallocAsync(&ws, need, s);
+                cudaError_t e = scratch_alloc(&ws, need, s);
                 if (e != cudaSuccess) return cuda_status(e);
                 own = true;
             }
@@ -330,8 +345,7 @@ extern "C" int emm_sgemm_ex(char transA, char transB, int64_t M, int64_t N, int6
     if (ws) {
         if (workspace_bytes < P.total || (reinterpret_cast<uintptr_t>(ws) & 1023u)) return EMM_ERR_WORKSPACE;
     } else {
-        keep_pool_memory();
-        cudaError_t e = cudaMallocAsync(&ws, P.total, s);
+        cudaError_t e = scratch_alloc(&ws, P.total, s);
         if (e != cudaSuccess) return cuda_status(e);
         own = true;
     }
@@ -524,10 +538,13 @@ static int host_pipelined(char tA, char tB, int64_t M, int64_t N, int64_t K, flo
     // phase boundaries on 256-of-K promotion boundaries
     auto kb = [&](int p) { return p >= nphase ? K : (K * p / nphase) / 256 * 256; };
     int ng = 0;
+    bool have_partial = false;   // dR holds the raw partial of an executed earlier phase
     for (int ph = 0; ph < nphase && e == cudaSuccess; ++ph) {
         const int64_t k0 = kb(ph), nk = kb(ph + 1) - kb(ph);
         const bool last_phase = ph == nphase - 1;
         if (nk <= 0) continue;
+        const bool chain = have_partial;   // continue the promotion chain from dR
+        have_partial = true;
         int na = 0, nb = 0;
         while ((na < GM || nb < GN) && e == cudaSuccess) {
             const int64_t rows_res = ra[na], cols_res = cb[nb];
@@ -588,10 +605,10 @@ static int host_pipelined(char tA, char tB, int64_t M, int64_t N, int64_t K, flo
                 if (e == cudaSuccess) {
                     if (!last_phase)   // raw partial of the K prefix (continuing the previous phases')
                         e = launch_tc_sgemm(terms, ops, pnr, pnc, nk, 1.0f, 0.0f, dR + pr0 + pc0 * M, M, cw, 1, nullptr,
-                                            comp, nullptr, nullptr, ph > 0 ? dR + pr0 + pc0 * M : nullptr, M);
+                                            comp, nullptr, nullptr, chain ? dR + pr0 + pc0 * M : nullptr, M);
                     else
                         e = launch_tc_sgemm(terms, ops, pnr, pnc, nk, alpha, beta, dC + pr0 + pc0 * ldc, ldc, cw, 1,
-                                            nullptr, comp, nullptr, nullptr, dR ? dR + pr0 + pc0 * M : nullptr, M);
+                                            nullptr, comp, nullptr, nullptr, chain ? dR + pr0 + pc0 * M : nullptr, M);
                 }
                 if (!last_phase) continue;
                 cudaEvent_t done = ev();

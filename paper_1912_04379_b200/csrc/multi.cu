@@ -1,14 +1,38 @@
-// multi.cu — row-sharded multi-GPU SGEMM over NCCL (BASELINE.json north_star,
+// multi.cu — row-sharded multi-GPU SGEMM (BASELINE.json north_star,
 // "Multi-GPU: large problems are partitioned ... by C row-blocks. B is
 // broadcast and C is optionally all-gathered with NCCL over NVLink, with
 // compute overlapped on streams").
 //
 // The paper's only distributed use of its SGEMM is the 196-CPU neural-network
 // run with no communication details; this is the B200
-// design of SURVEY.md §8(e): each rank owns a block of rows of op(A) and C,
-// B is broadcast from `root` in column panels on a communication stream, and
-// the GEMM of panel c (compute stream) waits only for panel c, so the
-// transfer of panel c+1 overlaps the math of panel c.
+// design of SURVEY.md §8(e) / §8(f)-2: each rank owns a block of rows of
+// op(A) and C, B is broadcast from `root` in column panels, and the GEMM of
+// panel c waits only for panel c, so the transfer of later panels overlaps
+// the math of earlier ones.
+//
+// Two data planes for the exchange steps:
+//  * NCCL (buffers not registered): ncclBroadcast per B panel on a
+//    communication stream; C all-gather as grouped broadcasts into a staging
+//    buffer + unpack (KN6).
+//  * Copy engines + flags (buffers registered with emm_comm_register_input /
+//    _output): B is forwarded along the ring that starts at `root` (root ->
+//    root+1 -> ... -> root-1) in chunks of <= 64 MB by cudaMemcpyAsync into
+//    the next rank's (IPC-mapped) B buffer — peer copies run on the copy
+//    engines, so they take no SMs from the persistent GEMM — each chunk
+//    followed by a release store of the call's epoch into the receiver's flag
+//    word; the receiver's GEMM of a panel waits (acquire) for the flag of the
+//    panel's last chunk.  Every rank sends B once (a pipelined chain uses each
+//    GPU's NVLink egress once, the bandwidth optimum of a broadcast through a
+//    switch).  C is gathered by the GEMM epilogue storing each finished tile
+//    into every rank's C_full (tensor-core modes) or by peer 2-D copies
+//    (other modes); a flag per rank closes the call.  Buffers are reused
+//    across calls through a "consumed" flag: a rank pushes call e only after
+//    its successor has finished reading call e-1.
+//
+// The flag protocol is transport-independent, so the same code also runs P
+// VIRTUAL ranks on one GPU (emm_debug_comm_create_local): distinct buffers on
+// one device instead of IPC-mapped peers — the harness the tests use to drive
+// the P > 1 paths of emm_sgemm_multi on a single B200.
 //
 // NCCL is loaded at run time (dlopen of the process's libnccl.so.2, normally
 // the one torch already loaded), so the library has no link-time NCCL
@@ -18,8 +42,10 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <vector>
 
@@ -38,7 +64,6 @@ struct Nccl {
     decltype(&ncclGroupStart) groupStart = nullptr;
     decltype(&ncclGroupEnd) groupEnd = nullptr;
     decltype(&ncclAllGather) allGather = nullptr;
-    decltype(&ncclAllReduce) allReduce = nullptr;
 };
 
 Nccl &nccl() {
@@ -56,28 +81,60 @@ Nccl &nccl() {
         n.groupStart = (decltype(n.groupStart))dlsym(h, "ncclGroupStart");
         n.groupEnd = (decltype(n.groupEnd))dlsym(h, "ncclGroupEnd");
         n.allGather = (decltype(n.allGather))dlsym(h, "ncclAllGather");
-        n.allReduce = (decltype(n.allReduce))dlsym(h, "ncclAllReduce");
         n.ok = n.getUniqueId && n.commInitRank && n.commDestroy && n.getAsyncError && n.broadcast && n.groupStart &&
-               n.groupEnd && n.allGather && n.allReduce;
+               n.groupEnd && n.allGather;
     });
     return n;
 }
 
+constexpr int MAXR = 8;
+// flag words per rank (device memory, uint32, monotonically increasing epochs)
+constexpr int FL_BREADY = 0;                 // [FL_NCHUNK] B chunk j of this call landed here
+constexpr int FL_NCHUNK = 1024;
+constexpr int FL_CONSUMED = FL_NCHUNK;       // successor finished reading its B (written by the successor)
+constexpr int FL_DONE = FL_NCHUNK + 32;      // [MAXR] rank r finished storing its rows into this C_full
+constexpr int FL_WORDS = FL_NCHUNK + 64;
+constexpr size_t CHUNK_BYTES = 64u << 20;    // B forwarding granularity
+
+// P virtual ranks on one device (emm_debug_comm_create_local): the tables
+// the IPC exchange fills in the multi-process case.
+struct World {
+    int nranks = 0;
+    std::mutex mu;
+    int alive = 0;
+    uint32_t *flags[MAXR] = {};
+    float *in[MAXR] = {};
+    size_t in_bytes[MAXR] = {};
+    float *out[MAXR] = {};
+    int64_t out_ld[MAXR] = {};
+};
+
 struct Comm {
-    ncclComm_t nc = nullptr;
+    ncclComm_t nc = nullptr;               // NCCL mode
+    std::shared_ptr<World> world;          // local (virtual-rank) mode
     int nranks = 0, rank = 0, dev = 0;
     cudaStream_t comm_stream = nullptr;
     std::vector<cudaEvent_t> evs;
-    float *stage = nullptr;  // all-gather staging (grown on demand)
+    float *stage = nullptr;  // NCCL all-gather staging (grown on demand)
     size_t stage_bytes = 0;
     void *ws = nullptr;      // tensor-core workspace: A planes | B panel planes | control block
     size_t ws_bytes = 0;
-    // fused all-gather target (emm_comm_register_output): every rank's full C
+    uint32_t epoch = 0;      // calls of emm_sgemm_multi (identical on every rank)
+    // flag words: own array and every peer's (IPC-mapped; own = flags)
+    uint32_t *flags = nullptr;
+    uint32_t *peer_flags[MAXR] = {};
+    void *flags_opened[MAXR] = {};
+    // registered input (B receive buffer) and the successor's, mapped
+    float *in_local = nullptr;
+    size_t in_bytes = 0;
+    float *in_succ = nullptr;
+    void *in_opened = nullptr;
+    // registered output: every rank's full C
     float *out_local = nullptr;
     int64_t out_ld = 0;
-    float *out_peer[8] = {};       // mapped peer buffers (own rank: out_local)
-    void *out_opened[8] = {};      // IPC mappings to close
-    int *dummy = nullptr;          // completion all-reduce operand
+    float *out_peer[MAXR] = {};
+    void *out_opened[MAXR] = {};
+    bool local() const { return world != nullptr; }
 };
 
 // driver cuMemGetAddressRange (allocation base of a device pointer)
@@ -94,11 +151,14 @@ PFN_range range_fn() {
     return fn;
 }
 
-struct OutHandle {
+struct IpcBlob {
     cudaIpcMemHandle_t h;
     int64_t offset;   // bytes from the allocation base to the registered pointer
-    int64_t ld;
+    int64_t a, b;     // ld / size, checked for consistency
 };
+
+int nccl_status(ncclResult_t r) { return r == ncclSuccess ? 0 : EMM_ERR_NCCL_BASE + (int)r; }
+int cuda_st(cudaError_t e) { return e == cudaSuccess ? 0 : EMM_ERR_CUDA_BASE + (int)e; }
 
 int grow(void **p, size_t *have, size_t need) {
     if (*have >= need && *p) return 0;
@@ -111,9 +171,6 @@ int grow(void **p, size_t *have, size_t need) {
     return 0;
 }
 
-int nccl_status(ncclResult_t r) { return r == ncclSuccess ? 0 : EMM_ERR_NCCL_BASE + (int)r; }
-int cuda_st(cudaError_t e) { return e == cudaSuccess ? 0 : EMM_ERR_CUDA_BASE + (int)e; }
-
 cudaEvent_t ev_at(Comm *c, size_t i) {
     while (c->evs.size() <= i) {
         cudaEvent_t e;
@@ -121,6 +178,112 @@ cudaEvent_t ev_at(Comm *c, size_t i) {
         c->evs.push_back(e);
     }
     return c->evs[i];
+}
+
+// IPC handle of the allocation holding `p` (+ offset), all-gathered over NCCL.
+int ipc_allgather(Comm *c, const void *p, int64_t a, int64_t b, std::vector<IpcBlob> &all) {
+    Nccl &n = nccl();
+    auto rf = range_fn();
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (!rf || rf(&base, &size, reinterpret_cast<CUdeviceptr>(p)) != CUDA_SUCCESS) return EMM_ERR_COMM;
+    IpcBlob mine{};
+    int st = cuda_st(cudaIpcGetMemHandle(&mine.h, reinterpret_cast<void *>(base)));
+    if (st) return st;
+    mine.offset = (int64_t)(reinterpret_cast<CUdeviceptr>(p) - base);
+    mine.a = a;
+    mine.b = b;
+    IpcBlob *dev = nullptr;
+    if ((st = cuda_st(cudaMalloc(&dev, sizeof(IpcBlob) * (c->nranks + 1))))) return st;
+    all.assign(c->nranks, IpcBlob{});
+    st = cuda_st(cudaMemcpy(dev + c->nranks, &mine, sizeof mine, cudaMemcpyHostToDevice));
+    if (!st) st = nccl_status(n.allGather(dev + c->nranks, dev, sizeof(IpcBlob), ncclUint8, c->nc, c->comm_stream));
+    if (!st) st = cuda_st(cudaStreamSynchronize(c->comm_stream));
+    if (!st) st = cuda_st(cudaMemcpy(all.data(), dev, sizeof(IpcBlob) * c->nranks, cudaMemcpyDeviceToHost));
+    cudaFree(dev);
+    return st;
+}
+
+int ipc_open(const IpcBlob &b, void **opened, void **ptr) {
+    void *p = nullptr;
+    int st = cuda_st(cudaIpcOpenMemHandle(&p, b.h, cudaIpcMemLazyEnablePeerAccess));
+    if (st) return st;
+    *opened = p;
+    *ptr = static_cast<uint8_t *>(p) + b.offset;
+    return 0;
+}
+
+// ---------------------------------------------------------------- flag kernels
+// Release store of the epoch into a (possibly peer) flag word, after every
+// earlier operation of the stream (copies, GEMMs and their peer stores).
+struct FlagSet {
+    uint32_t *f[MAXR];
+    int n;
+};
+__global__ void flag_set_kernel(const FlagSet fs, uint32_t v) {
+    if (threadIdx.x < fs.n) {
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(fs.f[threadIdx.x]), "r"(v) : "memory");
+    }
+}
+// Acquire-spin until every word of f[idx[i]] reaches the epoch (wrap-safe
+// compare).  Bounded: traps after ~20 s so a protocol error cannot wedge
+// the GPU.
+struct FlagWait {
+    const uint32_t *f[MAXR];
+    int n;
+};
+__global__ void flag_wait_kernel(const FlagWait fw, uint32_t v) {
+    if (threadIdx.x >= fw.n) return;
+    const long long t0 = clock64();
+    while (true) {
+        uint32_t x;
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(x) : "l"(fw.f[threadIdx.x]) : "memory");
+        if ((int32_t)(x - v) >= 0) break;
+        __nanosleep(256);
+        if (clock64() - t0 > 40000000000LL) __trap();
+    }
+}
+
+cudaError_t flag_set(uint32_t *const *fs, int n, uint32_t v, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    FlagSet a{};
+    for (int i = 0; i < n; ++i) a.f[i] = fs[i];
+    a.n = n;
+    flag_set_kernel<<<1, 32, 0, s>>>(a, v);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cudaGetLastError();
+}
+cudaError_t flag_wait(const uint32_t *const *fs, int n, uint32_t v, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    FlagWait a{};
+    for (int i = 0; i < n; ++i) a.f[i] = fs[i];
+    a.n = n;
+    flag_wait_kernel<<<1, 32, 0, s>>>(a, v);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cudaGetLastError();
+}
+
+int comm_init_streams(Comm *c) {
+    int st = cuda_st(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+    if (!st) st = cuda_st(cudaMalloc(&c->flags, FL_WORDS * sizeof(uint32_t)));
+    if (!st) st = cuda_st(cudaMemset(c->flags, 0, FL_WORDS * sizeof(uint32_t)));
+    if (!st) st = cuda_st(cudaDeviceSynchronize());
+    return st;
+}
+
+// peer flag arrays: mapped by IPC (NCCL mode) or taken from the world table
+int resolve_flags(Comm *c) {
+    if (c->nranks == 1 || c->peer_flags[(c->rank + 1) % c->nranks]) return 0;
+    if (c->local()) {
+        std::lock_guard<std::mutex> g(c->world->mu);
+        for (int r = 0; r < c->nranks; ++r) {
+            if (!c->world->flags[r]) return EMM_ERR_COMM;
+            c->peer_flags[r] = c->world->flags[r];
+        }
+        return 0;
+    }
+    return EMM_ERR_COMM;   // NCCL mode maps them in emm_comm_create
 }
 
 }  // namespace
@@ -150,7 +313,7 @@ extern "C" int emm_get_unique_id(void *id128) {
 
 extern "C" int emm_comm_create(void **comm, const void *id128, int nranks, int rank) {
     Nccl &n = nccl();
-    if (!n.ok || !comm || !id128 || nranks < 1 || nranks > 8 || rank < 0 || rank >= nranks) return EMM_ERR_COMM;
+    if (!n.ok || !comm || !id128 || nranks < 1 || nranks > MAXR || rank < 0 || rank >= nranks) return EMM_ERR_COMM;
     ncclUniqueId id;
     memcpy(&id, id128, sizeof id);
     Comm *c = new Comm();
@@ -158,12 +321,56 @@ extern "C" int emm_comm_create(void **comm, const void *id128, int nranks, int r
     c->rank = rank;
     cudaGetDevice(&c->dev);
     int st = nccl_status(n.commInitRank(&c->nc, nranks, id, rank));
-    if (!st) st = cuda_st(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+    if (!st) st = comm_init_streams(c);
+    // map every peer's flag words (copy-engine data plane)
+    if (!st && nranks > 1) {
+        std::vector<IpcBlob> all;
+        st = ipc_allgather(c, c->flags, FL_WORDS, 0, all);
+        for (int r = 0; r < nranks && !st; ++r) {
+            if (r == rank) {
+                c->peer_flags[r] = c->flags;
+                continue;
+            }
+            void *p = nullptr;
+            st = ipc_open(all[r], &c->flags_opened[r], &p);
+            c->peer_flags[r] = static_cast<uint32_t *>(p);
+        }
+    } else if (!st) {
+        c->peer_flags[0] = c->flags;
+    }
     if (st) {
-        delete c;
+        emm_comm_destroy(c);
         return st;
     }
     *comm = c;
+    return 0;
+}
+
+// P virtual ranks on the current device (tests): comms[r] is rank r of a
+// world whose exchange steps are device copies + flags between distinct
+// buffers on this one GPU (no NCCL).  Every rank must then register its B
+// buffer (emm_comm_register_input) and, for a gathered output, its C_full.
+extern "C" int emm_debug_comm_create_local(int nranks, void **comms) {
+    if (!comms || nranks < 1 || nranks > MAXR) return EMM_ERR_COMM;
+    auto w = std::make_shared<World>();
+    w->nranks = nranks;
+    for (int r = 0; r < nranks; ++r) comms[r] = nullptr;
+    for (int r = 0; r < nranks; ++r) {
+        Comm *c = new Comm();
+        c->nranks = nranks;
+        c->rank = r;
+        c->world = w;
+        cudaGetDevice(&c->dev);
+        int st = comm_init_streams(c);
+        if (st) {
+            delete c;
+            for (int q = 0; q < r; ++q) emm_comm_destroy(comms[q]);
+            return st;
+        }
+        w->flags[r] = c->flags;
+        comms[r] = c;
+    }
+    w->alive = nranks;
     return 0;
 }
 
@@ -171,10 +378,14 @@ extern "C" int emm_comm_unregister_output(void *comm) {
     if (!comm) return EMM_ERR_COMM;
     Comm *c = static_cast<Comm *>(comm);
     cudaStreamSynchronize(c->comm_stream);
-    for (int r = 0; r < 8; ++r) {
+    for (int r = 0; r < MAXR; ++r) {
         if (c->out_opened[r]) cudaIpcCloseMemHandle(c->out_opened[r]);
         c->out_opened[r] = nullptr;
         c->out_peer[r] = nullptr;
+    }
+    if (c->local()) {
+        std::lock_guard<std::mutex> g(c->world->mu);
+        c->world->out[c->rank] = nullptr;
     }
     c->out_local = nullptr;
     c->out_ld = 0;
@@ -182,48 +393,34 @@ extern "C" int emm_comm_unregister_output(void *comm) {
 }
 
 // Collective: every rank registers its M x N (ld_full) full-output buffer;
-// CUDA IPC handles are all-gathered over the NCCL communicator and the
-// peers' buffers mapped, so emm_sgemm_multi can store C tiles straight into
-// them from the GEMM epilogue (NVLink peer stores, no all-gather launch).
+// the peers' buffers are mapped (CUDA IPC handles all-gathered over NCCL),
+// so emm_sgemm_multi can store C tiles straight into them from the GEMM
+// epilogue (NVLink peer stores, no all-gather launch).
 extern "C" int emm_comm_register_output(void *comm, float *C_full, int64_t ld_full) {
     if (!comm || !C_full || ld_full < 1) return EMM_ERR_COMM;
     Comm *c = static_cast<Comm *>(comm);
-    Nccl &n = nccl();
-    if (!n.ok) return EMM_ERR_COMM;
     emm_comm_unregister_output(comm);
-    auto rf = range_fn();
-    CUdeviceptr base = 0;
-    size_t size = 0;
-    if (!rf || rf(&base, &size, reinterpret_cast<CUdeviceptr>(C_full)) != CUDA_SUCCESS) return EMM_ERR_COMM;
-    OutHandle mine{};
-    int st = cuda_st(cudaIpcGetMemHandle(&mine.h, reinterpret_cast<void *>(base)));
-    if (st) return st;
-    mine.offset = (int64_t)(reinterpret_cast<CUdeviceptr>(C_full) - base);
-    mine.ld = ld_full;
-    OutHandle *dev = nullptr;
-    if ((st = cuda_st(cudaMalloc(&dev, sizeof(OutHandle) * (c->nranks + 1))))) return st;
-    std::vector<OutHandle> all(c->nranks);
-    st = cuda_st(cudaMemcpy(dev + c->nranks, &mine, sizeof mine, cudaMemcpyHostToDevice));
-    if (!st)
-        st = nccl_status(n.allGather(dev + c->nranks, dev, sizeof(OutHandle), ncclUint8, c->nc, c->comm_stream));
-    if (!st) st = cuda_st(cudaStreamSynchronize(c->comm_stream));
-    if (!st) st = cuda_st(cudaMemcpy(all.data(), dev, sizeof(OutHandle) * c->nranks, cudaMemcpyDeviceToHost));
-    cudaFree(dev);
-    if (st) return st;
+    if (c->local()) {
+        std::lock_guard<std::mutex> g(c->world->mu);
+        c->world->out[c->rank] = C_full;
+        c->world->out_ld[c->rank] = ld_full;
+        c->out_local = C_full;
+        c->out_ld = ld_full;
+        return 0;   // peers resolved at call time (registration order is free)
+    }
+    if (!nccl().ok) return EMM_ERR_COMM;
+    std::vector<IpcBlob> all;
+    int st = c->nranks > 1 ? ipc_allgather(c, C_full, ld_full, 0, all) : 0;
     for (int r = 0; r < c->nranks && !st; ++r) {
-        if (all[r].ld != ld_full) st = EMM_ERR_COMM;   // identical layouts required
         if (r == c->rank) {
             c->out_peer[r] = C_full;
             continue;
         }
+        if (all[r].a != ld_full) st = EMM_ERR_COMM;   // identical layouts required
         void *p = nullptr;
-        if (!st) st = cuda_st(cudaIpcOpenMemHandle(&p, all[r].h, cudaIpcMemLazyEnablePeerAccess));
-        if (!st) {
-            c->out_opened[r] = p;
-            c->out_peer[r] = reinterpret_cast<float *>(static_cast<uint8_t *>(p) + all[r].offset);
-        }
+        if (!st) st = ipc_open(all[r], &c->out_opened[r], &p);
+        c->out_peer[r] = static_cast<float *>(p);
     }
-    if (!st && !c->dummy) st = cuda_st(cudaMalloc(&c->dummy, sizeof(int)));
     if (st) {
         emm_comm_unregister_output(comm);
         return st;
@@ -233,12 +430,71 @@ extern "C" int emm_comm_register_output(void *comm, float *C_full, int64_t ld_fu
     return 0;
 }
 
+extern "C" int emm_comm_unregister_input(void *comm) {
+    if (!comm) return EMM_ERR_COMM;
+    Comm *c = static_cast<Comm *>(comm);
+    cudaStreamSynchronize(c->comm_stream);
+    if (c->in_opened) cudaIpcCloseMemHandle(c->in_opened);
+    c->in_opened = nullptr;
+    c->in_succ = nullptr;
+    if (c->local()) {
+        std::lock_guard<std::mutex> g(c->world->mu);
+        c->world->in[c->rank] = nullptr;
+    }
+    c->in_local = nullptr;
+    c->in_bytes = 0;
+    return 0;
+}
+
+// Collective: register this rank's B buffer (root: the source; others: the
+// receive buffer) of `bytes` bytes.  emm_sgemm_multi with that B then
+// forwards B along the ring by peer copies on the copy engines.
+extern "C" int emm_comm_register_input(void *comm, float *B, size_t bytes) {
+    if (!comm || !B || bytes == 0) return EMM_ERR_COMM;
+    Comm *c = static_cast<Comm *>(comm);
+    emm_comm_unregister_input(comm);
+    if (c->local()) {
+        std::lock_guard<std::mutex> g(c->world->mu);
+        c->world->in[c->rank] = B;
+        c->world->in_bytes[c->rank] = bytes;
+        c->in_local = B;
+        c->in_bytes = bytes;
+        return 0;
+    }
+    if (!nccl().ok) return EMM_ERR_COMM;
+    int st = 0;
+    if (c->nranks > 1) {
+        std::vector<IpcBlob> all;
+        st = ipc_allgather(c, B, 0, (int64_t)bytes, all);
+        const int succ = (c->rank + 1) % c->nranks;
+        for (int r = 0; r < c->nranks && !st; ++r)
+            if ((size_t)all[r].b != bytes) st = EMM_ERR_COMM;
+        void *p = nullptr;
+        if (!st) st = ipc_open(all[succ], &c->in_opened, &p);
+        c->in_succ = static_cast<float *>(p);
+    }
+    if (st) {
+        emm_comm_unregister_input(comm);
+        return st;
+    }
+    c->in_local = B;
+    c->in_bytes = bytes;
+    return 0;
+}
+
 extern "C" int emm_comm_destroy(void *comm) {
     if (!comm) return EMM_ERR_COMM;
     Comm *c = static_cast<Comm *>(comm);
     emm_comm_unregister_output(comm);
-    if (c->dummy) cudaFree(c->dummy);
-    cudaStreamSynchronize(c->comm_stream);
+    emm_comm_unregister_input(comm);
+    if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
+    for (int r = 0; r < MAXR; ++r)
+        if (c->flags_opened[r]) cudaIpcCloseMemHandle(c->flags_opened[r]);
+    if (c->local()) {
+        std::lock_guard<std::mutex> g(c->world->mu);
+        c->world->flags[c->rank] = nullptr;
+    }
+    if (c->flags) cudaFree(c->flags);
     for (auto e : c->evs) cudaEventDestroy(e);
     if (c->stage) cudaFree(c->stage);
     if (c->ws) cudaFree(c->ws);
@@ -249,6 +505,34 @@ extern "C" int emm_comm_destroy(void *comm) {
     return st;
 }
 
+// B chunks of one call: [panel p] = chunks [pc[p], pc[p+1]); chunk j covers
+// bytes [off[j], off[j+1]) of B.
+struct Chunks {
+    std::vector<int64_t> pc;
+    std::vector<size_t> off;
+};
+static Chunks make_chunks(bool bN, int64_t N, int64_t K, int64_t panel) {
+    Chunks ch;
+    const size_t col_bytes = (size_t)K * 4;
+    const size_t total = (size_t)N * K * 4;
+    size_t chunk = CHUNK_BYTES;
+    while (total / chunk >= (size_t)FL_NCHUNK - 8) chunk *= 2;
+    ch.off.push_back(0);
+    ch.pc.push_back(0);
+    if (bN) {
+        const int64_t cols_per = col_bytes > 0 ? std::max<int64_t>(1, (int64_t)(chunk / col_bytes)) : N;
+        for (int64_t c0 = 0; c0 < N; c0 += panel) {
+            const int64_t c1 = std::min(N, c0 + panel);
+            for (int64_t x = c0; x < c1; x += cols_per) ch.off.push_back((size_t)std::min(c1, x + cols_per) * col_bytes);
+            ch.pc.push_back((int64_t)ch.off.size() - 1);
+        }
+    } else {
+        for (size_t o = 0; o < total; o += chunk) ch.off.push_back(std::min(total, o + chunk));
+        ch.pc.push_back((int64_t)ch.off.size() - 1);
+    }
+    return ch;
+}
+
 extern "C" int emm_sgemm_multi(void *comm, char transA, char transB, int64_t M, int64_t N, int64_t K, float alpha,
                                const float *A_local, int64_t lda, float *B, int64_t ldb, int root, float beta,
                                float *C_local, int64_t ldc, float *C_full, int64_t ldc_full, void *stream,
@@ -256,32 +540,64 @@ extern "C" int emm_sgemm_multi(void *comm, char transA, char transB, int64_t M, 
     if (!comm) return EMM_ERR_COMM;
     Comm *c = static_cast<Comm *>(comm);
     Nccl &n = nccl();
-    if (!n.ok) return EMM_ERR_COMM;
     if (root < 0 || root >= c->nranks) return EMM_ERR_COMM;
+    const int P = c->nranks;
     const bool bN = (transB == 'N' || transB == 'n');
     if (K >= 0 && ldb != (bN ? (K > 1 ? K : 1) : (N > 1 ? N : 1))) return -10;  // panels must be contiguous
-    ncclResult_t async_err = ncclSuccess;
-    n.getAsyncError(c->nc, &async_err);
-    if (async_err != ncclSuccess) return nccl_status(async_err);
-
+    if (!c->local()) {
+        if (!n.ok) return EMM_ERR_COMM;
+        ncclResult_t async_err = ncclSuccess;
+        n.getAsyncError(c->nc, &async_err);
+        if (async_err != ncclSuccess) return nccl_status(async_err);
+    }
     int64_t row0 = 0, rows = 0;
-    emm_row_partition(M, c->nranks, c->rank, &row0, &rows);
+    emm_row_partition(M, P, c->rank, &row0, &rows);
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    const int64_t b_elems = bN ? K * N : N * K;
+    const size_t b_bytes = (size_t)(bN ? K * N : N * K) * 4;
+    int st = check_args(transA, transB, rows, N, K, lda, ldb, ldc > 0 ? ldc : 1);
+    if (!st) st = check_device();
+    if (st) return st;
+    if (C_full && ldc_full < (M > 1 ? M : 1)) return -17;
+
+    // data plane: copy engines + flags when B (and C_full, if gathered) are
+    // registered; NCCL otherwise.  The choice depends only on arguments every
+    // rank passes identically (and registrations, which are collective), so
+    // all ranks take the same branch.
+    const bool ce_in = P > 1 && B == c->in_local && c->in_bytes >= b_bytes && (c->local() || c->in_succ);
+    const bool ce_out = C_full && C_full == c->out_local && ldc_full == c->out_ld;
+    if (c->local() && P > 1 && (!ce_in || (C_full && !ce_out))) return EMM_ERR_COMM;   // no NCCL to fall back on
+    if ((ce_in || (ce_out && P > 1)) && (st = resolve_flags(c))) return st;
+    float *in_succ = c->in_succ;
+    float *out_peer[MAXR] = {};
+    for (int r = 0; r < P; ++r) out_peer[r] = c->out_peer[r];
+    if (c->local()) {
+        std::lock_guard<std::mutex> g(c->world->mu);
+        in_succ = c->world->in[(c->rank + 1) % P];
+        if (ce_in && (!in_succ || c->world->in_bytes[(c->rank + 1) % P] < b_bytes)) return EMM_ERR_COMM;
+        if (ce_out)
+            for (int r = 0; r < P; ++r) {
+                out_peer[r] = c->world->out[r];
+                if (!out_peer[r] || c->world->out_ld[r] != ldc_full) return EMM_ERR_COMM;
+            }
+    } else if (ce_out) {
+        out_peer[c->rank] = c->out_local;
+    }
+    const uint32_t epoch = ++c->epoch;
+    const int pos = (c->rank - root + P) % P;       // position in the ring that starts at root
+    const int succ = (c->rank + 1) % P, pred = (c->rank - 1 + P) % P;
+    const bool has_succ = pos < P - 1, has_pred = pos > 0;
 
     // Gate the communication stream on the caller's stream (B / C ready).
     cudaEvent_t e0 = ev_at(c, 0);
     if (!e0) return EMM_ERR_NOMEM;
-    int st = cuda_st(cudaEventRecord(e0, s));
+    st = cuda_st(cudaEventRecord(e0, s));
     if (!st) st = cuda_st(cudaStreamWaitEvent(c->comm_stream, e0, 0));
     if (st) return st;
 
-    if ((st = check_args(transA, transB, rows, N, K, lda, ldb, ldc > 0 ? ldc : 1))) return st;
-    if ((st = check_device())) return st;
     const int64_t panel = bN ? emm_multi_panel_cols(N) : N;
     // Tensor-core modes: op(A)'s rows are re-buffered ONCE per call into
     // K-major planes in the communicator's cached workspace; each B panel is
-    // re-buffered after its broadcast and multiplied (one GEMM launch per
+    // re-buffered after it arrived and multiplied (one GEMM launch per
     // panel).  FFMA / alpha == 0 / K == 0 / skinny: one emm_sgemm_ex per panel.
     const bool tc = math != EMM_MATH_FFMA && !(alpha == 0.0f || K == 0) && rows > SKINNY_MAX &&
                     N > SKINNY_MAX && 2.0 * rows * (double)N * K > (double)(1 << 24);
@@ -293,12 +609,12 @@ extern "C" int emm_sgemm_multi(void *comm, char transA, char transB, int64_t M, 
     unsigned int *ctrl = nullptr;
     if (tc && rows > 0 && N > 0) {
         const size_t a_bytes = align_up((size_t)planes * rows * Kp * 4, 1024);
-        const size_t b_bytes = align_up((size_t)planes * panel * Kp * 4, 1024);
+        const size_t bp_bytes = align_up((size_t)planes * panel * Kp * 4, 1024);
         // stream-ordered reuse: the previous call's kernels on `s` are ordered before this one
-        if ((st = grow(&c->ws, &c->ws_bytes, a_bytes + b_bytes + 1024))) return st;
+        if ((st = grow(&c->ws, &c->ws_bytes, a_bytes + bp_bytes + 1024))) return st;
         Ap = reinterpret_cast<float *>(c->ws);
         Bp = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(c->ws) + a_bytes);
-        ctrl = reinterpret_cast<unsigned int *>(reinterpret_cast<uint8_t *>(c->ws) + a_bytes + b_bytes);
+        ctrl = reinterpret_cast<unsigned int *>(reinterpret_cast<uint8_t *>(c->ws) + a_bytes + bp_bytes);
         PackArgs pa;
         pa.X = A_local; pa.ld = lda; pa.R = rows; pa.kcontig = !(transA == 'N' || transA == 'n');
         pa.out0 = Ap; pa.ld0 = Kp; pa.out1 = Ap + (size_t)rows * Kp; pa.ld1 = Kp; pa.b_side = false;
@@ -306,7 +622,7 @@ extern "C" int emm_sgemm_multi(void *comm, char transA, char transB, int64_t M, 
     }
     // fused all-gather: C_full was registered -> the GEMM epilogue stores into
     // every rank's C_full directly (tensor-core modes)
-    const bool fused = tc && C_full && C_full == c->out_local && ldc_full == c->out_ld;
+    const bool fused = tc && ce_out;
     auto panel_gemm = [&](const float *bp, int64_t nc, float *cp) -> int {
         if (rows == 0 || nc == 0) return 0;
         if (!tc)
@@ -325,8 +641,8 @@ extern "C" int emm_sgemm_multi(void *comm, char transA, char transB, int64_t M, 
         }
         PeerOut pe;
         if (fused) {
-            pe.n = c->nranks;
-            for (int r = 0; r < c->nranks; ++r) pe.base[r] = c->out_peer[r];
+            pe.n = P;
+            for (int r = 0; r < P; ++r) pe.base[r] = out_peer[r];
             pe.ld = ldc_full;
             pe.row_off = row0;
             pe.col_off = (cp - C_local) / ldc;   // the panel's first column
@@ -337,14 +653,62 @@ extern "C" int emm_sgemm_multi(void *comm, char transA, char transB, int64_t M, 
         return cuda_st(e);
     };
 
-    if (!st && bN && N > 0) {
-        // column panels of B: contiguous K x nc ranges (emm_multi_panel_cols);
-        // the GEMM of panel c waits only for panel c's broadcast.
-        size_t idx = 1;
+    if (!st && ce_in) {
+        // ---- copy-engine ring: forward each chunk to the successor as soon
+        // as it is here; the GEMM of panel p waits for its last chunk.
+        const Chunks ch = make_chunks(bN, N, K, panel);
+        const int nchunk = (int)ch.off.size() - 1;
+        if (has_succ) {
+            // the successor finished reading the previous call's B
+            const uint32_t *fc = c->flags + FL_CONSUMED;
+            st = cuda_st(flag_wait(&fc, 1, epoch - 1, c->comm_stream));
+            for (int j = 0; j < nchunk && !st; ++j) {
+                if (has_pred) {
+                    const uint32_t *fb = c->flags + FL_BREADY + j;
+                    st = cuda_st(flag_wait(&fb, 1, epoch, c->comm_stream));
+                }
+                const size_t o = ch.off[j], nb = ch.off[j + 1] - o;
+                if (!st && nb)
+                    st = cuda_st(cudaMemcpyAsync(reinterpret_cast<uint8_t *>(in_succ) + o,
+                                                 reinterpret_cast<const uint8_t *>(B) + o, nb,
+                                                 cudaMemcpyDeviceToDevice, c->comm_stream));
+                uint32_t *fs = c->peer_flags[succ] + FL_BREADY + j;
+                if (!st) st = cuda_st(flag_set(&fs, 1, epoch, c->comm_stream));
+            }
+        }
+        const int npanel = (int)ch.pc.size() - 1;
+        for (int p = 0; p < npanel && !st; ++p) {
+            if (has_pred && ch.pc[p + 1] > ch.pc[p]) {
+                const uint32_t *fb = c->flags + FL_BREADY + (ch.pc[p + 1] - 1);
+                st = cuda_st(flag_wait(&fb, 1, epoch, s));
+            }
+            if (st) break;
+            if (bN) {
+                const int64_t c0 = (int64_t)p * panel, nc = std::min(panel, N - c0);
+                st = panel_gemm(B + c0 * ldb, nc, C_local + c0 * ldc);
+            } else {
+                st = panel_gemm(B, N, C_local);
+            }
+        }
+        // every read of this rank's B (GEMMs on s, forwarding on comm_stream)
+        // is done -> tell the predecessor it may overwrite it
+        cudaEvent_t ef = ev_at(c, 1);
+        if (!st && !ef) st = EMM_ERR_NOMEM;
+        if (!st) st = cuda_st(cudaEventRecord(ef, c->comm_stream));
+        if (!st) st = cuda_st(cudaStreamWaitEvent(s, ef, 0));
+        // (always, whatever this call's root: the ring predecessor waits for
+        // it before pushing the next call's B, which may start elsewhere)
+        uint32_t *fp = c->peer_flags[pred] + FL_CONSUMED;
+        if (!st) st = cuda_st(flag_set(&fp, 1, epoch, s));
+    } else if (!st && bN && N > 0) {
+        // ---- NCCL: column panels of B, contiguous K x nc ranges; the GEMM of
+        // panel c waits only for panel c's broadcast.
+        size_t idx = 2;
         for (int64_t c0 = 0; c0 < N && !st; c0 += panel, ++idx) {
             const int64_t nc = (N - c0 < panel) ? N - c0 : panel;
             float *bp = B + c0 * ldb;
-            if (K > 0) st = nccl_status(n.broadcast(bp, bp, (size_t)(K * nc), ncclFloat32, root, c->nc, c->comm_stream));
+            if (K > 0 && P > 1)
+                st = nccl_status(n.broadcast(bp, bp, (size_t)(K * nc), ncclFloat32, root, c->nc, c->comm_stream));
             cudaEvent_t ev = ev_at(c, idx);
             if (!st && !ev) st = EMM_ERR_NOMEM;
             if (!st) st = cuda_st(cudaEventRecord(ev, c->comm_stream));
@@ -352,26 +716,47 @@ extern "C" int emm_sgemm_multi(void *comm, char transA, char transB, int64_t M, 
             if (!st) st = panel_gemm(bp, nc, C_local + c0 * ldc);
         }
     } else if (!st && N > 0) {
-        // transB = 'T': B's stored columns run along K; broadcast it whole
-        // (no panel overlap), then one GEMM.
-        if (b_elems > 0) st = nccl_status(n.broadcast(B, B, (size_t)b_elems, ncclFloat32, root, c->nc, c->comm_stream));
-        cudaEvent_t ev = ev_at(c, 1);
+        // transB = 'T' over NCCL: B's stored columns run along K; broadcast it
+        // whole (no panel overlap), then one GEMM.
+        if (b_bytes > 0 && P > 1)
+            st = nccl_status(n.broadcast(B, B, b_bytes / 4, ncclFloat32, root, c->nc, c->comm_stream));
+        cudaEvent_t ev = ev_at(c, 2);
         if (!st) st = cuda_st(cudaEventRecord(ev, c->comm_stream));
         if (!st) st = cuda_st(cudaStreamWaitEvent(s, ev, 0));
         if (!st) st = panel_gemm(B, N, C_local);
     }
     if (st) return st;
 
-    if (C_full && fused) {
-        // every rank's epilogue stored its rows into all C_full buffers; a
-        // stream-ordered all-reduce completes only after every rank's GEMMs
-        // (and their peer stores, fenced at system scope) have finished.
-        st = nccl_status(n.allReduce(c->dummy, c->dummy, 1, ncclInt32, ncclSum, c->nc, s));
-        if (st) return st;
-    } else if (C_full) {
-        // all-gather of the row blocks: compact own block into the rank-major
-        // staging buffer, P broadcasts in one NCCL group, then unpack (KN6).
-        if (ldc_full < (M > 1 ? M : 1)) return -17;
+    if (C_full && ce_out) {
+        // ---- gathered output through the registered peers: the tensor-core
+        // epilogue already stored this rank's rows into every C_full (fused);
+        // other modes copy them (2-D peer copies, strided column-major rows).
+        if (!fused && rows > 0 && N > 0)
+            for (int r = 0; r < P && !st; ++r)
+                st = cuda_st(cudaMemcpy2DAsync(out_peer[r] + row0, (size_t)ldc_full * 4, C_local, (size_t)ldc * 4,
+                                               (size_t)rows * 4, (size_t)N, cudaMemcpyDeviceToDevice, s));
+        if (!st && P > 1) {
+            // every rank tells every rank its rows are in place, then waits
+            // for all of them: C_full is complete on `s` after this.
+            uint32_t *fs[MAXR];
+            const uint32_t *fw[MAXR];
+            int k = 0;
+            for (int r = 0; r < P; ++r)
+                if (r != c->rank) {
+                    fs[k] = c->peer_flags[r] + FL_DONE + c->rank;
+                    fw[k] = c->flags + FL_DONE + r;
+                    ++k;
+                }
+            st = cuda_st(flag_set(fs, k, epoch, s));
+            if (!st) st = cuda_st(flag_wait(fw, k, epoch, s));
+        }
+        return st;
+    }
+    if (C_full) {
+        if (c->local()) return EMM_ERR_COMM;
+        // ---- NCCL all-gather of the row blocks: compact own block into the
+        // rank-major staging buffer, P broadcasts in one NCCL group, then
+        // unpack (KN6).
         const size_t need = (size_t)M * (size_t)N * 4;
         if (c->stage_bytes < need) {
             if (c->stage) cudaFree(c->stage);
@@ -380,10 +765,10 @@ extern "C" int emm_sgemm_multi(void *comm, char transA, char transB, int64_t M, 
             if ((st = cuda_st(cudaMalloc(&c->stage, need)))) return st;
             c->stage_bytes = need;
         }
-        std::vector<int64_t> r0s(c->nranks), rws(c->nranks), offs(c->nranks);
+        std::vector<int64_t> r0s(P), rws(P), offs(P);
         int64_t off = 0;
-        for (int r = 0; r < c->nranks; ++r) {
-            emm_row_partition(M, c->nranks, r, &r0s[r], &rws[r]);
+        for (int r = 0; r < P; ++r) {
+            emm_row_partition(M, P, r, &r0s[r], &rws[r]);
             offs[r] = off;
             off += rws[r] * N;
         }
@@ -391,17 +776,16 @@ extern "C" int emm_sgemm_multi(void *comm, char transA, char transB, int64_t M, 
             st = cuda_st(cudaMemcpy2DAsync(c->stage + offs[c->rank], (size_t)rows * 4, C_local, (size_t)ldc * 4,
                                            (size_t)rows * 4, (size_t)N, cudaMemcpyDeviceToDevice, s));
         if (st) return st;
-        {
+        if (P > 1) {
             n.groupStart();
-            for (int r = 0; r < c->nranks; ++r)
+            for (int r = 0; r < P; ++r)
                 if (rws[r] > 0)
                     n.broadcast(c->stage + offs[r], c->stage + offs[r], (size_t)(rws[r] * N), ncclFloat32, r, c->nc,
                                 s);
             st = nccl_status(n.groupEnd());
             if (st) return st;
         }
-        st = cuda_st(launch_unpack_rows(c->stage, c->nranks, r0s.data(), rws.data(), N, C_full, ldc_full, s));
-        if (st) return st;
+        st = cuda_st(launch_unpack_rows(c->stage, P, r0s.data(), rws.data(), N, C_full, ldc_full, s));
     }
-    return 0;
+    return st;
 }

@@ -315,9 +315,9 @@ template <bool MC = false, bool TMAC = false>
 __device__ __forceinline__ void tc_epilogue_loop(const TcSched &S, uint32_t rank, int q, int h, int lane,
                                                  uint32_t tmem_base, uint64_t *acc_full, uint64_t *acc_empty,
                                                  int kc_stages, int M, int N, float alpha, float beta,
-                                                 float *__restrict__ C, int64_t ldc, float *__restrict__ partial,
+                                                 float *C, int64_t ldc, float *__restrict__ partial,
                                                  const TcSk &sk, const PeerOut &peers, int cl = 2,
-                                                 uint32_t leader = 0, const float *__restrict__ acc_init = nullptr,
+                                                 uint32_t leader = 0, const float *acc_init = nullptr,
                                                  int64_t ld_init = 0, const TcCin cin_tma = TcCin{}) {
     using namespace ptx;
     if (!MC) cl = 2, leader = 0;   // compile-time plain schedule

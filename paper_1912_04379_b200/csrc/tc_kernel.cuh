@@ -44,10 +44,10 @@ __global__ void __launch_bounds__(TC_THREADS_P, 1)
                     const __grid_constant__ CUtensorMap tmB0, const __grid_constant__ CUtensorMap tmB1,
                     const __grid_constant__ CUtensorMap tmB0h, const __grid_constant__ CUtensorMap tmB1h,
                     const __grid_constant__ CUtensorMap tmC, int M, int N,
-                    int Kp, float alpha, float beta, float *__restrict__ C, int64_t ldc, int tiles_m, int tiles_n,
+                    int Kp, float alpha, float beta, float *C, int64_t ldc, int tiles_m, int tiles_n,
                     int group_m, int kc_stages, unsigned int *__restrict__ wave_ctr, int splits,
                     float *__restrict__ partial, const TcSk sk, const __grid_constant__ PeerOut peers,
-                    const float *__restrict__ acc_init, int64_t ld_init) {
+                    const float *acc_init, int64_t ld_init) {   // acc_init may equal C (K-phased calls)
     if (threadIdx.x == 0) EMM_TL(0);
     using Cfg = TcCfg<TERMS>;
     constexpr bool A1_MN = TERMS == 3 ? A_MN : false;   // cross planes are K-major
@@ -337,6 +337,7 @@ static cudaError_t launch_tc_t(const TcOperands &ops, int64_t M, int64_t N, int6
         // size of 4 (two pairs sharing B by multicast; the B200 forms as many
         // 4-clusters as its GPCs hold and pairs on the remaining SMs)
         cudaLaunchAttribute at[3];
+        cudaLaunchAttribute at_sk[3];
         at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         at[0].val.programmaticStreamSerializationAllowed = 1;
         at[1].id = cudaLaunchAttributeClusterDimension;
@@ -354,10 +355,35 @@ static cudaError_t launch_tc_t(const TcOperands &ops, int64_t M, int64_t N, int6
         auto kern = mc ? (tmac ? tc_sgemm_kernel<TERMS, A_MN, B_MN, T2, T2> : tc_sgemm_kernel<TERMS, A_MN, B_MN, T2, false>)
                        : (tmac ? tc_sgemm_kernel<TERMS, A_MN, B_MN, false, T2>
                                : tc_sgemm_kernel<TERMS, A_MN, B_MN, false, false>);
-        cudaError_t le = cudaLaunchKernelEx(&cfg, kern, ta0, ta1, tb0, tb1, tb0h, tb1h, tcm, (int)M,
-                                            (int)N, (int)Kp, alpha, beta, C, ldc, tiles_m, tiles_n, group_m,
-                                            kc_stages, ctrl, splits, splits > 1 ? partial : nullptr, sk, peers,
-                                            acc_init, ld_init);
+        // Stream-K: an owner CTA waits for pieces published by other CTAs of
+        // the grid, so the grid must be co-resident even when other kernels
+        // (e.g. a concurrent GEMM on another stream) hold SMs: launch it
+        // cooperatively (the driver then starts it only as a whole).  If the
+        // cooperative launch is refused, run the data-parallel schedule.
+        if (sk.slots) {
+            at_sk[0] = at[0];
+            at_sk[1] = at[1];
+            at_sk[2].id = cudaLaunchAttributeCooperative;
+            at_sk[2].val.cooperative = 1;
+            cfg.attrs = at_sk;
+            cfg.numAttrs = 3;
+        }
+        auto launch = [&]() {
+            return cudaLaunchKernelEx(&cfg, kern, ta0, ta1, tb0, tb1, tb0h, tb1h, tcm, (int)M, (int)N, (int)Kp,
+                                      alpha, beta, C, ldc, tiles_m, tiles_n, group_m, kc_stages, ctrl, splits,
+                                      splits > 1 ? partial : nullptr, sk, peers, acc_init, ld_init);
+        };
+        cudaError_t le = launch();
+        if (le != cudaSuccess && sk.slots) {
+            cudaGetLastError();
+            sk = TcSk{0x7fffffff, nullptr, nullptr};
+            const int64_t dp_clusters = units < pairs ? units : pairs;
+            cfg.gridDim = dim3((unsigned)(2 * (max_clusters > 0 && dp_clusters > max_clusters ? max_clusters
+                                                                                                : dp_clusters)));
+            cfg.attrs = at;
+            cfg.numAttrs = 2;
+            le = launch();
+        }
         if (le != cudaSuccess) return le;
     }
     g_launches.fetch_add(1, std::memory_order_relaxed);

@@ -67,6 +67,12 @@ def lib() -> ctypes.CDLL:
     L.emm_comm_register_output.restype = i32
     L.emm_comm_unregister_output.argtypes = [vp]
     L.emm_comm_unregister_output.restype = i32
+    L.emm_comm_register_input.argtypes = [vp, vp, sz]
+    L.emm_comm_register_input.restype = i32
+    L.emm_comm_unregister_input.argtypes = [vp]
+    L.emm_comm_unregister_input.restype = i32
+    L.emm_debug_comm_create_local.argtypes = [i32, ctypes.POINTER(vp)]
+    L.emm_debug_comm_create_local.restype = i32
     L.emm_strerror.argtypes = [i32]
     L.emm_strerror.restype = ctypes.c_char_p
     L.emm_version.argtypes = []
@@ -238,10 +244,39 @@ class Comm:
     def unregister_output(self) -> None:
         lib().emm_comm_unregister_output(self.handle)
 
+    def register_input(self, B) -> None:
+        """Collective: register this rank's B buffer (source on root, receive
+        buffer elsewhere) so emm_sgemm_multi forwards B by peer copies along
+        the ring (copy engines + flags) instead of ncclBroadcast."""
+        nbytes = ((B.shape[1] - 1) * _ld(B) + B.shape[0]) * 4 if B.numel() else 0
+        st = lib().emm_comm_register_input(self.handle, B.data_ptr(), nbytes)
+        if st:
+            raise EmmError(st, "emm_comm_register_input")
+
+    def unregister_input(self) -> None:
+        lib().emm_comm_unregister_input(self.handle)
+
     def close(self):
         if self.handle:
             lib().emm_comm_destroy(self.handle)
             self.handle = None
+
+
+class _LocalComm(Comm):
+    def __init__(self, handle, rank, nranks):  # noqa: D401 - built by local_comms()
+        self.handle, self.rank, self.nranks = handle, rank, nranks
+
+
+def local_comms(nranks: int):
+    """emm_debug_comm_create_local: `nranks` virtual ranks on the current
+    device (test harness for the P > 1 paths on one GPU); returns one Comm per
+    rank.  Each rank needs its own stream; B (and a gathered C_full) must be
+    registered."""
+    arr = (ctypes.c_void_p * nranks)()
+    st = lib().emm_debug_comm_create_local(nranks, arr)
+    if st:
+        raise EmmError(st, "emm_debug_comm_create_local")
+    return [_LocalComm(ctypes.c_void_p(arr[r]), r, nranks) for r in range(nranks)]
 
 
 def sgemm_multi(comm: Comm, M, N, K, A_local, B, C_local, alpha=1.0, beta=0.0, transA="N", transB="N",
