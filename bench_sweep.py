@@ -101,6 +101,9 @@ def main():
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_sweep.jsonl"))
     ap.add_argument("--maths", default="3xtf32,tf32bf16,1xtf32,ffma")
     ap.add_argument("--only", default="")
+    ap.add_argument("--variants", default="",
+                    help="A/B of library switches: 'tag:VAR=v,VAR2=w;tag2:...' — every (config, math) row is run "
+                         "once per variant with those environment variables set (read per call by libemm)")
     ap.add_argument("--shape", default="", help="custom M,N,K,transA,transB (alpha=1, beta=0, uniform)")
     ap.add_argument("--cooldown", type=float, default=2.0,
                     help="idle seconds before each (config, path) row: the power-capped B200's clock depends on "
@@ -130,7 +133,15 @@ def main():
         C0 = datagen.matrix("uniform" if kind != "normal" or not name.startswith("c4") else "normal",
                             datagen.TAG_C, M, N, M + pad[2], sigma=sig, device=gdev)
         dA, dB, dC = (datagen.storage_of(x).to(dev) for x in (A, B, C0))
-        for math in args.maths.split(","):
+        variants = [("", {})]
+        if args.variants:
+            variants = []
+            for v in args.variants.split(";"):
+                tag, _, kv = v.partition(":")
+                variants.append((tag, dict(x.split("=", 1) for x in kv.split(",") if x)))
+        for math, (vtag, venv) in ((m, v) for m in args.maths.split(",") for v in variants):
+            saved = {k: os.environ.get(k) for k in venv}
+            os.environ.update(venv)
             nbytes = emm.workspace_bytes(tA, tB, M, N, K, math)
             ws = torch.empty(nbytes // 4 + 512, dtype=torch.float32, device=dev) if nbytes else None
             wsp = 0
@@ -194,9 +205,16 @@ def main():
                    "pct_roofline": 100.0 * fl / med / 1e9 / pk[math], "gbs": byt / med / 1e6,
                    "roofline_tflops": pk[math], "l2_flushed": True, "reps": args.reps, "cooldown_s": args.cooldown,
                    "b2b_graph_us": b2b, "clocks": clk}
+            if vtag:
+                rec["variant"] = vtag
             print(json.dumps(rec), flush=True)
             lines.append(rec)
             del ws
+            for k, v in saved.items():
+                if v is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = v
         del dA, dB, dC
         torch.cuda.empty_cache()
     with open(args.out, "w") as f:

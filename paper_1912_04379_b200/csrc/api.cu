@@ -136,6 +136,7 @@ struct Plan {
     int splits = 1;
     size_t a_off = 0, b_off = 0, p_off = 0, ctr_off = 0, total = 0;
     bool sk = false;          // stream-K: [flags | slots] follow the control block
+    bool xs = false;          // 3xTF32 split inside the GEMM (KN1X)
     int64_t lda1 = 0, ldb1 = 0;   // second-plane leading dimensions
 };
 
@@ -212,14 +213,38 @@ static bool prefer_inkernel_split(int64_t M, int64_t N, int64_t K) {
     return false;   // policy set from measurements
 }
 
-static Plan make_plan(char tA, char tB, int64_t M, int64_t N, int64_t K, emm_math_t math, bool direct) {
+// 3xTF32 on TMA-legal operands: split inside the TMA-fed GEMM (KN1X, no
+// split pass) or the split pass + KN1.  EMM_SPLIT=xform / pass force one
+// (tests, experiments), EMM_FORCE_PACK=1 forces the re-buffered pass.
+// Measured on B200 (profiles/r02_ab_xs.md, one box, back to back): KN1X is
+// faster on every TMA-legal config — c3 NN 52.3 -> 44.1 us, 1024^3 30.3 ->
+// 27.6, 2048^3 87 -> 76, 4096^3 523 -> 472, 8192^3 3.90 -> 3.70 ms, c4-i
+// 2.22 -> 1.88 ms, c4-ii 2.09 -> 1.98 ms, and the power-capped 32768^3 step
+// 264 TFLOP/s either way — so it is the default.
+static bool prefer_xs(int64_t M, int64_t N, int64_t K) {
+    (void)M;
+    (void)N;
+    (void)K;
+    if (const char *e = getenv("EMM_SPLIT")) {
+        if (!strcmp(e, "xform")) return true;
+        if (!strcmp(e, "pass") || !strcmp(e, "kernel")) return false;
+    }
+    return !env_on("EMM_FORCE_PACK");
+}
+
+static Plan make_plan(char tA, char tB, int64_t M, int64_t N, int64_t K, emm_math_t math, bool direct,
+                      bool xs = false) {
     Plan P;
     P.terms = terms_of(math);
     P.splits = tc_splits(M, N, K);
     P.direct = direct;
+    P.xs = xs;
     const int64_t Kp = tc_kpad(K);
     size_t a_bytes, b_bytes;
-    if (!direct) {
+    if (xs) {
+        P.pack_mode = -1;   // the small planes are made on chip
+        a_bytes = b_bytes = 0;
+    } else if (!direct) {
         const size_t pl = (size_t)planes_of(math);
         P.pack_mode = math == EMM_MATH_3XTF32 ? PK_FULL3_ : math == EMM_MATH_TF32_BF16 ? PK_FULLX_ : PK_FULL1_;
         P.lda1 = P.ldb1 = Kp;
@@ -338,8 +363,10 @@ extern "C" int emm_sgemm_ex(char transA, char transB, int64_t M, int64_t N, int6
         }
         return cuda_status(e);
     }
-    const bool direct = tma_legal(A, lda) && tma_legal(B, ldb) && prefer_direct(M, N, math);
-    const Plan P = make_plan(transA, transB, M, N, K, math, direct);
+    const bool legal = tma_legal(A, lda) && tma_legal(B, ldb);
+    const bool xs = legal && math == EMM_MATH_3XTF32 && prefer_xs(M, N, K);
+    const bool direct = legal && (xs || prefer_direct(M, N, math));
+    const Plan P = make_plan(transA, transB, M, N, K, math, direct, xs);
     void *ws = workspace;
     bool own = false;
     if (ws) {
@@ -388,10 +415,19 @@ extern "C" int emm_sgemm_ex(char transA, char transB, int64_t M, int64_t N, int6
     // zeroed before the GEMM: control block (+ stream-K flags)
     const size_t zero_bytes = TC_CTRL_BYTES + (P.sk ? TC_SK_FLAG_BYTES : 0);
     void *sk_ws = P.sk ? w + P.ctr_off + TC_CTRL_BYTES : nullptr;
-    if (P.pack_mode >= 0) e = launch_pack(P.pack_mode, pa, &pb, K, ctr, s, (int)(zero_bytes / 4));
-    else e = cudaMemsetAsync(ctr, 0, zero_bytes, s);
-    if (e == cudaSuccess)
-        e = launch_tc_sgemm(P.terms, ops, M, N, K, alpha, beta, C, ldc, ctr, P.splits, Pp, s, nullptr, sk_ws);
+    if (P.xs) {
+        // control block / stream-K flags only matter for multi-wave launches
+        const bool multiwave = P.sk || tc_units(M, N, P.splits) > tc_num_sms() / 2;
+        if (multiwave) e = cudaMemsetAsync(ctr, 0, zero_bytes, s);
+        if (e == cudaSuccess)
+            e = launch_tc_xs_sgemm(ops.a0, ops.b0, M, N, K, alpha, beta, C, ldc, multiwave ? ctr : nullptr, P.splits,
+                                   Pp, s, nullptr, sk_ws);
+    } else {
+        if (P.pack_mode >= 0) e = launch_pack(P.pack_mode, pa, &pb, K, ctr, s, (int)(zero_bytes / 4));
+        else e = cudaMemsetAsync(ctr, 0, zero_bytes, s);
+        if (e == cudaSuccess)
+            e = launch_tc_sgemm(P.terms, ops, M, N, K, alpha, beta, C, ldc, ctr, P.splits, Pp, s, nullptr, sk_ws);
+    }
     if (own) {
         cudaError_t e2 = cudaFreeAsync(ws, s);
         if (e == cudaSuccess) e = e2;

@@ -109,6 +109,15 @@ cudaError_t launch_tc_split_sgemm(bool a_kc, bool b_kc, const float *A, int64_t 
                                   int64_t M, int64_t N, int64_t K, float alpha, float beta, float *C, int64_t ldc,
                                   unsigned int *ctrl, int splits, float *partial, cudaStream_t s,
                                   const PeerOut *peers = nullptr);
+// KN1X (k_tcx.cu): 3xTF32 with the split inside the kernel, TMA-fed: the
+// raw operand planes a / b (the caller's arrays, TMA-legal, K- or MN-major)
+// are the big parts, a transform warpgroup writes small = rn_tf32(x -
+// trunc(x)) into SMEM beside them — bitwise identical to PK_DSMALL + KN1
+// direct.  ctrl: zeroed control block for multi-wave launches (NULL: no
+// lockstep); sk_ws: zeroed stream-K scratch or NULL.
+cudaError_t launch_tc_xs_sgemm(const TcPlane &a, const TcPlane &b, int64_t M, int64_t N, int64_t K, float alpha,
+                               float beta, float *C, int64_t ldc, unsigned int *ctrl, int splits, float *partial,
+                               cudaStream_t s, const PeerOut *peers = nullptr, void *sk_ws = nullptr);
 bool tma_legal(const void *ptr, int64_t ld);
 // A plane as the tcgen05 kernels' 2-D tensor map (K-major box {32, 128},
 // MN-major box {32, 32} with the 32B-atom 128B swizzle), OOB reads zero.

@@ -223,7 +223,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (TC_EPI_WARPS +
                 __syncwarp();
                 if (lane == 0) {
                     const uint32_t eb = leader_empty0 + (uint32_t)(h * sizeof(uint64_t));
-                    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(eb) : "memory");
+                    mbar_arrive_remote(eb);
                 }
                 float *cp = C + (int64_t)row + (int64_t)col0 * ldc;
                 const int jmax = min(128, N - col0);

@@ -99,10 +99,16 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity
         if (clock64() - t0 > 40000000000LL) __trap();
     }
 }
-// Arrive (release, cluster scope) on the mbarrier at shared::cluster address
-// `cluster_addr` (mapa-mapped, may be in the peer CTA).
+// Arrive on the mbarrier at shared::cluster address `cluster_addr` (mapa-
+// mapped, may be in the peer CTA), default semantics (release at CTA scope,
+// the form CUTLASS's ClusterBarrier::arrive uses for UMMA pipelines).  The
+// .release.cluster form compiles to MEMBAR.ALL.GPU + ERRBAR, which measured
+// as the dominant stall of KN1X's transform warps (ncu source page,
+// profiles/r02_ncu_xs.md); what the consumer needs — SMEM writes visible to
+// the tensor core's async-proxy reads, TMEM reads retired — is ordered by
+// fence.proxy.async / tcgen05.fence::before_thread_sync before the arrive.
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 __device__ __forceinline__ uint32_t mapa_leader(const void *p) {
     uint32_t r;

@@ -382,7 +382,7 @@ __device__ __forceinline__ void tc_epilogue_loop(const TcSched &S, uint32_t rank
             __syncwarp();
             if (lane == 0) {
                 const uint32_t eb = leader_empty0 + (uint32_t)(b * sizeof(uint64_t));
-                asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(eb) : "memory");
+                mbar_arrive_remote(eb);
             }
         }
         if (dummy) continue;   // mirrored partner item: drained, never stored

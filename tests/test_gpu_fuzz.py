@@ -54,6 +54,7 @@ def _cases():
                  "EMM_SK": rng.choice([None, None, "0", "1"]), "EMM_NO_SKINNY": rng.choice([None, None, "1"]),
                  "EMM_WIDE": rng.choice([None, None, "1"]), "EMM_FFMA_CLASSIC": rng.choice([None, None, "1"]),
                  "EMM_PREF4": rng.choice([None, "1", "1", "0"])}))
+        out[-1]["env"]["EMM_SPLIT"] = rng.choice([None, None, "pass"])   # KN1 instead of KN1X
     return out
 
 

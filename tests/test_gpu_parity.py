@@ -153,16 +153,21 @@ def test_integer_exact_bitwise(emm, math, tA, tB, shape):
             f"max |diff| {np.max(np.abs(G - R))}"
 
 
-@pytest.mark.parametrize("force_pack", ["0", "1"])
+@pytest.mark.parametrize("force_pack", ["0", "1", "pass"])
 @pytest.mark.parametrize("math", ["3xtf32", "1xtf32", "tf32bf16"])
 @pytest.mark.parametrize("tA", ["N", "T"])
 @pytest.mark.parametrize("tB", ["N", "T"])
 def test_direct_and_repacked_paths(emm, monkeypatch, force_pack, math, tA, tB):
     """TMA-legal leading dimensions take the direct path (operands read in
-    place, K- or MN-major per trans flag, transpose in the TMA box); with
-    EMM_FORCE_PACK=1 the same call takes the re-buffering fallback.  Both
-    must be bitwise exact on integer inputs and within tolerance on random
-    ones, including ragged M/N/K tails (M, N, K not multiples of 32/256)."""
+    place, K- or MN-major per trans flag, transpose in the TMA box; 3xTF32:
+    the in-kernel split KN1X by default, the split pass + KN1 with
+    EMM_SPLIT=pass); with EMM_FORCE_PACK=1 the same call takes the
+    re-buffering fallback.  All must be bitwise exact on integer inputs and
+    within tolerance on random ones, including ragged M/N/K tails (M, N, K
+    not multiples of 32/256)."""
+    if force_pack == "pass":
+        monkeypatch.setenv("EMM_SPLIT", "pass")
+        force_pack = "0"
     monkeypatch.setenv("EMM_FORCE_PACK", force_pack)
     monkeypatch.setenv("EMM_FORCE_DIRECT", "1" if force_pack == "0" else "0")
     for (M, N, K) in [(520, 388, 200), (260, 1000, 72)]:

@@ -32,6 +32,7 @@ def no_small_paths(monkeypatch):
     monkeypatch.setenv("EMM_SMALL_FLOPS", "0")
     monkeypatch.setenv("EMM_NO_SKINNY", "1")
     monkeypatch.setenv("EMM_SK", "0")
+    monkeypatch.setenv("EMM_SPLIT", "pass")   # KN1 (preferred clusters of 4 are a KN1 launch mode)
 
 
 SHAPES = [((4096, 4096, 1024), "NN"), ((3000, 2000, 700), "TT"), ((8192, 2048, 512), "NT"),

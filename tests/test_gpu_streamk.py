@@ -38,9 +38,10 @@ def emm():
     return e
 
 
-@pytest.fixture(autouse=True)
-def no_small_path(monkeypatch):
+@pytest.fixture(autouse=True, params=["xform", "pass"])
+def no_small_path(monkeypatch, request):
     monkeypatch.setenv("EMM_SMALL_FLOPS", "0")
+    monkeypatch.setenv("EMM_SPLIT", request.param)   # KN1X (default) and KN1
     # force stream-K wherever it is legal (the default policy enables it only
     # where it measured faster, e.g. 4096^3 3xTF32 and (2560, 2560, 600))
     monkeypatch.setenv("EMM_SK", "1")

@@ -37,7 +37,13 @@ def no_small_paths(monkeypatch):
     ((8192, 4096, 4096), "NN", {"EMM_PREF4": "1"}),       # preferred clusters of 4 (dummies in the last wave)
     ((2820, 4100, 2049), "TN", {}),                       # ragged M / N (TMA clips the C boxes)
 ], ids=lambda v: "x".join(map(str, v)) if isinstance(v, tuple) else (v if isinstance(v, str) else "-".join(v) or "default"))
-def test_tmac_bitwise(emm, monkeypatch, math, shape, trans, env):
+@pytest.mark.parametrize("split", ["xform", "pass"])
+def test_tmac_bitwise(emm, monkeypatch, math, shape, trans, env, split):
+    """KN1 (EMM_SPLIT=pass) and KN1X (the default 3xTF32 kernel on TMA-legal
+    operands) read C_in through TMA or per thread: same bits."""
+    if split == "xform" and (math != "3xtf32" or env.get("EMM_PREF4")):
+        pytest.skip("KN1X is the 3xTF32 kernel, launched on clusters of 2")
+    monkeypatch.setenv("EMM_SPLIT", split)
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     M, N, K = shape

@@ -18,6 +18,8 @@ WANT = {
     "dram__throughput.avg.pct_of_peak_sustained_elapsed": "dram%",
     "lts__throughput.avg.pct_of_peak_sustained_elapsed": "l2%",
     "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed": "smem_lsu%",
+    "l1tex__data_bank_reads.avg.pct_of_peak_sustained_elapsed": "smem_rd%",
+    "l1tex__data_bank_writes.avg.pct_of_peak_sustained_elapsed": "smem_wr%",
     "launch__grid_size": "grid",
 }
 
