@@ -25,7 +25,7 @@ VARIANT_FLAGS = os.environ.get("EMM_VARIANT_FLAGS", "").split() if VARIANT else 
 _TAG = "tl" if TIMELINE else VARIANT
 OBJ = os.path.join(PKG, f"build_{_TAG}" if _TAG else "build")
 LIB = os.path.join(PKG, f"libemm_{_TAG}.so" if _TAG else "libemm.so")
-SOURCES = ["api.cu", "k_tc.cu", "k_tc_t1.cu", "k_tc_t2.cu", "k_tc_t3.cu", "k_tcl.cu", "k_tcx.cu", "k_tc1w.cu", "k_ffma.cu", "k_ffma_tma.cu", "k_skinny.cu", "k_tiny.cu", "k_misc.cu", "multi.cu", "k_probe.cu"]
+SOURCES = ["api.cu", "k_tc.cu", "k_tc_t1.cu", "k_tc_t2.cu", "k_tc_t3.cu", "k_tcl.cu", "k_tcx.cu", "k_tc1w.cu", "k_ffma.cu", "k_ffma_tma.cu", "k_skinny.cu", "k_skinny_tc.cu", "k_tiny.cu", "k_misc.cu", "multi.cu", "k_probe.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

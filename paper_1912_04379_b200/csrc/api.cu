@@ -278,8 +278,9 @@ static Plan make_plan(char tA, char tB, int64_t M, int64_t N, int64_t K, emm_mat
 }
 
 static size_t ws_bytes(int64_t M, int64_t N, int64_t K, emm_math_t math) {
-    if (math == EMM_MATH_FFMA || M == 0 || N == 0 || K == 0 || small_problem(M, N, K)) return 0;
-    if (M <= SKINNY_MAX || N <= SKINNY_MAX) return 0;
+    if (math == EMM_MATH_FFMA || M == 0 || N == 0 || K == 0) return 0;
+    if (M <= SKINNY_MAX || N <= SKINNY_MAX) return skinny_tc_workspace_bytes(M, N, K);   // KN9T (upper bound)
+    if (small_problem(M, N, K)) return 0;
     return make_plan('N', 'N', M, N, K, math, /*direct=*/false).total;
 }
 
@@ -321,9 +322,31 @@ extern "C" int emm_sgemm_ex(char transA, char transB, int64_t M, int64_t N, int6
 
     if (!ab_used) return cuda_status(launch_scale_c(M, N, beta, C, ldc, s));
 
-    if ((M <= SKINNY_MAX || N <= SKINNY_MAX) && !env_on("EMM_NO_SKINNY"))
+    if ((M <= SKINNY_MAX || N <= SKINNY_MAX) && !env_on("EMM_NO_SKINNY")) {
+        if (math != EMM_MATH_FFMA &&
+            skinny_tc_wanted(terms_of(math), !is_n(transA), !is_n(transB), M, N, K, A, lda, B, ldb)) {
+            // tensor cores (KN9T): scratch for the short operand's planes
+            const size_t need = skinny_tc_workspace_bytes(M, N, K);
+            void *ws = workspace;
+            bool own = false;
+            if (ws) {
+                if (workspace_bytes < need || (reinterpret_cast<uintptr_t>(ws) & 1023u)) return EMM_ERR_WORKSPACE;
+            } else {
+                cudaError_t e = scratch_alloc(&ws, need, s);
+                if (e != cudaSuccess) return cuda_status(e);
+                own = true;
+            }
+            cudaError_t e = launch_skinny_tc_sgemm(terms_of(math), !is_n(transA), !is_n(transB), M, N, K, alpha, A,
+                                                   lda, B, ldb, beta, C, ldc, ws, s);
+            if (own) {
+                cudaError_t e2 = cudaFreeAsync(ws, s);
+                if (e == cudaSuccess) e = e2;
+            }
+            return cuda_status(e);
+        }
         return cuda_status(
             launch_skinny_sgemm(!is_n(transA), !is_n(transB), M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, s));
+    }
 
     if (small_problem(M, N, K))
         return cuda_status(

@@ -157,6 +157,18 @@ cudaError_t launch_skinny_sgemm(bool tA, bool tB, int64_t M, int64_t N, int64_t 
                                 int64_t lda, const float *B, int64_t ldb, float beta, float *C, int64_t ldc,
                                 cudaStream_t s);
 
+// KN9T (k_skinny_tc.cu): the same roles on the tensor cores — the long
+// operand TMA-streamed, split in the kernel and fed to tcgen05.mma from TMEM,
+// the short one split once by the KN4 pass into `ws` (skinny_tc_workspace_bytes,
+// 1024-byte aligned).  Default for 1xTF32 / TF32+BF16 with a short side > 8
+// and a large, TMA-legal long operand (skinny_tc_wanted; EMM_SKINNY_TC=0/1).
+bool skinny_tc_wanted(int terms, bool tA, bool tB, int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
+                      const float *B, int64_t ldb);
+size_t skinny_tc_workspace_bytes(int64_t M, int64_t N, int64_t K);
+cudaError_t launch_skinny_tc_sgemm(int terms, bool tA, bool tB, int64_t M, int64_t N, int64_t K, float alpha,
+                                   const float *A, int64_t lda, const float *B, int64_t ldb, float beta, float *C,
+                                   int64_t ldc, void *ws, cudaStream_t s);
+
 // ---- latency-bound small problems (k_tiny.cu) -----------------------------
 cudaError_t launch_tiny_sgemm(bool tA, bool tB, int64_t M, int64_t N, int64_t K, float alpha, const float *A,
                               int64_t lda, const float *B, int64_t ldb, float beta, float *C, int64_t ldc,

@@ -60,16 +60,16 @@ __device__ __forceinline__ float tx_small(float x) {
     return __uint_as_float(cvt_tf32_rn(lo));
 }
 
-// RN: the transform also rounds the big part in place (big = rn_tf32(x) over
-// the raw tile, small = rn_tf32(x - big)): the re-buffered planes' numerics
-// (bitwise equal to PK_FULL3 + KN1), with zeroed low mantissa bits in the
-// tensor core's operands (lower switching power under the 1 kW cap) for
-// 21 B/clk more SMEM writes.  EMM_XS_RN=1.
 __device__ __forceinline__ void tx_split_rn(float x, float &big, float &small) {
     big = __uint_as_float(cvt_tf32_rn(x));
     small = isfinite(x) ? __uint_as_float(cvt_tf32_rn(x - big)) : 0.0f;   // x - big exact
 }
 
+// RN: the transform also rounds the big part in place (big = rn_tf32(x) over
+// the raw tile, small = rn_tf32(x - big)): the re-buffered planes' numerics
+// (bitwise equal to PK_FULL3 + KN1), with zeroed low mantissa bits in the
+// tensor core's operands (lower switching power under the 1 kW cap) for
+// 21 B/clk more SMEM writes.  EMM_XS_RN=1.
 template <bool A_MN, bool B_MN, bool TMAC, bool RN>
 __global__ void __launch_bounds__(TX_THREADS, 1)
     tc_xs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -77,6 +77,7 @@ __global__ void __launch_bounds__(TX_THREADS, 1)
                  int64_t ldc, int tiles_m, int tiles_n, int group_m, int kc_stages,
                  unsigned int *__restrict__ wave_ctr, int splits, float *__restrict__ partial, const TcSk sk,
                  const __grid_constant__ PeerOut peers) {
+    if (threadIdx.x == 0) EMM_TL(0);
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     float *cbuf = reinterpret_cast<float *>(smem + TX_STAGES * TX_STAGE_BYTES);   // TMAC: C_in ring
@@ -118,9 +119,11 @@ __global__ void __launch_bounds__(TX_THREADS, 1)
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (threadIdx.x == 0) EMM_TL(1);
     // PDL: the prologue above may overlap the previous kernel on the stream
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (threadIdx.x == 0) EMM_TL(2);
 
     const int n_it = S.n_items;
     if (warp < TX_XF_WARP0) {
@@ -236,6 +239,7 @@ __global__ void __launch_bounds__(TX_THREADS, 1)
         tc_fence_after();
         tmem_dealloc_2sm<TC_TMEM_COLS>(tmem_base);
     }
+    if (threadIdx.x == 0) EMM_TL(7);
 }
 
 template <bool A_MN, bool B_MN>
@@ -341,3 +345,11 @@ cudaError_t launch_tc_xs_sgemm(const TcPlane &a, const TcPlane &b, int64_t M, in
 }
 
 }  // namespace emm
+
+#ifdef EMM_TIMELINE
+// the timeline buffer of this translation unit (KN1X launches)
+extern "C" int emm_debug_timeline_xs(unsigned long long *out, int n) {
+    const int m = n < 512 * emm::TL_SLOTS ? n : 512 * emm::TL_SLOTS;
+    return (int)cudaMemcpyFromSymbol(out, emm::g_emm_timeline, (size_t)m * 8);
+}
+#endif

@@ -17,3 +17,4 @@ run c2-8192_pass     tc_sgemm       2 --only c2-8192 --maths 3xtf32 --variants p
 run c3-NN_xform      tc_xs_kernel   2 --only c3-NN   --maths 3xtf32 --variants xform:EMM_SPLIT=xform
 run c3-NN_reduce     splitk_reduce  2 --only c3-NN   --maths 3xtf32 --variants xform:EMM_SPLIT=xform
 run c2-1024_xform    tc_xs_kernel   2 --only c2-1024 --maths 3xtf32 --variants xform:EMM_SPLIT=xform
+run c6-N16_skinnytc  skinny_tc      1 --only c6-skinny-N16 --maths 3xtf32 --variants tc:EMM_SKINNY_TC=1

@@ -32,13 +32,15 @@ def main():
     ap.add_argument("--shape", default="1024,1024,1024,N,N")
     ap.add_argument("--math", default="3xtf32")
     ap.add_argument("--flush", type=int, default=1)
+    ap.add_argument("--xs", type=int, default=1, help="read the KN1X (k_tcx.cu) timeline, else KN1's")
     a = ap.parse_args()
     M, N, K, tA, tB = a.shape.split(",")
     M, N, K = int(M), int(N), int(K)
     dev = torch.device("cuda", 0)
     L = emm.lib()
-    L.emm_debug_timeline.argtypes = [ctypes.c_void_p, ctypes.c_int]
-    L.emm_debug_timeline.restype = ctypes.c_int
+    tl = L.emm_debug_timeline_xs if a.xs else L.emm_debug_timeline
+    tl.argtypes = [ctypes.c_void_p, ctypes.c_int]
+    tl.restype = ctypes.c_int
     ra, ca = (M, K) if tA == "N" else (K, M)
     rb, cb = (K, N) if tB == "N" else (N, K)
     A = torch.rand(ca, ra, device=dev).t()
@@ -51,10 +53,10 @@ def main():
             flush.fill_(1.0)
         torch.cuda.synchronize()
         buf = np.zeros(512 * 8, dtype=np.uint64)
-        L.emm_debug_timeline(buf.ctypes.data, 0)
+        tl(buf.ctypes.data, 0)
         emm.sgemm_ex(A, B, C, 1.0, 0.0, tA, tB, math=a.math, workspace=ws)
         torch.cuda.synchronize()
-        st = L.emm_debug_timeline(buf.ctypes.data, buf.size)
+        st = tl(buf.ctypes.data, buf.size)
         assert st == 0
     t = buf.reshape(512, 8).astype(np.int64)
     ncta = int(np.count_nonzero(t[:, 0]))
