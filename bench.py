@@ -424,8 +424,9 @@ def main():
                 "peak_kind": f"{pname}, from {src} bf16 sustained {bf16_sus} TF x 1.1/2.25",
                 "peak_derived": peak, "frac_derived": (achieved / peak) if achieved else None,
                 "peak_burst": peak_b, "frac_burst": (achieved / peak_b) if achieved else None,
-                "kernel": {"ffma": "ffma_tma_kernel (KN3b)", "1xtf32": "tc1w_kernel (KN2w, 256x512 tiles)"}.get(
-                    math, "tc_sgemm_kernel"),
+                "kernel": {"ffma": "ffma_tma_kernel (KN3b)", "1xtf32": "tc1w_kernel (KN2w, 256x512 tiles)",
+                           "3xtf32": "tc_xs_kernel (KN1X, 3xTF32 split in the kernel)"}.get(
+                    math, "tc_sgemm_kernel (KN1)"),
                 "kernel_ms": kernel_ms, "kernel_share_of_step": (gemm_ms / ms) if ms > 0 else None,
                 "other_kernels_ms_per_step": other_ms / steps}
         if math != "ffma":
@@ -485,12 +486,16 @@ def main():
         e2e = {"value": flops * e_steps / dt / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": 4 * (M * K + K * N),
                "d2h_bytes_per_step": 4 * M * N, "steps": e_steps,
                "api": "emm_sgemm_host (pinned host A,B -> device, C -> host, synchronous)"}
-        # spot-check the e2e result against a device call of the same path
-        # (deterministic: must be bitwise equal)
+        # spot-check the e2e result against a device call of the same
+        # arithmetic (the host pipeline multiplies re-buffered PK_FULL3 planes
+        # with KN1: EMM_FORCE_PACK=1 makes the device call do the same;
+        # deterministic, so bitwise equal)
         ws = None
+        os.environ["EMM_FORCE_PACK"] = "1"
         with torch.cuda.stream(stream):
             emm.sgemm(A, B, C, 1.0, 0.0, math=args.math, stream=stream)
         stream.synchronize()
+        del os.environ["EMM_FORCE_PACK"]
         Cd = C[:64, :64].cpu()
         hv = hC.reshape(N, M)[:64, :64].t()
         assert torch.equal(Cd, hv), "e2e result differs from device result"

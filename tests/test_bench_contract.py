@@ -12,7 +12,7 @@ import sys
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-FINAL = os.path.join(ROOT, "profiles", "r01_bench_v12.jsonl")
+FINAL = os.path.join(ROOT, "profiles", "r02_bench_v1.jsonl")
 
 
 def last_line(path):
@@ -41,6 +41,8 @@ def test_final_bench_line_has_the_contract():
         assert k in r, k
     assert r["bound"] == "tensor" and r["unit"] == "TFLOP/s"
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    assert r["frac"] <= 1.0, "the roofline peak is the measured tensor-pipe ceiling: a kernel cannot exceed it"
+    assert r["peak_nominal"] > r["peak"]
     assert r["traffic"] and r["traffic"] > 1e9
     c = d["cpu_baseline"]
     assert c["kind"] == "oracle" and c["cores"] >= 1 and c["value"] > 0 and c["sample"]
