@@ -70,7 +70,14 @@ __device__ __forceinline__ void tx_split_rn(float x, float &big, float &small) {
 // (bitwise equal to PK_FULL3 + KN1), with zeroed low mantissa bits in the
 // tensor core's operands (lower switching power under the 1 kW cap) for
 // 21 B/clk more SMEM writes.  EMM_XS_RN=1.
-template <bool A_MN, bool B_MN, bool TMAC, bool RN>
+// CSK (cluster split-K, sub-wave shapes): the grid is one cluster of S CTA
+// pairs per output tile, pair p computing K split p; each CTA keeps its raw
+// partial in its (then idle) SMEM ring and the cluster reduces the tile over
+// DSMEM — CTA (p, r) sums the S partials of its 128 rows on the column range
+// p*256/S .. (p+1)*256/S in the fixed order s = 0..S-1 (KN8's order: bitwise
+// equal to global split-K + the reduce launch), applies alpha/beta and stores
+// C.  No partial slots in HBM, no reduce launch.
+template <bool A_MN, bool B_MN, bool TMAC, bool RN, bool CSK>
 __global__ void __launch_bounds__(TX_THREADS, 1)
     tc_xs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmC, int M, int N, int Kp, float alpha, float beta, float *C,
@@ -90,9 +97,14 @@ __global__ void __launch_bounds__(TX_THREADS, 1)
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(cfull + 2 * TC_CB_N);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t rank = cluster_ctarank() & 1u;
-    const int nclus = (int)(gridDim.x >> 1);
-    const int cid = (int)(blockIdx.x >> 1);
+    const uint32_t crank = cluster_ctarank();
+    const uint32_t rank = crank & 1u;                 // rank in the CTA pair
+    const uint32_t leader = crank & ~1u;              // the pair leader's cluster rank
+    const int pairc = CSK ? (int)(crank >> 1) : 0;    // CSK: the pair's K split
+    // CSK: pair p of cluster k runs unit (split p, tile k) of the split-K schedule
+    const int ntile = tiles_m * tiles_n;
+    const int nclus = CSK ? ntile * splits : (int)(gridDim.x >> 1);
+    const int cid = CSK ? pairc * ntile + (int)(blockIdx.x / (2 * splits)) : (int)(blockIdx.x >> 1);
     const TcSched S(tiles_m, tiles_n, group_m, Kp, splits, sk.dp_tiles, TC_SK_CHUNK, nclus, cid);
 
     if (threadIdx.x == 0) {
@@ -108,6 +120,7 @@ __global__ void __launch_bounds__(TX_THREADS, 1)
         if (TMAC)
             for (int b = 0; b < 2 * TC_CB_N; ++b) mbar_init(&cfull[b], 1);
         fence_mbar_init();
+        EMM_TL(8);
     }
     if (warp == 1 && lane == 0) {
         prefetch_tmap(&tmA);
@@ -115,8 +128,10 @@ __global__ void __launch_bounds__(TX_THREADS, 1)
         if (TMAC) prefetch_tmap(&tmC);
     }
     if (warp == 0) tmem_alloc_2sm<TC_TMEM_COLS>(tmem_slot);
+    if (warp == 0 && lane == 0) EMM_TL(9);
     tc_fence_before();
     cluster_sync();
+    if (threadIdx.x == 0) EMM_TL(10);
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     if (threadIdx.x == 0) EMM_TL(1);
@@ -129,8 +144,8 @@ __global__ void __launch_bounds__(TX_THREADS, 1)
     if (warp < TX_XF_WARP0) {
         setmaxnreg_dec<TX_REGS_WG0>();
         if (warp == 0 && rank == 0 && lane == 0) {
-            tc_mma_loop<3, A_MN, B_MN, A_MN, B_MN, 2, TX_STAGES, TX_STAGE_BYTES>(S, smem, full, empty, acc_full,
-                                                                              acc_empty, tmem_base, kc_stages);
+            tc_mma_loop<3, A_MN, B_MN, A_MN, B_MN, 2, TX_STAGES, TX_STAGE_BYTES, CSK>(
+                S, smem, full, empty, acc_full, acc_empty, tmem_base, kc_stages, 2, pairc);
         } else if (warp == 1 && lane == 0) {
             // ===== TMA producer (each CTA: its 128 rows of A and of B, raw) =====
             const uint64_t pol = policy_evict_normal();
@@ -189,7 +204,8 @@ __global__ void __launch_bounds__(TX_THREADS, 1)
         setmaxnreg_dec<TX_REGS_XF>();
         // ===== transform: small = rn_tf32(x - trunc(x)) beside each raw tile =====
         const int t = threadIdx.x - 32 * TX_XF_WARP0;   // 0..127
-        const uint32_t leader_full0 = mapa_leader(&full[0]);
+        uint32_t leader_full0;   // the pair leader's full[0]
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(leader_full0) : "r"(smem_u32(&full[0])), "r"(leader));
         int it = 0;
         for (int i = 0; i < n_it; ++i) {
             TcWork wk;
@@ -228,13 +244,59 @@ __global__ void __launch_bounds__(TX_THREADS, 1)
         }
     } else {
         setmaxnreg_inc<TX_REGS_EPI>();
-        tc_epilogue_loop<false, TMAC>(S, rank, warp & 3, (warp - TX_EPI_WARP0) >> 2, lane, tmem_base, acc_full,
-                                      acc_empty, kc_stages, M, N, alpha, beta, C, ldc, partial, sk, peers, 2, 0,
-                                      nullptr, 0, TcCin{&tmC, cbuf, cfull});
+        tc_epilogue_loop<CSK, TMAC>(S, rank, warp & 3, (warp - TX_EPI_WARP0) >> 2, lane, tmem_base, acc_full,
+                                    acc_empty, kc_stages, M, N, alpha, beta, C, ldc, partial, sk, peers, 2, leader,
+                                    nullptr, 0, TcCin{&tmC, cbuf, cfull},
+                                    CSK ? reinterpret_cast<float *>(smem) : nullptr);
     }
 
     tc_fence_before();
     cluster_sync();
+    if (CSK && warp >= TX_EPI_WARP0) {
+        // ===== cluster reduce of the tile's S partials (DSMEM), alpha/beta, C =====
+        TcWork w;
+        S.item(0, w);
+        const int t = threadIdx.x - 32 * TX_EPI_WARP0;   // 0..255
+        const int rl = t & 127, par = t >> 7;
+        const int row = w.m0 + (int)rank * TC_BM + rl;
+        const int c0 = pairc * TC_BN / splits, c1 = (pairc + 1) * TC_BN / splits;
+        const uint32_t lbase = smem_u32(smem) + (uint32_t)rl * 4u;
+        uint32_t rb[4];
+#pragma unroll
+        for (int sp = 0; sp < 4; ++sp) {
+            const uint32_t target = (uint32_t)(2 * (sp < splits ? sp : 0)) + rank;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb[sp]) : "r"(lbase), "r"(target));
+        }
+        for (int col = c0 + par; col < c1; col += 8) {
+            float v[4][4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int cc = col + 2 * u;
+#pragma unroll
+                for (int sp = 0; sp < 4; ++sp) {
+                    v[u][sp] = 0.0f;
+                    if (sp < splits && cc < c1)
+                        asm volatile("ld.shared::cluster.f32 %0, [%1];"
+                                     : "=f"(v[u][sp])
+                                     : "r"(rb[sp] + (uint32_t)(cc * 128 * 4))
+                                     : "memory");
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int cc = col + 2 * u, gc = w.n0 + cc;
+                float acc = v[u][0];
+#pragma unroll
+                for (int sp = 1; sp < 4; ++sp)
+                    if (sp < splits) acc += v[u][sp];
+                if (cc < c1 && row < M && gc < N) {
+                    float *cp = C + (int64_t)row + (int64_t)gc * ldc;
+                    *cp = beta == 0.0f ? alpha * acc : fmaf(beta, *cp, alpha * acc);
+                }
+            }
+        }
+    }
+    if (CSK) cluster_sync();   // no CTA leaves while others read its SMEM
     if (warp == 0) {
         tc_fence_after();
         tmem_dealloc_2sm<TC_TMEM_COLS>(tmem_base);
@@ -249,11 +311,12 @@ static cudaError_t launch_tx_t(const TcPlane &pa, const TcPlane &pb, int64_t M, 
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(once, [] {
-        const void *fs[4] = {(const void *)tc_xs_kernel<A_MN, B_MN, false, false>,
-                             (const void *)tc_xs_kernel<A_MN, B_MN, true, false>,
-                             (const void *)tc_xs_kernel<A_MN, B_MN, false, true>,
-                             (const void *)tc_xs_kernel<A_MN, B_MN, true, true>};
-        for (int i = 0; i < 4 && attr_err == cudaSuccess; ++i)
+        const void *fs[5] = {(const void *)tc_xs_kernel<A_MN, B_MN, false, false, false>,
+                             (const void *)tc_xs_kernel<A_MN, B_MN, true, false, false>,
+                             (const void *)tc_xs_kernel<A_MN, B_MN, false, true, false>,
+                             (const void *)tc_xs_kernel<A_MN, B_MN, true, true, false>,
+                             (const void *)tc_xs_kernel<A_MN, B_MN, false, false, true>};
+        for (int i = 0; i < 5 && attr_err == cudaSuccess; ++i)
             attr_err = cudaFuncSetAttribute(fs[i], cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             TX_SMEM_BYTES + ((i & 1) ? TC_CBUF_BYTES : 0));
     });
@@ -306,12 +369,40 @@ static cudaError_t launch_tx_t(const TcPlane &pa, const TcPlane &pb, int64_t M, 
         unsigned int *wc = units > clusters ? ctrl : nullptr;
         const char *ern = getenv("EMM_XS_RN");
         const bool rn = ern && ern[0] == '1';
-        auto kern = tmac ? (rn ? tc_xs_kernel<A_MN, B_MN, true, true> : tc_xs_kernel<A_MN, B_MN, true, false>)
-                         : (rn ? tc_xs_kernel<A_MN, B_MN, false, true> : tc_xs_kernel<A_MN, B_MN, false, false>);
+        auto kern = tmac ? (rn ? tc_xs_kernel<A_MN, B_MN, true, true, false> : tc_xs_kernel<A_MN, B_MN, true, false, false>)
+                         : (rn ? tc_xs_kernel<A_MN, B_MN, false, true, false>
+                               : tc_xs_kernel<A_MN, B_MN, false, false, false>);
         auto launch = [&]() {
             return cudaLaunchKernelEx(&cfg, kern, ta, tb, tcm, (int)M, (int)N, (int)Kp, alpha, beta, C, ldc, tiles_m,
                                       tiles_n, 8, kc_stages, wc, splits, splits > 1 ? partial : nullptr, sk, peers);
         };
+        // cluster split-K (sub-wave shapes, S <= 4 splits): one cluster of S
+        // pairs per tile, reduced over DSMEM in the same kernel.  Opt-in
+        // (EMM_CSK=1): measured slower on B200 (profiles/r02_ab_csk.md) —
+        // clusters of 6-8 CTAs do not all fit at once (1024^3: 16 clusters of
+        // 8, c3: 24 of 6 ran in two rounds, 27.6 -> 45 us, 44 -> 106 us) and
+        // even where they fit (512^3: 4 clusters of 8) 19.4 -> 21.5 us.
+        const char *ecs = getenv("EMM_CSK");
+        if (splits > 1 && splits <= 4 && !sk.slots && !rn && peers.n == 0 && ecs && ecs[0] == '1') {
+            cudaLaunchConfig_t c2 = cfg;
+            cudaLaunchAttribute a2[2];
+            a2[0] = at[0];
+            a2[1] = at[1];
+            a2[1].val.clusterDim.x = (unsigned)(2 * splits);
+            c2.attrs = a2;
+            c2.numAttrs = 2;
+            c2.gridDim = dim3((unsigned)(2 * units));
+            c2.dynamicSmemBytes = TX_SMEM_BYTES;
+            cudaError_t ce = cudaLaunchKernelEx(&c2, tc_xs_kernel<A_MN, B_MN, false, false, true>, ta, tb, tcm, (int)M,
+                                                (int)N, (int)Kp, alpha, beta, C, ldc, tiles_m, tiles_n, 8, kc_stages,
+                                                (unsigned int *)nullptr, splits, (float *)nullptr, sk, peers);
+            if (ce == cudaSuccess) {
+                g_launches.fetch_add(1, std::memory_order_relaxed);
+                prof_end(s, true, ev);
+                return cudaGetLastError();
+            }
+            cudaGetLastError();   // cluster shape not schedulable: global split-K below
+        }
         cudaError_t le = launch();
         if (le != cudaSuccess && sk.slots) {   // cooperative launch refused: data-parallel schedule
             cudaGetLastError();

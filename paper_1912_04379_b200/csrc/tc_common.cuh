@@ -23,7 +23,7 @@ namespace emm {
 // product library): %globaltimer stamps per CTA at fixed points of the
 // kernel, read back with emm_debug_timeline().
 #ifdef EMM_TIMELINE
-constexpr int TL_SLOTS = 8;
+constexpr int TL_SLOTS = 12;
 static __device__ unsigned long long g_emm_timeline[512][TL_SLOTS];
 __device__ __forceinline__ void emm_tl_mark(int slot) {
     unsigned long long t;
@@ -245,7 +245,8 @@ __device__ __forceinline__ void tc_mma_loop(const TcSched &S, uint8_t *smem, uin
     // stage slots are released to both pairs of a 4-cluster (each slot
     // receives the partner's multicast B); the accumulator only to this pair
     if (!MC) cl = 2, pair = 0;   // compile-time plain schedule
-    const uint16_t rel_mask = (uint16_t)(cl == 4 ? 0xF : 0x3);
+    // (cluster split-K, KN1X: clusters of S pairs with cl == 2 — this pair only)
+    const uint16_t rel_mask = (uint16_t)(cl == 4 ? 0xF : (0x3u << (2 * pair)));
     const uint16_t acc_mask = (uint16_t)(0x3u << (2 * pair));
     const int n_it = tc_n_items(S, cl);
     for (int i = 0; i < n_it; ++i) {
@@ -318,7 +319,8 @@ __device__ __forceinline__ void tc_epilogue_loop(const TcSched &S, uint32_t rank
                                                  float *C, int64_t ldc, float *__restrict__ partial,
                                                  const TcSk &sk, const PeerOut &peers, int cl = 2,
                                                  uint32_t leader = 0, const float *acc_init = nullptr,
-                                                 int64_t ld_init = 0, const TcCin cin_tma = TcCin{}) {
+                                                 int64_t ld_init = 0, const TcCin cin_tma = TcCin{},
+                                                 float *csk_part = nullptr) {
     using namespace ptx;
     if (!MC) cl = 2, leader = 0;   // compile-time plain schedule
     uint32_t leader_empty0;   // the pair leader's acc_empty[0]
@@ -430,6 +432,14 @@ __device__ __forceinline__ void tc_epilogue_loop(const TcSched &S, uint32_t rank
                     }
                 }
             }
+        }
+        if (w.kind == TW_SPLITK && csk_part) {
+            // cluster split-K (KN1X): the raw partial stays in this CTA's SMEM
+            // ([256 columns][128 rows]); the cluster reduces it over DSMEM
+            float *pp = csk_part + h * 128 * 128 + 32 * q + lane;
+#pragma unroll
+            for (int j = 0; j < 128; ++j) pp[j * 128] = acc[j];
+            continue;
         }
         if (w.kind == TW_SPLITK) {
             // split-K: publish the raw FP32 partial of split sp into its slot

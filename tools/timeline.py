@@ -24,7 +24,8 @@ import torch  # noqa: E402
 
 import paper_1912_04379_b200 as emm  # noqa: E402
 
-NAMES = ["entry", "prologue", "gdc_wait", "mma_first", "mma_last", "epi_first", "epi_done", "exit"]
+NAMES = ["entry", "prologue", "gdc_wait", "mma_first", "mma_last", "epi_first", "epi_done", "exit",
+         "mbar_init", "tmem_alloc", "cluster_sync", "-"]
 
 
 def main():
@@ -52,13 +53,13 @@ def main():
         if a.flush:
             flush.fill_(1.0)
         torch.cuda.synchronize()
-        buf = np.zeros(512 * 8, dtype=np.uint64)
+        buf = np.zeros(512 * 12, dtype=np.uint64)
         tl(buf.ctypes.data, 0)
         emm.sgemm_ex(A, B, C, 1.0, 0.0, tA, tB, math=a.math, workspace=ws)
         torch.cuda.synchronize()
         st = tl(buf.ctypes.data, buf.size)
         assert st == 0
-    t = buf.reshape(512, 8).astype(np.int64)
+    t = buf.reshape(512, 12).astype(np.int64)
     ncta = int(np.count_nonzero(t[:, 0]))
     t = t[:ncta]
     t0 = t[:, 0].min()
