@@ -137,6 +137,7 @@ struct Plan {
     size_t a_off = 0, b_off = 0, p_off = 0, ctr_off = 0, total = 0;
     bool sk = false;          // stream-K: [flags | slots] follow the control block
     bool xs = false;          // 3xTF32 split inside the GEMM (KN1X)
+    bool rp_a = false, rp_b = false;   // KN1X on a raw re-pitched copy (PK_RAW) of a TMA-illegal operand
     int64_t lda1 = 0, ldb1 = 0;   // second-plane leading dimensions
 };
 
@@ -233,17 +234,27 @@ static bool prefer_xs(int64_t M, int64_t N, int64_t K) {
 }
 
 static Plan make_plan(char tA, char tB, int64_t M, int64_t N, int64_t K, emm_math_t math, bool direct,
-                      bool xs = false) {
+                      bool xs = false, bool rp_a = false, bool rp_b = false) {
     Plan P;
     P.terms = terms_of(math);
     P.splits = tc_splits(M, N, K);
     P.direct = direct;
     P.xs = xs;
+    P.rp_a = rp_a;
+    P.rp_b = rp_b;
     const int64_t Kp = tc_kpad(K);
     size_t a_bytes, b_bytes;
     if (xs) {
-        P.pack_mode = -1;   // the small planes are made on chip
-        a_bytes = b_bytes = 0;
+        // the small planes are made on chip; a TMA-illegal operand is first
+        // copied raw into a 16-byte-pitched buffer (its stored layout, ld
+        // rounded up to a multiple of 4 floats)
+        P.pack_mode = (rp_a || rp_b) ? PK_RAW_ : -1;
+        const int64_t ar = is_n(tA) ? M : K, ac = is_n(tA) ? K : M;
+        const int64_t br = is_n(tB) ? K : N, bc = is_n(tB) ? N : K;
+        P.lda1 = up4(ar);
+        P.ldb1 = up4(br);
+        a_bytes = rp_a ? (size_t)ac * P.lda1 * 4 : 0;
+        b_bytes = rp_b ? (size_t)bc * P.ldb1 * 4 : 0;
     } else if (!direct) {
         const size_t pl = (size_t)planes_of(math);
         P.pack_mode = math == EMM_MATH_3XTF32 ? PK_FULL3_ : math == EMM_MATH_TF32_BF16 ? PK_FULLX_ : PK_FULL1_;
@@ -386,10 +397,13 @@ extern "C" int emm_sgemm_ex(char transA, char transB, int64_t M, int64_t N, int6
         }
         return cuda_status(e);
     }
-    const bool legal = tma_legal(A, lda) && tma_legal(B, ldb);
-    const bool xs = legal && math == EMM_MATH_3XTF32 && prefer_xs(M, N, K);
-    const bool direct = legal && (xs || prefer_direct(M, N, math));
-    const Plan P = make_plan(transA, transB, M, N, K, math, direct, xs);
+    const bool legal_a = tma_legal(A, lda), legal_b = tma_legal(B, ldb);
+    const bool legal = legal_a && legal_b;
+    // 3xTF32: KN1X on the caller's arrays, or (TMA-illegal leading dimension,
+    // e.g. c3's lda = K + 13) on a raw re-pitched copy of that operand
+    const bool xs = math == EMM_MATH_3XTF32 && prefer_xs(M, N, K) && (legal || !env_on("EMM_NO_REPITCH"));
+    const bool direct = xs || (legal && prefer_direct(M, N, math));
+    const Plan P = make_plan(transA, transB, M, N, K, math, direct, xs, xs && !legal_a, xs && !legal_b);
     void *ws = workspace;
     bool own = false;
     if (ws) {
@@ -441,7 +455,18 @@ extern "C" int emm_sgemm_ex(char transA, char transB, int64_t M, int64_t N, int6
     if (P.xs) {
         // control block / stream-K flags only matter for multi-wave launches
         const bool multiwave = P.sk || tc_units(M, N, P.splits) > tc_num_sms() / 2;
-        if (multiwave) e = cudaMemsetAsync(ctr, 0, zero_bytes, s);
+        if (P.rp_a || P.rp_b) {
+            // raw re-pitch of the TMA-illegal operand(s); the same launch zeroes ctrl
+            PackArgs ra = pa, rb = pb;
+            ra.out0 = a1; ra.ld0 = P.lda1;
+            rb.out0 = b1; rb.ld0 = P.ldb1;
+            if (P.rp_a) ops.a0 = TcPlane{a1, P.lda1, !a_kc, K};
+            if (P.rp_b) ops.b0 = TcPlane{b1, P.ldb1, !b_kc, K};
+            e = launch_pack(PK_RAW_, P.rp_a ? ra : rb, (P.rp_a && P.rp_b) ? &rb : nullptr, K,
+                            multiwave ? ctr : nullptr, s, multiwave ? (int)(zero_bytes / 4) : 0);
+        } else if (multiwave) {
+            e = cudaMemsetAsync(ctr, 0, zero_bytes, s);
+        }
         if (e == cudaSuccess)
             e = launch_tc_xs_sgemm(ops.a0, ops.b0, M, N, K, alpha, beta, C, ldc, multiwave ? ctr : nullptr, P.splits,
                                    Pp, s, nullptr, sk_ws);

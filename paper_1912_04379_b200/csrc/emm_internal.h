@@ -58,7 +58,7 @@ struct PackArgs {
     int64_t ld1 = 0;
     bool b_side = false;    // B side of the cross operand (halves swapped)
 };
-enum { PK_FULL1_ = 0, PK_FULL3_ = 1, PK_FULLX_ = 2, PK_DSMALL_ = 3, PK_DCROSS_ = 4 };
+enum { PK_FULL1_ = 0, PK_FULL3_ = 1, PK_FULLX_ = 2, PK_DSMALL_ = 3, PK_DCROSS_ = 4, PK_RAW_ = 5 };
 // One launch for A (and B if non-NULL); also zeroes `ctrl_words` words at
 // ctrl (the control block, and the stream-K flags that follow it).
 cudaError_t launch_pack(int mode, const PackArgs &a, const PackArgs *b, int64_t K, unsigned int *ctrl,

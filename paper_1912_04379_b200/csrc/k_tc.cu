@@ -66,6 +66,9 @@ int64_t tc_kpad(int64_t K) { return (K + TC_BK - 1) / TC_BK * TC_BK; }
 //             (direct 3xTF32: the tensor core reads trunc(x) from the user array)
 //   PK_DCROSS plane 1 only = BF16 cross operand with big = trunc(x), K-major
 //             (direct TF32+BF16)
+//   PK_RAW    plane 0 = x unchanged in the SOURCE layout with a 16-byte-
+//             multiple leading dimension ld0 (re-pitch of a TMA-illegal
+//             operand for the in-kernel-split GEMM KN1X)
 // BF16 cross operand: for every group of 8 along K, 16 bf16 = [bf16(big) x8 |
 // bf16(x - big) x8] (A side) or the halves swapped (B side), so that ONE K16
 // BF16 MMA computes a_big*b_small + a_small*b_big.
@@ -79,7 +82,8 @@ int64_t tc_kpad(int64_t K) { return (K + TC_BK - 1) / TC_BK * TC_BK; }
 //  * transpose: MN-contiguous source -> K-major planes (the re-buffered
 //    FULL modes and PK_DCROSS): 64 (r) x 32 (p) tiles through shared memory.
 // =====================================================================
-enum { PK_FULL1 = PK_FULL1_, PK_FULL3 = PK_FULL3_, PK_FULLX = PK_FULLX_, PK_DSMALL = PK_DSMALL_, PK_DCROSS = PK_DCROSS_ };
+enum { PK_FULL1 = PK_FULL1_, PK_FULL3 = PK_FULL3_, PK_FULLX = PK_FULLX_, PK_DSMALL = PK_DSMALL_, PK_DCROSS = PK_DCROSS_,
+       PK_RAW = PK_RAW_ };
 
 constexpr int PK_THREADS = 256;
 constexpr int PK_GROUPS = 2;                                   // 8-element groups per thread (element-wise)
@@ -116,6 +120,11 @@ __device__ __forceinline__ void split_one(const PackOperand &op, float x, float 
 // One element (r, p) of op(X) -> its output position(s) (scalar tails).
 template <int MODE>
 __device__ __forceinline__ void pack_store(const PackOperand &op, int64_t r, int64_t p, float x) {
+    if (MODE == PK_RAW) {
+        if (op.kcontig) op.out0[r * op.ld0 + p] = x;
+        else op.out0[r + p * op.ld0] = x;
+        return;
+    }
     float big, lo;
     split_one<MODE>(op, x, big, lo);
     const bool direct = MODE == PK_DSMALL || MODE == PK_DCROSS;
@@ -140,6 +149,10 @@ __device__ __forceinline__ void pack_store(const PackOperand &op, int64_t r, int
 // vector stores.  FULL/cross: K-major row r; DSMALL: the line's own layout.
 template <int MODE>
 __device__ __forceinline__ void pack_store4(const PackOperand &op, float *o0, float *o1, int64_t e, const float (&x)[4]) {
+    if (MODE == PK_RAW) {
+        *reinterpret_cast<float4 *>(o0 + e) = make_float4(x[0], x[1], x[2], x[3]);
+        return;
+    }
     float big[4], lo[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) split_one<MODE>(op, x[i], big[i], lo[i]);
@@ -277,7 +290,7 @@ __global__ void __launch_bounds__(PK_THREADS) pack_split_kernel(PackOperand opA,
 }
 
 static void pack_geometry(PackOperand &o, int mode, int64_t K) {
-    const bool dsmall = mode == PK_DSMALL;
+    const bool dsmall = mode == PK_DSMALL || mode == PK_RAW;   // source orientation, K unpadded
     const int64_t Kext = dsmall ? K : tc_kpad(K);        // FULL / cross planes are zero-padded to Kp
     o.vec = ((reinterpret_cast<uintptr_t>(o.X) & 15u) == 0 && (o.ld & 3) == 0) ? 1 : 0;
     if (o.kcontig || dsmall) {
@@ -326,6 +339,7 @@ cudaError_t launch_pack(int mode, const PackArgs &a, const PackArgs *b, int64_t 
         case PK_FULLX: pack_split_kernel<PK_FULLX><<<grid, PK_THREADS, 0, s>>>(oa, ob, K, ctrl, ctrl_words); break;
         case PK_DSMALL: pack_split_kernel<PK_DSMALL><<<grid, PK_THREADS, 0, s>>>(oa, ob, K, ctrl, ctrl_words); break;
         case PK_DCROSS: pack_split_kernel<PK_DCROSS><<<grid, PK_THREADS, 0, s>>>(oa, ob, K, ctrl, ctrl_words); break;
+        case PK_RAW: pack_split_kernel<PK_RAW><<<grid, PK_THREADS, 0, s>>>(oa, ob, K, ctrl, ctrl_words); break;
         default: return cudaErrorInvalidValue;
     }
     g_launches.fetch_add(1, std::memory_order_relaxed);
