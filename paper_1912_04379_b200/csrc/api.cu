@@ -556,7 +556,7 @@ cudaError_t copy_rows(float *d, const float *h, bool rows_contig_in_col, int64_t
 
 static int host_pipelined(char tA, char tB, int64_t M, int64_t N, int64_t K, float alpha, const float *A, int64_t lda,
                           const float *B, int64_t ldb, float beta, float *C, int64_t ldc, emm_math_t math, float *dA,
-                          float *dB, float *dC, void *dW, float *dR) {
+                          float *dB, float *dC, void *dW, float *dR, bool xs) {
     int dev = 0;
     cudaGetDevice(&dev);
     if (g_hs.dev != dev) {
@@ -591,10 +591,12 @@ static int host_pipelined(char tA, char tB, int64_t M, int64_t N, int64_t K, flo
     const int64_t Kp = tc_kpad(K);
     const int terms = terms_of(math), pl = planes_of(math);
     const int pmode = math == EMM_MATH_3XTF32 ? PK_FULL3_ : math == EMM_MATH_TF32_BF16 ? PK_FULLX_ : PK_FULL1_;
+    // xs (3xTF32 on TMA-legal copies): KN1X reads each landed block of the
+    // device copies of A and B in place, no re-buffering (dW = control words)
     float *Ap = reinterpret_cast<float *>(dW);
     float *Bp = Ap + (size_t)pl * M * Kp;
     unsigned int *ctrl = reinterpret_cast<unsigned int *>(
-        reinterpret_cast<uint8_t *>(dW) + align_up((size_t)pl * (M + N) * Kp * 4, 1024));
+        reinterpret_cast<uint8_t *>(dW) + (xs ? 0 : align_up((size_t)pl * (M + N) * Kp * 4, 1024)));
     const bool a_rows_ld = is_n(tA);    // op(A) rows contiguous in a stored column
     const bool b_rows_ld = !is_n(tB);   // op(B)^T rows (= B columns) contiguous: transB = 'T'
     cudaStream_t h2d = g_hs.h2d, comp = g_hs.comp, d2h = g_hs.d2h;
@@ -668,7 +670,7 @@ static int host_pipelined(char tA, char tB, int64_t M, int64_t N, int64_t K, flo
                 pk.out1 = Bp + (size_t)N * Kp + (size_t)c0 * Kp + k0; pk.ld1 = Kp;
                 ++nb;
             }
-            if (e == cudaSuccess) e = launch_pack(pmode, pk, nullptr, nk, nullptr, comp);
+            if (e == cudaSuccess && !xs) e = launch_pack(pmode, pk, nullptr, nk, nullptr, comp);
             if (nr == 0 || nc == 0 || e != cudaSuccess) continue;
             // the region in pieces along its long side: GEMM, then D2H of the piece
             const bool split_cols = nc >= nr;
@@ -686,13 +688,23 @@ static int host_pipelined(char tA, char tB, int64_t M, int64_t N, int64_t K, flo
                 }
                 unsigned int *cw = ctrl + 32 * (ng & 63);   // zeroed once for the first 64 GEMMs
                 if (ng++ >= 64) e = cudaMemsetAsync(cw, 0, 128, comp);
+                if (xs) {
+                    // the block's raw rows / columns, K range [k0, k0 + nk), in place
+                    ops.a0 = a_rows_ld ? TcPlane{dA + pr0 + k0 * lda, lda, true, nk}
+                                       : TcPlane{dA + pr0 * lda + k0, lda, false, nk};
+                    ops.b0 = b_rows_ld ? TcPlane{dB + pc0 + k0 * ldb, ldb, true, nk}
+                                       : TcPlane{dB + pc0 * ldb + k0, ldb, false, nk};
+                }
                 if (e == cudaSuccess) {
-                    if (!last_phase)   // raw partial of the K prefix (continuing the previous phases')
-                        e = launch_tc_sgemm(terms, ops, pnr, pnc, nk, 1.0f, 0.0f, dR + pr0 + pc0 * M, M, cw, 1, nullptr,
-                                            comp, nullptr, nullptr, chain ? dR + pr0 + pc0 * M : nullptr, M);
-                    else
-                        e = launch_tc_sgemm(terms, ops, pnr, pnc, nk, alpha, beta, dC + pr0 + pc0 * ldc, ldc, cw, 1,
-                                            nullptr, comp, nullptr, nullptr, chain ? dR + pr0 + pc0 * M : nullptr, M);
+                    const float *ai = chain ? dR + pr0 + pc0 * M : nullptr;
+                    float *co = last_phase ? dC + pr0 + pc0 * ldc : dR + pr0 + pc0 * M;
+                    const int64_t ldo = last_phase ? ldc : M;
+                    // not last: raw partial of the K prefix (continuing the previous phases')
+                    const float al = last_phase ? alpha : 1.0f, be = last_phase ? beta : 0.0f;
+                    e = xs ? launch_tc_xs_sgemm(ops.a0, ops.b0, pnr, pnc, nk, al, be, co, ldo, cw, 1, nullptr, comp,
+                                                nullptr, nullptr, ai, M)
+                           : launch_tc_sgemm(terms, ops, pnr, pnc, nk, al, be, co, ldo, cw, 1, nullptr, comp, nullptr,
+                                             nullptr, ai, M);
                 }
                 if (!last_phase) continue;
                 cudaEvent_t done = ev();
@@ -739,14 +751,18 @@ extern "C" int emm_sgemm_host(char transA, char transB, int64_t M, int64_t N, in
     const size_t nC = (size_t)((N - 1) * ldc + M) * 4;
     const size_t nW = ab_used ? ws_bytes(M, N, K, math) : 0;
     if ((st = ensure(&g_hc.dA, &g_hc.nA, nA)) || (st = ensure(&g_hc.dB, &g_hc.nB, nB)) ||
-        (st = ensure(&g_hc.dC, &g_hc.nC, nC)) || (st = ensure(&g_hc.dW, &g_hc.nW, nW)))
+        (st = ensure(&g_hc.dC, &g_hc.nC, nC)))
         return st;
     cudaStream_t s = g_hc.s;
     cudaError_t e = cudaSuccess;
     if (ab_used && math != EMM_MATH_FFMA && M >= 4096 && N >= 4096 && K >= 256 && !env_on("EMM_HOST_NO_PIPELINE")) {
         const int64_t Kp = tc_kpad(K);
         const size_t pl = (size_t)planes_of(math);
-        const size_t nP = align_up(pl * (size_t)(M + N) * Kp * 4, 1024) + 64 * 128;
+        // 3xTF32 on TMA-legal device copies: KN1X on the landed blocks in
+        // place (no re-buffered planes); EMM_HOST_PACK=1 keeps the planes
+        const bool xs = math == EMM_MATH_3XTF32 && prefer_xs(M, N, K) && tma_legal(g_hc.dA, lda) &&
+                        tma_legal(g_hc.dB, ldb) && !env_on("EMM_HOST_PACK");
+        const size_t nP = (xs ? 0 : align_up(pl * (size_t)(M + N) * Kp * 4, 1024)) + 64 * 128;
         if ((st = ensure(&g_hc.dW, &g_hc.nW, nP))) return st;
         // K phases for the FP32-accurate splits at large K (EMM_HOST_KSPLIT=0/1)
         const char *ek = getenv("EMM_HOST_KSPLIT");
@@ -754,8 +770,9 @@ extern "C" int emm_sgemm_host(char transA, char transB, int64_t M, int64_t N, in
         if (ksplit && (st = ensure(&g_hc.dR, &g_hc.nR, (size_t)M * N * 4))) return st;
         return host_pipelined(transA, transB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, math,
                               (float *)g_hc.dA, (float *)g_hc.dB, (float *)g_hc.dC, g_hc.dW,
-                              ksplit ? (float *)g_hc.dR : nullptr);
+                              ksplit ? (float *)g_hc.dR : nullptr, xs);
     }
+    if ((st = ensure(&g_hc.dW, &g_hc.nW, nW))) return st;
     if (ab_used) {
         e = cudaMemcpyAsync(g_hc.dA, A, nA, cudaMemcpyHostToDevice, s);
         if (e == cudaSuccess) e = cudaMemcpyAsync(g_hc.dB, B, nB, cudaMemcpyHostToDevice, s);

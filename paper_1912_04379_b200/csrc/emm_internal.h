@@ -117,7 +117,8 @@ cudaError_t launch_tc_split_sgemm(bool a_kc, bool b_kc, const float *A, int64_t 
 // lockstep); sk_ws: zeroed stream-K scratch or NULL.
 cudaError_t launch_tc_xs_sgemm(const TcPlane &a, const TcPlane &b, int64_t M, int64_t N, int64_t K, float alpha,
                                float beta, float *C, int64_t ldc, unsigned int *ctrl, int splits, float *partial,
-                               cudaStream_t s, const PeerOut *peers = nullptr, void *sk_ws = nullptr);
+                               cudaStream_t s, const PeerOut *peers = nullptr, void *sk_ws = nullptr,
+                               const float *acc_init = nullptr, int64_t ld_init = 0);
 bool tma_legal(const void *ptr, int64_t ld);
 // A plane as the tcgen05 kernels' 2-D tensor map (K-major box {32, 128},
 // MN-major box {32, 32} with the 32B-atom 128B swizzle), OOB reads zero.

@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(TX_THREADS, 1)
                  const __grid_constant__ CUtensorMap tmC, int M, int N, int Kp, float alpha, float beta, float *C,
                  int64_t ldc, int tiles_m, int tiles_n, int group_m, int kc_stages,
                  unsigned int *__restrict__ wave_ctr, int splits, float *__restrict__ partial, const TcSk sk,
-                 const __grid_constant__ PeerOut peers) {
+                 const __grid_constant__ PeerOut peers, const float *acc_init, int64_t ld_init) {
     if (threadIdx.x == 0) EMM_TL(0);
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(TX_THREADS, 1)
         setmaxnreg_inc<TX_REGS_EPI>();
         tc_epilogue_loop<CSK, TMAC>(S, rank, warp & 3, (warp - TX_EPI_WARP0) >> 2, lane, tmem_base, acc_full,
                                     acc_empty, kc_stages, M, N, alpha, beta, C, ldc, partial, sk, peers, 2, leader,
-                                    nullptr, 0, TcCin{&tmC, cbuf, cfull},
+                                    acc_init, ld_init, TcCin{&tmC, cbuf, cfull},
                                     CSK ? reinterpret_cast<float *>(smem) : nullptr);
     }
 
@@ -307,7 +307,10 @@ __global__ void __launch_bounds__(TX_THREADS, 1)
 template <bool A_MN, bool B_MN>
 static cudaError_t launch_tx_t(const TcPlane &pa, const TcPlane &pb, int64_t M, int64_t N, int64_t Kp, float alpha,
                                float beta, float *C, int64_t ldc, unsigned int *ctrl, int splits, float *partial,
-                               cudaStream_t s, const PeerOut &peers, void *sk_ws) {
+                               cudaStream_t s, const PeerOut &peers, void *sk_ws, const float *acc_init,
+                               int64_t ld_init) {
+    if (acc_init && splits != 1) return cudaErrorInvalidValue;
+    if (acc_init) sk_ws = nullptr;   // whole tiles only
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(once, [] {
@@ -374,7 +377,8 @@ static cudaError_t launch_tx_t(const TcPlane &pa, const TcPlane &pb, int64_t M, 
                                : tc_xs_kernel<A_MN, B_MN, false, false, false>);
         auto launch = [&]() {
             return cudaLaunchKernelEx(&cfg, kern, ta, tb, tcm, (int)M, (int)N, (int)Kp, alpha, beta, C, ldc, tiles_m,
-                                      tiles_n, 8, kc_stages, wc, splits, splits > 1 ? partial : nullptr, sk, peers);
+                                      tiles_n, 8, kc_stages, wc, splits, splits > 1 ? partial : nullptr, sk, peers,
+                                      acc_init, ld_init);
         };
         // cluster split-K (sub-wave shapes, S <= 4 splits): one cluster of S
         // pairs per tile, reduced over DSMEM in the same kernel.  Opt-in
@@ -395,7 +399,8 @@ static cudaError_t launch_tx_t(const TcPlane &pa, const TcPlane &pb, int64_t M, 
             c2.dynamicSmemBytes = TX_SMEM_BYTES;
             cudaError_t ce = cudaLaunchKernelEx(&c2, tc_xs_kernel<A_MN, B_MN, false, false, true>, ta, tb, tcm, (int)M,
                                                 (int)N, (int)Kp, alpha, beta, C, ldc, tiles_m, tiles_n, 8, kc_stages,
-                                                (unsigned int *)nullptr, splits, (float *)nullptr, sk, peers);
+                                                (unsigned int *)nullptr, splits, (float *)nullptr, sk, peers,
+                                                (const float *)nullptr, (int64_t)0);
             if (ce == cudaSuccess) {
                 g_launches.fetch_add(1, std::memory_order_relaxed);
                 prof_end(s, true, ev);
@@ -423,16 +428,17 @@ static cudaError_t launch_tx_t(const TcPlane &pa, const TcPlane &pb, int64_t M, 
 
 cudaError_t launch_tc_xs_sgemm(const TcPlane &a, const TcPlane &b, int64_t M, int64_t N, int64_t K, float alpha,
                                float beta, float *C, int64_t ldc, unsigned int *ctrl, int splits, float *partial,
-                               cudaStream_t s, const PeerOut *peers, void *sk_ws) {
+                               cudaStream_t s, const PeerOut *peers, void *sk_ws, const float *acc_init,
+                               int64_t ld_init) {
     if (M > 0x7fffffffLL || N > 0x7fffffffLL || K > 0x7fffffffLL - 32) return cudaErrorInvalidValue;
     if (splits < 1 || (splits > 1 && !partial)) return cudaErrorInvalidValue;
     if (peers && (peers->n < 0 || peers->n > 8 || splits > 1)) return cudaErrorInvalidValue;
     const PeerOut pe = peers ? *peers : PeerOut{};
     const int64_t Kp = tc_kpad(K);
-    if (!a.mn && !b.mn) return launch_tx_t<false, false>(a, b, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe, sk_ws);
-    if (!a.mn && b.mn) return launch_tx_t<false, true>(a, b, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe, sk_ws);
-    if (a.mn && !b.mn) return launch_tx_t<true, false>(a, b, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe, sk_ws);
-    return launch_tx_t<true, true>(a, b, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe, sk_ws);
+    if (!a.mn && !b.mn) return launch_tx_t<false, false>(a, b, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe, sk_ws, acc_init, ld_init);
+    if (!a.mn && b.mn) return launch_tx_t<false, true>(a, b, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe, sk_ws, acc_init, ld_init);
+    if (a.mn && !b.mn) return launch_tx_t<true, false>(a, b, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe, sk_ws, acc_init, ld_init);
+    return launch_tx_t<true, true>(a, b, M, N, Kp, alpha, beta, C, ldc, ctrl, splits, partial, s, pe, sk_ws, acc_init, ld_init);
 }
 
 }  // namespace emm

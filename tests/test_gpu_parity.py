@@ -432,13 +432,18 @@ def test_torch_binding_colmajor(emm):
 @pytest.mark.parametrize("beta", [0.0, 0.5])
 @pytest.mark.parametrize("blocks", [None, (256, 512), "ksplit", "ksplit3"],
                          ids=["default", "first256-chunk512", "ksplit", "ksplit3"])
-def test_host_buffer_pipelined(emm, monkeypatch, tA, tB, beta, blocks):
+@pytest.mark.parametrize("host_pack", [False, True], ids=["xs", "planes"])
+def test_host_buffer_pipelined(emm, monkeypatch, tA, tB, beta, blocks, host_pack):
     """emm_sgemm_host above 4096 x 4096 runs the copy/compute pipeline (L-
     shaped growth over 2048-row/column blocks, the first two 1024, ragged
-    last blocks here; three streams, re-buffered planes; each GEMM region in
-    pieces with its own copy-back): same bits as the re-buffered device call
-    (K = 300 < 512: stream-K pieces sum like the sequential K loop), ldc
-    padding intact, sampled rows against the oracle."""
+    last blocks here; three streams; KN1X on the landed blocks in place, or
+    with EMM_HOST_PACK=1 re-buffered planes + KN1; each GEMM region in
+    pieces with its own copy-back): same bits as the device call of the same
+    arithmetic (default KN1X / EMM_FORCE_PACK=1; K = 300 < 512: stream-K
+    pieces sum like the sequential K loop), ldc padding intact, sampled rows
+    against the oracle."""
+    if host_pack:
+        monkeypatch.setenv("EMM_HOST_PACK", "1")
     M, N, K = 4500, 4200, 300
     if blocks == "ksplit3":   # three K phases (the middle one both reads and writes the partials)
         monkeypatch.setenv("EMM_HOST_KPHASES", "3")
@@ -460,7 +465,8 @@ def test_host_buffer_pipelined(emm, monkeypatch, tA, tB, beta, blocks):
     emm.sgemm_host(tA, tB, M, N, K, 1.25, Af, case.lda, Bf, case.ldb, beta, Cf, case.ldc)
     case.check_untouched(Cf)
     assert_close(case, Cf, R, S, T, 1e-5, rows=rows)
-    monkeypatch.setenv("EMM_FORCE_PACK", "1")
+    if host_pack:
+        monkeypatch.setenv("EMM_FORCE_PACK", "1")
     Cd = case.run(emm, "3xtf32")
     assert torch.equal(Cd.view(torch.int32), Cf.view(torch.int32))
 
