@@ -190,9 +190,13 @@ int emm_comm_unregister_input(void *comm);
 /* Test harness: `nranks` VIRTUAL ranks on the current device.  comms[r]
  * (r < nranks) receives rank r's communicator; each is used and destroyed
  * like one from emm_comm_create.  Their exchange steps run as device copies
- * + flags between distinct buffers on this GPU (no NCCL), so B and, when
- * gathered, C_full must be registered.  Each virtual rank needs its OWN
- * stream (a rank's stream waits on device flags other ranks' streams set).
+ * between distinct buffers on this GPU (no NCCL), ordered by CUDA events
+ * instead of device flags (no kernel spins on another rank's work on one
+ * GPU), so B and, when gathered, C_full must be registered.  Each virtual
+ * rank needs its OWN stream.  A call enqueues nothing until every rank of
+ * the world has made it; the last caller enqueues all ranks' work (earlier
+ * callers get 0; errors are returned to the last caller), and until then a
+ * rank's stream must receive no other work.
  * Returns 0 or EMM_ERR_COMM / 1000 + cudaError_t. */
 int emm_debug_comm_create_local(int nranks, void **comms);
 

@@ -29,10 +29,12 @@
 //    across calls through a "consumed" flag: a rank pushes call e only after
 //    its successor has finished reading call e-1.
 //
-// The flag protocol is transport-independent, so the same code also runs P
-// VIRTUAL ranks on one GPU (emm_debug_comm_create_local): distinct buffers on
-// one device instead of IPC-mapped peers — the harness the tests use to drive
-// the P > 1 paths of emm_sgemm_multi on a single B200.
+// The same code also runs P VIRTUAL ranks on one GPU
+// (emm_debug_comm_create_local): distinct buffers on one device instead of
+// IPC-mapped peers, and — since kernels on one GPU must never spin on each
+// other — the signal / wait points as CUDA events, all ranks' work enqueued
+// in dependency order once the last rank has called.  The harness the tests
+// use to drive the P > 1 paths of emm_sgemm_multi on a single B200.
 //
 // NCCL is loaded at run time (dlopen of the process's libnccl.so.2, normally
 // the one torch already loaded), so the library has no link-time NCCL
@@ -98,10 +100,35 @@ constexpr size_t CHUNK_BYTES = 64u << 20;    // B forwarding granularity
 
 // P virtual ranks on one device (emm_debug_comm_create_local): the tables
 // the IPC exchange fills in the multi-process case.
+// Arguments of one emm_sgemm_multi call (kept by virtual ranks until the
+// last rank of the world has called, see emm_sgemm_multi).
+struct MultiArgs {
+    char transA, transB;
+    int64_t M, N, K;
+    float alpha;
+    const float *A_local;
+    int64_t lda;
+    float *B;
+    int64_t ldb;
+    int root;
+    float beta;
+    float *C_local;
+    int64_t ldc;
+    float *C_full;
+    int64_t ldc_full;
+    cudaStream_t s;
+    emm_math_t math;
+};
+
+struct Comm;
 struct World {
     int nranks = 0;
     std::mutex mu;
     int alive = 0;
+    std::vector<cudaEvent_t> ev[MAXR];   // per rank: the signal slots as events
+    MultiArgs pending[MAXR] = {};         // per rank: the call waiting for the others
+    Comm *pending_comm[MAXR] = {};
+    int arrived = 0;
     uint32_t *flags[MAXR] = {};
     float *in[MAXR] = {};
     size_t in_bytes[MAXR] = {};
@@ -493,6 +520,9 @@ extern "C" int emm_comm_destroy(void *comm) {
     if (c->local()) {
         std::lock_guard<std::mutex> g(c->world->mu);
         c->world->flags[c->rank] = nullptr;
+        for (auto e : c->world->ev[c->rank]) cudaEventDestroy(e);
+        c->world->ev[c->rank].clear();
+        c->world->pending_comm[c->rank] = nullptr;
     }
     if (c->flags) cudaFree(c->flags);
     for (auto e : c->evs) cudaEventDestroy(e);
@@ -533,32 +563,79 @@ static Chunks make_chunks(bool bN, int64_t N, int64_t K, int64_t panel) {
     return ch;
 }
 
-extern "C" int emm_sgemm_multi(void *comm, char transA, char transB, int64_t M, int64_t N, int64_t K, float alpha,
-                               const float *A_local, int64_t lda, float *B, int64_t ldb, int root, float beta,
-                               float *C_local, int64_t ldc, float *C_full, int64_t ldc_full, void *stream,
-                               emm_math_t math) {
-    if (!comm) return EMM_ERR_COMM;
-    Comm *c = static_cast<Comm *>(comm);
+namespace emm {
+namespace {
+
+// ---- device-side synchronisation of the copy-engine data plane -----------
+// Across GPUs (one process per GPU, IPC-mapped flag words): release-store /
+// acquire-spin kernels on the epoch.  Virtual ranks on ONE GPU must not spin
+// on each other (nothing guarantees that separately launched kernels run at
+// the same time): there the same signal / wait points are CUDA events, and
+// the world enqueues all ranks' work in dependency order once every rank has
+// called (emm_sgemm_multi).
+cudaEvent_t world_event(World *w, int rank, int slot) {
+    std::lock_guard<std::mutex> g(w->mu);
+    auto &v = w->ev[rank];
+    while ((int)v.size() <= slot) {
+        cudaEvent_t e;
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+        v.push_back(e);
+    }
+    return v[slot];
+}
+// signal slot `slot` of each rank in targets[0..n)
+int sync_signal(Comm *c, const int *targets, int n, int slot, uint32_t epoch, cudaStream_t s) {
+    if (n <= 0) return 0;
+    if (c->local()) {
+        for (int i = 0; i < n; ++i) {
+            cudaEvent_t e = world_event(c->world.get(), targets[i], slot);
+            if (!e) return EMM_ERR_NOMEM;
+            int st = cuda_st(cudaEventRecord(e, s));
+            if (st) return st;
+        }
+        return 0;
+    }
+    uint32_t *fs[MAXR];
+    for (int i = 0; i < n; ++i) fs[i] = c->peer_flags[targets[i]] + slot;
+    return cuda_st(flag_set(fs, n, epoch, s));
+}
+// wait for this rank's slots[0..n) to reach the epoch
+int sync_wait(Comm *c, const int *slots, int n, uint32_t epoch, cudaStream_t s) {
+    if (n <= 0) return 0;
+    if (c->local()) {
+        for (int i = 0; i < n; ++i) {
+            cudaEvent_t e = world_event(c->world.get(), c->rank, slots[i]);
+            if (!e) return EMM_ERR_NOMEM;
+            int st = cuda_st(cudaStreamWaitEvent(s, e, 0));
+            if (st) return st;
+        }
+        return 0;
+    }
+    const uint32_t *fw[MAXR];
+    for (int i = 0; i < n; ++i) fw[i] = c->flags + slots[i];
+    return cuda_st(flag_wait(fw, n, epoch, s));
+}
+
+// Everything one rank enqueues for a call, up to (and including) its "done"
+// signals; done_wait then completes the gathered output.
+int enqueue_main(Comm *c, const MultiArgs &a, bool *done_pending) {
+    *done_pending = false;
+    const char transA = a.transA, transB = a.transB;
+    const int64_t M = a.M, N = a.N, K = a.K;
+    const float alpha = a.alpha, beta = a.beta;
+    const float *A_local = a.A_local;
+    const int64_t lda = a.lda, ldb = a.ldb, ldc = a.ldc, ldc_full = a.ldc_full;
+    float *B = a.B, *C_local = a.C_local, *C_full = a.C_full;
+    const int root = a.root;
+    const emm_math_t math = a.math;
+    cudaStream_t s = a.s;
     Nccl &n = nccl();
-    if (root < 0 || root >= c->nranks) return EMM_ERR_COMM;
     const int P = c->nranks;
     const bool bN = (transB == 'N' || transB == 'n');
-    if (K >= 0 && ldb != (bN ? (K > 1 ? K : 1) : (N > 1 ? N : 1))) return -10;  // panels must be contiguous
-    if (!c->local()) {
-        if (!n.ok) return EMM_ERR_COMM;
-        ncclResult_t async_err = ncclSuccess;
-        n.getAsyncError(c->nc, &async_err);
-        if (async_err != ncclSuccess) return nccl_status(async_err);
-    }
     int64_t row0 = 0, rows = 0;
     emm_row_partition(M, P, c->rank, &row0, &rows);
-    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const size_t b_bytes = (size_t)(bN ? K * N : N * K) * 4;
-    int st = check_args(transA, transB, rows, N, K, lda, ldb, ldc > 0 ? ldc : 1);
-    if (!st) st = check_device();
-    if (st) return st;
-    if (C_full && ldc_full < (M > 1 ? M : 1)) return -17;
-
+    int st = 0;
     // data plane: copy engines + flags when B (and C_full, if gathered) are
     // registered; NCCL otherwise.  The choice depends only on arguments every
     // rank passes identically (and registrations, which are collective), so
@@ -582,16 +659,14 @@ extern "C" int emm_sgemm_multi(void *comm, char transA, char transB, int64_t M, 
     } else if (ce_out) {
         out_peer[c->rank] = c->out_local;
     }
-    const uint32_t epoch = ++c->epoch;
+    const uint32_t epoch = ++c->epoch;   // identical on every rank (collective call order)
     const int pos = (c->rank - root + P) % P;       // position in the ring that starts at root
     const int succ = (c->rank + 1) % P, pred = (c->rank - 1 + P) % P;
     const bool has_succ = pos < P - 1, has_pred = pos > 0;
 
-    // Gate the communication stream on the caller's stream (B / C ready).
-    cudaEvent_t e0 = ev_at(c, 0);
-    if (!e0) return EMM_ERR_NOMEM;
-    st = cuda_st(cudaEventRecord(e0, s));
-    if (!st) st = cuda_st(cudaStreamWaitEvent(c->comm_stream, e0, 0));
+    // Gate the communication stream on the caller's stream (B / C ready;
+    // e0 was recorded on it when the call was made).
+    st = cuda_st(cudaStreamWaitEvent(c->comm_stream, ev_at(c, 0), 0));
     if (st) return st;
 
     const int64_t panel = bN ? emm_multi_panel_cols(N) : N;
@@ -660,27 +735,26 @@ extern "C" int emm_sgemm_multi(void *comm, char transA, char transB, int64_t M, 
         const int nchunk = (int)ch.off.size() - 1;
         if (has_succ) {
             // the successor finished reading the previous call's B
-            const uint32_t *fc = c->flags + FL_CONSUMED;
-            st = cuda_st(flag_wait(&fc, 1, epoch - 1, c->comm_stream));
+            const int sc = FL_CONSUMED;
+            st = sync_wait(c, &sc, 1, epoch - 1, c->comm_stream);
             for (int j = 0; j < nchunk && !st; ++j) {
                 if (has_pred) {
-                    const uint32_t *fb = c->flags + FL_BREADY + j;
-                    st = cuda_st(flag_wait(&fb, 1, epoch, c->comm_stream));
+                    const int sb = FL_BREADY + j;
+                    st = sync_wait(c, &sb, 1, epoch, c->comm_stream);
                 }
                 const size_t o = ch.off[j], nb = ch.off[j + 1] - o;
                 if (!st && nb)
                     st = cuda_st(cudaMemcpyAsync(reinterpret_cast<uint8_t *>(in_succ) + o,
                                                  reinterpret_cast<const uint8_t *>(B) + o, nb,
                                                  cudaMemcpyDeviceToDevice, c->comm_stream));
-                uint32_t *fs = c->peer_flags[succ] + FL_BREADY + j;
-                if (!st) st = cuda_st(flag_set(&fs, 1, epoch, c->comm_stream));
+                if (!st) st = sync_signal(c, &succ, 1, FL_BREADY + j, epoch, c->comm_stream);
             }
         }
         const int npanel = (int)ch.pc.size() - 1;
         for (int p = 0; p < npanel && !st; ++p) {
             if (has_pred && ch.pc[p + 1] > ch.pc[p]) {
-                const uint32_t *fb = c->flags + FL_BREADY + (ch.pc[p + 1] - 1);
-                st = cuda_st(flag_wait(&fb, 1, epoch, s));
+                const int sb = FL_BREADY + (int)(ch.pc[p + 1] - 1);
+                st = sync_wait(c, &sb, 1, epoch, s);
             }
             if (st) break;
             if (bN) {
@@ -698,8 +772,7 @@ extern "C" int emm_sgemm_multi(void *comm, char transA, char transB, int64_t M, 
         if (!st) st = cuda_st(cudaStreamWaitEvent(s, ef, 0));
         // (always, whatever this call's root: the ring predecessor waits for
         // it before pushing the next call's B, which may start elsewhere)
-        uint32_t *fp = c->peer_flags[pred] + FL_CONSUMED;
-        if (!st) st = cuda_st(flag_set(&fp, 1, epoch, s));
+        if (!st) st = sync_signal(c, &pred, 1, FL_CONSUMED, epoch, s);
     } else if (!st && bN && N > 0) {
         // ---- NCCL: column panels of B, contiguous K x nc ranges; the GEMM of
         // panel c waits only for panel c's broadcast.
@@ -736,19 +809,13 @@ extern "C" int emm_sgemm_multi(void *comm, char transA, char transB, int64_t M, 
                 st = cuda_st(cudaMemcpy2DAsync(out_peer[r] + row0, (size_t)ldc_full * 4, C_local, (size_t)ldc * 4,
                                                (size_t)rows * 4, (size_t)N, cudaMemcpyDeviceToDevice, s));
         if (!st && P > 1) {
-            // every rank tells every rank its rows are in place, then waits
-            // for all of them: C_full is complete on `s` after this.
-            uint32_t *fs[MAXR];
-            const uint32_t *fw[MAXR];
-            int k = 0;
+            // every rank tells every rank its rows are in place (then, in
+            // done_wait, waits for all of them: C_full is complete on `s`)
+            int targets[MAXR], k = 0;
             for (int r = 0; r < P; ++r)
-                if (r != c->rank) {
-                    fs[k] = c->peer_flags[r] + FL_DONE + c->rank;
-                    fw[k] = c->flags + FL_DONE + r;
-                    ++k;
-                }
-            st = cuda_st(flag_set(fs, k, epoch, s));
-            if (!st) st = cuda_st(flag_wait(fw, k, epoch, s));
+                if (r != c->rank) targets[k++] = r;
+            st = sync_signal(c, targets, k, FL_DONE + c->rank, epoch, s);
+            *done_pending = !st;
         }
         return st;
     }
@@ -789,3 +856,76 @@ extern "C" int emm_sgemm_multi(void *comm, char transA, char transB, int64_t M, 
     }
     return st;
 }
+
+int done_wait(Comm *c, cudaStream_t s) {
+    int slots[MAXR], k = 0;
+    for (int r = 0; r < c->nranks; ++r)
+        if (r != c->rank) slots[k++] = FL_DONE + r;
+    return sync_wait(c, slots, k, c->epoch, s);
+}
+
+}  // namespace
+}  // namespace emm
+
+extern "C" int emm_sgemm_multi(void *comm, char transA, char transB, int64_t M, int64_t N, int64_t K, float alpha,
+                               const float *A_local, int64_t lda, float *B, int64_t ldb, int root, float beta,
+                               float *C_local, int64_t ldc, float *C_full, int64_t ldc_full, void *stream,
+                               emm_math_t math) {
+    if (!comm) return EMM_ERR_COMM;
+    Comm *c = static_cast<Comm *>(comm);
+    Nccl &n = nccl();
+    if (root < 0 || root >= c->nranks) return EMM_ERR_COMM;
+    const int P = c->nranks;
+    const bool bN = (transB == 'N' || transB == 'n');
+    if (K >= 0 && ldb != (bN ? (K > 1 ? K : 1) : (N > 1 ? N : 1))) return -10;  // panels must be contiguous
+    if (!c->local()) {
+        if (!n.ok) return EMM_ERR_COMM;
+        ncclResult_t async_err = ncclSuccess;
+        n.getAsyncError(c->nc, &async_err);
+        if (async_err != ncclSuccess) return nccl_status(async_err);
+    }
+    int64_t row0 = 0, rows = 0;
+    emm_row_partition(M, P, c->rank, &row0, &rows);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    int st = check_args(transA, transB, rows, N, K, lda, ldb, ldc > 0 ? ldc : 1);
+    if (!st) st = check_device();
+    if (st) return st;
+    if (C_full && ldc_full < (M > 1 ? M : 1)) return -17;
+    // the caller's stream gates this call's reads of B / C
+    cudaEvent_t e0 = ev_at(c, 0);
+    if (!e0) return EMM_ERR_NOMEM;
+    if ((st = cuda_st(cudaEventRecord(e0, s)))) return st;
+    const MultiArgs args{transA, transB, M, N, K, alpha, A_local, lda, B, ldb, root, beta,
+                         C_local, ldc, C_full, ldc_full, s, math};
+    if (!c->local() || P == 1) {
+        bool dw = false;
+        st = enqueue_main(c, args, &dw);
+        if (!st && dw) st = done_wait(c, s);
+        return st;
+    }
+    // Virtual ranks: nothing is enqueued until every rank of the world has
+    // called; the last caller enqueues all ranks' work in dependency order
+    // (the ring from root, then every rank's wait for the others' "done"),
+    // so that each event a stream waits on is recorded first.  Earlier calls
+    // return 0 (errors surface on the last call); until then a rank's stream
+    // must not receive other work.
+    World *w = c->world.get();
+    std::vector<std::pair<Comm *, MultiArgs>> calls;
+    {
+        std::lock_guard<std::mutex> g(w->mu);
+        w->pending[c->rank] = args;
+        w->pending_comm[c->rank] = c;
+        if (++w->arrived < P) return 0;
+        w->arrived = 0;
+        for (int k = 0; k < P; ++k) {
+            const int r = (root + k) % P;
+            calls.emplace_back(w->pending_comm[r], w->pending[r]);
+        }
+    }
+    bool dw[MAXR] = {};
+    for (int k = 0; k < P && !st; ++k) st = enqueue_main(calls[k].first, calls[k].second, &dw[k]);
+    for (int k = 0; k < P && !st; ++k)
+        if (dw[k]) st = done_wait(calls[k].first, calls[k].second.s);
+    return st;
+}
+

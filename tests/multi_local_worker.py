@@ -1,16 +1,16 @@
 """Worker: emm_sgemm_multi with P VIRTUAL ranks on one GPU
-(emm_debug_comm_create_local).  Run as a subprocess by
-tests/test_gpu_multi_local.py with CUDA_DEVICE_MAX_CONNECTIONS=32 set before
-CUDA starts: every virtual rank has its own stream (plus the library's
-communication stream), and the ranks' streams wait on device flags other
-ranks' streams set, so no two of them may share a hardware queue.
+(emm_debug_comm_create_local), run as a subprocess by
+tests/test_gpu_multi_local.py.
 
 For each case the P ranks are driven through the UNMODIFIED library entry
-points in one host thread (rank 0 .. P-1 one after the other: all waits are
-device-side), each with its own row block of op(A) (emm_row_partition), its
-own B buffer (B valid on `root` only; registered, so B travels along the ring
-by copy-engine peer copies + flags) and its own C_full (registered: the
-tensor-core epilogue stores every tile into all P copies, other modes copy).
+points in one host thread (rank 0 .. P-1 one after the other; the library
+enqueues the whole collective when the last rank has called, with the ranks'
+signal / wait points as CUDA events — no kernel ever spins on another rank's
+work on this one GPU), each with its own stream, its own row block of op(A)
+(emm_row_partition), its own B buffer (B valid on `root` only; registered, so
+B travels along the ring by peer copies in chunks) and its own C_full
+(registered: the tensor-core epilogue stores every tile into all P copies,
+other modes copy).
 
 Checks (SURVEY.md §4 "fake multi-GPU on one device"):
 * every rank's B buffer ends bit-identical to root's;
