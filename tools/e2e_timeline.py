@@ -43,7 +43,7 @@ def main():
                  key=lambda x: x[0])
     t_first = min([k[0] for k in kern] + [c[0] for c in cpy])
     t_last = max([k[1] for k in kern] + [c[1] for c in cpy])
-    gemm = [k for k in kern if "sgemm" in k[2] or "tc1w" in k[2]]
+    gemm = [k for k in kern if "sgemm" in k[2] or "tc1w" in k[2] or "tc_xs" in k[2]]
     busy, last_end = 0.0, None
     for s, e, _ in kern:   # union of kernel intervals
         if last_end is None or s >= last_end:
