@@ -55,6 +55,9 @@ def _cases():
                  "EMM_WIDE": rng.choice([None, None, "1"]), "EMM_FFMA_CLASSIC": rng.choice([None, None, "1"]),
                  "EMM_PREF4": rng.choice([None, "1", "1", "0"])}))
         out[-1]["env"]["EMM_SPLIT"] = rng.choice([None, None, "pass"])   # KN1 instead of KN1X
+        out[-1]["env"]["EMM_SKINNY_TC"] = rng.choice([None, None, "1"])   # KN9T at any size
+        out[-1]["env"]["EMM_CSK"] = rng.choice([None, None, "1"])          # cluster split-K
+        out[-1]["env"]["EMM_XS_RN"] = rng.choice([None, None, None, "1"])  # KN1X with rounded big parts
     return out
 
 
