@@ -45,3 +45,14 @@ def run(cases, timeout=900):
 @pytest.mark.parametrize("case", CASES, ids=lambda c: "P{}_{}x{}x{}_{}_{}_{}{}".format(*c[:7], "_gather" if c[7] else ""))
 def test_virtual_ranks(case):
     run([list(case)])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P", [2, 8])
+def test_virtual_ranks_c5_fullsize(P):
+    """BASELINE configs[4] (32768^3) row-sharded over P virtual ranks in the
+    bench's multi-GPU launch configuration: B intact on every rank, sampled
+    shard rows vs the oracle, Freivalds over all of C."""
+    p = subprocess.run([sys.executable, os.path.join(HERE, "multi_c5_worker.py"), str(P)],
+                       capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0 and "ALL OK" in p.stdout, (p.stdout[-3000:] + p.stderr[-3000:])
