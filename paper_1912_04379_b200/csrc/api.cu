@@ -856,7 +856,9 @@ extern "C" const char *emm_strerror(int status) {
     return "unknown status";
 }
 
-extern "C" const char *emm_version(void) { return "emm 0.2 (sm_100a: tcgen05 3xTF32 / TF32+BF16 / 1xTF32, TMA-fed FFMA)"; }
+extern "C" const char *emm_version(void) {
+    return "emm 0.3 (sm_100a: tcgen05 3xTF32 split in the kernel / TF32+BF16 / 1xTF32, TMA-fed FFMA, TMEM-fed skinny)";
+}
 
 extern "C" uint64_t emm_launch_count(void) { return g_launches.load(); }
 
