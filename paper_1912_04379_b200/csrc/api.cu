@@ -113,10 +113,20 @@ static bool math_ok(emm_math_t m) {
 // prohibitive" regime): one launch of the tiny FFMA kernel (KN10),
 // which is FP32-accurate.
 // EMM_SMALL_FLOPS (environment) overrides the threshold; 0 disables it.
-static bool small_problem(int64_t M, int64_t N, int64_t K) {
+// Tensor-core modes also need the tiny kernel's 32 x 32 tiles to fit one
+// wave: past it (e.g. 400^3: 169 tiles on 148 SMs) the tiny kernel takes a
+// second round (24.6 us) while KN1X takes 19.5 (round 2, measured:
+// 352-384^3 tiny 16.4 vs 19.4-21.2 us; 400-420^3 tiny 24.6 vs 18.4-19.5 us).
+// The FFMA mode keeps the flop threshold alone (its CUDA-core kernels take
+// 39-46 us there).
+static bool small_problem(int64_t M, int64_t N, int64_t K, emm_math_t math = EMM_MATH_FFMA) {
     double thr = (double)(1 << 27);   // measured crossover tiny vs tensor core: between 333^3 and 512^3
-    if (const char *e = getenv("EMM_SMALL_FLOPS")) thr = atof(e);
-    return 2.0 * (double)M * (double)N * (double)K <= thr;
+    const char *e = getenv("EMM_SMALL_FLOPS");
+    if (e) thr = atof(e);
+    if (2.0 * (double)M * (double)N * (double)K > thr) return false;
+    if (e || math == EMM_MATH_FFMA) return true;
+    const double tiles = (double)((M + 31) / 32) * (double)((N + 31) / 32);
+    return tiles <= (double)tc_num_sms();
 }
 
 // How one tensor-core call runs:
@@ -291,7 +301,7 @@ static Plan make_plan(char tA, char tB, int64_t M, int64_t N, int64_t K, emm_mat
 static size_t ws_bytes(int64_t M, int64_t N, int64_t K, emm_math_t math) {
     if (math == EMM_MATH_FFMA || M == 0 || N == 0 || K == 0) return 0;
     if (M <= SKINNY_MAX || N <= SKINNY_MAX) return skinny_tc_workspace_bytes(M, N, K);   // KN9T (upper bound)
-    if (small_problem(M, N, K)) return 0;
+    if (small_problem(M, N, K, math)) return 0;
     return make_plan('N', 'N', M, N, K, math, /*direct=*/false).total;
 }
 
@@ -359,7 +369,7 @@ extern "C" int emm_sgemm_ex(char transA, char transB, int64_t M, int64_t N, int6
             launch_skinny_sgemm(!is_n(transA), !is_n(transB), M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, s));
     }
 
-    if (small_problem(M, N, K))
+    if (small_problem(M, N, K, math))
         return cuda_status(
             launch_tiny_sgemm(!is_n(transA), !is_n(transB), M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, s));
     if (math == EMM_MATH_FFMA)
