@@ -4,8 +4,8 @@
 // (PAPER.md:418-420): for a 64^3 or 100^3 problem the cost is launches and
 // DRAM round trips, not flops.  One launch, no workspace, 32x32 output tiles
 // (many CTAs even for tiny M, N), each 64-wide K chunk loaded with all of a
-// thread's loads in flight at once (16 per operand), FP32 FFMA in increasing
-// k with promotion every 256 of K (FP32-accurate for every math mode).
+// thread's loads in flight at once (8 per operand), FP32 FFMA with promotion
+// every 256 of K (FP32-accurate for every math mode).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -17,17 +17,30 @@ namespace emm {
 constexpr int TY_T = 32;    // output tile (rows and columns)
 constexpr int TY_KC = 64;   // K per chunk
 
+// Block = 256 threads on one 32 x 32 tile: four groups of 64 threads split
+// each 64-wide K chunk in quarters (group g: k = 16g .. 16g+15), a thread
+// computes a 4 x 4 sub-tile from two 128-bit shared loads per k (16 FMAs per
+// 2 loads; round 1's 2 x 2 per thread needed one load per FMA and was
+// LDS-bound), promotes into its master every 256 of K, and the four groups'
+// masters are added in fixed order g = 0..3 at the end (deterministic).
+constexpr int TY_LD = TY_T + 4;   // shared row pitch: 16-B aligned 4-row / 4-column groups
+
 template <bool TA, bool TB>
 __global__ void __launch_bounds__(256) tiny_sgemm_kernel(int64_t M, int64_t N, int64_t K, float alpha,
                                                          const float *__restrict__ A, int64_t lda,
                                                          const float *__restrict__ B, int64_t ldb, float beta,
                                                          float *__restrict__ C, int64_t ldc) {
-    __shared__ float As[TY_KC][TY_T + 1];   // As[k][row]
-    __shared__ float Bs[TY_KC][TY_T + 1];   // Bs[k][col]
+    __shared__ __align__(16) float sm[2 * TY_KC * TY_LD];   // As[k][row] | Bs[k][col]; reused for the reduction
+    float *As = sm, *Bs = sm + TY_KC * TY_LD;
     const int tid = threadIdx.x;
     const int64_t m0 = (int64_t)blockIdx.x * TY_T, n0 = (int64_t)blockIdx.y * TY_T;
-    const int tx = tid & 15, ty = tid >> 4;   // outputs rows ty*2+{0,1}, cols tx*2+{0,1}
-    float acc[2][2] = {{0.f, 0.f}, {0.f, 0.f}}, mas[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+    const int g = tid >> 6, lt = tid & 63;
+    const int ty = lt >> 3, tx = lt & 7;   // rows 4ty..4ty+3, cols 4tx..4tx+3
+    float acc[4][4], mas[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = mas[i][j] = 0.0f;
     float ra[8], rb[8];
     // element e of a 32 x 64 chunk: consecutive threads along the contiguous dimension
     auto load = [&](int64_t k0) {
@@ -51,41 +64,51 @@ __global__ void __launch_bounds__(256) tiny_sgemm_kernel(int64_t M, int64_t N, i
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             const int e = tid + 256 * i;
-            As[TA ? e % TY_KC : e / TY_T][TA ? e / TY_KC : e % TY_T] = ra[i];
-            Bs[TB ? e / TY_T : e % TY_KC][TB ? e % TY_T : e / TY_KC] = rb[i];
+            As[(TA ? e % TY_KC : e / TY_T) * TY_LD + (TA ? e / TY_KC : e % TY_T)] = ra[i];
+            Bs[(TB ? e / TY_T : e % TY_KC) * TY_LD + (TB ? e % TY_T : e / TY_KC)] = rb[i];
         }
         __syncthreads();
         if (ch + 1 < nchunks) load((ch + 1) * TY_KC);
-#pragma unroll 16
-        for (int k = 0; k < TY_KC; ++k) {
-            const float a0 = As[k][ty * 2], a1 = As[k][ty * 2 + 1];
-            const float b0 = Bs[k][tx * 2], b1 = Bs[k][tx * 2 + 1];
-            acc[0][0] = fmaf(a0, b0, acc[0][0]);
-            acc[0][1] = fmaf(a0, b1, acc[0][1]);
-            acc[1][0] = fmaf(a1, b0, acc[1][0]);
-            acc[1][1] = fmaf(a1, b1, acc[1][1]);
+#pragma unroll
+        for (int kk = 0; kk < TY_KC / 4; ++kk) {
+            const int k = 16 * g + kk;
+            const float4 a = *reinterpret_cast<const float4 *>(As + k * TY_LD + 4 * ty);
+            const float4 b = *reinterpret_cast<const float4 *>(Bs + k * TY_LD + 4 * tx);
+            const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
         }
         if ((ch + 1) % (256 / TY_KC) == 0 || ch + 1 == nchunks) {
 #pragma unroll
-            for (int i = 0; i < 2; ++i)
+            for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int j = 0; j < 2; ++j) {
+                for (int j = 0; j < 4; ++j) {
                     mas[i][j] += acc[i][j];
                     acc[i][j] = 0.0f;
                 }
         }
     }
+    // the four K-groups' partials: red[g][col][row], summed in order g = 0..3
+    __syncthreads();
+    float *red = sm;   // 4 x 32 x 32 floats = 16 KB <= 2 x 64 x 36 x 4
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-        const int64_t col = n0 + tx * 2 + j;
-        if (col >= N) continue;
+    for (int j = 0; j < 4; ++j)
+        *reinterpret_cast<float4 *>(red + g * 1024 + (4 * tx + j) * 32 + 4 * ty) =
+            make_float4(mas[0][j], mas[1][j], mas[2][j], mas[3][j]);
+    __syncthreads();
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-            const int64_t row = m0 + ty * 2 + i;
-            if (row < M) {
-                float *d = C + row + col * ldc;
-                *d = beta == 0.0f ? alpha * mas[i][j] : fmaf(beta, *d, alpha * mas[i][j]);
-            }
+    for (int q = 0; q < 4; ++q) {
+        const int o = tid + 256 * q;   // output (row = o % 32, col = o / 32): coalesced along rows
+        const int row = o & 31, colo = o >> 5;
+        float v = red[o];
+#pragma unroll
+        for (int gg = 1; gg < 4; ++gg) v += red[gg * 1024 + o];
+        const int64_t grow = m0 + row, gcol = n0 + colo;
+        if (grow < M && gcol < N) {
+            float *d = C + grow + gcol * ldc;
+            *d = beta == 0.0f ? alpha * v : fmaf(beta, *d, alpha * v);
         }
     }
 }
