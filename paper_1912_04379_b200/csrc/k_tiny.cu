@@ -23,15 +23,28 @@ constexpr int TY_KC = 64;   // K per chunk
 // 2 loads; round 1's 2 x 2 per thread needed one load per FMA and was
 // LDS-bound), promotes into its master every 256 of K, and the four groups'
 // masters are added in fixed order g = 0..3 at the end (deterministic).
+// Operands reach shared memory by cp.async (4-byte, zero-filled outside the
+// matrices, transposed on the fly) in a TY_ST-deep ring of K chunks, so up to
+// TY_ST chunks' DRAM latencies overlap instead of one per chunk.
 constexpr int TY_LD = TY_T + 4;   // shared row pitch: 16-B aligned 4-row / 4-column groups
+constexpr int TY_ST = 4;          // chunks in flight
+constexpr int TY_STAGE = 2 * TY_KC * TY_LD;   // floats per stage: As[k][row] | Bs[k][col]
+constexpr int TY_SMEM = TY_ST * TY_STAGE * 4;
+
+// 4-byte async copy, zero-filled (nothing read; `base` is a valid dummy
+// address) when the element is outside the matrix
+__device__ __forceinline__ void ty_cp4(float *dst, const float *src, const float *base, bool ok) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(ok ? src : base), "r"(ok ? 4 : 0)
+                 : "memory");
+}
 
 template <bool TA, bool TB>
 __global__ void __launch_bounds__(256) tiny_sgemm_kernel(int64_t M, int64_t N, int64_t K, float alpha,
                                                          const float *__restrict__ A, int64_t lda,
                                                          const float *__restrict__ B, int64_t ldb, float beta,
                                                          float *__restrict__ C, int64_t ldc) {
-    __shared__ __align__(16) float sm[2 * TY_KC * TY_LD];   // As[k][row] | Bs[k][col]; reused for the reduction
-    float *As = sm, *Bs = sm + TY_KC * TY_LD;
+    extern __shared__ __align__(16) float sm[];
     const int tid = threadIdx.x;
     const int64_t m0 = (int64_t)blockIdx.x * TY_T, n0 = (int64_t)blockIdx.y * TY_T;
     const int g = tid >> 6, lt = tid & 63;
@@ -41,34 +54,36 @@ __global__ void __launch_bounds__(256) tiny_sgemm_kernel(int64_t M, int64_t N, i
     for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = mas[i][j] = 0.0f;
-    float ra[8], rb[8];
-    // element e of a 32 x 64 chunk: consecutive threads along the contiguous dimension
-    auto load = [&](int64_t k0) {
+    // chunk ch into its ring stage: element e of a 32 x 64 chunk, consecutive
+    // threads along the contiguous dimension of the source
+    auto issue = [&](int64_t ch) {
+        float *As = sm + (ch % TY_ST) * TY_STAGE, *Bs = As + TY_KC * TY_LD;
+        const int64_t k0 = ch * TY_KC;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             const int e = tid + 256 * i;
             const int r = TA ? e / TY_KC : e % TY_T;
             const int k = TA ? e % TY_KC : e / TY_T;
             const int64_t gr = m0 + r, gk = k0 + k;
-            ra[i] = (gr < M && gk < K) ? __ldg(TA ? A + gk + gr * lda : A + gr + gk * lda) : 0.0f;
+            ty_cp4(As + k * TY_LD + r, TA ? A + gk + gr * lda : A + gr + gk * lda, A, gr < M && gk < K);
             const int c = TB ? e % TY_T : e / TY_KC;
             const int kb = TB ? e / TY_T : e % TY_KC;
             const int64_t gc = n0 + c, gkb = k0 + kb;
-            rb[i] = (gc < N && gkb < K) ? __ldg(TB ? B + gc + gkb * ldb : B + gkb + gc * ldb) : 0.0f;
+            ty_cp4(Bs + kb * TY_LD + c, TB ? B + gc + gkb * ldb : B + gkb + gc * ldb, B, gc < N && gkb < K);
         }
+        asm volatile("cp.async.commit_group;" ::: "memory");
     };
     const int64_t nchunks = (K + TY_KC - 1) / TY_KC;
-    load(0);
-    for (int64_t ch = 0; ch < nchunks; ++ch) {
-        __syncthreads();
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int e = tid + 256 * i;
-            As[(TA ? e % TY_KC : e / TY_T) * TY_LD + (TA ? e / TY_KC : e % TY_T)] = ra[i];
-            Bs[(TB ? e / TY_T : e % TY_KC) * TY_LD + (TB ? e % TY_T : e / TY_KC)] = rb[i];
-        }
-        __syncthreads();
-        if (ch + 1 < nchunks) load((ch + 1) * TY_KC);
+    for (int c = 0; c < TY_ST - 1; ++c)
+        if (c < nchunks) issue(c);
+        else asm volatile("cp.async.commit_group;" ::: "memory");   // keep the group count uniform
+    for (int64_t ch = 0; ch < nchunks; ++ch) {
+        if (ch + TY_ST - 1 < nchunks) issue(ch + TY_ST - 1);
+        else asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group %0;" ::"n"(TY_ST - 1) : "memory");   // chunk ch (this thread's copies)
+        __syncthreads();                                                         // ... and everyone's
+        const float *As = sm + (ch % TY_ST) * TY_STAGE, *Bs = As + TY_KC * TY_LD;
 #pragma unroll
         for (int kk = 0; kk < TY_KC / 4; ++kk) {
             const int k = 16 * g + kk;
@@ -89,10 +104,11 @@ __global__ void __launch_bounds__(256) tiny_sgemm_kernel(int64_t M, int64_t N, i
                     acc[i][j] = 0.0f;
                 }
         }
+        __syncthreads();   // stage ch % TY_ST is refilled by the next iteration's issue
     }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
     // the four K-groups' partials: red[g][col][row], summed in order g = 0..3
-    __syncthreads();
-    float *red = sm;   // 4 x 32 x 32 floats = 16 KB <= 2 x 64 x 36 x 4
+    float *red = sm;   // 4 x 32 x 32 floats = 16 KB <= the ring
 #pragma unroll
     for (int j = 0; j < 4; ++j)
         *reinterpret_cast<float4 *>(red + g * 1024 + (4 * tx + j) * 32 + 4 * ty) =
@@ -119,12 +135,21 @@ cudaError_t launch_tiny_sgemm(bool tA, bool tB, int64_t M, int64_t N, int64_t K,
     const int64_t gx = (M + TY_T - 1) / TY_T, gy = (N + TY_T - 1) / TY_T;
     if (gx > 0x7fffffffLL || gy > 65535) return cudaErrorInvalidConfiguration;
     const dim3 grid((unsigned)gx, (unsigned)gy);
+    static const cudaError_t attr = [] {
+        cudaError_t e = cudaSuccess;
+        const void *fs[4] = {(const void *)tiny_sgemm_kernel<false, false>, (const void *)tiny_sgemm_kernel<false, true>,
+                             (const void *)tiny_sgemm_kernel<true, false>, (const void *)tiny_sgemm_kernel<true, true>};
+        for (int i = 0; i < 4 && e == cudaSuccess; ++i)
+            e = cudaFuncSetAttribute(fs[i], cudaFuncAttributeMaxDynamicSharedMemorySize, TY_SMEM);
+        return e;
+    }();
+    if (attr != cudaSuccess) return attr;
     cudaEvent_t ev = nullptr;
     prof_begin(s, true, &ev);
-    if (!tA && !tB) tiny_sgemm_kernel<false, false><<<grid, 256, 0, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
-    else if (!tA && tB) tiny_sgemm_kernel<false, true><<<grid, 256, 0, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
-    else if (tA && !tB) tiny_sgemm_kernel<true, false><<<grid, 256, 0, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
-    else tiny_sgemm_kernel<true, true><<<grid, 256, 0, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    if (!tA && !tB) tiny_sgemm_kernel<false, false><<<grid, 256, TY_SMEM, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    else if (!tA && tB) tiny_sgemm_kernel<false, true><<<grid, 256, TY_SMEM, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    else if (tA && !tB) tiny_sgemm_kernel<true, false><<<grid, 256, TY_SMEM, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    else tiny_sgemm_kernel<true, true><<<grid, 256, TY_SMEM, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     prof_end(s, true, ev);
     return cudaGetLastError();
