@@ -113,20 +113,16 @@ static bool math_ok(emm_math_t m) {
 // prohibitive" regime): one launch of the tiny FFMA kernel (KN10),
 // which is FP32-accurate.
 // EMM_SMALL_FLOPS (environment) overrides the threshold; 0 disables it.
-// Tensor-core modes also need the tiny kernel's 32 x 32 tiles to fit one
-// wave: past it (e.g. 400^3: 169 tiles on 148 SMs) the tiny kernel takes a
-// second round (24.6 us) while KN1X takes 19.5 (round 2, measured:
-// 352-384^3 tiny 16.4 vs 19.4-21.2 us; 400-420^3 tiny 24.6 vs 18.4-19.5 us).
-// The FFMA mode keeps the flop threshold alone (its CUDA-core kernels take
-// 39-46 us there).
+// Thresholds measured with the round-2 tiny kernel (4x4 outputs per thread,
+// cp.async ring; profiles/r02_small_threshold.md): tensor-core modes cross
+// over near 2^27 flops (400^3 tiny 19.2 vs KN1X 21.1 us, 448^3 equal, 512^3
+// 22.5 vs 19.4); the FFMA mode's CUDA-core kernels (128x128 tiles, one CTA
+// per SM) lose to it up to ~1e9 flops (512^3 22.5 vs 51.2 us, 700^3 47 vs
+// 68; 1024^3 107 vs 94).
 static bool small_problem(int64_t M, int64_t N, int64_t K, emm_math_t math = EMM_MATH_FFMA) {
-    double thr = (double)(1 << 27);   // measured crossover tiny vs tensor core: between 333^3 and 512^3
-    const char *e = getenv("EMM_SMALL_FLOPS");
-    if (e) thr = atof(e);
-    if (2.0 * (double)M * (double)N * (double)K > thr) return false;
-    if (e || math == EMM_MATH_FFMA) return true;
-    const double tiles = (double)((M + 31) / 32) * (double)((N + 31) / 32);
-    return tiles <= (double)tc_num_sms();
+    double thr = math == EMM_MATH_FFMA ? 1.0e9 : (double)(1 << 27);
+    if (const char *e = getenv("EMM_SMALL_FLOPS")) thr = atof(e);
+    return 2.0 * (double)M * (double)N * (double)K <= thr;
 }
 
 // How one tensor-core call runs:
