@@ -117,10 +117,11 @@ static bool math_ok(emm_math_t m) {
 // cp.async ring; profiles/r02_small_threshold.md): tensor-core modes cross
 // over near 2^27 flops (400^3 tiny 19.2 vs KN1X 21.1 us, 448^3 equal, 512^3
 // 22.5 vs 19.4); the FFMA mode's CUDA-core kernels (128x128 tiles, one CTA
-// per SM) lose to it up to ~1e9 flops (512^3 22.5 vs 51.2 us, 700^3 47 vs
-// 68; 1024^3 107 vs 94).
+// per SM) lose to it (64 x 64 tiles past 2 blocks per SM) up to ~2.2e9
+// flops (512^3 22.5 vs 51.2 us, 700^3 38.9 vs 67.6, 1024^3 88.0 vs 94.6;
+// c3 254 vs 238 and 1536^3 240 vs 140 stay on KN3 / KN3b).
 static bool small_problem(int64_t M, int64_t N, int64_t K, emm_math_t math = EMM_MATH_FFMA) {
-    double thr = math == EMM_MATH_FFMA ? 1.0e9 : (double)(1 << 27);
+    double thr = math == EMM_MATH_FFMA ? 2.2e9 : (double)(1 << 27);
     if (const char *e = getenv("EMM_SMALL_FLOPS")) thr = atof(e);
     return 2.0 * (double)M * (double)N * (double)K <= thr;
 }

@@ -394,11 +394,13 @@ def test_same_sign_accumulation(emm, math, K):
 @pytest.mark.parametrize("tA", ["N", "T"])
 @pytest.mark.parametrize("tB", ["N", "T"])
 @pytest.mark.parametrize("shape", [(1, 1, 1), (33, 65, 129), (300, 260, 333), (517, 389, 1025), (64, 64, 64)])
-def test_tiny_kernel_every_layout(emm, monkeypatch, tA, tB, shape):
+@pytest.mark.parametrize("tile", ["32", "64"])
+def test_tiny_kernel_every_layout(emm, monkeypatch, tA, tB, shape, tile):
     """KN10 (forced for every size): 4x4 outputs per thread, K split over four
     thread groups added in fixed order, cp.async ring with zero-filled edges —
     bitwise on integers, FP32-accurate on random data, padding untouched."""
     monkeypatch.setenv("EMM_SMALL_FLOPS", "1e15")
+    monkeypatch.setenv("EMM_TINY_T", tile)
     M, N, K = shape
     case = Case(tA, tB, M, N, K, 2.0, -1.0, kind="ints", c_kind="ints", pad=(3, 1, 2))
     R, S, T, _ = case.oracle()
@@ -412,13 +414,14 @@ def test_tiny_kernel_every_layout(emm, monkeypatch, tA, tB, shape):
     assert_close(case, Cg, R, S, T, 1e-5)
 
 
-@pytest.mark.parametrize("shape", [(64, 64, 64), (100, 100, 100), (7, 300, 5), (333, 333, 333), (700, 650, 600)])
+@pytest.mark.parametrize("shape", [(64, 64, 64), (100, 100, 100), (7, 300, 5), (333, 333, 333), (700, 650, 600),
+                                   (1000, 1000, 1000)])
 def test_small_problem_default_path(emm, monkeypatch, shape):
     monkeypatch.delenv("EMM_SMALL_FLOPS")
     M, N, K = shape
     case = Case("N", "N", M, N, K, 1.0, 0.0)
     R, S, T, _ = case.oracle()
-    tiny_all = 2 * M * N * K <= 1 << 27   # tiny kernel for every mode; above, only for FFMA (<= 1e9 flops)
+    tiny_all = 2 * M * N * K <= 1 << 27   # tiny kernel for every mode; above, only for FFMA (<= 2.2e9 flops)
     for math in MATHS:
         Cg = case.run(emm, math)
         case.check_untouched(Cg)
