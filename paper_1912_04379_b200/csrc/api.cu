@@ -134,8 +134,9 @@ static bool small_problem(int64_t M, int64_t N, int64_t K, emm_math_t math = EMM
 //    1xTF32: nothing).
 //  * full (fallback, or EMM_FORCE_PACK=1): both planes re-buffered K-major.
 // Workspace: [A plane(s) | B plane(s) | split-K partials | control block],
-// 1024-byte aligned regions.  emm_sgemm_workspace_bytes returns the full
-// (larger) layout, valid for every pointer/ld.
+// 1024-byte aligned regions.  emm_sgemm_workspace_bytes returns the largest
+// layout the call can take for any pointer / ld (KN1X: both operands
+// re-pitched; other splits: the re-buffered planes).
 struct Plan {
     bool direct = false;
     int pack_mode = -1;      // -1: no split pass
@@ -295,10 +296,14 @@ static Plan make_plan(char tA, char tB, int64_t M, int64_t N, int64_t K, emm_mat
     return P;
 }
 
-static size_t ws_bytes(int64_t M, int64_t N, int64_t K, emm_math_t math) {
+static size_t ws_bytes(char tA, char tB, int64_t M, int64_t N, int64_t K, emm_math_t math) {
     if (math == EMM_MATH_FFMA || M == 0 || N == 0 || K == 0) return 0;
     if (M <= SKINNY_MAX || N <= SKINNY_MAX) return skinny_tc_workspace_bytes(M, N, K);   // KN9T (upper bound)
     if (small_problem(M, N, K, math)) return 0;
+    // 3xTF32 on KN1X: at most the raw re-pitch of both operands (when their
+    // leading dimensions are TMA-illegal) + split-K / stream-K scratch; the
+    // other splits (and EMM_SPLIT=pass / EMM_FORCE_PACK): the re-buffered planes
+    if (math == EMM_MATH_3XTF32 && prefer_xs(M, N, K)) return make_plan(tA, tB, M, N, K, math, true, true, true, true).total;
     return make_plan('N', 'N', M, N, K, math, /*direct=*/false).total;
 }
 
@@ -309,10 +314,8 @@ using namespace emm;
 
 extern "C" size_t emm_sgemm_workspace_bytes(char transA, char transB, int64_t M, int64_t N, int64_t K,
                                             emm_math_t math) {
-    (void)transA;
-    (void)transB;
     if (M < 0 || N < 0 || K < 0) return 0;
-    return ws_bytes(M, N, K, math);
+    return ws_bytes(transA, transB, M, N, K, math);
 }
 
 extern "C" int emm_sgemm_ex(char transA, char transB, int64_t M, int64_t N, int64_t K, float alpha, const float *A,
@@ -756,7 +759,7 @@ extern "C" int emm_sgemm_host(char transA, char transB, int64_t M, int64_t N, in
     const size_t nA = ab_used ? (size_t)((ac - 1) * lda + ar) * 4 : 0;
     const size_t nB = ab_used ? (size_t)((bc - 1) * ldb + br) * 4 : 0;
     const size_t nC = (size_t)((N - 1) * ldc + M) * 4;
-    const size_t nW = ab_used ? ws_bytes(M, N, K, math) : 0;
+    const size_t nW = ab_used ? ws_bytes(transA, transB, M, N, K, math) : 0;
     if ((st = ensure(&g_hc.dA, &g_hc.nA, nA)) || (st = ensure(&g_hc.dB, &g_hc.nB, nB)) ||
         (st = ensure(&g_hc.dC, &g_hc.nC, nC)))
         return st;

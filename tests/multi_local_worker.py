@@ -15,8 +15,8 @@ other modes copy).
 Checks (SURVEY.md §4 "fake multi-GPU on one device"):
 * every rank's B buffer ends bit-identical to root's;
 * every rank's C_local is bitwise equal to the same rows of the P = 1 call
-  (same code, one rank: the per-element summation order does not depend on
-  the row partition);
+  (same code, one rank: the per-element summation order of the tensor-core
+  paths does not depend on the row partition; FFMA: integer inputs only);
 * the P copies of C_full are bitwise equal to each other and to the
   assembled C_local blocks;
 * the result is within the north_star tolerance of the oracle (bitwise equal
@@ -116,7 +116,12 @@ def main():
         beta = 1.0 if kind == "ints" else 0.0
         ref = run_world(1, M, N, K, transB, math, kind, [0], gather, beta)
         got = run_world(P, M, N, K, transB, math, kind, [0, P - 1, P // 2], gather, beta)
-        assert torch.equal(ref, got), f"P={P} differs from P=1 (bitwise)"
+        # tensor-core paths: each element's summation order does not depend on
+        # the row partition -> bitwise; the FFMA mode picks its kernel by the
+        # shard's size (tiny kernel tile / KN3b), so there both runs are only
+        # held to the oracle bound (checked in run_world)
+        if math != "ffma" or kind == "ints":
+            assert torch.equal(ref, got), f"P={P} differs from P=1 (bitwise)"
         print(f"ok {cs}", flush=True)
     print("ALL OK", flush=True)
 

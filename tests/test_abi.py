@@ -116,23 +116,33 @@ def test_row_partition_c5(emm):
 
 
 def test_workspace_bytes(emm):
-    # layout: [A planes | B planes | split-K slots | ctrl 1 KB | (stream-K: flags 8 KB | slots)]
+    # layout: [A region | B region | split-K slots | ctrl 1 KB | (stream-K: flags 8 KB | slots)]
     CTRL, FLAGS, SLOT = 1024, 8192, 256 * 256 * 4
+
+    def al(b):
+        return -(-b // 1024) * 1024
+
+    def repitch(rows, cols):   # KN1X upper bound: raw copy of a stored rows x cols operand, ld rounded up to 4
+        return al(cols * (-(-rows // 4) * 4) * 4)
+
     assert emm.workspace_bytes("N", "N", 64, 64, 64, "ffma") == 0
-    # 3xTF32: 2 planes of M x Kp and N x Kp floats, Kp = K rounded up to 32
-    assert emm.workspace_bytes("N", "N", 2048, 1024, 33, "3xtf32") == 2 * 4 * 64 * (2048 + 1024) + CTRL
+    # 3xTF32 (KN1X): at most a raw re-pitch of both operands
+    assert emm.workspace_bytes("N", "N", 2048, 1024, 33, "3xtf32") == repitch(2048, 33) + repitch(33, 1024) + CTRL
+    assert emm.workspace_bytes("T", "T", 2048, 1024, 33, "3xtf32") == repitch(33, 2048) + repitch(1024, 33) + CTRL
+    # 1xTF32: re-buffered planes (1 plane of M x Kp and N x Kp floats, Kp = K rounded up to 32)
     assert emm.workspace_bytes("N", "T", 2048, 1024, 64, "1xtf32") == 4 * 64 * (2048 + 1024) + CTRL
     # latency-bound problems (2MNK <= 2^27) take the tiny FFMA kernel: no workspace
     assert emm.workspace_bytes("N", "N", 64, 64, 64, "3xtf32") == 0
     assert emm.workspace_bytes("N", "N", 333, 333, 333, "3xtf32") == 0
     # sub-wave problems add split-K slots: BJ configs[2] -> 24 tiles x 3 splits of 256 x 256 floats
     M, N, K = 1531, 997, 2049
-    base = -(-2 * 4 * 2080 * M // 1024) * 1024 + -(-2 * 4 * 2080 * N // 1024) * 1024
-    assert emm.workspace_bytes("N", "N", M, N, K, "3xtf32") == base + 24 * 3 * SLOT + CTRL
+    assert emm.workspace_bytes("N", "N", M, N, K, "3xtf32") == repitch(M, K) + repitch(K, N) + 24 * 3 * SLOT + CTRL
     # stream-K shapes add one slot per CTA pair (4096^3 3xTF32: 256 tiles = 3.46 waves)
-    base = 2 * 2 * 4 * 4096 * 4096
+    base = 2 * 4 * 4096 * 4096
     assert emm.workspace_bytes("N", "N", 4096, 4096, 4096, "3xtf32") == base + CTRL + FLAGS + 74 * SLOT
-    assert emm.workspace_bytes("N", "N", 4096, 4096, 4096, "1xtf32") == base // 2 + CTRL
+    assert emm.workspace_bytes("N", "N", 4096, 4096, 4096, "1xtf32") == base + CTRL
+    # TF32+BF16 keeps the re-buffered planes (2 per operand)
+    assert emm.workspace_bytes("N", "N", 4096, 4096, 4096, "tf32bf16") == 2 * base + CTRL + FLAGS + 74 * SLOT
 
 
 def test_strerror_and_version(emm):
