@@ -241,6 +241,8 @@ static bool prefer_xs(int64_t M, int64_t N, int64_t K) {
     return !env_on("EMM_FORCE_PACK");
 }
 
+bool tc_prefer_xs(int64_t M, int64_t N, int64_t K) { return prefer_xs(M, N, K); }
+
 static Plan make_plan(char tA, char tB, int64_t M, int64_t N, int64_t K, emm_math_t math, bool direct,
                       bool xs = false, bool rp_a = false, bool rp_b = false) {
     Plan P;

@@ -119,6 +119,9 @@ cudaError_t launch_tc_xs_sgemm(const TcPlane &a, const TcPlane &b, int64_t M, in
                                float beta, float *C, int64_t ldc, unsigned int *ctrl, int splits, float *partial,
                                cudaStream_t s, const PeerOut *peers = nullptr, void *sk_ws = nullptr,
                                const float *acc_init = nullptr, int64_t ld_init = 0);
+// the 3xTF32 policy of emm_sgemm_ex: KN1X (split in the kernel) unless
+// EMM_SPLIT=pass / EMM_FORCE_PACK select the split pass + KN1 (api.cu)
+bool tc_prefer_xs(int64_t M, int64_t N, int64_t K);
 bool tma_legal(const void *ptr, int64_t ld);
 // A plane as the tcgen05 kernels' 2-D tensor map (K-major box {32, 128},
 // MN-major box {32, 32} with the 32B-atom 128B swizzle), OOB reads zero.

@@ -682,7 +682,14 @@ int enqueue_main(Comm *c, const MultiArgs &a, bool *done_pending) {
     const int64_t Kp = tc_kpad(K);
     float *Ap = nullptr, *Bp = nullptr;
     unsigned int *ctrl = nullptr;
-    if (tc && rows > 0 && N > 0) {
+    // 3xTF32 on TMA-legal operands: KN1X reads op(A)'s rows and each B panel
+    // in place (no re-buffering, the split in the kernel) — emm_sgemm_ex's
+    // default; otherwise op(A) re-buffered once and each panel after arrival
+    const bool xs = tc && terms == 3 && tc_prefer_xs(rows, N, K) && tma_legal(A_local, lda) && tma_legal(B, ldb);
+    if (xs && rows > 0 && N > 0) {
+        if ((st = grow(&c->ws, &c->ws_bytes, 1024))) return st;
+        ctrl = reinterpret_cast<unsigned int *>(c->ws);
+    } else if (tc && rows > 0 && N > 0) {
         const size_t a_bytes = align_up((size_t)planes * rows * Kp * 4, 1024);
         const size_t bp_bytes = align_up((size_t)planes * panel * Kp * 4, 1024);
         // stream-ordered reuse: the previous call's kernels on `s` are ordered before this one
@@ -703,6 +710,23 @@ int enqueue_main(Comm *c, const MultiArgs &a, bool *done_pending) {
         if (!tc)
             return emm_sgemm_ex(transA, transB, rows, nc, K, alpha, A_local, lda, bp, ldb, beta, cp, ldc, s, math,
                                 nullptr, 0);
+        PeerOut pe;
+        if (fused) {
+            pe.n = P;
+            for (int r = 0; r < P; ++r) pe.base[r] = out_peer[r];
+            pe.ld = ldc_full;
+            pe.row_off = row0;
+            pe.col_off = (cp - C_local) / ldc;   // the panel's first column
+        }
+        if (xs) {
+            cudaError_t e = cudaMemsetAsync(ctrl, 0, 128, s);   // the panel's wave-lockstep counter
+            const TcPlane a0{A_local, lda, transA == 'N' || transA == 'n', K};
+            const TcPlane b0{bp, ldb, !bN, K};
+            if (e == cudaSuccess)
+                e = launch_tc_xs_sgemm(a0, b0, rows, nc, K, alpha, beta, cp, ldc, ctrl, 1, nullptr, s,
+                                       fused ? &pe : nullptr);
+            return cuda_st(e);
+        }
         PackArgs pb;
         pb.X = bp; pb.ld = ldb; pb.R = nc; pb.kcontig = bN;
         pb.out0 = Bp; pb.ld0 = Kp; pb.out1 = Bp + (size_t)nc * Kp; pb.ld1 = Kp; pb.b_side = true;
@@ -713,14 +737,6 @@ int enqueue_main(Comm *c, const MultiArgs &a, bool *done_pending) {
         if (planes == 2) {
             ops.a1 = TcPlane{Ap + (size_t)rows * Kp, Kp, false, Kp};
             ops.b1 = TcPlane{Bp + (size_t)nc * Kp, Kp, false, Kp};
-        }
-        PeerOut pe;
-        if (fused) {
-            pe.n = P;
-            for (int r = 0; r < P; ++r) pe.base[r] = out_peer[r];
-            pe.ld = ldc_full;
-            pe.row_off = row0;
-            pe.col_off = (cp - C_local) / ldc;   // the panel's first column
         }
         if (e == cudaSuccess)
             e = launch_tc_sgemm(terms, ops, rows, nc, K, alpha, beta, cp, ldc, ctrl, 1, nullptr, s,
