@@ -578,14 +578,18 @@ static int host_pipelined(char tA, char tB, int64_t M, int64_t N, int64_t K, flo
         }
         g_hs.dev = dev;
     }
-    // Blocks of op(A) rows / op(B) columns: 2048 (EMM_HOST_BLOCK; at most 64
+    // Blocks of op(A) rows / op(B) columns: 3072 (EMM_HOST_BLOCK; at most 64
     // blocks per operand); EMM_HOST_FIRST sizes the first two of each operand
     // and EMM_HOST_CHUNK splits each GEMM region into pieces with their own
     // copy-back.  Both default off: at 32768^3 first = 1024 starts the first
     // GEMM 4.9 ms earlier but the smaller GEMMs cost more (307 vs 304 ms), and
     // 8192-wide pieces cut the copy-back tail 5 -> 1.5 ms but fall off whole
     // waves (316 ms; profiles/r01_e2e_timeline.txt).
-    int64_t blk = 2048;
+    // 3072 with the KN1X pipeline (no re-buffering): bigger blocks make the
+    // GEMMs more efficient and the start-up is still short (32768^3 e2e 233.6
+    // -> 236.8 TFLOP/s, tools/e2e_timeline.py span 291 -> 287 ms); 2048 was the
+    // round-1 choice with re-buffered planes
+    int64_t blk = 3072;
     if (const char *eb = getenv("EMM_HOST_BLOCK")) blk = std::max<int64_t>(256, atoll(eb) / 256 * 256);
     blk = std::max(blk, ((std::max(M, N) + 31) / 32 + 255) / 256 * 256);
     int64_t first = blk;
