@@ -235,6 +235,12 @@ int emm_debug_mma_probe(int terms, int stages, void *stream, float *ms, double *
  * schedule), 8 ints each (pair, i, m0, n0, kb0, kb1, dummy, multicast).
  * Both return the item count, or -1 when `cap` items do not fit in `out`. */
 int emm_debug_schedule(int64_t M, int64_t N, int64_t K, int use_sk, int terms, int *out, int cap);
+/* Host replay of emm_sgemm_multi's B chunk plan (copy-engine ring): chunk j
+ * covers bytes [out_off[j], out_off[j+1]) of B (n + 1 offsets), panel p
+ * chunks [out_pc[p], out_pc[p+1]).  Returns n, or -1 if cap_off / cap_pc are
+ * too small. */
+int emm_debug_ring_chunks(int64_t N, int64_t K, char transB, int64_t *out_off, int cap_off, int64_t *out_pc,
+                          int cap_pc);
 int emm_debug_pair_schedule(int64_t M, int64_t N, int64_t K, int *out, int cap);
 
 #ifdef __cplusplus

@@ -541,26 +541,43 @@ struct Chunks {
     std::vector<int64_t> pc;
     std::vector<size_t> off;
 };
+// transB = 'N': whole columns per chunk (<= CHUNK_BYTES unless one column is
+// larger), chunk boundaries at every panel boundary; 'T': one panel of byte
+// chunks.  The chunk size doubles until the count fits the flag words.
 static Chunks make_chunks(bool bN, int64_t N, int64_t K, int64_t panel) {
-    Chunks ch;
     const size_t col_bytes = (size_t)K * 4;
     const size_t total = (size_t)N * K * 4;
-    size_t chunk = CHUNK_BYTES;
-    while (total / chunk >= (size_t)FL_NCHUNK - 8) chunk *= 2;
-    ch.off.push_back(0);
-    ch.pc.push_back(0);
-    if (bN) {
-        const int64_t cols_per = col_bytes > 0 ? std::max<int64_t>(1, (int64_t)(chunk / col_bytes)) : N;
-        for (int64_t c0 = 0; c0 < N; c0 += panel) {
-            const int64_t c1 = std::min(N, c0 + panel);
-            for (int64_t x = c0; x < c1; x += cols_per) ch.off.push_back((size_t)std::min(c1, x + cols_per) * col_bytes);
+    for (size_t chunk = CHUNK_BYTES;; chunk *= 2) {
+        Chunks ch;
+        ch.off.push_back(0);
+        ch.pc.push_back(0);
+        if (bN) {
+            const int64_t cols_per = col_bytes > 0 ? std::max<int64_t>(1, (int64_t)(chunk / col_bytes)) : N;
+            for (int64_t c0 = 0; c0 < N; c0 += panel) {
+                const int64_t c1 = std::min(N, c0 + panel);
+                for (int64_t x = c0; x < c1; x += cols_per)
+                    ch.off.push_back((size_t)std::min(c1, x + cols_per) * col_bytes);
+                ch.pc.push_back((int64_t)ch.off.size() - 1);
+            }
+        } else {
+            for (size_t o = 0; o < total; o += chunk) ch.off.push_back(std::min(total, o + chunk));
             ch.pc.push_back((int64_t)ch.off.size() - 1);
         }
-    } else {
-        for (size_t o = 0; o < total; o += chunk) ch.off.push_back(std::min(total, o + chunk));
-        ch.pc.push_back((int64_t)ch.off.size() - 1);
+        if ((int64_t)ch.off.size() - 1 <= FL_NCHUNK) return ch;
     }
-    return ch;
+}
+
+// Host replay of the B chunk plan (tests): chunk byte offsets off[0..n] in
+// out_off (n + 1 entries) and, per panel p, the index of its first chunk in
+// out_pc (npanel + 1 entries).  Returns n, or -1 if a buffer is too small.
+extern "C" int emm_debug_ring_chunks(int64_t N, int64_t K, char transB, int64_t *out_off, int cap_off,
+                                     int64_t *out_pc, int cap_pc) {
+    const bool bN = transB == 'N' || transB == 'n';
+    const Chunks ch = make_chunks(bN, N, K, bN ? emm_multi_panel_cols(N) : N);
+    if ((int)ch.off.size() > cap_off || (int)ch.pc.size() > cap_pc) return -1;
+    for (size_t i = 0; i < ch.off.size(); ++i) out_off[i] = (int64_t)ch.off[i];
+    for (size_t i = 0; i < ch.pc.size(); ++i) out_pc[i] = ch.pc[i];
+    return (int)ch.off.size() - 1;
 }
 
 namespace emm {
