@@ -237,3 +237,35 @@ def test_repitched_illegal_ld_bitwise_equal_to_legal(emm, tA, tB, shape):
     rows = np.r_[0:8, M - 8:M]
     R, S, T, _ = bad.oracle(rows=rows)
     assert_close(bad, Cb, R, S, T, 1e-5, rows=rows)
+
+
+@pytest.mark.parametrize("which", ["A", "B", "AB"])
+@pytest.mark.parametrize("tA,tB", [("N", "N"), ("T", "T"), ("N", "T")])
+def test_unaligned_base_pointers(emm, which, tA, tB):
+    """Operands that start 4 bytes past a 16-byte boundary are TMA-illegal
+    whatever their leading dimension: KN1X runs on a raw re-pitched copy —
+    same bits as the same matrices at aligned addresses."""
+    M, N, K = 700, 520, 300
+    case = Case(tA, tB, M, N, K, 1.5, -0.5, kind="normal", pad=(4 - (M if tA == "N" else K) % 4,
+                                                                 4 - (K if tB == "N" else N) % 4, 1))
+    dA = case.flat(case.A).cuda()
+    dB = case.flat(case.B).cuda()
+    def shifted(x):
+        buf = torch.empty(x.numel() + 4, dtype=torch.float32, device="cuda")
+        buf[1:1 + x.numel()] = x
+        return buf, buf[1:]
+    keepA, sA = shifted(dA) if "A" in which else (None, dA)
+    keepB, sB = shifted(dB) if "B" in which else (None, dB)
+    out = []
+    for a, b in ((sA, sB), (dA, dB)):
+        dC = case.Cflat.cuda()
+        st = emm.sgemm_ptr(tA, tB, M, N, K, 1.5, a.data_ptr(), case.lda, b.data_ptr(), case.ldb, -0.5, dC.data_ptr(),
+                           case.ldc, torch.cuda.current_stream().cuda_stream, "3xtf32")
+        torch.cuda.synchronize()
+        assert st == 0
+        out.append(dC.cpu())
+    case.check_untouched(out[0])
+    assert torch.equal(out[0].view(torch.int32), out[1].view(torch.int32))
+    rows = np.r_[0:8, M - 8:M]
+    R, S, T, _ = case.oracle(rows=rows)
+    assert_close(case, out[0], R, S, T, 1e-5, rows=rows)
