@@ -31,6 +31,10 @@ struct TcPlane {
     int64_t ld = 0;
     bool mn = false;
     int64_t kext = 0;
+    // TMA rounds each FP32 element to TF32 on load (tensor map data type
+    // TFLOAT32: bit-identical to cvt.rn.tf32.f32, tools/tma_tf32_probe.cu);
+    // the 1xTF32 direct path's operands (R7c)
+    bool rn = false;
 };
 // plane 0 = big (the user array itself in the direct path), plane 1 = small
 // (3xTF32) or BF16 cross (TF32+BF16); plane 1 unused for 1xTF32.

@@ -64,8 +64,8 @@ int64_t tc_kpad(int64_t K) { return (K + TC_BK - 1) / TC_BK * TC_BK; }
 //   PK_FULLX  + plane 1 = BF16 cross operand, K-major     (fallback TF32+BF16)
 //   PK_DSMALL plane 1 only = rn_tf32(x - trunc(x)) in the SOURCE layout
 //             (direct 3xTF32: the tensor core reads trunc(x) from the user array)
-//   PK_DCROSS plane 1 only = BF16 cross operand with big = trunc(x), K-major
-//             (direct TF32+BF16)
+//   PK_DCROSS plane 1 only = BF16 cross operand with big = rn_tf32(x), K-major
+//             (direct TF32+BF16: the GEMM's TMA rounds x to that big part)
 //   PK_RAW    plane 0 = x unchanged in the SOURCE layout with a 16-byte-
 //             multiple leading dimension ld0 (re-pitch of a TMA-illegal
 //             operand for the in-kernel-split GEMM KN1X)
@@ -100,6 +100,7 @@ struct PackOperand {
     int64_t ld1;
     int cross_swap;   // B side of the cross operand
     int raw_big;      // test hook (EMM_DEBUG_RAW_BIG): FULL big = x unrounded
+    int trunc_big;    // PK_DCROSS with big = trunc(x) (EMM_TMA_TRUNC=1, experiments)
     // launch geometry (host-computed)
     int transpose;    // 1: tile path, 0: element-wise lines
     int vec;          // 16-B vector loads legal on the source (aligned base, ld % 4 == 0)
@@ -112,8 +113,12 @@ __device__ __forceinline__ float trunc_tf32(float x) { return __uint_as_float(__
 
 template <int MODE>
 __device__ __forceinline__ void split_one(const PackOperand &op, float x, float &big, float &lo) {
-    const bool direct = MODE == PK_DSMALL || MODE == PK_DCROSS;
-    big = direct ? trunc_tf32(x) : (op.raw_big ? x : __uint_as_float(cvt_tf32_rn(x)));
+    // PK_DSMALL: the tensor core truncates the raw user operand (R7b).
+    // PK_DCROSS: the direct GEMM's TMA rounds the user operand to
+    // rn_tf32(x) on load (TFLOAT32 tensor map, R7c), so the cross plane is
+    // made against that same big part
+    if (MODE == PK_DSMALL || (MODE == PK_DCROSS && op.trunc_big)) big = trunc_tf32(x);
+    else big = op.raw_big ? x : __uint_as_float(cvt_tf32_rn(x));
     lo = isfinite(x) ? x - big : 0.0f;   // exact
 }
 
@@ -316,11 +321,14 @@ cudaError_t launch_pack(int mode, const PackArgs &a, const PackArgs *b, int64_t 
         const char *e = getenv("EMM_DEBUG_RAW_BIG");
         return e && e[0] == '1' ? 1 : 0;
     }();
+    const char *et = getenv("EMM_TMA_TRUNC");
+    const bool tma_trunc = et && et[0] == '1';
     auto mk = [&](const PackArgs &x, bool b_side) {
         PackOperand o{};
         o.X = x.X; o.ld = x.ld; o.R = x.R; o.kcontig = x.kcontig ? 1 : 0;
         o.out0 = x.out0; o.ld0 = x.ld0; o.out1 = x.out1; o.ld1 = x.ld1;
         o.cross_swap = b_side ? 1 : 0; o.raw_big = raw;
+        o.trunc_big = mode == PK_DCROSS && tma_trunc ? 1 : 0;
         pack_geometry(o, mode, K);
         return o;
     };
@@ -482,7 +490,8 @@ bool tc_make_tmap_rows(CUtensorMap *tm, const TcPlane &p, int64_t R, int box_row
         box[0] = (cuuint32_t)TC_BK;
         box[1] = (cuuint32_t)box_rows;
     }
-    CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(p.ptr), dims, strides, box, estr,
+    CUresult r = enc(tm, p.rn ? CU_TENSOR_MAP_DATA_TYPE_TFLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                     const_cast<float *>(p.ptr), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE,
                      p.mn ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
