@@ -1,15 +1,76 @@
-import time, torch, sys, os
-sys.path.insert(0, os.getcwd())
-import paper_1912_04379_b200 as emm
-for n in (64, 512, 1024):
-    A = torch.rand(n, n, device="cuda").t(); B = torch.rand(n, n, device="cuda").t(); C = torch.empty(n, n, device="cuda").t()
-    ws = torch.empty(max(emm.workspace_bytes("N","N",n,n,n,"3xtf32"),1)+1024, dtype=torch.uint8, device="cuda")
-    s = torch.cuda.current_stream().cuda_stream
-    L = emm.lib()
-    args = (b"N", b"N", n, n, n, 1.0, A.data_ptr(), n, B.data_ptr(), n, 0.0, C.data_ptr(), n, s, 0, (ws.data_ptr()+1023)//1024*1024, ws.numel()-1024)
-    for _ in range(50): L.emm_sgemm_ex(*args)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter(); N = 2000
-    for _ in range(N): L.emm_sgemm_ex(*args)
-    t1 = time.perf_counter(); torch.cuda.synchronize(); t2 = time.perf_counter()
-    print(f"n={n}: host enqueue {1e6*(t1-t0)/N:.2f} us/call, wall incl. GPU {1e6*(t2-t0)/N:.2f} us/call")
+#!/usr/bin/env python
+"""Host-side enqueue cost of one emm call (GPU tool, not a test): the stream
+is parked behind a long device sleep, then R calls are enqueued and timed on
+the host (perf_counter); the GPU never stalls the host here, so the number
+is the library's CPU cost per call (validation, planning, tensor-map
+encodes, launch API).
+
+    python tools/host_overhead.py [--reps 200]
+"""
+import argparse
+import os
+import statistics
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_1912_04379_b200 as emm  # noqa: E402
+
+SHAPES = [("c3-NN", 1531, 997, 2049, "N", "N", (13, 7, 5)), ("c3-TN", 1531, 997, 2049, "T", "N", (13, 7, 5)),
+          ("1024", 1024, 1024, 1024, "N", "N", (0, 0, 0)), ("333", 333, 333, 333, "N", "N", (0, 0, 0)),
+          ("64", 64, 64, 64, "N", "N", (0, 0, 0))]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--reps", type=int, default=200)
+    ap.add_argument("--maths", default="3xtf32,1xtf32,ffma")
+    a = ap.parse_args()
+    dev = torch.device("cuda", 0)
+    s = torch.cuda.current_stream(dev)
+    for name, M, N, K, tA, tB, pad in SHAPES:
+        ra, ca = (M, K) if tA == "N" else (K, M)
+        rb, cb = (K, N) if tB == "N" else (N, K)
+        lda, ldb, ldc = ra + pad[0], rb + pad[1], M + pad[2]
+        A = torch.rand(ca * lda, device=dev)
+        B = torch.rand(cb * ldb, device=dev)
+        C = torch.zeros(N * ldc, device=dev)
+        L = emm.lib()
+        for math in a.maths.split(","):
+            fn = L.emm_sgemm_ex
+            args = (tA.encode(), tB.encode(), M, N, K, 1.0, A.data_ptr(), lda, B.data_ptr(), ldb, 0.0,
+                    C.data_ptr(), ldc, s.cuda_stream, emm.MATH[math], None, 0)
+
+            def call():
+                return fn(*args)
+            for _ in range(5):
+                call()
+            torch.cuda.synchronize()
+            ts = []
+            torch.cuda._sleep(int(2e9))   # ~1 s of device sleep
+            for _ in range(a.reps):
+                t0 = time.perf_counter()
+                call()
+                ts.append(time.perf_counter() - t0)
+            torch.cuda.synchronize()
+            n0 = emm.launch_count()
+            call()
+            torch.cuda.synchronize()
+            print(f"{name:6s} {math:7s} host us/call: median {statistics.median(ts) * 1e6:7.2f}  "
+                  f"min {min(ts) * 1e6:7.2f}  launches/call {emm.launch_count() - n0}", flush=True)
+    # ctypes floor: a trivial exported call with the same marshalling path
+    f = emm.lib().emm_launch_count
+    ts = []
+    for _ in range(1000):
+        t0 = time.perf_counter()
+        f()
+        ts.append(time.perf_counter() - t0)
+    print(f"ctypes floor (emm_launch_count): median {statistics.median(ts) * 1e6:.2f} us")
+
+
+if __name__ == "__main__":
+    main()
