@@ -116,12 +116,12 @@ static bool math_ok(emm_math_t m) {
 // Thresholds measured with the round-2 tiny kernel (4x4 outputs per thread,
 // cp.async ring; profiles/r02_small_threshold.md): tensor-core modes cross
 // over near 2^27 flops (400^3 tiny 19.2 vs KN1X 21.1 us, 448^3 equal, 512^3
-// 22.5 vs 19.4); the FFMA mode's CUDA-core kernels (128x128 tiles, one CTA
-// per SM) lose to it (64 x 64 tiles past 2 blocks per SM) up to ~2.2e9
-// flops (512^3 22.5 vs 51.2 us, 700^3 38.9 vs 67.6, 1024^3 88.0 vs 94.6;
-// c3 254 vs 238 and 1536^3 240 vs 140 stay on KN3 / KN3b).
+// 22.5 vs 19.4); the FFMA mode's KN3b (128x128 tiles, one CTA per SM,
+// split-K on sub-wave grids) overtakes it (64 x 64 tiles past 2 blocks per
+// SM) near 7e8 flops (profiles/r02_ffma_relayout.md: 512^3 tiny 22.5 vs 35.8
+// us, 700^3 39.4 vs 39.9, 768^3 41.0 vs 37.9, 1024^3 86.5 vs 60.4).
 static bool small_problem(int64_t M, int64_t N, int64_t K, emm_math_t math = EMM_MATH_FFMA) {
-    double thr = math == EMM_MATH_FFMA ? 2.2e9 : (double)(1 << 27);
+    double thr = math == EMM_MATH_FFMA ? 7.0e8 : (double)(1 << 27);
     if (const char *e = getenv("EMM_SMALL_FLOPS")) thr = atof(e);
     return 2.0 * (double)M * (double)N * (double)K <= thr;
 }
@@ -298,8 +298,46 @@ static Plan make_plan(char tA, char tB, int64_t M, int64_t N, int64_t K, emm_mat
     return P;
 }
 
+// FFMA on layouts the TMA-fed KN3b does not cover (TN: both operands
+// K-contiguous; TMA-illegal base / leading dimension): one HBM-bound copy
+// pass first — the smaller operand of a TN call transposed to MN-contiguous
+// (PK_RAWT), a TMA-illegal operand re-pitched in its own layout (PK_RAW) —
+// then KN3b on the copies.  Measured on B200 (profiles/r02_ffma_relayout.md):
+// c3 TN 246 -> 212 us, TT 243 -> 206, 4096^3 TN 2.61 -> 2.43 ms.
+struct FfmaRelayout {
+    bool on = false, t_a = false, t_b = false, rp_a = false, rp_b = false;
+    int64_t lda1 = 0, ldb1 = 0;
+    size_t a_bytes = 0, b_bytes = 0, total = 0;
+};
+static FfmaRelayout ffma_relayout(bool tA, bool tB, int64_t M, int64_t N, int64_t K, bool legal_a, bool legal_b) {
+    FfmaRelayout R;
+    const bool tn = tA && !tB;
+    if (!tn && legal_a && legal_b) return R;
+    R.on = true;
+    if (tn) {
+        // transpose the smaller operand; K-major [R][kpad] rows = MN-contiguous copy
+        (M <= N ? R.t_a : R.t_b) = true;
+    }
+    R.rp_a = !R.t_a && !legal_a;
+    R.rp_b = !R.t_b && !legal_b;
+    const int64_t ar = tA ? K : M, ac = tA ? M : K;   // A stored ar x ac
+    const int64_t br = tB ? N : K, bc = tB ? K : N;
+    if (R.t_a) R.lda1 = tc_kpad(M), R.a_bytes = (size_t)K * R.lda1 * 4;
+    if (R.rp_a) R.lda1 = (ar + 3) / 4 * 4, R.a_bytes = (size_t)ac * R.lda1 * 4;
+    if (R.t_b) R.ldb1 = tc_kpad(N), R.b_bytes = (size_t)K * R.ldb1 * 4;
+    if (R.rp_b) R.ldb1 = (br + 3) / 4 * 4, R.b_bytes = (size_t)bc * R.ldb1 * 4;
+    R.total = align_up(R.a_bytes, 1024) + R.b_bytes;
+    return R;
+}
+
 static size_t ws_bytes(char tA, char tB, int64_t M, int64_t N, int64_t K, emm_math_t math) {
-    if (math == EMM_MATH_FFMA || M == 0 || N == 0 || K == 0) return 0;
+    if (M == 0 || N == 0 || K == 0) return 0;
+    if (math == EMM_MATH_FFMA) {
+        // upper bound: the relayout copies with both operands TMA-illegal
+        if (M <= SKINNY_MAX || N <= SKINNY_MAX || small_problem(M, N, K, math)) return 0;
+        return align_up(ffma_relayout(!is_n(tA), !is_n(tB), M, N, K, false, false).total, 1024) +
+               ffma_splitk_bytes(M, N, ffma_splits(M, N, K));
+    }
     if (M <= SKINNY_MAX || N <= SKINNY_MAX) return skinny_tc_workspace_bytes(M, N, K);   // KN9T (upper bound)
     if (small_problem(M, N, K, math)) return 0;
     // 3xTF32 on KN1X: at most the raw re-pitch of both operands (when their
@@ -374,9 +412,62 @@ extern "C" int emm_sgemm_ex(char transA, char transB, int64_t M, int64_t N, int6
     if (small_problem(M, N, K, math))
         return cuda_status(
             launch_tiny_sgemm(!is_n(transA), !is_n(transB), M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, s));
-    if (math == EMM_MATH_FFMA)
-        return cuda_status(
-            launch_ffma_sgemm(!is_n(transA), !is_n(transB), M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, s));
+    if (math == EMM_MATH_FFMA) {
+        const bool tA = !is_n(transA), tB = !is_n(transB);
+        FfmaRelayout R = ffma_relayout(tA, tB, M, N, K, tma_legal(A, lda), tma_legal(B, ldb));
+        const bool classic = env_on("EMM_FFMA_CLASSIC");
+        if (classic || env_on("EMM_FFMA_NORELAYOUT")) R = FfmaRelayout{};
+        // KN3b runs unless forced classic or left on an uncovered layout: split-K for sub-wave grids
+        const int splits = !classic && (R.on || ffma_tma_eligible(tA, tB, A, lda, B, ldb)) ? ffma_splits(M, N, K) : 1;
+        const size_t r_bytes = align_up(R.total, 1024), need = r_bytes + ffma_splitk_bytes(M, N, splits);
+        if (need == 0)
+            return cuda_status(launch_ffma_sgemm(tA, tB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, s));
+        void *ws = workspace;
+        bool own = false;
+        if (ws) {
+            if (workspace_bytes < need || (reinterpret_cast<uintptr_t>(ws) & 1023u)) return EMM_ERR_WORKSPACE;
+        } else {
+            cudaError_t e = scratch_alloc(&ws, need, s);
+            if (e != cudaSuccess) return cuda_status(e);
+            own = true;
+        }
+        float *a1 = reinterpret_cast<float *>(ws);
+        float *b1 = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(ws) + align_up(R.a_bytes, 1024));
+        float *part = splits > 1 ? reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(ws) + r_bytes) : nullptr;
+        const float *A2 = A, *B2 = B;
+        int64_t lda2 = lda, ldb2 = ldb;
+        bool tA2 = tA, tB2 = tB;
+        cudaError_t e = cudaSuccess;
+        if (R.t_a) {
+            // op(A)(r, p) = A[p + r*lda] read as an MN-contiguous K x M operand,
+            // written K-major: A2[r + p*lda1] (transA = N)
+            PackArgs x;
+            x.X = A; x.ld = lda; x.R = K; x.kcontig = false; x.out0 = a1; x.ld0 = R.lda1;
+            e = launch_pack(PK_RAWT_, x, nullptr, M, nullptr, s, 0);
+            A2 = a1, lda2 = R.lda1, tA2 = false;
+        } else if (R.t_b) {
+            // op(B)(p, j) = B[p + j*ldb] -> B2[j + p*ldb1] (transB = T)
+            PackArgs x;
+            x.X = B; x.ld = ldb; x.R = K; x.kcontig = false; x.out0 = b1; x.ld0 = R.ldb1;
+            e = launch_pack(PK_RAWT_, x, nullptr, N, nullptr, s, 0);
+            B2 = b1, ldb2 = R.ldb1, tB2 = true;
+        }
+        if (e == cudaSuccess && (R.rp_a || R.rp_b)) {
+            PackArgs ra, rb;
+            ra.X = A; ra.ld = lda; ra.R = M; ra.kcontig = tA; ra.out0 = a1; ra.ld0 = R.lda1;
+            rb.X = B; rb.ld = ldb; rb.R = N; rb.kcontig = !tB; rb.out0 = b1; rb.ld0 = R.ldb1;
+            e = launch_pack(PK_RAW_, R.rp_a ? ra : rb, (R.rp_a && R.rp_b) ? &rb : nullptr, K, nullptr, s, 0);
+            if (R.rp_a) A2 = a1, lda2 = R.lda1;
+            if (R.rp_b) B2 = b1, ldb2 = R.ldb1;
+        }
+        if (e == cudaSuccess)
+            e = launch_ffma_sgemm(tA2, tB2, M, N, K, alpha, A2, lda2, B2, ldb2, beta, C, ldc, s, splits, part);
+        if (own) {
+            cudaError_t e2 = cudaFreeAsync(ws, s);
+            if (e == cudaSuccess) e = e2;
+        }
+        return cuda_status(e);
+    }
 
     // tensor-core paths
     if (math == EMM_MATH_3XTF32 && prefer_inkernel_split(M, N, K)) {

@@ -62,7 +62,7 @@ struct PackArgs {
     int64_t ld1 = 0;
     bool b_side = false;    // B side of the cross operand (halves swapped)
 };
-enum { PK_FULL1_ = 0, PK_FULL3_ = 1, PK_FULLX_ = 2, PK_DSMALL_ = 3, PK_DCROSS_ = 4, PK_RAW_ = 5 };
+enum { PK_FULL1_ = 0, PK_FULL3_ = 1, PK_FULLX_ = 2, PK_DSMALL_ = 3, PK_DCROSS_ = 4, PK_RAW_ = 5, PK_RAWT_ = 6 };
 // One launch for A (and B if non-NULL); also zeroes `ctrl_words` words at
 // ctrl (the control block, and the stream-K flags that follow it).
 cudaError_t launch_pack(int mode, const PackArgs &a, const PackArgs *b, int64_t K, unsigned int *ctrl,
@@ -147,7 +147,7 @@ int tc_num_sms();
 // ---- CUDA-core path (k_ffma.cu) ------------------------------------------
 cudaError_t launch_ffma_sgemm(bool tA, bool tB, int64_t M, int64_t N, int64_t K, float alpha, const float *A,
                               int64_t lda, const float *B, int64_t ldb, float beta, float *C, int64_t ldc,
-                              cudaStream_t s);
+                              cudaStream_t s, int splits = 1, float *partial = nullptr);
 
 // KN3b (k_ffma_tma.cu): warp-specialised FFMA SGEMM, TMA-fed SMEM ring.
 // Returns false (nothing launched) when the shape / layout is not covered
@@ -155,7 +155,10 @@ cudaError_t launch_ffma_sgemm(bool tA, bool tB, int64_t M, int64_t N, int64_t K,
 bool ffma_tma_eligible(bool tA, bool tB, const float *A, int64_t lda, const float *B, int64_t ldb);
 cudaError_t launch_ffma_tma_sgemm(bool tA, bool tB, int64_t M, int64_t N, int64_t K, float alpha, const float *A,
                                   int64_t lda, const float *B, int64_t ldb, float beta, float *C, int64_t ldc,
-                                  cudaStream_t s);
+                                  cudaStream_t s, int splits = 1, float *partial = nullptr);
+// KN3b split-K (sub-wave grids): factor and partial-slab bytes
+int ffma_splits(int64_t M, int64_t N, int64_t K);
+size_t ffma_splitk_bytes(int64_t M, int64_t N, int splits);
 
 // ---- skinny / memory-bound path (k_skinny.cu) ----------------------------
 // min(M, N) <= SKINNY_MAX: stream the long operand once, FP32 FFMA with

@@ -190,13 +190,14 @@ __global__ void __launch_bounds__(FB_THREADS, 1) ffma_sgemm_kernel(int64_t M, in
 
 cudaError_t launch_ffma_sgemm(bool tA, bool tB, int64_t M, int64_t N, int64_t K, float alpha, const float *A,
                               int64_t lda, const float *B, int64_t ldb, float beta, float *C, int64_t ldc,
-                              cudaStream_t s) {
-    // KN3b (TMA-fed, warp-specialised) whenever it covers the layout;
-    // EMM_FFMA_CLASSIC=1 keeps KN3 (A/B comparisons, tests)
+                              cudaStream_t s, int splits, float *partial) {
+    // KN3b (TMA-fed, warp-specialised) whenever it covers the layout, split
+    // over K when the caller planned it (sub-wave grids); EMM_FFMA_CLASSIC=1
+    // keeps KN3 (A/B comparisons, tests; never split)
     const char *cv = getenv("EMM_FFMA_CLASSIC");
     const bool classic = cv && *cv && *cv != '0';
     if (!classic && ffma_tma_eligible(tA, tB, A, lda, B, ldb))
-        return launch_ffma_tma_sgemm(tA, tB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, s);
+        return launch_ffma_tma_sgemm(tA, tB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, s, splits, partial);
     const int64_t gx = (M + FB_M - 1) / FB_M, gy = (N + FB_N - 1) / FB_N;
     if (gx > 0x7fffffffLL || gy > 65535) return cudaErrorInvalidConfiguration;
     dim3 grid((unsigned)gx, (unsigned)gy);

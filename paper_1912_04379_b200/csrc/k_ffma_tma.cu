@@ -23,7 +23,9 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "emm_internal.h"
 #include "ptx.cuh"
@@ -107,7 +109,8 @@ __device__ __forceinline__ int slot_pos(bool mn, int t, int e) { return mn ? (e 
 template <bool A_MN, bool B_MN, bool SEP>
 __global__ void __launch_bounds__(FtCfg<SEP>::BLOCK, 1)
     ffma_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-                    int K, float alpha, float beta, float *__restrict__ C, int64_t ldc, int tiles_m, int tiles_n) {
+                    int K, float alpha, float beta, float *__restrict__ C, int64_t ldc, int tiles_m, int tiles_n,
+                    int splits, float *__restrict__ partial) {
     static_assert(A_MN || B_MN, "TN (both K-contiguous) runs on KN3");
     constexpr bool PAIR_J = B_MN;
     constexpr int STAGES = FtCfg<SEP>::STAGES;
@@ -120,14 +123,23 @@ __global__ void __launch_bounds__(FtCfg<SEP>::BLOCK, 1)
     uint64_t *empty = full + STAGES;                                               // SEP only
     unsigned int *done_cnt = reinterpret_cast<unsigned int *>(empty + STAGES);    // !SEP only
 
+    // split-K (sub-wave problems, splits > 1): block = (split sp, tile),
+    // split-major; split sp runs the promotion chunks [sp*nch/S, (sp+1)*nch/S)
+    // of K and stores its raw master to partial slab sp (the fixed-order
+    // reduce launch adds the slabs)
+    const int ntiles = tiles_m * tiles_n;
+    const int sp = (int)blockIdx.x / ntiles;
     // grouped raster: FT_GROUP_M tile-rows share each B panel while it is in L2
-    const int bid = (int)blockIdx.x;
+    const int bid = (int)blockIdx.x - sp * ntiles;
     const int per_group = FT_GROUP_M * tiles_n;
     const int first_m = (bid / per_group) * FT_GROUP_M;
     const int gsize = min(tiles_m - first_m, FT_GROUP_M);
     const int m0 = (first_m + (bid % per_group) % gsize) * FT_M;
     const int n0 = ((bid % per_group) / gsize) * FT_N;
-    const int nk = (K + FT_K - 1) / FT_K;
+    const int nk_all = (K + FT_K - 1) / FT_K;
+    const int nch = (nk_all + FT_PROMOTE - 1) / FT_PROMOTE;
+    const int kt0 = min(nk_all, (int)((long long)sp * nch / splits) * FT_PROMOTE);
+    const int nk = min(nk_all, (int)((long long)(sp + 1) * nch / splits) * FT_PROMOTE);   // end stage
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -144,7 +156,7 @@ __global__ void __launch_bounds__(FtCfg<SEP>::BLOCK, 1)
     // loads of K-stage kt into ring slot kt % STAGES (one thread; the slot
     // is known to be free)
     auto issue = [&](int kt) {
-        const int s = kt % STAGES;
+        const int s = (kt - kt0) % STAGES;
         mbar_arrive_expect_tx(&full[s], FT_STAGE_BYTES);
         const uint32_t st = smem_u32(smem + s * FT_STAGE_BYTES);
         const uint32_t sb = st + FT_TILE_FLOATS * 4;
@@ -168,15 +180,15 @@ __global__ void __launch_bounds__(FtCfg<SEP>::BLOCK, 1)
             if (lane == 0) {
                 prefetch_tmap(&tmA);
                 prefetch_tmap(&tmB);
-                for (int kt = 0; kt < nk; ++kt) {
-                    mbar_wait(&empty[kt % STAGES], ((uint32_t)(kt / STAGES) & 1u) ^ 1u);
+                for (int kt = kt0; kt < nk; ++kt) {
+                    mbar_wait(&empty[(kt - kt0) % STAGES], ((uint32_t)((kt - kt0) / STAGES) & 1u) ^ 1u);
                     issue(kt);
                 }
             }
             return;
         }
     } else if (threadIdx.x == 0) {
-        for (int kt = 0; kt < STAGES && kt < nk; ++kt) issue(kt);   // fill the ring
+        for (int kt = kt0; kt < kt0 + STAGES && kt < nk; ++kt) issue(kt);   // fill the ring
     }
 
     // ===== consumers =====
@@ -193,9 +205,9 @@ __global__ void __launch_bounds__(FtCfg<SEP>::BLOCK, 1)
         for (int e = 0; e < 64; ++e) master_s[e * FT_CONSUMERS + c] = 0.0f;
     }
 
-    for (int kt = 0; kt < nk; ++kt) {
-        const int s = kt % STAGES;
-        mbar_wait(&full[s], (uint32_t)(kt / STAGES) & 1u);
+    for (int kt = kt0; kt < nk; ++kt) {
+        const int s = (kt - kt0) % STAGES;
+        mbar_wait(&full[s], (uint32_t)((kt - kt0) / STAGES) & 1u);
         const float *As = reinterpret_cast<const float *>(smem + s * FT_STAGE_BYTES);
         const float *Bs = As + FT_TILE_FLOATS;
         // operand groups double-buffered: group g+1 is read from SMEM while
@@ -275,11 +287,66 @@ __global__ void __launch_bounds__(FtCfg<SEP>::BLOCK, 1)
             const int row = m0 + slot_pos(A_MN, tm, i);
             if (row < M) {
                 const float v = SEP ? master_s[(i * 8 + j) * FT_CONSUMERS + c] : master_r[(i * 8 + j) % (SEP ? 1 : 64)];
-                float *d = C + row + (int64_t)col * ldc;
-                *d = beta == 0.0f ? alpha * v : fmaf(beta, *d, alpha * v);
+                if (partial) {
+                    partial[((size_t)sp * N + col) * M + row] = v;
+                } else {
+                    float *d = C + row + (int64_t)col * ldc;
+                    *d = beta == 0.0f ? alpha * v : fmaf(beta, *d, alpha * v);
+                }
             }
         }
     }
+}
+
+// Fixed-order split-K reduce of KN3b: C <- alpha*(P_0 + ... + P_{S-1}) (+ beta*C),
+// the slabs column-major M x N (ld = M); consecutive threads take
+// consecutive rows (coalesced slab reads and C accesses).
+__global__ void __launch_bounds__(256) ffma_splitk_reduce_kernel(const float *__restrict__ P, int S, int64_t M,
+                                                                 int64_t N, float alpha, float beta, float *C,
+                                                                 int64_t ldc) {
+    const int64_t total = M * N, slab = M * N;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        float r = __ldcs(P + idx);
+        for (int sp = 1; sp < S; ++sp) r += __ldcs(P + (size_t)sp * slab + idx);
+        const int64_t col = idx / M, row = idx - col * M;
+        float *d = C + row + col * ldc;
+        *d = beta == 0.0f ? alpha * r : fmaf(beta, *d, alpha * r);
+    }
+}
+
+// Split-K factor for sub-wave KN3b grids (one 288-thread CTA per SM):
+// minimise waves(S) * stages_per_split(S) * t_stage + the reduce's HBM
+// round trip ((2S + 1) M N 4 bytes at ~5 TB/s + a launch), with splits of
+// whole promotion chunks (256 of K).  t_stage ~ 2.7 us (128 x 128 x 32 FFMA
+// per SM at ~80 % of the FP32 pipe).  EMM_FFMA_SPLITS overrides.
+int ffma_splits(int64_t M, int64_t N, int64_t K) {
+    const int64_t tiles = ((M + FT_M - 1) / FT_M) * ((N + FT_N - 1) / FT_N);
+    const int64_t nk = (K + FT_K - 1) / FT_K, nch = (nk + FT_PROMOTE - 1) / FT_PROMOTE;
+    const int64_t slots = tc_num_sms();
+    if (const char *e = getenv("EMM_FFMA_SPLITS")) {   // > 0: forced (0: the policy below)
+        const int64_t v = atoi(e);
+        if (v > 0) return (int)std::max<int64_t>(1, std::min<int64_t>({v, nch, 16}));
+    }
+    if (tiles >= slots || nch < 2) return 1;
+    const double t_stage = 2.7e-6;
+    double best = 0.0;
+    int bs = 1;
+    for (int S = 1; S <= 16 && S <= nch; ++S) {
+        const int64_t waves = (tiles * S + slots - 1) / slots;
+        int64_t st = 0;   // stages of the longest split
+        for (int q = 0; q < S; ++q)
+            st = std::max<int64_t>(st, std::min<int64_t>(nk, (int64_t)(q + 1) * nch / S * FT_PROMOTE) -
+                                           std::min<int64_t>(nk, (int64_t)q * nch / S * FT_PROMOTE));
+        double t = (double)waves * (double)st * t_stage;
+        if (S > 1) t += (double)(2 * S + 1) * (double)M * (double)N * 4.0 / 5.0e12 + 3.0e-6;
+        if (S == 1 || t < best) best = t, bs = S;
+    }
+    return bs;
+}
+
+size_t ffma_splitk_bytes(int64_t M, int64_t N, int splits) {
+    return splits > 1 ? (size_t)splits * (size_t)M * (size_t)N * sizeof(float) : 0;
 }
 
 bool ffma_tma_eligible(bool tA, bool tB, const float *A, int64_t lda, const float *B, int64_t ldb) {
@@ -289,8 +356,10 @@ bool ffma_tma_eligible(bool tA, bool tB, const float *A, int64_t lda, const floa
 
 cudaError_t launch_ffma_tma_sgemm(bool tA, bool tB, int64_t M, int64_t N, int64_t K, float alpha, const float *A,
                                   int64_t lda, const float *B, int64_t ldb, float beta, float *C, int64_t ldc,
-                                  cudaStream_t s) {
+                                  cudaStream_t s, int splits, float *partial) {
     const bool a_mn = !tA, b_mn = tB;
+    if (splits < 1 || (splits > 1 && !partial)) return cudaErrorInvalidValue;
+    if (splits == 1) partial = nullptr;
     if (!a_mn && !b_mn) return cudaErrorInvalidValue;
     if (M > 0x7fffff00LL || N > 0x7fffff00LL || K > 0x7fffff00LL) return cudaErrorInvalidValue;
     const int64_t tiles_m = (M + FT_M - 1) / FT_M, tiles_n = (N + FT_N - 1) / FT_N;
@@ -315,20 +384,29 @@ cudaError_t launch_ffma_tma_sgemm(bool tA, bool tB, int64_t M, int64_t N, int64_
         return e;
     }();
     if (attr != cudaSuccess) return attr;
-    const unsigned grid = (unsigned)(tiles_m * tiles_n);
+    if (tiles_m * tiles_n * splits > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+    const unsigned grid = (unsigned)(tiles_m * tiles_n * splits);
     cudaEvent_t ev = nullptr;
     prof_begin(s, true, &ev);
     if (a_mn && !b_mn)
         ffma_tma_kernel<true, false, FT_SEP><<<grid, FtCfg<FT_SEP>::BLOCK, FtCfg<FT_SEP>::SMEM, s>>>(ta, tb, (int)M, (int)N, (int)K, alpha, beta, C,
-                                                                       ldc, (int)tiles_m, (int)tiles_n);
+                                                                       ldc, (int)tiles_m, (int)tiles_n, splits, partial);
     else if (a_mn)
         ffma_tma_kernel<true, true, FT_SEP><<<grid, FtCfg<FT_SEP>::BLOCK, FtCfg<FT_SEP>::SMEM, s>>>(ta, tb, (int)M, (int)N, (int)K, alpha, beta, C,
-                                                                      ldc, (int)tiles_m, (int)tiles_n);
+                                                                      ldc, (int)tiles_m, (int)tiles_n, splits, partial);
     else
         ffma_tma_kernel<false, true, FT_SEP><<<grid, FtCfg<FT_SEP>::BLOCK, FtCfg<FT_SEP>::SMEM, s>>>(ta, tb, (int)M, (int)N, (int)K, alpha, beta, C,
-                                                                       ldc, (int)tiles_m, (int)tiles_n);
+                                                                       ldc, (int)tiles_m, (int)tiles_n, splits, partial);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     prof_end(s, true, ev);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess || !partial) return e;
+    const int64_t total = M * N;
+    const unsigned rg = (unsigned)std::min<int64_t>((total + 255) / 256, (int64_t)tc_num_sms() * 8);
+    prof_begin(s, false, &ev);
+    ffma_splitk_reduce_kernel<<<rg, 256, 0, s>>>(partial, splits, M, N, alpha, beta, C, ldc);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    prof_end(s, false, ev);
     return cudaGetLastError();
 }
 

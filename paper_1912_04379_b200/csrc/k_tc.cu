@@ -69,6 +69,9 @@ int64_t tc_kpad(int64_t K) { return (K + TC_BK - 1) / TC_BK * TC_BK; }
 //   PK_RAW    plane 0 = x unchanged in the SOURCE layout with a 16-byte-
 //             multiple leading dimension ld0 (re-pitch of a TMA-illegal
 //             operand for the in-kernel-split GEMM KN1X)
+//   PK_RAWT   plane 0 = x unchanged, K-major [R][ld0], zero padded to Kp
+//             (transposing copy of an MN-contiguous source; the FFMA path
+//             uses it to turn a TN call into one the TMA-fed KN3b covers)
 // BF16 cross operand: for every group of 8 along K, 16 bf16 = [bf16(big) x8 |
 // bf16(x - big) x8] (A side) or the halves swapped (B side), so that ONE K16
 // BF16 MMA computes a_big*b_small + a_small*b_big.
@@ -82,7 +85,7 @@ int64_t tc_kpad(int64_t K) { return (K + TC_BK - 1) / TC_BK * TC_BK; }
 //  * transpose: MN-contiguous source -> K-major planes (the re-buffered
 //    FULL modes and PK_DCROSS): 64 (r) x 32 (p) tiles through shared memory.
 // =====================================================================
-enum { PK_FULL1 = PK_FULL1_, PK_FULL3 = PK_FULL3_, PK_FULLX = PK_FULLX_, PK_DSMALL = PK_DSMALL_, PK_DCROSS = PK_DCROSS_,
+enum { PK_FULL1 = PK_FULL1_, PK_FULL3 = PK_FULL3_, PK_FULLX = PK_FULLX_, PK_DSMALL = PK_DSMALL_, PK_DCROSS = PK_DCROSS_, PK_RAWT = PK_RAWT_,
        PK_RAW = PK_RAW_ };
 
 constexpr int PK_THREADS = 256;
@@ -117,7 +120,8 @@ __device__ __forceinline__ void split_one(const PackOperand &op, float x, float 
     // PK_DCROSS: the direct GEMM's TMA rounds the user operand to
     // rn_tf32(x) on load (TFLOAT32 tensor map, R7c), so the cross plane is
     // made against that same big part
-    if (MODE == PK_DSMALL || (MODE == PK_DCROSS && op.trunc_big)) big = trunc_tf32(x);
+    if (MODE == PK_RAWT) big = x;
+    else if (MODE == PK_DSMALL || (MODE == PK_DCROSS && op.trunc_big)) big = trunc_tf32(x);
     else big = op.raw_big ? x : __uint_as_float(cvt_tf32_rn(x));
     lo = isfinite(x) ? x - big : 0.0f;   // exact
 }
@@ -161,7 +165,7 @@ __device__ __forceinline__ void pack_store4(const PackOperand &op, float *o0, fl
     float big[4], lo[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) split_one<MODE>(op, x[i], big[i], lo[i]);
-    if (MODE == PK_FULL1 || MODE == PK_FULL3 || MODE == PK_FULLX)
+    if (MODE == PK_FULL1 || MODE == PK_FULL3 || MODE == PK_FULLX || MODE == PK_RAWT)
         *reinterpret_cast<float4 *>(o0 + e) = make_float4(big[0], big[1], big[2], big[3]);
     if (MODE == PK_FULL3 || MODE == PK_DSMALL)
         *reinterpret_cast<float4 *>(o1 + e) =
@@ -348,6 +352,7 @@ cudaError_t launch_pack(int mode, const PackArgs &a, const PackArgs *b, int64_t 
         case PK_DSMALL: pack_split_kernel<PK_DSMALL><<<grid, PK_THREADS, 0, s>>>(oa, ob, K, ctrl, ctrl_words); break;
         case PK_DCROSS: pack_split_kernel<PK_DCROSS><<<grid, PK_THREADS, 0, s>>>(oa, ob, K, ctrl, ctrl_words); break;
         case PK_RAW: pack_split_kernel<PK_RAW><<<grid, PK_THREADS, 0, s>>>(oa, ob, K, ctrl, ctrl_words); break;
+        case PK_RAWT: pack_split_kernel<PK_RAWT><<<grid, PK_THREADS, 0, s>>>(oa, ob, K, ctrl, ctrl_words); break;
         default: return cudaErrorInvalidValue;
     }
     g_launches.fetch_add(1, std::memory_order_relaxed);

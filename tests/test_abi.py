@@ -126,6 +126,10 @@ def test_workspace_bytes(emm):
         return al(cols * (-(-rows // 4) * 4) * 4)
 
     assert emm.workspace_bytes("N", "N", 64, 64, 64, "ffma") == 0
+    # FFMA: room for the relayout copies (TN: the smaller operand transposed,
+    # rows padded to 32; the other re-pitched, ld rounded up to 4)
+    assert emm.workspace_bytes("T", "N", 4096, 2048, 512, "ffma") == repitch(512, 4096) + 4 * 512 * 2048
+    assert emm.workspace_bytes("N", "N", 4096, 2048, 512, "ffma") == repitch(4096, 512) + repitch(512, 2048)
     # 3xTF32 (KN1X): at most a raw re-pitch of both operands
     assert emm.workspace_bytes("N", "N", 2048, 1024, 33, "3xtf32") == repitch(2048, 33) + repitch(33, 1024) + CTRL
     assert emm.workspace_bytes("T", "T", 2048, 1024, 33, "3xtf32") == repitch(33, 2048) + repitch(1024, 33) + CTRL

@@ -421,7 +421,7 @@ def test_small_problem_default_path(emm, monkeypatch, shape):
     M, N, K = shape
     case = Case("N", "N", M, N, K, 1.0, 0.0)
     R, S, T, _ = case.oracle()
-    tiny_all = 2 * M * N * K <= 1 << 27   # tiny kernel for every mode; above, only for FFMA (<= 2.2e9 flops)
+    tiny_all = 2 * M * N * K <= 1 << 27   # tiny kernel for every mode; above, only for FFMA (<= 7e8 flops)
     for math in MATHS:
         Cg = case.run(emm, math)
         case.check_untouched(Cg)
