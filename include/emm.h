@@ -99,7 +99,11 @@ int emm_sgemm_ex(char transA, char transB, int64_t M, int64_t N, int64_t K,
                  float beta, float *C, int64_t ldc, void *stream,
                  emm_math_t math, void *workspace, size_t workspace_bytes);
 
-/* Device workspace the call above needs (0 for EMM_MATH_FFMA).  Host-only. */
+/* Device workspace the call above needs (an upper bound over leading
+ * dimensions and pointer alignment: TMA-illegal operands need a re-pitched
+ * copy; EMM_MATH_FFMA also a transposed copy for transA = T / transB = N and
+ * split-K partial slabs on sub-wave grids; 0 for latency-bound sizes that
+ * take the tiny kernel).  Host-only. */
 size_t emm_sgemm_workspace_bytes(char transA, char transB, int64_t M, int64_t N,
                                  int64_t K, emm_math_t math);
 
