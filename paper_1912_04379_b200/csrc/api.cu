@@ -332,13 +332,17 @@ static FfmaRelayout ffma_relayout(bool tA, bool tB, int64_t M, int64_t N, int64_
 
 static size_t ws_bytes(char tA, char tB, int64_t M, int64_t N, int64_t K, emm_math_t math) {
     if (M == 0 || N == 0 || K == 0) return 0;
+    if (M <= SKINNY_MAX || N <= SKINNY_MAX) {
+        // KN9T planes (tensor-core modes) or the FFMA skinny path's split-K slabs
+        const size_t ff = skinny_split_bytes(!is_n(tA), !is_n(tB), M, N, K, nullptr, 0, nullptr, 0);
+        return math == EMM_MATH_FFMA ? ff : std::max(ff, skinny_tc_workspace_bytes(M, N, K));
+    }
     if (math == EMM_MATH_FFMA) {
         // upper bound: the relayout copies with both operands TMA-illegal
-        if (M <= SKINNY_MAX || N <= SKINNY_MAX || small_problem(M, N, K, math)) return 0;
+        if (small_problem(M, N, K, math)) return 0;
         return align_up(ffma_relayout(!is_n(tA), !is_n(tB), M, N, K, false, false).total, 1024) +
                ffma_splitk_bytes(M, N, ffma_splits(M, N, K));
     }
-    if (M <= SKINNY_MAX || N <= SKINNY_MAX) return skinny_tc_workspace_bytes(M, N, K);   // KN9T (upper bound)
     if (small_problem(M, N, K, math)) return 0;
     // 3xTF32 on KN1X: at most the raw re-pitch of both operands (when their
     // leading dimensions are TMA-illegal) + split-K / stream-K scratch; the
@@ -405,8 +409,26 @@ extern "C" int emm_sgemm_ex(char transA, char transB, int64_t M, int64_t N, int6
             }
             return cuda_status(e);
         }
-        return cuda_status(
-            launch_skinny_sgemm(!is_n(transA), !is_n(transB), M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, s));
+        // FFMA skinny (KN9): split-K slabs when the row blocks do not fill the SMs
+        const size_t need = skinny_split_bytes(!is_n(transA), !is_n(transB), M, N, K, A, lda, B, ldb);
+        void *ws = workspace;
+        bool own = false;
+        if (need) {
+            if (ws) {
+                if (workspace_bytes < need || (reinterpret_cast<uintptr_t>(ws) & 1023u)) return EMM_ERR_WORKSPACE;
+            } else {
+                cudaError_t e = scratch_alloc(&ws, need, s);
+                if (e != cudaSuccess) return cuda_status(e);
+                own = true;
+            }
+        }
+        cudaError_t e = launch_skinny_sgemm(!is_n(transA), !is_n(transB), M, N, K, alpha, A, lda, B, ldb, beta, C,
+                                            ldc, s, need ? reinterpret_cast<float *>(ws) : nullptr, need);
+        if (own) {
+            cudaError_t e2 = cudaFreeAsync(ws, s);
+            if (e == cudaSuccess) e = e2;
+        }
+        return cuda_status(e);
     }
 
     if (small_problem(M, N, K, math))

@@ -166,7 +166,11 @@ size_t ffma_splitk_bytes(int64_t M, int64_t N, int splits);
 constexpr int64_t SKINNY_MAX = 16;
 cudaError_t launch_skinny_sgemm(bool tA, bool tB, int64_t M, int64_t N, int64_t K, float alpha, const float *A,
                                 int64_t lda, const float *B, int64_t ldb, float beta, float *C, int64_t ldc,
-                                cudaStream_t s);
+                                cudaStream_t s, float *ws = nullptr, size_t ws_bytes = 0);
+// split-K slab bytes of the FFMA skinny path for this call (0: no split;
+// A = B = null: the upper bound over pointers / leading dimensions)
+size_t skinny_split_bytes(bool tA, bool tB, int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
+                          const float *B, int64_t ldb);
 
 // KN9T (k_skinny_tc.cu): the same roles on the tensor cores — the long
 // operand TMA-streamed, split in the kernel and fed to tcgen05.mma from TMEM,

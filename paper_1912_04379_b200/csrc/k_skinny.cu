@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 
@@ -184,42 +185,67 @@ constexpr int SKT_TPB = 256, SKT_KC = 32;        // compute threads per CTA, K p
 constexpr int SKT_THREADS = SKT_TPB + 32;        // + one producer warp
 }  // namespace
 
-// RPT rows of C' per compute thread (rows tid, tid + 256, ...): the B'
-// broadcast loads are shared by RPT rows.
-template <bool TA, bool TB, int NC, int RPT>
-__global__ void __launch_bounds__(SKT_THREADS, 1)
+// RPT rows of C' per compute thread (RPT = 1: row tid; RPT = 2: rows 2 tid,
+// 2 tid + 1 as an FFMA2 pair): the B' broadcast loads are shared by RPT rows.
+template <bool TA, bool TB, int NC, int RPT, int TPB>
+__global__ void __launch_bounds__(TPB + 32, 1)
     skinny_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int64_t Mr,
-                      int Nc, int64_t K, float alpha, float beta, float *__restrict__ C, int64_t rs, int64_t cs) {
+                      int Nc, int64_t K, float alpha, float beta, float *__restrict__ C, int64_t rs, int64_t cs,
+                      int splits, float *__restrict__ partial) {
     using namespace ptx;
-    constexpr int SKT_ROWS = SKT_TPB * RPT;
+    constexpr int SKT_ROWS = TPB * RPT;
     constexpr int SKT_STAGES = RPT == 1 ? 4 : 3;
     constexpr int SKT_A_BYTES = SKT_ROWS * SKT_KC * 4;
     constexpr int B_BYTES = SKT_KC * NC * 4;
     constexpr int STAGE = SKT_A_BYTES + ((B_BYTES + 1023) / 1024) * 1024;
     extern __shared__ uint8_t skt_raw[];
-    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(skt_raw) + 1023) & ~uintptr_t(1023));
+    // offset arithmetic on the shared array (an integer round trip would turn
+    // the operand reads into generic LD, long-scoreboard loads)
+    uint8_t *smem = skt_raw + ((1024u - (ptx::smem_u32(skt_raw) & 1023u)) & 1023u);
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + SKT_STAGES * STAGE);
     uint64_t *empty = full + SKT_STAGES;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t nblocks = (Mr + SKT_ROWS - 1) / SKT_ROWS;
     const int64_t nchunks = (K + SKT_KC - 1) / SKT_KC;
+    // split-K (few row blocks, long K): unit u = (row block u % nblocks,
+    // split u / nblocks); split sp runs the 256-of-K promotion groups
+    // [sp*ng/S, (sp+1)*ng/S) and stores its raw master to partial slab sp
+    constexpr int PROM = 256 / SKT_KC;
+    const int64_t ngroups = (nchunks + PROM - 1) / PROM, nunits = nblocks * splits;
+    auto unit = [&](int64_t u, int64_t &rb, int &sp, int64_t &c0, int64_t &c1) {
+        rb = u % nblocks;
+        sp = (int)(u / nblocks);
+        c0 = min(nchunks, sp * ngroups / splits * PROM);
+        c1 = min(nchunks, (sp + 1) * ngroups / splits * PROM);
+    };
+    auto store = [&](int64_t row, int c, int sp, float v) {
+        if (partial) {
+            partial[((size_t)sp * Nc + c) * Mr + row] = v;
+        } else {
+            float *d = C + row * rs + (int64_t)c * cs;
+            *d = beta == 0.0f ? alpha * v : fmaf(beta, *d, alpha * v);
+        }
+    };
     if (tid == 0) {
         for (int s = 0; s < SKT_STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], SKT_TPB / 32);
+            mbar_init(&empty[s], TPB / 32);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (warp == SKT_TPB / 32) {
+    if (warp == TPB / 32) {
         // ===== producer =====
         if (lane == 0) {
             prefetch_tmap(&tmA);
             prefetch_tmap(&tmB);
             const uint64_t pa = policy_evict_first(), pb = policy_evict_last();
             int64_t it = 0;
-            for (int64_t rb = blockIdx.x; rb < nblocks; rb += gridDim.x) {
-                for (int64_t ch = 0; ch < nchunks; ++ch, ++it) {
+            for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+                int64_t rb, ch0, ch1;
+                int sp;
+                unit(u, rb, sp, ch0, ch1);
+                for (int64_t ch = ch0; ch < ch1; ++ch, ++it) {
                     const int s = (int)(it % SKT_STAGES);
                     mbar_wait(&empty[s], ((uint32_t)(it / SKT_STAGES) & 1u) ^ 1u);
                     mbar_arrive_expect_tx(&full[s], (uint32_t)(SKT_A_BYTES + B_BYTES));
@@ -227,8 +253,8 @@ __global__ void __launch_bounds__(SKT_THREADS, 1)
                     const int32_t r0 = (int32_t)(rb * SKT_ROWS), k0 = (int32_t)(ch * SKT_KC);
 #pragma unroll
                     for (int h = 0; h < RPT; ++h) {   // 256-row boxes
-                        if (!TA) tma_load_2d(st + h * SKT_TPB * SKT_KC * 4, &tmA, &full[s], r0 + h * SKT_TPB, k0, pa);
-                        else tma_load_2d(st + h * SKT_TPB * SKT_KC * 4, &tmA, &full[s], k0, r0 + h * SKT_TPB, pa);
+                        if (!TA) tma_load_2d(st + h * TPB * SKT_KC * 4, &tmA, &full[s], r0 + h * TPB, k0, pa);
+                        else tma_load_2d(st + h * TPB * SKT_KC * 4, &tmA, &full[s], k0, r0 + h * TPB, pa);
                     }
                     if (!TB) tma_load_2d(st + SKT_A_BYTES, &tmB, &full[s], k0, 0, pb);
                     else tma_load_2d(st + SKT_A_BYTES, &tmB, &full[s], 0, k0, pb);
@@ -239,13 +265,88 @@ __global__ void __launch_bounds__(SKT_THREADS, 1)
     }
     // ===== compute warps: RPT rows of C' per thread =====
     int64_t it = 0;
-    for (int64_t rb = blockIdx.x; rb < nblocks; rb += gridDim.x) {
+    if (RPT == 2 && !TA) {
+        // rows 2t and 2t+1 of the 512-row block: one float2 of A' per k is
+        // an FFMA2 operand pair (the two rows), the column value of B' the
+        // broadcast one — two FP32 FMAs per issue slot, each entry's sum in
+        // increasing k exactly as the scalar form (same bits)
+        const int rl = 2 * tid;                                 // row pair within the block
+        const int hb = rl / TPB, rb_l = rl % TPB;       // its TPB-row box, row in the box
+        for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+            int64_t rb, ch0, ch1;
+            int sp;
+            unit(u, rb, sp, ch0, ch1);
+            float2 acc[NC], master[NC];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) acc[c] = master[c] = make_float2(0.0f, 0.0f);
+            for (int64_t ch = ch0; ch < ch1; ++ch, ++it) {
+                const int s = (int)(it % SKT_STAGES);
+                mbar_wait(&full[s], (uint32_t)(it / SKT_STAGES) & 1u);
+                const float *Ah = reinterpret_cast<const float *>(smem + s * STAGE) + hb * TPB * SKT_KC;
+                const float *Bs = reinterpret_cast<const float *>(smem + s * STAGE + SKT_A_BYTES);
+#pragma unroll 1
+                for (int j = 0; j < SKT_KC / 4; ++j) {   // not unrolled: B' values of one j only (no spills)
+                    float2 a[4];
+                    if (!TA) {
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk)
+                            a[kk] = *reinterpret_cast<const float2 *>(Ah + (4 * j + kk) * TPB + rb_l);
+                    } else {   // 128B swizzle: 16-byte chunk j of row r sits at chunk j ^ (r & 7)
+                        const float4 x0 = *reinterpret_cast<const float4 *>(Ah + rb_l * SKT_KC + 4 * (j ^ (rb_l & 7)));
+                        const float4 x1 =
+                            *reinterpret_cast<const float4 *>(Ah + (rb_l + 1) * SKT_KC + 4 * (j ^ ((rb_l + 1) & 7)));
+                        a[0] = make_float2(x0.x, x1.x);
+                        a[1] = make_float2(x0.y, x1.y);
+                        a[2] = make_float2(x0.z, x1.z);
+                        a[3] = make_float2(x0.w, x1.w);
+                    }
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) {
+                        float b[4];
+                        if (!TB) {
+                            const float4 v = *reinterpret_cast<const float4 *>(Bs + c * SKT_KC + 4 * j);
+                            b[0] = v.x; b[1] = v.y; b[2] = v.z; b[3] = v.w;
+                        } else {
+#pragma unroll
+                            for (int kk = 0; kk < 4; ++kk) b[kk] = Bs[(4 * j + kk) * NC + c];
+                        }
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk) acc[c] = __ffma2_rn(a[kk], make_float2(b[kk], b[kk]), acc[c]);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);
+                if ((ch + 1) % PROM == 0 || ch + 1 == ch1) {
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) {
+                        master[c].x += acc[c].x;
+                        master[c].y += acc[c].y;
+                        acc[c] = make_float2(0.0f, 0.0f);
+                    }
+                }
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t row = rb * SKT_ROWS + rl + h;
+                if (row < Mr) {
+#pragma unroll
+                    for (int c = 0; c < NC; ++c)
+                        if (c < Nc) store(row, c, sp, h ? master[c].y : master[c].x);
+                }
+            }
+        }
+        return;
+    }
+    for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+        int64_t rb, ch0, ch1;
+        int sp;
+        unit(u, rb, sp, ch0, ch1);
         float acc[RPT][NC], master[RPT][NC];
 #pragma unroll
         for (int h = 0; h < RPT; ++h)
 #pragma unroll
             for (int c = 0; c < NC; ++c) acc[h][c] = master[h][c] = 0.0f;
-        for (int64_t ch = 0; ch < nchunks; ++ch, ++it) {
+        for (int64_t ch = ch0; ch < ch1; ++ch, ++it) {
             const int s = (int)(it % SKT_STAGES);
             mbar_wait(&full[s], (uint32_t)(it / SKT_STAGES) & 1u);
             const float *As = reinterpret_cast<const float *>(smem + s * STAGE);
@@ -255,12 +356,12 @@ __global__ void __launch_bounds__(SKT_THREADS, 1)
                 float4 a[RPT];
 #pragma unroll
                 for (int h = 0; h < RPT; ++h) {
-                    const float *Ah = As + h * SKT_TPB * SKT_KC;   // box h
+                    const float *Ah = As + h * TPB * SKT_KC;   // box h
                     if (!TA) {
-                        a[h].x = Ah[(4 * j + 0) * SKT_TPB + tid];
-                        a[h].y = Ah[(4 * j + 1) * SKT_TPB + tid];
-                        a[h].z = Ah[(4 * j + 2) * SKT_TPB + tid];
-                        a[h].w = Ah[(4 * j + 3) * SKT_TPB + tid];
+                        a[h].x = Ah[(4 * j + 0) * TPB + tid];
+                        a[h].y = Ah[(4 * j + 1) * TPB + tid];
+                        a[h].z = Ah[(4 * j + 2) * TPB + tid];
+                        a[h].w = Ah[(4 * j + 3) * TPB + tid];
                     } else {   // 128B swizzle: 16-byte chunk j of row tid sits at chunk j ^ (tid & 7)
                         a[h] = *reinterpret_cast<const float4 *>(Ah + tid * SKT_KC + 4 * (j ^ (tid & 7)));
                     }
@@ -287,7 +388,7 @@ __global__ void __launch_bounds__(SKT_THREADS, 1)
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);
-            if ((ch + 1) % (256 / SKT_KC) == 0 || ch + 1 == nchunks) {
+            if ((ch + 1) % PROM == 0 || ch + 1 == ch1) {
 #pragma unroll
                 for (int h = 0; h < RPT; ++h)
 #pragma unroll
@@ -299,14 +400,11 @@ __global__ void __launch_bounds__(SKT_THREADS, 1)
         }
 #pragma unroll
         for (int h = 0; h < RPT; ++h) {
-            const int64_t row = rb * SKT_ROWS + h * SKT_TPB + tid;
+            const int64_t row = rb * SKT_ROWS + h * TPB + tid;
             if (row < Mr) {
 #pragma unroll
                 for (int c = 0; c < NC; ++c)
-                    if (c < Nc) {
-                        float *d = C + row * rs + (int64_t)c * cs;
-                        *d = beta == 0.0f ? alpha * master[h][c] : fmaf(beta, *d, alpha * master[h][c]);
-                    }
+                    if (c < Nc) store(row, c, sp, master[h][c]);
             }
         }
     }
@@ -335,35 +433,83 @@ static bool skinny_tmap(CUtensorMap *tm, const float *ptr, int64_t ld, uint64_t 
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <bool TA, bool TB, int NC, int RPT>
+// Fixed-order reduce of the split-K slabs: C'(r, c) <- alpha * (P_0 + ... +
+// P_{S-1})(r, c) (+ beta * C'), slab layout [c][r] (r contiguous).
+__global__ void __launch_bounds__(256) skinny_splitk_reduce_kernel(const float *__restrict__ P, int S, int64_t Mr,
+                                                                   int Nc, float alpha, float beta, float *C,
+                                                                   int64_t rs, int64_t cs) {
+    const int64_t total = Mr * Nc;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        float v = __ldcs(P + idx);
+        for (int sp = 1; sp < S; ++sp) v += __ldcs(P + (size_t)sp * total + idx);
+        const int64_t c = idx / Mr, r = idx - c * Mr;
+        float *d = C + r * rs + c * cs;
+        *d = beta == 0.0f ? alpha * v : fmaf(beta, *d, alpha * v);
+    }
+}
+
+// Launch plan of the TMA streaming kernel: compute threads per CTA (rows per
+// block = 2 TPB) and K splits.  Row blocks < SMs and K long: split K over
+// whole 256-of-K promotion groups (>= 2 per split) so that blocks * S fill
+// the SMs (16384 x 16 x 16384: 32 blocks x 4 splits).
+struct SkPlan {
+    int tpb = SKT_TPB, splits = 1;
+};
+static SkPlan skinny_plan(bool TA, int64_t Mr, int64_t K) {
+    SkPlan P;
+    const int64_t sms = tc_num_sms();
+    auto span = [&](int64_t rows) { return ((Mr + rows - 1) / rows + sms - 1) / sms * rows; };
+    // rows per CTA 2 * TPB: 512 or 448, whichever finishes the persistent
+    // grid in fewer row-slots per SM (65536 rows: 128 blocks of 512 leave 20
+    // SMs idle, 147 blocks of 448 fill them)
+    P.tpb = span(448) < span(512) ? 224 : 256;
+    if (const char *e = getenv("EMM_SKINNY_TPB")) P.tpb = atoi(e) == 224 ? 224 : 256;   // experiments
+    const int64_t nb = (Mr + 2 * P.tpb - 1) / (2 * P.tpb);
+    const int64_t ngroups = ((K + SKT_KC - 1) / SKT_KC + 7) / 8;
+    int64_t S = nb < sms ? std::min<int64_t>(sms / nb, ngroups / 2) : 1;
+    if (const char *e = getenv("EMM_SKINNY_SPLITS")) {   // > 0: forced (0: the policy)
+        if (atoi(e) > 0) S = std::min<int64_t>(atoi(e), std::max<int64_t>(ngroups, 1));
+    }
+    P.splits = (int)std::max<int64_t>(1, std::min<int64_t>(S, 64));
+    return P;
+}
+
+template <bool TA, bool TB, int NC, int RPT, int TPB = SKT_TPB>
 static cudaError_t launch_tma_nc(int64_t Mr, int Nc, int64_t K, float alpha, const float *Ap, int64_t lda,
                                  const float *Bp, int64_t ldb, float beta, float *C, int64_t rs, int64_t cs,
-                                 cudaStream_t s) {
-    constexpr int ROWS = SKT_TPB * RPT;
+                                 cudaStream_t s, int splits = 1, float *partial = nullptr) {
+    constexpr int ROWS = TPB * RPT;
     constexpr int STAGES = RPT == 1 ? 4 : 3;
     constexpr int B_BYTES = SKT_KC * NC * 4;
     constexpr int STAGE = ROWS * SKT_KC * 4 + ((B_BYTES + 1023) / 1024) * 1024;
     constexpr int SMEM = STAGES * STAGE + 1024 + 128;
-    static cudaError_t attr = cudaFuncSetAttribute(skinny_tma_kernel<TA, TB, NC, RPT>,
+    static cudaError_t attr = cudaFuncSetAttribute(skinny_tma_kernel<TA, TB, NC, RPT, TPB>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     if (attr != cudaSuccess) return attr;
     CUtensorMap ta, tb;
-    const bool ok_a = !TA ? skinny_tmap(&ta, Ap, lda, (uint64_t)Mr, (uint64_t)K, SKT_TPB, SKT_KC, false)
-                          : skinny_tmap(&ta, Ap, lda, (uint64_t)K, (uint64_t)Mr, SKT_KC, SKT_TPB, true);
+    const bool ok_a = !TA ? skinny_tmap(&ta, Ap, lda, (uint64_t)Mr, (uint64_t)K, TPB, SKT_KC, false)
+                          : skinny_tmap(&ta, Ap, lda, (uint64_t)K, (uint64_t)Mr, SKT_KC, TPB, true);
     const bool ok_b = !TB ? skinny_tmap(&tb, Bp, ldb, (uint64_t)K, (uint64_t)Nc, SKT_KC, NC, false)
                           : skinny_tmap(&tb, Bp, ldb, (uint64_t)Nc, (uint64_t)K, NC, SKT_KC, false);
     if (!ok_a || !ok_b) return cudaErrorInvalidValue;
-    const int64_t nblocks = (Mr + ROWS - 1) / ROWS;
-    const int64_t grid = nblocks < tc_num_sms() ? nblocks : tc_num_sms();
-    skinny_tma_kernel<TA, TB, NC, RPT><<<(unsigned)grid, SKT_THREADS, SMEM, s>>>(ta, tb, Mr, Nc, K, alpha, beta, C,
-                                                                                  rs, cs);
+    const int64_t units = (Mr + ROWS - 1) / ROWS * splits;
+    const int64_t grid = units < tc_num_sms() ? units : tc_num_sms();
+    skinny_tma_kernel<TA, TB, NC, RPT, TPB><<<(unsigned)grid, TPB + 32, SMEM, s>>>(
+        ta, tb, Mr, Nc, K, alpha, beta, C, rs, cs, splits, splits > 1 ? partial : nullptr);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess || splits == 1) return e;
+    const int64_t total = Mr * Nc;
+    const unsigned rg = (unsigned)std::min<int64_t>((total + 255) / 256, (int64_t)tc_num_sms() * 8);
+    skinny_splitk_reduce_kernel<<<rg, 256, 0, s>>>(partial, splits, Mr, Nc, alpha, beta, C, rs, cs);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
     return cudaGetLastError();
 }
 
 template <bool TA, bool TB>
 static cudaError_t launch_tma(int64_t Mr, int Nc, int64_t K, float alpha, const float *Ap, int64_t lda,
                               const float *Bp, int64_t ldb, float beta, float *C, int64_t rs, int64_t cs,
-                              cudaStream_t s) {
+                              cudaStream_t s, float *ws, size_t ws_bytes) {
     int rpt = 2;
     if (const char *e = getenv("EMM_SKINNY_RPT")) rpt = atoi(e);   // experiments
     if (rpt == 1) {
@@ -371,44 +517,79 @@ static cudaError_t launch_tma(int64_t Mr, int Nc, int64_t K, float alpha, const 
         if (Nc <= 8) return launch_tma_nc<TA, TB, 8, 1>(Mr, Nc, K, alpha, Ap, lda, Bp, ldb, beta, C, rs, cs, s);
         return launch_tma_nc<TA, TB, 16, 1>(Mr, Nc, K, alpha, Ap, lda, Bp, ldb, beta, C, rs, cs, s);
     }
-    if (Nc <= 4) return launch_tma_nc<TA, TB, 4, 2>(Mr, Nc, K, alpha, Ap, lda, Bp, ldb, beta, C, rs, cs, s);
-    if (Nc <= 8) return launch_tma_nc<TA, TB, 8, 2>(Mr, Nc, K, alpha, Ap, lda, Bp, ldb, beta, C, rs, cs, s);
-    return launch_tma_nc<TA, TB, 16, 2>(Mr, Nc, K, alpha, Ap, lda, Bp, ldb, beta, C, rs, cs, s);
+    SkPlan P = skinny_plan(TA, Mr, K);
+    if (P.splits > 1 && (!ws || ws_bytes < (size_t)P.splits * Mr * Nc * 4)) P.splits = 1;
+    const int S = P.splits;
+    if (P.tpb == 224) {
+        if (Nc <= 4) return launch_tma_nc<TA, TB, 4, 2, 224>(Mr, Nc, K, alpha, Ap, lda, Bp, ldb, beta, C, rs, cs, s, S, ws);
+        if (Nc <= 8) return launch_tma_nc<TA, TB, 8, 2, 224>(Mr, Nc, K, alpha, Ap, lda, Bp, ldb, beta, C, rs, cs, s, S, ws);
+        return launch_tma_nc<TA, TB, 16, 2, 224>(Mr, Nc, K, alpha, Ap, lda, Bp, ldb, beta, C, rs, cs, s, S, ws);
+    }
+    if (Nc <= 4) return launch_tma_nc<TA, TB, 4, 2>(Mr, Nc, K, alpha, Ap, lda, Bp, ldb, beta, C, rs, cs, s, S, ws);
+    if (Nc <= 8) return launch_tma_nc<TA, TB, 8, 2>(Mr, Nc, K, alpha, Ap, lda, Bp, ldb, beta, C, rs, cs, s, S, ws);
+    return launch_tma_nc<TA, TB, 16, 2>(Mr, Nc, K, alpha, Ap, lda, Bp, ldb, beta, C, rs, cs, s, S, ws);
 }
 
-cudaError_t launch_skinny_sgemm(bool tA, bool tB, int64_t M, int64_t N, int64_t K, float alpha, const float *A,
-                                int64_t lda, const float *B, int64_t ldb, float beta, float *C, int64_t ldc,
-                                cudaStream_t s) {
-    // Roles: the long output dimension is streamed (rows of C'), the short one
-    // (<= SKINNY_MAX) is resident.  N short: C' = C, A' = op(A), B' = op(B).
-    // M short: C' = C^T = op(B)^T op(A)^T, A' = op(B)^T, B' = op(A)^T.
+// The skinny call's roles (see launch_skinny_sgemm).
+struct SkRoles {
     bool TA, TB;
     int64_t Mr, lda2, ldb2, rs, cs;
     int Nc;
     const float *Ap, *Bp;
+};
+static SkRoles skinny_roles(bool tA, bool tB, int64_t M, int64_t N, const float *A, int64_t lda, const float *B,
+                            int64_t ldb, int64_t ldc) {
+    SkRoles R;
     if (N <= SKINNY_MAX) {
-        Mr = M; Nc = (int)N;
-        Ap = A; lda2 = lda; TA = tA;          // op(A)(r,p): tA ? A[p + r*lda] : A[r + p*lda]
-        Bp = B; ldb2 = ldb; TB = tB;          // op(B)(p,c): tB ? B[c + p*ldb] : B[p + c*ldb]
-        rs = 1; cs = ldc;
+        R.Mr = M; R.Nc = (int)N;
+        R.Ap = A; R.lda2 = lda; R.TA = tA;    // op(A)(r,p): tA ? A[p + r*lda] : A[r + p*lda]
+        R.Bp = B; R.ldb2 = ldb; R.TB = tB;    // op(B)(p,c): tB ? B[c + p*ldb] : B[p + c*ldb]
+        R.rs = 1; R.cs = ldc;
     } else {
-        Mr = N; Nc = (int)M;
+        R.Mr = N; R.Nc = (int)M;
         // A'(r,p) = op(B)(p,r): tB ? B[r + p*ldb] (r contiguous: !TA) : B[p + r*ldb] (TA)
-        Ap = B; lda2 = ldb; TA = !tB;
+        R.Ap = B; R.lda2 = ldb; R.TA = !tB;
         // B'(p,c) = op(A)(c,p): tA ? A[p + c*lda] (!TB form) : A[c + p*lda] (TB form)
-        Bp = A; ldb2 = lda; TB = !tA;
-        rs = ldc; cs = 1;
+        R.Bp = A; R.ldb2 = lda; R.TB = !tA;
+        R.rs = ldc; R.cs = 1;
     }
+    return R;
+}
+
+static bool skinny_tma_ok(const SkRoles &R, int64_t K) {
+    return tma_legal(R.Ap, R.lda2) && tma_legal(R.Bp, R.ldb2) && !getenv("EMM_SKINNY_NO_TMA") && K > 0;
+}
+
+// Workspace of the split-K slabs for this call (0: no split).  Upper bound
+// without pointers (A = B = null: assumes the TMA path).
+size_t skinny_split_bytes(bool tA, bool tB, int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
+                          const float *B, int64_t ldb) {
+    const SkRoles R = skinny_roles(tA, tB, M, N, A, lda, B, ldb, 1);
+    if (A && B && !skinny_tma_ok(R, K)) return 0;
+    const SkPlan P = skinny_plan(R.TA, R.Mr, K);
+    return P.splits > 1 ? (size_t)P.splits * R.Mr * R.Nc * 4 : 0;
+}
+
+cudaError_t launch_skinny_sgemm(bool tA, bool tB, int64_t M, int64_t N, int64_t K, float alpha, const float *A,
+                                int64_t lda, const float *B, int64_t ldb, float beta, float *C, int64_t ldc,
+                                cudaStream_t s, float *ws, size_t ws_bytes) {
+    // Roles: the long output dimension is streamed (rows of C'), the short one
+    // (<= SKINNY_MAX) is resident.  N short: C' = C, A' = op(A), B' = op(B).
+    // M short: C' = C^T = op(B)^T op(A)^T, A' = op(B)^T, B' = op(A)^T.
+    const SkRoles R = skinny_roles(tA, tB, M, N, A, lda, B, ldb, ldc);
+    const bool TA = R.TA, TB = R.TB;
+    const int64_t Mr = R.Mr, lda2 = R.lda2, ldb2 = R.ldb2, rs = R.rs, cs = R.cs;
+    const int Nc = R.Nc;
+    const float *Ap = R.Ap, *Bp = R.Bp;
     if ((Mr + 127) / 128 > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
     cudaEvent_t ev = nullptr;
     prof_begin(s, true, &ev);
     cudaError_t e;
-    const bool tma = tma_legal(Ap, lda2) && tma_legal(Bp, ldb2) && !getenv("EMM_SKINNY_NO_TMA") && K > 0;
-    if (tma) {
-        if (!TA && !TB) e = launch_tma<false, false>(Mr, Nc, K, alpha, Ap, lda2, Bp, ldb2, beta, C, rs, cs, s);
-        else if (!TA && TB) e = launch_tma<false, true>(Mr, Nc, K, alpha, Ap, lda2, Bp, ldb2, beta, C, rs, cs, s);
-        else if (TA && !TB) e = launch_tma<true, false>(Mr, Nc, K, alpha, Ap, lda2, Bp, ldb2, beta, C, rs, cs, s);
-        else e = launch_tma<true, true>(Mr, Nc, K, alpha, Ap, lda2, Bp, ldb2, beta, C, rs, cs, s);
+    if (skinny_tma_ok(R, K)) {
+        if (!TA && !TB) e = launch_tma<false, false>(Mr, Nc, K, alpha, Ap, lda2, Bp, ldb2, beta, C, rs, cs, s, ws, ws_bytes);
+        else if (!TA && TB) e = launch_tma<false, true>(Mr, Nc, K, alpha, Ap, lda2, Bp, ldb2, beta, C, rs, cs, s, ws, ws_bytes);
+        else if (TA && !TB) e = launch_tma<true, false>(Mr, Nc, K, alpha, Ap, lda2, Bp, ldb2, beta, C, rs, cs, s, ws, ws_bytes);
+        else e = launch_tma<true, true>(Mr, Nc, K, alpha, Ap, lda2, Bp, ldb2, beta, C, rs, cs, s, ws, ws_bytes);
     } else if (!TA && !TB) e = launch_nc<false, false>(Mr, Nc, K, alpha, Ap, lda2, Bp, ldb2, beta, C, rs, cs, s);
     else if (!TA && TB) e = launch_nc<false, true>(Mr, Nc, K, alpha, Ap, lda2, Bp, ldb2, beta, C, rs, cs, s);
     else if (TA && !TB) e = launch_nc<true, false>(Mr, Nc, K, alpha, Ap, lda2, Bp, ldb2, beta, C, rs, cs, s);

@@ -314,13 +314,17 @@ bool skinny_tc_wanted(int terms, bool tA, bool tB, int64_t M, int64_t N, int64_t
     const int64_t Mr = nshort ? M : N;
     const float *Ap = nshort ? A : B;
     const int64_t lda2 = nshort ? lda : ldb;
-    (void)tA;
-    (void)tB;
     if (!tma_legal(Ap, lda2) || K < 1 || Mr > 0x7fffff00LL || K > 0x7fffff00LL) return false;
     if (e && e[0] == '1') return true;
     const int64_t Nc = nshort ? N : M;
-    // small problems: the FFMA streaming kernel needs no split pass (one launch)
-    return terms <= 2 && Nc > 8 && (double)Mr * (double)K >= (double)(1 << 22);
+    // Measured against the FFMA streaming kernel KN9 (round 2: LDS operand
+    // reads, FFMA2 row pairs, 448-row blocks, split-K for few blocks;
+    // profiles/r02_skinny_ffma.md): KN9 is as fast or faster (and FP32-
+    // accurate) everywhere except 1xTF32 with a K-contiguous long operand
+    // (65536 x 16 x 4096 TN: 218 vs 244 us).  Small problems: KN9 needs no
+    // split pass (one launch).
+    const bool a_kcontig = nshort ? tA : !tB;
+    return terms == 1 && a_kcontig && Nc > 8 && (double)Mr * (double)K >= (double)(1 << 22);
 }
 
 size_t skinny_tc_workspace_bytes(int64_t M, int64_t N, int64_t K) {

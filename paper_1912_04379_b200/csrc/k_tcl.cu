@@ -190,7 +190,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TL_THREADS, 1)
                           int kc_stages, unsigned int *__restrict__ wave_ctr, int splits,
                           float *__restrict__ partial, const __grid_constant__ PeerOut peers) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // keeps LDS/STS (no generic)
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + TL_STAGES * TL_STAGE_BYTES);
     uint64_t *empty = full + TL_STAGES;
     uint64_t *acc_full = empty + TL_STAGES;     // [2]

@@ -189,9 +189,9 @@ def test_direct_and_repacked_paths(emm, monkeypatch, force_pack, math, tA, tB):
 @pytest.mark.parametrize("shape", [(20000, 16, 700), (5003, 3, 1000), (9, 30001, 300), (16, 7000, 257)])
 def test_skinny_path(emm, math, tA, tB, shape):
     """min(M, N) <= 16: the streaming kernels (operand-role swap when M is the
-    short side; FFMA KN9, or the tensor-core KN9T for 1xTF32 / TF32+BF16 at a
-    short side > 8); bitwise on integers, the requested mode's bound on
-    random data, ldc padding untouched."""
+    short side; FFMA KN9, or the tensor-core KN9T for 1xTF32 with a
+    K-contiguous long operand and a short side > 8); bitwise on integers, the
+    requested mode's bound on random data, ldc padding untouched."""
     M, N, K = shape
     case = cached_case(tA, tB, M, N, K, 1.0, 2.0, kind="ints", c_kind="ints", pad=(1, 2, 3))
     R, S, T, _ = case.oracle()
@@ -202,6 +202,37 @@ def test_skinny_path(emm, math, tA, tB, shape):
     R, S, T, _ = case.oracle()
     Cg = case.run(emm, math)
     assert_close(case, Cg, R, S, T, TOL[math])
+
+
+@pytest.mark.parametrize("tA", ["N", "T"])
+@pytest.mark.parametrize("tB", ["N", "T"])
+@pytest.mark.parametrize("shape", [(4000, 16, 9000), (16, 3000, 5000), (9000, 5, 2049), (7, 2000, 40000)])
+def test_skinny_ffma_splitk(emm, monkeypatch, tA, tB, shape):
+    """FFMA skinny kernel (KN9) with few row blocks and a long K: split over
+    256-of-K promotion groups + the fixed-order reduce launch (2 launches);
+    bitwise on integers (beta != 0 included), FP32 bound on random data,
+    deterministic, and within the bound of the unsplit run."""
+    monkeypatch.setenv("EMM_SKINNY_TC", "0")
+    M, N, K = shape
+    # TMA-legal leading dimensions (the split runs in the TMA streaming kernel)
+    pa = (-(M if tA == "N" else K)) % 4 + 4
+    pb = (-(K if tB == "N" else N)) % 4 + 4
+    case = Case(tA, tB, M, N, K, 2.0, -1.0, kind="ints", c_kind="ints", pad=(pa, pb, 3))
+    R, S, T, _ = case.oracle()
+    n0 = emm.launch_count()
+    Cg = case.run(emm, "ffma")
+    assert emm.launch_count() - n0 == 2, "expected the split kernel + its reduce"
+    case.check_untouched(Cg)
+    assert np.array_equal(case.logical(Cg), R.astype(np.float32).astype(np.float64))
+    case = Case(tA, tB, M, N, K, -0.5, 0.25, kind="normal", pad=(pa, pb, 1), sigma=1.0 / np.sqrt(K))
+    R, S, T, _ = case.oracle()
+    G1 = case.run(emm, "ffma")
+    G2 = case.run(emm, "ffma")
+    assert torch.equal(G1.view(torch.int32), G2.view(torch.int32))
+    assert_close(case, G1, R, S, T, TOL["ffma"])
+    monkeypatch.setenv("EMM_SKINNY_SPLITS", "1")
+    G0 = case.run(emm, "ffma")
+    assert_close(case, G0, R, S, T, TOL["ffma"])
 
 
 def test_spec_worked_example_bitwise(emm):

@@ -117,11 +117,12 @@ def test_same_sign_accumulation(emm):
     assert assert_close(case, Cg, R, S, T, 1e-5, rows=rows) <= 1.0
 
 
-@pytest.mark.parametrize("math,tc", [("1xtf32", True), ("tf32bf16", True), ("3xtf32", False), ("ffma", False)])
+@pytest.mark.parametrize("math,tc", [("1xtf32", True), ("tf32bf16", False), ("3xtf32", False), ("ffma", False)])
 def test_default_policy(emm, monkeypatch, math, tc):
-    """Without the override: large skinny problems with a short side > 8 take
-    the tensor cores (split pass + one GEMM launch) in the 1- and 2-term
-    modes; 3xTF32 / FFMA and small problems keep the one-launch FFMA kernel."""
+    """Without the override: large skinny problems take the tensor cores
+    (split pass + one GEMM launch) only in 1xTF32 with a K-contiguous long
+    operand (TN: 218 vs 244 us); everything else (and NN 1xTF32, where KN9 is
+    as fast) keeps the one-launch FFMA kernel KN9 (profiles/r02_skinny_ffma.md)."""
     monkeypatch.delenv("EMM_SKINNY_TC")
     small = Case("N", "N", 1000, 16, 300, 1.0, 0.0, kind="ints")
     n0 = emm.launch_count()
@@ -130,4 +131,8 @@ def test_default_policy(emm, monkeypatch, math, tc):
     big = cached_case("N", "N", 65536, 16, 4096, 1.0, 0.0, kind="uniform")
     n0 = emm.launch_count()
     big.run(emm, math)
+    assert emm.launch_count() - n0 == 1
+    big_t = cached_case("T", "N", 65536, 16, 1024, 1.0, 0.0, kind="uniform")
+    n0 = emm.launch_count()
+    big_t.run(emm, math)
     assert emm.launch_count() - n0 == (2 if tc else 1)
