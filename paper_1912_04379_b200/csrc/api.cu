@@ -554,8 +554,10 @@ extern "C" int emm_sgemm_ex(char transA, char transB, int64_t M, int64_t N, int6
         ops.b0 = TcPlane{B, ldb, !b_kc, K};
         // 1xTF32, TF32+BF16: the TMA rounds x to rn_tf32(x) on load (the
         // tensor core alone would truncate, R7b) -- the re-buffered numerics
-        // (EMM_TMA_TRUNC=1: raw operands, the round-1 numerics; experiments)
-        ops.a0.rn = ops.b0.rn = (math == EMM_MATH_1XTF32 || math == EMM_MATH_TF32_BF16) && !env_on("EMM_TMA_TRUNC");
+        // (EMM_TMA_TRUNC=1, 1xTF32 only: raw operands, the round-1 numerics;
+        // experiments)
+        ops.a0.rn = ops.b0.rn =
+            math == EMM_MATH_TF32_BF16 || (math == EMM_MATH_1XTF32 && !env_on("EMM_TMA_TRUNC"));
         if (P.pack_mode == PK_DSMALL_) {
             ops.a1 = TcPlane{a1, P.lda1, !a_kc, K};
             ops.b1 = TcPlane{b1, P.ldb1, !b_kc, K};

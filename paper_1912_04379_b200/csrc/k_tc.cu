@@ -103,7 +103,6 @@ struct PackOperand {
     int64_t ld1;
     int cross_swap;   // B side of the cross operand
     int raw_big;      // test hook (EMM_DEBUG_RAW_BIG): FULL big = x unrounded
-    int trunc_big;    // PK_DCROSS with big = trunc(x) (EMM_TMA_TRUNC=1, experiments)
     // launch geometry (host-computed)
     int transpose;    // 1: tile path, 0: element-wise lines
     int vec;          // 16-B vector loads legal on the source (aligned base, ld % 4 == 0)
@@ -121,7 +120,7 @@ __device__ __forceinline__ void split_one(const PackOperand &op, float x, float 
     // rn_tf32(x) on load (TFLOAT32 tensor map, R7c), so the cross plane is
     // made against that same big part
     if (MODE == PK_RAWT) big = x;
-    else if (MODE == PK_DSMALL || (MODE == PK_DCROSS && op.trunc_big)) big = trunc_tf32(x);
+    else if (MODE == PK_DSMALL) big = trunc_tf32(x);
     else big = op.raw_big ? x : __uint_as_float(cvt_tf32_rn(x));
     lo = isfinite(x) ? x - big : 0.0f;   // exact
 }
@@ -325,14 +324,11 @@ cudaError_t launch_pack(int mode, const PackArgs &a, const PackArgs *b, int64_t 
         const char *e = getenv("EMM_DEBUG_RAW_BIG");
         return e && e[0] == '1' ? 1 : 0;
     }();
-    const char *et = getenv("EMM_TMA_TRUNC");
-    const bool tma_trunc = et && et[0] == '1';
     auto mk = [&](const PackArgs &x, bool b_side) {
         PackOperand o{};
         o.X = x.X; o.ld = x.ld; o.R = x.R; o.kcontig = x.kcontig ? 1 : 0;
         o.out0 = x.out0; o.ld0 = x.ld0; o.out1 = x.out1; o.ld1 = x.ld1;
         o.cross_swap = b_side ? 1 : 0; o.raw_big = raw;
-        o.trunc_big = mode == PK_DCROSS && tma_trunc ? 1 : 0;
         pack_geometry(o, mode, K);
         return o;
     };
