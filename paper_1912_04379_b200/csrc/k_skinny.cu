@@ -337,6 +337,74 @@ __global__ void __launch_bounds__(TPB + 32, 1)
         }
         return;
     }
+    if (RPT == 2 && TA && TB) {
+        // K-contiguous long operand, B' tile [32 k][NC]: rows tid and tid+TPB
+        // (one float4 along k each), column pairs (c, c+1) as FFMA2 operand
+        // pairs from one 128-bit broadcast of B' — same per-entry order
+        for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+            int64_t rb, ch0, ch1;
+            int sp;
+            unit(u, rb, sp, ch0, ch1);
+            float2 acc[2][NC / 2], master[2][NC / 2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int c = 0; c < NC / 2; ++c) acc[h][c] = master[h][c] = make_float2(0.0f, 0.0f);
+            for (int64_t ch = ch0; ch < ch1; ++ch, ++it) {
+                const int s = (int)(it % SKT_STAGES);
+                mbar_wait(&full[s], (uint32_t)(it / SKT_STAGES) & 1u);
+                const float *As = reinterpret_cast<const float *>(smem + s * STAGE);
+                const float *Bs = reinterpret_cast<const float *>(smem + s * STAGE + SKT_A_BYTES);
+#pragma unroll 1
+                for (int j = 0; j < SKT_KC / 4; ++j) {
+                    float a[2][4];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {   // 128B swizzle: chunk j of row tid sits at chunk j ^ (tid & 7)
+                        const float4 x = *reinterpret_cast<const float4 *>(As + h * TPB * SKT_KC + tid * SKT_KC +
+                                                                            4 * (j ^ (tid & 7)));
+                        a[h][0] = x.x; a[h][1] = x.y; a[h][2] = x.z; a[h][3] = x.w;
+                    }
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        float b[NC];
+#pragma unroll
+                        for (int c = 0; c < NC; c += 4) {
+                            const float4 v = *reinterpret_cast<const float4 *>(Bs + (4 * j + kk) * NC + c);
+                            b[c] = v.x; b[c + 1] = v.y; b[c + 2] = v.z; b[c + 3] = v.w;
+                        }
+#pragma unroll
+                        for (int h = 0; h < 2; ++h)
+#pragma unroll
+                            for (int c = 0; c < NC / 2; ++c)
+                                acc[h][c] = __ffma2_rn(make_float2(a[h][kk], a[h][kk]), make_float2(b[2 * c], b[2 * c + 1]),
+                                                       acc[h][c]);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);
+                if ((ch + 1) % PROM == 0 || ch + 1 == ch1) {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+#pragma unroll
+                        for (int c = 0; c < NC / 2; ++c) {
+                            master[h][c].x += acc[h][c].x;
+                            master[h][c].y += acc[h][c].y;
+                            acc[h][c] = make_float2(0.0f, 0.0f);
+                        }
+                }
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t row = rb * SKT_ROWS + h * TPB + tid;
+                if (row < Mr) {
+#pragma unroll
+                    for (int c = 0; c < NC; ++c)
+                        if (c < Nc) store(row, c, sp, (c & 1) ? master[h][c >> 1].y : master[h][c >> 1].x);
+                }
+            }
+        }
+        return;
+    }
     for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
         int64_t rb, ch0, ch1;
         int sp;
@@ -560,14 +628,26 @@ static bool skinny_tma_ok(const SkRoles &R, int64_t K) {
     return tma_legal(R.Ap, R.lda2) && tma_legal(R.Bp, R.ldb2) && !getenv("EMM_SKINNY_NO_TMA") && K > 0;
 }
 
-// Workspace of the split-K slabs for this call (0: no split).  Upper bound
-// without pointers (A = B = null: assumes the TMA path).
+// K-contiguous long operand with a K-contiguous B' (TA && !TB): B' is first
+// transposed (PK_RAWT, 32 floats a row, zero padded) so the kernel reads
+// [32 k][NC] tiles and pairs columns for FFMA2.  EMM_SKINNY_BT=0 disables.
+static bool skinny_bt(const SkRoles &R) {
+    const char *e = getenv("EMM_SKINNY_BT");
+    return R.TA && !R.TB && !(e && e[0] == '0');
+}
+static size_t skinny_slab_bytes(const SkRoles &R, int64_t K) {
+    const SkPlan P = skinny_plan(R.TA, R.Mr, K);
+    return P.splits > 1 ? align_up((size_t)P.splits * R.Mr * R.Nc * 4, 1024) : 0;
+}
+
+// Workspace of this call's FFMA skinny path: split-K slabs + the transposed
+// B' copy (0: none).  Upper bound without pointers (A = B = null: assumes
+// the TMA path).
 size_t skinny_split_bytes(bool tA, bool tB, int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
                           const float *B, int64_t ldb) {
     const SkRoles R = skinny_roles(tA, tB, M, N, A, lda, B, ldb, 1);
     if (A && B && !skinny_tma_ok(R, K)) return 0;
-    const SkPlan P = skinny_plan(R.TA, R.Mr, K);
-    return P.splits > 1 ? (size_t)P.splits * R.Mr * R.Nc * 4 : 0;
+    return skinny_slab_bytes(R, K) + (skinny_bt(R) ? (size_t)K * 32 * 4 : 0);
 }
 
 cudaError_t launch_skinny_sgemm(bool tA, bool tB, int64_t M, int64_t N, int64_t K, float alpha, const float *A,
@@ -586,7 +666,16 @@ cudaError_t launch_skinny_sgemm(bool tA, bool tB, int64_t M, int64_t N, int64_t 
     prof_begin(s, true, &ev);
     cudaError_t e;
     if (skinny_tma_ok(R, K)) {
-        if (!TA && !TB) e = launch_tma<false, false>(Mr, Nc, K, alpha, Ap, lda2, Bp, ldb2, beta, C, rs, cs, s, ws, ws_bytes);
+        const size_t slab = skinny_slab_bytes(R, K);
+        if (skinny_bt(R) && ws && ws_bytes >= slab + (size_t)K * 32 * 4) {
+            // B'(p, c) = Bp[p + c*ldb2] -> Bt[p*32 + c], then the TA x TB kernel
+            float *Bt = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(ws) + slab);
+            PackArgs x;
+            x.X = Bp; x.ld = ldb2; x.R = K; x.kcontig = false; x.out0 = Bt; x.ld0 = 32;
+            e = launch_pack(PK_RAWT_, x, nullptr, Nc, nullptr, s, 0);
+            if (e == cudaSuccess)
+                e = launch_tma<true, true>(Mr, Nc, K, alpha, Ap, lda2, Bt, 32, beta, C, rs, cs, s, ws, slab);
+        } else if (!TA && !TB) e = launch_tma<false, false>(Mr, Nc, K, alpha, Ap, lda2, Bp, ldb2, beta, C, rs, cs, s, ws, ws_bytes);
         else if (!TA && TB) e = launch_tma<false, true>(Mr, Nc, K, alpha, Ap, lda2, Bp, ldb2, beta, C, rs, cs, s, ws, ws_bytes);
         else if (TA && !TB) e = launch_tma<true, false>(Mr, Nc, K, alpha, Ap, lda2, Bp, ldb2, beta, C, rs, cs, s, ws, ws_bytes);
         else e = launch_tma<true, true>(Mr, Nc, K, alpha, Ap, lda2, Bp, ldb2, beta, C, rs, cs, s, ws, ws_bytes);

@@ -209,7 +209,7 @@ def test_skinny_path(emm, math, tA, tB, shape):
 @pytest.mark.parametrize("shape", [(4000, 16, 9000), (16, 3000, 5000), (9000, 5, 2049), (7, 2000, 40000)])
 def test_skinny_ffma_splitk(emm, monkeypatch, tA, tB, shape):
     """FFMA skinny kernel (KN9) with few row blocks and a long K: split over
-    256-of-K promotion groups + the fixed-order reduce launch (2 launches);
+    256-of-K promotion groups + the fixed-order reduce launch (2-3 launches);
     bitwise on integers (beta != 0 included), FP32 bound on random data,
     deterministic, and within the bound of the unsplit run."""
     monkeypatch.setenv("EMM_SKINNY_TC", "0")
@@ -221,7 +221,8 @@ def test_skinny_ffma_splitk(emm, monkeypatch, tA, tB, shape):
     R, S, T, _ = case.oracle()
     n0 = emm.launch_count()
     Cg = case.run(emm, "ffma")
-    assert emm.launch_count() - n0 == 2, "expected the split kernel + its reduce"
+    # the split kernel + its reduce (+ the B' transpose for a K-contiguous long operand)
+    assert emm.launch_count() - n0 in (2, 3), "expected the split kernel + its reduce"
     case.check_untouched(Cg)
     assert np.array_equal(case.logical(Cg), R.astype(np.float32).astype(np.float64))
     case = Case(tA, tB, M, N, K, -0.5, 0.25, kind="normal", pad=(pa, pb, 1), sigma=1.0 / np.sqrt(K))

@@ -132,7 +132,13 @@ def test_default_policy(emm, monkeypatch, math, tc):
     n0 = emm.launch_count()
     big.run(emm, math)
     assert emm.launch_count() - n0 == 1
+    # TN: two launches either way (KN9T: split pass + GEMM; KN9: B' transpose +
+    # kernel); which kernel ran shows in the bits: KN9 equals the forced-FFMA
+    # (EMM_SKINNY_TC=0) result, KN9T (TF32 products) does not
     big_t = cached_case("T", "N", 65536, 16, 1024, 1.0, 0.0, kind="uniform")
     n0 = emm.launch_count()
-    big_t.run(emm, math)
-    assert emm.launch_count() - n0 == (2 if tc else 1)
+    Cd = big_t.run(emm, math)
+    assert emm.launch_count() - n0 == 2
+    monkeypatch.setenv("EMM_SKINNY_TC", "0")
+    Cf = big_t.run(emm, math)
+    assert torch.equal(Cd.view(torch.int32), Cf.view(torch.int32)) != tc
