@@ -29,6 +29,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=200)
     ap.add_argument("--maths", default="3xtf32,1xtf32,ffma")
+    ap.add_argument("--ws", type=int, default=0, help="pass a caller workspace (no library scratch allocation)")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     s = torch.cuda.current_stream(dev)
@@ -42,8 +43,11 @@ def main():
         L = emm.lib()
         for math in a.maths.split(","):
             fn = L.emm_sgemm_ex
+            wsb = emm.workspace_bytes(tA, tB, M, N, K, math) if a.ws else 0
+            ws = torch.empty(wsb // 4 + 512, device=dev) if wsb else None
+            wsp = (ws.data_ptr() + (-ws.data_ptr()) % 1024) if wsb else None
             args = (tA.encode(), tB.encode(), M, N, K, 1.0, A.data_ptr(), lda, B.data_ptr(), ldb, 0.0,
-                    C.data_ptr(), ldc, s.cuda_stream, emm.MATH[math], None, 0)
+                    C.data_ptr(), ldc, s.cuda_stream, emm.MATH[math], wsp, wsb)
 
             def call():
                 return fn(*args)
