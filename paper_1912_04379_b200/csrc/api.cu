@@ -352,6 +352,21 @@ static size_t ws_bytes(char tA, char tB, int64_t M, int64_t N, int64_t K, emm_ma
 }
 
 
+// Workspace one call with these operands needs (pointer-aware where the
+// FFMA relayout depends on alignment; else the ws_bytes upper bound).
+static size_t call_ws_bytes(char tA, char tB, int64_t M, int64_t N, int64_t K, emm_math_t math, const float *A,
+                            int64_t lda, const float *B, int64_t ldb) {
+    if (M == 0 || N == 0 || K == 0) return 0;
+    if (math == EMM_MATH_FFMA) {
+        if (M <= SKINNY_MAX || N <= SKINNY_MAX)
+            return skinny_split_bytes(!is_n(tA), !is_n(tB), M, N, K, A, lda, B, ldb);
+        if (small_problem(M, N, K, math)) return 0;
+        const FfmaRelayout R = ffma_relayout(!is_n(tA), !is_n(tB), M, N, K, tma_legal(A, lda), tma_legal(B, ldb));
+        return align_up(R.total, 1024) + ffma_splitk_bytes(M, N, ffma_splits(M, N, K));
+    }
+    return ws_bytes(tA, tB, M, N, K, math);
+}
+
 }  // namespace emm
 
 using namespace emm;
@@ -884,10 +899,14 @@ extern "C" int emm_sgemm_host(char transA, char transB, int64_t M, int64_t N, in
     const size_t nA = ab_used ? (size_t)((ac - 1) * lda + ar) * 4 : 0;
     const size_t nB = ab_used ? (size_t)((bc - 1) * ldb + br) * 4 : 0;
     const size_t nC = (size_t)((N - 1) * ldc + M) * 4;
-    const size_t nW = ab_used ? ws_bytes(transA, transB, M, N, K, math) : 0;
     if ((st = ensure(&g_hc.dA, &g_hc.nA, nA)) || (st = ensure(&g_hc.dB, &g_hc.nB, nB)) ||
         (st = ensure(&g_hc.dC, &g_hc.nC, nC)))
         return st;
+    // device copies keep the caller's leading dimensions: size the workspace
+    // for them (the FFMA relayout only when they are TN / TMA-illegal)
+    const size_t nW = ab_used ? call_ws_bytes(transA, transB, M, N, K, math, (const float *)g_hc.dA, lda,
+                                              (const float *)g_hc.dB, ldb)
+                              : 0;
     cudaStream_t s = g_hc.s;
     cudaError_t e = cudaSuccess;
     if (ab_used && math != EMM_MATH_FFMA && M >= 4096 && N >= 4096 && K >= 256 && !env_on("EMM_HOST_NO_PIPELINE")) {

@@ -540,6 +540,20 @@ def test_host_buffer_entry(emm):
     assert_close(case, Cf, R, S, T, 1e-5)
 
 
+@pytest.mark.parametrize("tA,tB", [("T", "N"), ("N", "N"), ("T", "T")])
+def test_host_buffer_entry_ffma_relayout(emm, tA, tB):
+    """emm_sgemm_host in the FFMA mode on c3 (TMA-illegal / TN device copies:
+    relayout copy + split-K KN3b through the host path's cached workspace)."""
+    M, N, K = 1531, 997, 2049
+    case = cached_case(tA, tB, M, N, K, -0.75, 1.25, pad=(13, 7, 5), kind="normal")
+    R, S, T, _ = case.oracle()
+    Cf = case.Cflat.clone().pin_memory()
+    emm.sgemm_host(tA, tB, M, N, K, -0.75, case.flat(case.A), case.lda, case.flat(case.B), case.ldb, 1.25, Cf,
+                   case.ldc, math="ffma")
+    case.check_untouched(Cf)
+    assert_close(case, Cf, R, S, T, 1e-5)
+
+
 @pytest.mark.parametrize("math", ["3xtf32", "tf32bf16", "ffma"])
 @pytest.mark.parametrize("shape,tA,tB", [((1 << 20, 256, 64), "N", "N"),      # 4096 tile rows, multi-wave
                                          ((256, 256, 1 << 20), "T", "N"),      # K = 2^20: split-K x16, 2048 stages each
