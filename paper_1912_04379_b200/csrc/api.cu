@@ -298,11 +298,10 @@ static Plan make_plan(char tA, char tB, int64_t M, int64_t N, int64_t K, emm_mat
     return P;
 }
 
-// FFMA on layouts the TMA-fed KN3b does not cover (TN: both operands
-// K-contiguous; TMA-illegal base / leading dimension): one HBM-bound copy
-// pass first — the smaller operand of a TN call transposed to MN-contiguous
-// (PK_RAWT), a TMA-illegal operand re-pitched in its own layout (PK_RAW) —
-// then KN3b on the copies.  Measured on B200 (profiles/r02_ffma_relayout.md):
+// FFMA relayout: HBM-bound copy passes before KN3b — K-contiguous operands
+// transposed to MN-contiguous (PK_RAWT; always one for TN, which KN3b does
+// not cover; by size otherwise, see ffma_relayout), TMA-illegal ones
+// re-pitched in their own layout (PK_RAW) — then KN3b on the copies.  Measured on B200 (profiles/r02_ffma_relayout.md):
 // c3 TN 246 -> 212 us, TT 243 -> 206, 4096^3 TN 2.61 -> 2.43 ms.
 struct FfmaRelayout {
     bool on = false, t_a = false, t_b = false, rp_a = false, rp_b = false;
@@ -311,13 +310,23 @@ struct FfmaRelayout {
 };
 static FfmaRelayout ffma_relayout(bool tA, bool tB, int64_t M, int64_t N, int64_t K, bool legal_a, bool legal_b) {
     FfmaRelayout R;
-    const bool tn = tA && !tB;
-    if (!tn && legal_a && legal_b) return R;
-    R.on = true;
-    if (tn) {
-        // transpose the smaller operand; K-major [R][kpad] rows = MN-contiguous copy
-        (M <= N ? R.t_a : R.t_b) = true;
-    }
+    // KN3b runs fastest with BOTH operands MN-contiguous (the NT layout: 128-bit
+    // operand loads on both sides; 4096^3: NT 84.1 % of the FP32 pipe, NN 73.4,
+    // TT 75.3, TN-after-one-transpose 73.5, profiles/r02_ffma_relayout.md).
+    // A K-contiguous operand is transposed when the copy is cheap next to the
+    // GEMM (its cost relative to the GEMM ~ 44 / (the other extent)): op(A)
+    // when N >= 1280, op(B) when M >= 1280 (measured: 1024^3 loses 2 us to the
+    // copy, 1531 x 997 x 2049 NN gains 8 us, 2048^3 +8 %, 8192^3 +13 %); a TN
+    // call transposes at least the smaller one (KN3b needs one MN-contiguous
+    // operand).  EMM_FFMA_NT_MIN moves the 1280 (0: never by size).
+    int64_t thr = 1280;
+    if (const char *e = getenv("EMM_FFMA_NT_MIN")) thr = atoll(e) > 0 ? atoll(e) : INT64_MAX;
+    const bool a_kc = tA, b_kc = !tB;
+    R.t_a = a_kc && N >= thr;
+    R.t_b = b_kc && M >= thr;
+    if (a_kc && b_kc && !R.t_a && !R.t_b) (M <= N ? R.t_a : R.t_b) = true;
+    R.on = R.t_a || R.t_b || !legal_a || !legal_b;
+    if (!R.on) return R;
     R.rp_a = !R.t_a && !legal_a;
     R.rp_b = !R.t_b && !legal_b;
     const int64_t ar = tA ? K : M, ac = tA ? M : K;   // A stored ar x ac
@@ -482,7 +491,8 @@ extern "C" int emm_sgemm_ex(char transA, char transB, int64_t M, int64_t N, int6
             x.X = A; x.ld = lda; x.R = K; x.kcontig = false; x.out0 = a1; x.ld0 = R.lda1;
             e = launch_pack(PK_RAWT_, x, nullptr, M, nullptr, s, 0);
             A2 = a1, lda2 = R.lda1, tA2 = false;
-        } else if (R.t_b) {
+        }
+        if (R.t_b && e == cudaSuccess) {
             // op(B)(p, j) = B[p + j*ldb] -> B2[j + p*ldb1] (transB = T)
             PackArgs x;
             x.X = B; x.ld = ldb; x.R = K; x.kcontig = false; x.out0 = b1; x.ld0 = R.ldb1;

@@ -107,7 +107,7 @@ def test_relayout_bitwise_equal_to_kn3_in_place(emm, monkeypatch, trans, pad, sh
     n0 = emm.launch_count()
     G3 = case.run(emm, "ffma")
     assert emm.launch_count() - n0 == 1
-    assert n_relayout in (2, 3), n_relayout
+    assert 2 <= n_relayout <= 5, n_relayout
     assert torch.equal(G.view(torch.int32), G3.view(torch.int32)), "relayout + KN3b and KN3 differ"
     case.check_untouched(G)
     R, S, T, st = case.oracle()
