@@ -627,8 +627,15 @@ extern "C" int emm_sgemm_ex(char transA, char transB, int64_t M, int64_t N, int6
             e = launch_tc_xs_sgemm(ops.a0, ops.b0, M, N, K, alpha, beta, C, ldc, multiwave ? ctr : nullptr, P.splits,
                                    Pp, s, nullptr, sk_ws);
     } else {
-        if (P.pack_mode >= 0) e = launch_pack(P.pack_mode, pa, &pb, K, ctr, s, (int)(zero_bytes / 4));
-        else e = cudaMemsetAsync(ctr, 0, zero_bytes, s);
+        if (P.pack_mode >= 0) {
+            e = launch_pack(P.pack_mode, pa, &pb, K, ctr, s, (int)(zero_bytes / 4));
+        } else if (P.sk || (P.terms > 1 && tc_units(M, N, P.splits) > tc_num_sms() / 2)) {
+            // no pass to zero the control block in: a memset, only when the
+            // GEMM reads it (wave lockstep of a multi-wave 2/3-term grid,
+            // stream-K flags; 1xTF32 grids never do, tc_kernel.cuh) — a
+            // memset node costs ~2-4 us of latency on sub-wave calls
+            e = cudaMemsetAsync(ctr, 0, zero_bytes, s);
+        }
         if (e == cudaSuccess)
             e = launch_tc_sgemm(P.terms, ops, M, N, K, alpha, beta, C, ldc, ctr, P.splits, Pp, s, nullptr, sk_ws);
     }
