@@ -277,21 +277,37 @@ __global__ void __launch_bounds__(FtCfg<SEP>::BLOCK, 1)
         }
     }
 
-    // epilogue: alpha*acc + beta*C (C not read when beta == 0), predicated
+    // epilogue: alpha*acc + beta*C (C not read when beta == 0), predicated.
+    // beta != 0: the C_in loads of two columns (16 values) are issued before
+    // their stores — a store could alias a later load through ldc, so the
+    // compiler would otherwise serialise 64 load round trips per thread.
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        const int col = n0 + slot_pos(B_MN, tn, j);
-        if (col >= N) continue;
+    for (int j0 = 0; j0 < 8; j0 += 2) {
+        float cin[2][8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int row = m0 + slot_pos(A_MN, tm, i);
-            if (row < M) {
-                const float v = SEP ? master_s[(i * 8 + j) * FT_CONSUMERS + c] : master_r[(i * 8 + j) % (SEP ? 1 : 64)];
-                if (partial) {
-                    partial[((size_t)sp * N + col) * M + row] = v;
-                } else {
-                    float *d = C + row + (int64_t)col * ldc;
-                    *d = beta == 0.0f ? alpha * v : fmaf(beta, *d, alpha * v);
+        for (int jj = 0; jj < 2; ++jj) {
+            const int col = n0 + slot_pos(B_MN, tn, j0 + jj);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int row = m0 + slot_pos(A_MN, tm, i);
+                cin[jj][i] = (!partial && beta != 0.0f && col < N && row < M) ? C[row + (int64_t)col * ldc] : 0.0f;
+            }
+        }
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+            const int j = j0 + jj;
+            const int col = n0 + slot_pos(B_MN, tn, j);
+            if (col >= N) continue;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int row = m0 + slot_pos(A_MN, tm, i);
+                if (row < M) {
+                    const float v = SEP ? master_s[(i * 8 + j) * FT_CONSUMERS + c] : master_r[(i * 8 + j) % (SEP ? 1 : 64)];
+                    if (partial) {
+                        partial[((size_t)sp * N + col) * M + row] = v;
+                    } else {
+                        C[row + (int64_t)col * ldc] = beta == 0.0f ? alpha * v : fmaf(beta, cin[jj][i], alpha * v);
+                    }
                 }
             }
         }
