@@ -130,13 +130,12 @@ __global__ void __launch_bounds__(SK_ROWS) skinny_sgemm_kernel(int64_t Mr, int N
         __syncthreads();
     }
     if (!row_ok) return;
+    float cin[NC];   // C_in loads before the stores (see skinny_tma_kernel)
 #pragma unroll
-    for (int c = 0; c < NC; ++c) {
-        if (c < Nc) {
-            float *d = C + row * rs + (int64_t)c * cs;
-            *d = beta == 0.0f ? alpha * master[c] : fmaf(beta, *d, alpha * master[c]);
-        }
-    }
+    for (int c = 0; c < NC; ++c) cin[c] = (beta != 0.0f && c < Nc) ? C[row * rs + (int64_t)c * cs] : 0.0f;
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+        if (c < Nc) C[row * rs + (int64_t)c * cs] = beta == 0.0f ? alpha * master[c] : fmaf(beta, cin[c], alpha * master[c]);
 }
 
 template <bool TA, bool TB, int ROWS, int KC>
@@ -218,12 +217,21 @@ __global__ void __launch_bounds__(TPB + 32, 1)
         c0 = min(nchunks, sp * ngroups / splits * PROM);
         c1 = min(nchunks, (sp + 1) * ngroups / splits * PROM);
     };
-    auto store = [&](int64_t row, int c, int sp, float v) {
-        if (partial) {
-            partial[((size_t)sp * Nc + c) * Mr + row] = v;
-        } else {
-            float *d = C + row * rs + (int64_t)c * cs;
-            *d = beta == 0.0f ? alpha * v : fmaf(beta, *d, alpha * v);
+    auto store = [&](int64_t row, int c, int sp, float v, float cin) {
+        if (partial) partial[((size_t)sp * Nc + c) * Mr + row] = v;
+        else C[row * rs + (int64_t)c * cs] = beta == 0.0f ? alpha * v : fmaf(beta, cin, alpha * v);
+    };
+    // beta != 0: a thread's C_in values (rows row0 + h*step) loaded before any
+    // of its stores (a store could alias a later load through ldc, so they
+    // would otherwise run one round trip each)
+    auto load_cin = [&](int64_t row0, int64_t step, auto &cin) {
+        constexpr int H = sizeof(cin) / sizeof(cin[0]);
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+            const int64_t row = row0 + h * step;
+#pragma unroll
+            for (int c = 0; c < NC; ++c)
+                cin[h][c] = (!partial && beta != 0.0f && row < Mr && c < Nc) ? C[row * rs + (int64_t)c * cs] : 0.0f;
         }
     };
     if (tid == 0) {
@@ -325,13 +333,15 @@ __global__ void __launch_bounds__(TPB + 32, 1)
                     }
                 }
             }
+            float cin[2][NC];
+            load_cin(rb * SKT_ROWS + rl, 1, cin);
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const int64_t row = rb * SKT_ROWS + rl + h;
                 if (row < Mr) {
 #pragma unroll
                     for (int c = 0; c < NC; ++c)
-                        if (c < Nc) store(row, c, sp, h ? master[c].y : master[c].x);
+                        if (c < Nc) store(row, c, sp, h ? master[c].y : master[c].x, cin[h][c]);
                 }
             }
         }
@@ -393,13 +403,15 @@ __global__ void __launch_bounds__(TPB + 32, 1)
                         }
                 }
             }
+            float cin[2][NC];
+            load_cin(rb * SKT_ROWS + tid, TPB, cin);
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const int64_t row = rb * SKT_ROWS + h * TPB + tid;
                 if (row < Mr) {
 #pragma unroll
                     for (int c = 0; c < NC; ++c)
-                        if (c < Nc) store(row, c, sp, (c & 1) ? master[h][c >> 1].y : master[h][c >> 1].x);
+                        if (c < Nc) store(row, c, sp, (c & 1) ? master[h][c >> 1].y : master[h][c >> 1].x, cin[h][c]);
                 }
             }
         }
@@ -466,13 +478,15 @@ __global__ void __launch_bounds__(TPB + 32, 1)
                     }
             }
         }
+        float cin[RPT][NC];
+        load_cin(rb * SKT_ROWS + tid, TPB, cin);
 #pragma unroll
         for (int h = 0; h < RPT; ++h) {
             const int64_t row = rb * SKT_ROWS + h * TPB + tid;
             if (row < Mr) {
 #pragma unroll
                 for (int c = 0; c < NC; ++c)
-                    if (c < Nc) store(row, c, sp, master[h][c]);
+                    if (c < Nc) store(row, c, sp, master[h][c], cin[h][c]);
             }
         }
     }

@@ -126,6 +126,15 @@ __global__ void __launch_bounds__(256) tiny_sgemm_kernel(int64_t M, int64_t N, i
         *reinterpret_cast<float4 *>(red + g * T * T + (4 * tx + j) * T + 4 * ty) =
             make_float4(mas[0][j], mas[1][j], mas[2][j], mas[3][j]);
     __syncthreads();
+    // beta != 0: all of this thread's C_in loads first (a store could alias a
+    // later load through ldc, so they would otherwise run one round trip each)
+    float cin[T * T / 256];
+#pragma unroll
+    for (int q = 0; q < T * T / 256; ++q) {
+        const int o = tid + 256 * q;
+        const int64_t grow = m0 + o % T, gcol = n0 + o / T;
+        cin[q] = (beta != 0.0f && grow < M && gcol < N) ? C[grow + gcol * ldc] : 0.0f;
+    }
 #pragma unroll
     for (int q = 0; q < T * T / 256; ++q) {
         const int o = tid + 256 * q;   // output (row = o % T, col = o / T): coalesced along rows
@@ -134,10 +143,7 @@ __global__ void __launch_bounds__(256) tiny_sgemm_kernel(int64_t M, int64_t N, i
 #pragma unroll
         for (int gg = 1; gg < G; ++gg) v += red[gg * T * T + o];
         const int64_t grow = m0 + row, gcol = n0 + colo;
-        if (grow < M && gcol < N) {
-            float *d = C + grow + gcol * ldc;
-            *d = beta == 0.0f ? alpha * v : fmaf(beta, *d, alpha * v);
-        }
+        if (grow < M && gcol < N) C[grow + gcol * ldc] = beta == 0.0f ? alpha * v : fmaf(beta, cin[q], alpha * v);
     }
 }
 
