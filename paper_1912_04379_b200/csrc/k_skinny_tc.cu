@@ -276,13 +276,12 @@ __global__ void __launch_bounds__(ST_THREADS, 1)
             const int64_t row = t * ST_ROWS + 32 * q + lane;
             if (row < Mr) {
                 float *cp = C + row * rs;
+                float cin[ST_NC];   // all C_in loads before the stores (no aliasing-forced round trips)
 #pragma unroll
-                for (int c = 0; c < ST_NC; ++c) {
-                    if (c < Nc) {
-                        const float o = beta == 0.0f ? alpha * master[c] : fmaf(beta, cp[c * cs], alpha * master[c]);
-                        cp[c * cs] = o;
-                    }
-                }
+                for (int c = 0; c < ST_NC; ++c) cin[c] = (beta != 0.0f && c < Nc) ? cp[c * cs] : 0.0f;
+#pragma unroll
+                for (int c = 0; c < ST_NC; ++c)
+                    if (c < Nc) cp[c * cs] = beta == 0.0f ? alpha * master[c] : fmaf(beta, cin[c], alpha * master[c]);
             }
         }
     }
