@@ -474,6 +474,12 @@ extern "C" int emm_sgemm_ex(char transA, char transB, int64_t M, int64_t N, int6
             if (workspace_bytes < need || (reinterpret_cast<uintptr_t>(ws) & 1023u)) return EMM_ERR_WORKSPACE;
         } else {
             cudaError_t e = scratch_alloc(&ws, need, s);
+            if (e == cudaErrorMemoryAllocation) {
+                // no room for the copies: the operands in place (KN3b where it
+                // covers the layout, else KN3), unsplit: the same FP32 bound
+                cudaGetLastError();
+                return cuda_status(launch_ffma_sgemm(tA, tB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, s));
+            }
             if (e != cudaSuccess) return cuda_status(e);
             own = true;
         }
