@@ -421,7 +421,8 @@ def main():
                 traffic = None
         roof = {"bound": "tensor" if math != "ffma" else "alu", "achieved": achieved, "peak": peak,
                 "unit": "TFLOP/s", "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                "peak_kind": f"{pname}, from {src} bf16 sustained {bf16_sus} TF x 1.1/2.25",
+                "peak_kind": (f"{pname}, from {src} bf16 sustained {bf16_sus} TF x 1.1/2.25" if math != "ffma"
+                              else f"{pname}: derived from the guide's unit counts and the max clock (DESIGN.md §6)"),
                 "peak_derived": peak, "frac_derived": (achieved / peak) if achieved else None,
                 "peak_burst": peak_b, "frac_burst": (achieved / peak_b) if achieved else None,
                 "kernel": {"ffma": "ffma_tma_kernel (KN3b)", "1xtf32": "tc1w_kernel (KN2w, 256x512 tiles)",
