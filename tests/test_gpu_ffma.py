@@ -93,7 +93,10 @@ def test_kn3b_deterministic(emm):
 @pytest.mark.parametrize("trans,pad,shape", [("TN", (0, 0, 0), (1000, 600, 700)), ("TN", (0, 0, 0), (600, 1000, 700)),
                                              ("TN", (13, 7, 5), (1531, 997, 2049)), ("TT", (13, 7, 5), (1531, 997, 2049)),
                                              ("NN", (1, 3, 0), (1000, 600, 700)), ("NT", (0, 1, 0), (257, 129, 2049)),
-                                             ("TN", (1, 3, 0), (129, 257, 33))])
+                                             ("TN", (1, 3, 0), (129, 257, 33)),
+                                             # >= 1280 on both sides: K-contiguous operands transposed to NT
+                                             ("NN", (0, 0, 0), (1300, 1400, 300)), ("TT", (0, 0, 0), (1300, 1400, 300)),
+                                             ("TN", (4, 0, 2), (1300, 1400, 300)), ("NT", (0, 0, 0), (1300, 1400, 300))])
 def test_relayout_bitwise_equal_to_kn3_in_place(emm, monkeypatch, trans, pad, shape):
     """TN / TMA-illegal FFMA calls: copy pass (PK_RAWT transpose of the
     smaller TN operand, PK_RAW re-pitch of an illegal one) + KN3b, two or three
@@ -107,7 +110,7 @@ def test_relayout_bitwise_equal_to_kn3_in_place(emm, monkeypatch, trans, pad, sh
     n0 = emm.launch_count()
     G3 = case.run(emm, "ffma")
     assert emm.launch_count() - n0 == 1
-    assert 2 <= n_relayout <= 5, n_relayout
+    assert (1 if (trans == "NT" and pad == (0, 0, 0)) else 2) <= n_relayout <= 5, n_relayout
     assert torch.equal(G.view(torch.int32), G3.view(torch.int32)), "relayout + KN3b and KN3 differ"
     case.check_untouched(G)
     R, S, T, st = case.oracle()
