@@ -171,18 +171,25 @@ __global__ void __launch_bounds__(FB_THREADS, 1) ffma_sgemm_kernel(int64_t M, in
         __syncthreads();
     }
 
-    // epilogue: alpha*acc + beta*C (C not read when beta == 0), predicated
+    // epilogue: alpha*acc + beta*C (C not read when beta == 0), predicated;
+    // a column's 8 C_in loads are issued before its stores (a store could
+    // alias a later load through ldc: one round trip each otherwise)
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
         const int64_t col = n0 + (j < 4 ? tn * 4 + j : 64 + tn * 4 + (j - 4));
         if (col >= N) continue;
+        float cin[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int64_t row = m0 + (i < 4 ? tm * 4 + i : 64 + tm * 4 + (i - 4));
+            cin[i] = (beta != 0.0f && row < M) ? C[row + col * ldc] : 0.0f;
+        }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             const int64_t row = m0 + (i < 4 ? tm * 4 + i : 64 + tm * 4 + (i - 4));
             if (row < M) {
                 const float v = master[(i * 8 + j) * FB_THREADS + tid];
-                float *d = C + row + col * ldc;
-                *d = beta == 0.0f ? alpha * v : fmaf(beta, *d, alpha * v);
+                C[row + col * ldc] = beta == 0.0f ? alpha * v : fmaf(beta, cin[i], alpha * v);
             }
         }
     }
