@@ -3,7 +3,9 @@ structured cases): random M, N, K (log-uniform, 1..3000 / 1..5000), trans,
 leading-dimension padding, alpha / beta (including 0), math mode, data
 distribution and the policy switches (tiny-kernel threshold, re-buffered vs
 direct operands, stream-K forced / off, skinny path off, 1xTF32 256x512 tiles
-forced, the FFMA kernel without TMA, preferred clusters of 4 forced / off).  Each case checks
+forced, the FFMA kernel without TMA, preferred clusters of 4 forced / off;
+round 2: FFMA relayout / NT threshold / split-K, skinny split-K / block rows /
+B' transpose, 1xTF32 on truncated operands).  Each case checks
 the tolerance predicate against the oracle (every entry, or sampled rows for
 large cases), that ldc padding and the guard region keep their sentinel, and
 that A and B are not written.
@@ -58,6 +60,15 @@ def _cases():
         out[-1]["env"]["EMM_SKINNY_TC"] = rng.choice([None, None, "1"])   # KN9T at any size
         out[-1]["env"]["EMM_CSK"] = rng.choice([None, None, "1"])          # cluster split-K
         out[-1]["env"]["EMM_XS_RN"] = rng.choice([None, None, None, "1"])  # KN1X with rounded big parts
+        # round-2 switches: FFMA relayout / NT threshold / split-K, skinny
+        # split-K / block rows / B' transpose, 1xTF32 on truncated operands
+        out[-1]["env"]["EMM_FFMA_NORELAYOUT"] = rng.choice([None, None, None, "1"])
+        out[-1]["env"]["EMM_FFMA_NT_MIN"] = rng.choice([None, None, "0", "256"])
+        out[-1]["env"]["EMM_FFMA_SPLITS"] = rng.choice([None, None, "1", "3"])
+        out[-1]["env"]["EMM_SKINNY_SPLITS"] = rng.choice([None, None, "1", "4"])
+        out[-1]["env"]["EMM_SKINNY_TPB"] = rng.choice([None, None, "224", "256"])
+        out[-1]["env"]["EMM_SKINNY_BT"] = rng.choice([None, None, "0"])
+        out[-1]["env"]["EMM_TMA_TRUNC"] = rng.choice([None, None, None, "1"])
     return out
 
 
