@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(TX_THREADS, 1)
                  const __grid_constant__ CUtensorMap tmC, int M, int N, int Kp, float alpha, float beta, float *C,
                  int64_t ldc, int tiles_m, int tiles_n, int group_m, int kc_stages,
                  unsigned int *__restrict__ wave_ctr, int splits, float *__restrict__ partial, const TcSk sk,
-                 const __grid_constant__ PeerOut peers, const float *acc_init, int64_t ld_init) {
+                 const __grid_constant__ PeerOut peers, const float *acc_init, int64_t ld_init, int early) {
     if (threadIdx.x == 0) EMM_TL(0);
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -107,7 +107,83 @@ __global__ void __launch_bounds__(TX_THREADS, 1)
     const int cid = CSK ? pairc * ntile + (int)(blockIdx.x / (2 * splits)) : (int)(blockIdx.x >> 1);
     const TcSched S(tiles_m, tiles_n, group_m, Kp, splits, sk.dp_tiles, TC_SK_CHUNK, nclus, cid);
 
-    if (threadIdx.x == 0) {
+    const int n_it = S.n_items;
+    // ===== TMA producer state (warp 1, one lane; each CTA: its 128 rows of A
+    // and of B, raw).  The producer's barriers are its own CTA's, so it
+    // issues the first ring pass between the cluster barrier's arrive and its
+    // wait, overlapping the pair's TMEM allocation / cluster handshake
+    // (griddepcontrol.wait first: A and B may be written by the previous
+    // kernel).  EMM_XS_EARLY=0 issues after the full handshake.
+    const bool producer = warp == 1 && lane == 0;
+    const uint64_t pol = policy_evict_normal();
+    int p_i = 0, p_kb = 0, p_kb1 = 0, p_it = 0, cur_wave = 0;
+    unsigned int done_target = 0;
+    bool lockstep = wave_ctr != nullptr, p_open = false;
+    int arow = 0, brow = 0;
+    // one K-stage of loads; false when the unit list is exhausted
+    auto produce = [&]() -> bool {
+        while (!p_open || p_kb >= p_kb1) {
+            if (p_open) {
+                // the item is done: wave counter, next item
+                if (wave_ctr && (p_i + 1 == n_it || S.wave_of(p_i + 1) != cur_wave))
+                    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(wave_ctr) : "memory");
+                ++p_i;
+                p_open = false;
+            }
+            if (p_i >= n_it) return false;
+            const int w = S.wave_of(p_i);
+            if (w != cur_wave || p_i == 0) {
+                if (w > 0 && lockstep) {
+                    // wave lockstep (tc_kernel.cuh): an L2 optimisation, dropped
+                    // after ~1 ms if the grid is not co-resident
+                    for (int v = cur_wave; v < w; ++v) done_target += 2u * (unsigned)S.pairs_in_wave(v);
+                    const long long t0 = clock64();
+                    while (true) {
+                        unsigned int v;
+                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(wave_ctr) : "memory");
+                        if (v >= done_target) break;
+                        __nanosleep(128);
+                        if (clock64() - t0 > TC_LOCKSTEP_TIMEOUT) {
+                            lockstep = false;
+                            break;
+                        }
+                    }
+                }
+                cur_wave = w;
+            }
+            TcWork wk;
+            S.item(p_i, wk);
+            arow = wk.m0 + (int)rank * TC_BM;
+            brow = wk.n0 + (int)rank * TC_BM;
+            p_kb = wk.kb0;
+            p_kb1 = wk.kb1;
+            p_open = true;
+        }
+        const int s = p_it % TX_STAGES;
+        const uint32_t ph = (uint32_t)(p_it / TX_STAGES) & 1u;
+        mbar_wait(&empty[s], ph ^ 1u);
+        mbar_arrive_expect_tx(&rawfull[s], 2u * TC_TILE_BYTES);
+        const uint32_t st = smem_u32(smem + s * TX_STAGE_BYTES);
+        auto load = [&](const CUtensorMap *tm, uint32_t dst, int row0, bool mn) {
+            if (mn) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    tma_load_2d(dst + c * 4096, tm, &rawfull[s], row0 + 32 * c, p_kb * TC_BK, pol);
+            } else {
+                tma_load_2d(dst, tm, &rawfull[s], p_kb * TC_BK, row0, pol);
+            }
+        };
+        load(&tmA, st, arow, A_MN);
+        load(&tmB, st + 2 * TC_TILE_BYTES, brow, B_MN);
+        ++p_kb;
+        ++p_it;
+        return true;
+    };
+
+    if (producer) {
+        prefetch_tmap(&tmA);
+        prefetch_tmap(&tmB);
+        if (TMAC) prefetch_tmap(&tmC);
         for (int s = 0; s < TX_STAGES; ++s) {
             mbar_init(&full[s], 2 * TX_XF_WARPS);   // leader's: transform warps of both CTAs
             mbar_init(&empty[s], 1);                // the pair's stage-release commit
@@ -122,15 +198,18 @@ __global__ void __launch_bounds__(TX_THREADS, 1)
         fence_mbar_init();
         EMM_TL(8);
     }
-    if (warp == 1 && lane == 0) {
-        prefetch_tmap(&tmA);
-        prefetch_tmap(&tmB);
-        if (TMAC) prefetch_tmap(&tmC);
-    }
     if (warp == 0) tmem_alloc_2sm<TC_TMEM_COLS>(tmem_slot);
     if (warp == 0 && lane == 0) EMM_TL(9);
     tc_fence_before();
-    cluster_sync();
+    __syncwarp();
+    cluster_arrive();
+    if (producer && early) {
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        for (int k = 0; k < TX_STAGES; ++k)
+            if (!produce()) break;
+    }
+    __syncwarp();
+    cluster_wait();
     if (threadIdx.x == 0) EMM_TL(10);
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
@@ -140,64 +219,13 @@ __global__ void __launch_bounds__(TX_THREADS, 1)
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (threadIdx.x == 0) EMM_TL(2);
 
-    const int n_it = S.n_items;
     if (warp < TX_XF_WARP0) {
         setmaxnreg_dec<TX_REGS_WG0>();
         if (warp == 0 && rank == 0 && lane == 0) {
             tc_mma_loop<3, A_MN, B_MN, A_MN, B_MN, 2, TX_STAGES, TX_STAGE_BYTES, CSK>(
                 S, smem, full, empty, acc_full, acc_empty, tmem_base, kc_stages, 2, pairc);
-        } else if (warp == 1 && lane == 0) {
-            // ===== TMA producer (each CTA: its 128 rows of A and of B, raw) =====
-            const uint64_t pol = policy_evict_normal();
-            int it = 0;
-            unsigned int done_target = 0;
-            int cur_wave = 0;
-            bool lockstep = wave_ctr != nullptr;
-            for (int i = 0; i < n_it; ++i) {
-                const int w = S.wave_of(i);
-                if (w != cur_wave || i == 0) {
-                    if (w > 0 && lockstep) {
-                        // wave lockstep (tc_kernel.cuh): an L2 optimisation, dropped
-                        // after ~1 ms if the grid is not co-resident
-                        for (int v = cur_wave; v < w; ++v) done_target += 2u * (unsigned)S.pairs_in_wave(v);
-                        const long long t0 = clock64();
-                        while (true) {
-                            unsigned int v;
-                            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(wave_ctr) : "memory");
-                            if (v >= done_target) break;
-                            __nanosleep(128);
-                            if (clock64() - t0 > TC_LOCKSTEP_TIMEOUT) {
-                                lockstep = false;
-                                break;
-                            }
-                        }
-                    }
-                    cur_wave = w;
-                }
-                TcWork wk;
-                S.item(i, wk);
-                const int arow = wk.m0 + (int)rank * TC_BM;
-                const int brow = wk.n0 + (int)rank * TC_BM;
-                for (int kb = wk.kb0; kb < wk.kb1; ++kb, ++it) {
-                    const int s = it % TX_STAGES;
-                    const uint32_t ph = (uint32_t)(it / TX_STAGES) & 1u;
-                    mbar_wait(&empty[s], ph ^ 1u);
-                    mbar_arrive_expect_tx(&rawfull[s], 2u * TC_TILE_BYTES);
-                    const uint32_t st = smem_u32(smem + s * TX_STAGE_BYTES);
-                    auto load = [&](const CUtensorMap *tm, uint32_t dst, int row0, bool mn) {
-                        if (mn) {
-#pragma unroll
-                            for (int c = 0; c < 4; ++c)
-                                tma_load_2d(dst + c * 4096, tm, &rawfull[s], row0 + 32 * c, kb * TC_BK, pol);
-                        } else {
-                            tma_load_2d(dst, tm, &rawfull[s], kb * TC_BK, row0, pol);
-                        }
-                    };
-                    load(&tmA, st, arow, A_MN);
-                    load(&tmB, st + 2 * TC_TILE_BYTES, brow, B_MN);
-                }
-                if (wave_ctr && (i + 1 == n_it || S.wave_of(i + 1) != cur_wave))
-                    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(wave_ctr) : "memory");
+        } else if (producer) {
+            while (produce()) {
             }
         }
     } else if (warp < TX_EPI_WARP0) {
@@ -348,6 +376,8 @@ static cudaError_t launch_tx_t(const TcPlane &pa, const TcPlane &pb, int64_t M, 
     }
     const int64_t clusters = sk.slots ? pairs : (units < pairs ? units : pairs);
     const int kc_stages = 256 / TC_BK;
+    const char *eearly = getenv("EMM_XS_EARLY");
+    const int early = (eearly && eearly[0] == '0') ? 0 : 1;
     cudaEvent_t ev = nullptr;
     prof_begin(s, true, &ev);
     {
@@ -378,7 +408,7 @@ static cudaError_t launch_tx_t(const TcPlane &pa, const TcPlane &pb, int64_t M, 
         auto launch = [&]() {
             return cudaLaunchKernelEx(&cfg, kern, ta, tb, tcm, (int)M, (int)N, (int)Kp, alpha, beta, C, ldc, tiles_m,
                                       tiles_n, 8, kc_stages, wc, splits, splits > 1 ? partial : nullptr, sk, peers,
-                                      acc_init, ld_init);
+                                      acc_init, ld_init, early);
         };
         // cluster split-K (sub-wave shapes, S <= 4 splits): one cluster of S
         // pairs per tile, reduced over DSMEM in the same kernel.  Opt-in
@@ -400,7 +430,7 @@ static cudaError_t launch_tx_t(const TcPlane &pa, const TcPlane &pb, int64_t M, 
             cudaError_t ce = cudaLaunchKernelEx(&c2, tc_xs_kernel<A_MN, B_MN, false, false, true>, ta, tb, tcm, (int)M,
                                                 (int)N, (int)Kp, alpha, beta, C, ldc, tiles_m, tiles_n, 8, kc_stages,
                                                 (unsigned int *)nullptr, splits, (float *)nullptr, sk, peers,
-                                                (const float *)nullptr, (int64_t)0);
+                                                (const float *)nullptr, (int64_t)0, early);
             if (ce == cudaSuccess) {
                 g_launches.fetch_add(1, std::memory_order_relaxed);
                 prof_end(s, true, ev);
