@@ -525,7 +525,8 @@ int tc_splits(int64_t M, int64_t N, int64_t K) {
     const int64_t nkb = tc_kpad(K) / TC_BK;
     const int64_t clusters = tc_num_sms() / 2;
     int64_t s;
-    if (const char *e = getenv("EMM_SPLITS")) {   // experiments: force S (clamped below)
+    const char *e = getenv("EMM_SPLITS");         // experiments: > 0 forces S (clamped below); 0: the policy
+    if (e && atoi(e) > 0) {
         s = atoi(e);
     } else {
         if (tiles <= 0 || tiles * 2 > clusters) return 1;
