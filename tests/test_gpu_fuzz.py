@@ -10,7 +10,8 @@ the tolerance predicate against the oracle (every entry, or sampled rows for
 large cases), that ldc padding and the guard region keep their sentinel, and
 that A and B are not written.
 
-EMM_FUZZ_CASES (default 48) sets the number of cases; EMM_FUZZ_SEED the seed.
+EMM_FUZZ_CASES (default 48) sets the number of cases; EMM_FUZZ_SEED the seed;
+EMM_FUZZ_MAX_MN the largest M / N (default 3000).
 """
 from __future__ import annotations
 
@@ -26,6 +27,7 @@ from test_gpu_parity import TOL, Case, assert_close
 pytestmark = pytest.mark.gpu
 
 N_CASES = int(os.environ.get("EMM_FUZZ_CASES", "48"))
+MAX_MN = int(os.environ.get("EMM_FUZZ_MAX_MN", "3000"))   # larger extents: EMM_FUZZ_MAX_MN=8000
 SEED = int(os.environ.get("EMM_FUZZ_SEED", "20261019"))
 
 
@@ -45,7 +47,7 @@ def _cases():
     for i in range(N_CASES):
         def lu(lo, hi):
             return int(round(math.exp(rng.uniform(math.log(lo), math.log(hi)))))
-        M, N, K = lu(1, 3000), lu(1, 3000), lu(1, 5000)
+        M, N, K = lu(1, MAX_MN), lu(1, MAX_MN), lu(1, 5000)
         out.append(dict(
             i=i, M=M, N=N, K=K, tA=rng.choice("NT"), tB=rng.choice("NT"),
             pad=(rng.choice([0, 0, 1, 3, 4, 7]), rng.choice([0, 0, 1, 2, 4]), rng.choice([0, 0, 1, 5])),
