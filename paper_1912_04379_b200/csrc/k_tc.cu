@@ -362,16 +362,25 @@ cudaError_t launch_pack(int mode, const PackArgs &a, const PackArgs *b, int64_t 
 // is the 256 x 256 slot (s*tiles + t) in the epilogue's coalesced layout
 // [rank][warp w = h*4 + q][32 float4 column groups][lane] (tc_common.cuh):
 // row = m0 + 128 rank + 32 q + lane, columns n0 + 128 h + 4g .. +3.
-// Block = one (tile, rank, warp) 32 x 128 part: 8 threads per lane-row set,
-// thread handles 4 column groups; grid (tiles * 16, 1).
+// Block = a quarter of one (tile, rank, warp) 32 x 128 part: thread (lane,
+// gq) owns the KN8_J = 2 column groups 8*J*sub + J*gq + j.  The kernel runs
+// after the GEMM's last CTA (its register file leaves no room to co-reside),
+// so its time is the L2 round trips it exposes: every thread issues ALL of
+// its partial loads (S <= KN8_SMAX, one instantiation per S) and its C_in loads before the
+// first add — one round trip instead of one per split — and the grid is
+// 4x finer (a sub-wave GEMM's reduce fits in one wave of resident blocks).
+// Round 2: c2-1024 / c3 reduce tails measured in DESIGN.md §4.
 // =====================================================================
-__global__ void __launch_bounds__(256) splitk_reduce_kernel(const float *__restrict__ P, int S, int M, int N,
+constexpr int KN8_J = 2, KN8_SUB = 32 / (8 * KN8_J), KN8_SMAX = 16;
+template <int S>
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const float *__restrict__ P, int M, int N,
                                                             float alpha, float beta, float *__restrict__ C,
                                                             int64_t ldc, int tiles_m, int tiles_n, int group_m) {
     asm volatile("griddepcontrol.wait;" ::: "memory");   // PDL: the GEMM's partials
-    const int part = blockIdx.x & 15, t = blockIdx.x >> 4;
+    const int sub = blockIdx.x % KN8_SUB, part = (blockIdx.x / KN8_SUB) & 15, t = blockIdx.x / (16 * KN8_SUB);
     const int rank = part >> 3, wslot = part & 7, h = wslot >> 2, q = wslot & 3;
-    const int lane = threadIdx.x & 31, gq = threadIdx.x >> 5;   // 8 x 4 column groups
+    const int lane = threadIdx.x & 31, gq = threadIdx.x >> 5;
+    const int g0 = KN8_J * (8 * sub + gq);   // first of this thread's column groups
     // tile origin: the same grouped raster as the GEMM's schedule
     const int per_group = group_m * tiles_n;
     const int gidx = t / per_group, first_m = gidx * group_m;
@@ -382,41 +391,47 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float *__restr
     const float4 *base = reinterpret_cast<const float4 *>(P) + (size_t)t * (TC_SK_SLOT_FLOATS / 4) +
                          (size_t)wslot * 1024 + (size_t)rank * 8 * 1024 + lane;
     const size_t sstride = (size_t)tiles * (TC_SK_SLOT_FLOATS / 4);
-    float4 acc[4];
+    const int c0 = n0 + 128 * h + 4 * g0;    // first column
+    const bool live = row < M;
+    float cin[4 * KN8_J];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[j] = __ldcg(base + (4 * gq + j) * 32);
-    for (int s = 1; s < S; ++s) {
-        float4 v[4];
+    for (int e = 0; e < 4 * KN8_J; ++e)
+        cin[e] = (live && beta != 0.0f && c0 + e < N) ? C[(int64_t)row + (int64_t)(c0 + e) * ldc] : 0.0f;
+    float4 v[S][KN8_J];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) v[j] = __ldcg(base + (size_t)s * sstride + (4 * gq + j) * 32);
+    for (int s = 0; s < S; ++s)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            acc[j].x += v[j].x;
-            acc[j].y += v[j].y;
-            acc[j].z += v[j].z;
-            acc[j].w += v[j].w;
+        for (int j = 0; j < KN8_J; ++j) v[s][j] = __ldcg(base + (size_t)s * sstride + (g0 + j) * 32);
+    float4 acc[KN8_J];
+#pragma unroll
+    for (int j = 0; j < KN8_J; ++j) acc[j] = v[0][j];
+#pragma unroll
+    for (int s = 1; s < S; ++s)
+#pragma unroll
+        for (int j = 0; j < KN8_J; ++j) {
+            acc[j].x += v[s][j].x;
+            acc[j].y += v[s][j].y;
+            acc[j].z += v[s][j].z;
+            acc[j].w += v[s][j].w;
         }
-    }
-    if (row >= M) return;
+    if (!live) return;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < KN8_J; ++j) {
         const float r[4] = {acc[j].x, acc[j].y, acc[j].z, acc[j].w};
-        const int c0 = n0 + 128 * h + 4 * (4 * gq + j);
-        float cin[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
-            cin[e] = (beta != 0.0f && c0 + e < N) ? C[(int64_t)row + (int64_t)(c0 + e) * ldc] : 0.0f;
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-            if (c0 + e < N)
-                C[(int64_t)row + (int64_t)(c0 + e) * ldc] = beta == 0.0f ? alpha * r[e] : fmaf(beta, cin[e], alpha * r[e]);
+        for (int e = 0; e < 4; ++e) {
+            const int c = c0 + 4 * j + e;
+            if (c < N)
+                C[(int64_t)row + (int64_t)c * ldc] = beta == 0.0f ? alpha * r[e] : fmaf(beta, cin[4 * j + e], alpha * r[e]);
+        }
     }
 }
 
 cudaError_t launch_splitk_reduce(const float *partial, int splits, int64_t M, int64_t N, float alpha, float beta,
                                  float *C, int64_t ldc, cudaStream_t s) {
+    if (splits < 1 || splits > KN8_SMAX) return cudaErrorInvalidValue;
     const int tiles_m = (int)((M + 2 * TC_BM - 1) / (2 * TC_BM)), tiles_n = (int)((N + TC_BN - 1) / TC_BN);
-    const int64_t blocks = (int64_t)tiles_m * tiles_n * 16;
+    const int64_t blocks = (int64_t)tiles_m * tiles_n * 16 * KN8_SUB;
     if (blocks > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
     cudaEvent_t ev = nullptr;
     prof_begin(s, false, &ev);
@@ -430,8 +445,17 @@ cudaError_t launch_splitk_reduce(const float *partial, int splits, int64_t M, in
         at[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        cudaError_t le = cudaLaunchKernelEx(&cfg, splitk_reduce_kernel, partial, splits, (int)M, (int)N, alpha, beta,
-                                            C, ldc, tiles_m, tiles_n, 8);
+        cudaError_t le = cudaErrorInvalidValue;
+        switch (splits) {
+#define EMM_KN8(S_)                                                                                            \
+    case S_:                                                                                                   \
+        le = cudaLaunchKernelEx(&cfg, splitk_reduce_kernel<S_>, partial, (int)M, (int)N, alpha, beta, C, ldc, \
+                                tiles_m, tiles_n, 8);                                                          \
+        break;
+            EMM_KN8(1) EMM_KN8(2) EMM_KN8(3) EMM_KN8(4) EMM_KN8(5) EMM_KN8(6) EMM_KN8(7) EMM_KN8(8)
+            EMM_KN8(9) EMM_KN8(10) EMM_KN8(11) EMM_KN8(12) EMM_KN8(13) EMM_KN8(14) EMM_KN8(15) EMM_KN8(16)
+#undef EMM_KN8
+        }
         if (le != cudaSuccess) return le;
     }
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -532,8 +556,8 @@ int tc_splits(int64_t M, int64_t N, int64_t K) {
         if (tiles <= 0 || tiles * 2 > clusters) return 1;
         s = clusters / tiles;
         if (s > nkb / 4) s = nkb / 4;
-        if (s > 16) s = 16;
     }
+    if (s > 16) s = 16;   // KN8_SMAX: the reduce keeps every split's loads in flight
     if (s < 1) s = 1;
     while (s > 1 && (tiles * s > clusters || ((nkb + s - 1) / s) * (s - 1) >= nkb)) --s;
     return (int)s;
