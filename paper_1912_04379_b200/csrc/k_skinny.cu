@@ -642,12 +642,24 @@ static bool skinny_tma_ok(const SkRoles &R, int64_t K) {
     return tma_legal(R.Ap, R.lda2) && tma_legal(R.Bp, R.ldb2) && !getenv("EMM_SKINNY_NO_TMA") && K > 0;
 }
 
-// K-contiguous long operand with a K-contiguous B' (TA && !TB): B' is first
-// transposed (PK_RAWT, 32 floats a row, zero padded) so the kernel reads
-// [32 k][NC] tiles and pairs columns for FFMA2.  EMM_SKINNY_BT=0 disables.
-static bool skinny_bt(const SkRoles &R) {
+// K-contiguous B' (!TB): B' is first transposed (PK_RAWT, 32 floats a row,
+// zero padded) so the kernel reads [32 k][NC] tiles — with a K-contiguous
+// long operand (TA) it pairs columns for FFMA2; with an MN-contiguous one
+// (!TA, N' > 8) the row-pair kernel reads 4 columns per broadcast instead of
+// 4 k.  EMM_SKINNY_BT=0 disables both.
+static bool skinny_bt(const SkRoles &R, int64_t K) {
     const char *e = getenv("EMM_SKINNY_BT");
-    return R.TA && !R.TB && !(e && e[0] == '0');
+    if (e && e[0] == '0') return false;
+    if (!R.TA && !R.TB) {
+        // MN-contiguous long operand: the [32 k][NC] B' tiles measured ~4 %
+        // faster for N' > 8 (c6 N = 16: 209 -> 202 us incl. the transpose
+        // launch) and slower for N' <= 8 (65536 x 8 x 4096: 173 -> 179 us);
+        // the extra launch pays only on a long operand of >= 2^26 elements.
+        // EMM_SKINNY_BT_NN=0 / 1 forces it off / on.
+        const char *n = getenv("EMM_SKINNY_BT_NN");
+        return n ? n[0] == '1' : R.Nc > 8 && R.Mr * K >= ((int64_t)1 << 26);
+    }
+    return R.TA && !R.TB;
 }
 static size_t skinny_slab_bytes(const SkRoles &R, int64_t K) {
     const SkPlan P = skinny_plan(R.TA, R.Mr, K);
@@ -661,7 +673,7 @@ size_t skinny_split_bytes(bool tA, bool tB, int64_t M, int64_t N, int64_t K, con
                           const float *B, int64_t ldb) {
     const SkRoles R = skinny_roles(tA, tB, M, N, A, lda, B, ldb, 1);
     if (A && B && !skinny_tma_ok(R, K)) return 0;
-    return skinny_slab_bytes(R, K) + (skinny_bt(R) ? (size_t)K * 32 * 4 : 0);
+    return skinny_slab_bytes(R, K) + (skinny_bt(R, K) ? (size_t)K * 32 * 4 : 0);
 }
 
 cudaError_t launch_skinny_sgemm(bool tA, bool tB, int64_t M, int64_t N, int64_t K, float alpha, const float *A,
@@ -681,14 +693,15 @@ cudaError_t launch_skinny_sgemm(bool tA, bool tB, int64_t M, int64_t N, int64_t 
     cudaError_t e;
     if (skinny_tma_ok(R, K)) {
         const size_t slab = skinny_slab_bytes(R, K);
-        if (skinny_bt(R) && ws && ws_bytes >= slab + (size_t)K * 32 * 4) {
+        if (skinny_bt(R, K) && ws && ws_bytes >= slab + (size_t)K * 32 * 4) {
             // B'(p, c) = Bp[p + c*ldb2] -> Bt[p*32 + c], then the TA x TB kernel
             float *Bt = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(ws) + slab);
             PackArgs x;
             x.X = Bp; x.ld = ldb2; x.R = K; x.kcontig = false; x.out0 = Bt; x.ld0 = 32;
             e = launch_pack(PK_RAWT_, x, nullptr, Nc, nullptr, s, 0);
             if (e == cudaSuccess)
-                e = launch_tma<true, true>(Mr, Nc, K, alpha, Ap, lda2, Bt, 32, beta, C, rs, cs, s, ws, slab);
+                e = TA ? launch_tma<true, true>(Mr, Nc, K, alpha, Ap, lda2, Bt, 32, beta, C, rs, cs, s, ws, slab)
+                       : launch_tma<false, true>(Mr, Nc, K, alpha, Ap, lda2, Bt, 32, beta, C, rs, cs, s, ws, slab);
         } else if (!TA && !TB) e = launch_tma<false, false>(Mr, Nc, K, alpha, Ap, lda2, Bp, ldb2, beta, C, rs, cs, s, ws, ws_bytes);
         else if (!TA && TB) e = launch_tma<false, true>(Mr, Nc, K, alpha, Ap, lda2, Bp, ldb2, beta, C, rs, cs, s, ws, ws_bytes);
         else if (TA && !TB) e = launch_tma<true, false>(Mr, Nc, K, alpha, Ap, lda2, Bp, ldb2, beta, C, rs, cs, s, ws, ws_bytes);

@@ -574,3 +574,40 @@ def test_extreme_extents(emm, math, shape, tA, tB):
         assert np.array_equal(G, R.astype(np.float32).astype(np.float64))
     else:
         assert_close(case, Cg, R, S, T, TOL[math], rows=rows)
+
+
+@pytest.mark.parametrize("tA,tB,shape", [("N", "N", (20000, 16, 700)), ("N", "N", (9001, 9, 1500)), ("N", "N", (70001, 16, 1000)),
+                                         ("N", "N", (4000, 12, 9000)), ("T", "T", (16, 30000, 300)),
+                                         ("N", "T", (20000, 16, 700))])
+def test_skinny_bt_nn_bitwise(emm, monkeypatch, tA, tB, shape):
+    """MN-contiguous long operand with a K-contiguous B' and N' > 8 (NN with N
+    short, TT with M short): B' transposed to [k][N'] tiles first
+    (EMM_SKINNY_BT_NN=1; the default for N' > 8 on a long operand of >= 2^26
+    elements) is bitwise equal to reading the [N'][k] tiles directly (=0) —
+    each entry is the same FFMA sequence in increasing k — and within the FP32
+    bound of the oracle; ldc padding untouched."""
+    monkeypatch.setenv("EMM_SKINNY_TC", "0")
+    M, N, K = shape
+    pa = (-(M if tA == "N" else K)) % 4 + 4
+    pb = (-(K if tB == "N" else N)) % 4 + 4
+    case = Case(tA, tB, M, N, K, -0.5, 0.25, kind="normal", pad=(pa, pb, 1), sigma=1.0 / np.sqrt(K))
+    R, S, T, _ = case.oracle()
+    runs = {}
+    for bt in ("1", "0", None):   # forced on, forced off, default policy
+        if bt is None:
+            monkeypatch.delenv("EMM_SKINNY_BT_NN")
+        else:
+            monkeypatch.setenv("EMM_SKINNY_BT_NN", bt)
+        n0 = emm.launch_count()
+        G = case.run(emm, "3xtf32")
+        runs[bt] = (G, emm.launch_count() - n0)
+        case.check_untouched(G)
+        assert_close(case, G, R, S, T, TOL["3xtf32"])
+        assert torch.equal(G.view(torch.int32), runs["1"][0].view(torch.int32))
+    # the transpose launch is there only for a K-contiguous B' (not NT) ...
+    kcontig = (tA, tB) != ("N", "T")
+    assert runs["1"][1] - runs["0"][1] == (1 if kcontig else 0)
+    # ... and by default only for N' > 8 and a long operand of >= 2^26 elements
+    mr, nc = (M, N) if N <= 16 else (N, M)
+    want = kcontig and nc > 8 and mr * K >= 1 << 26
+    assert runs[None][1] == runs["1" if want else "0"][1]

@@ -131,7 +131,8 @@ def test_default_policy(emm, monkeypatch, math, tc):
     big = cached_case("N", "N", 65536, 16, 4096, 1.0, 0.0, kind="uniform")
     n0 = emm.launch_count()
     big.run(emm, math)
-    assert emm.launch_count() - n0 == 1
+    # KN9 after the B' transpose (MN-contiguous long operand of >= 2^26 elements, N' > 8)
+    assert emm.launch_count() - n0 == 2
     # TN: two launches either way (KN9T: split pass + GEMM; KN9: B' transpose +
     # kernel); which kernel ran shows in the bits: KN9 equals the forced-FFMA
     # (EMM_SKINNY_TC=0) result, KN9T (TF32 products) does not
