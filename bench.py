@@ -338,12 +338,22 @@ def main():
             ws = ws[(1024 - ws.data_ptr() % 1024) // 4:]
     comm = emm.Comm(rank, world) if multi else None
     if multi and args.bcast == "ce":
-        comm.register_input(B)
+        try:
+            comm.register_input(B)
+        except emm.EmmError as e:
+            # registration outcomes are agreed across ranks (multi.cu), so
+            # every rank falls back together
+            print(f"rank {rank}: B registration failed ({e}); ncclBroadcast data plane", file=sys.stderr)
+            args.bcast = "nccl"
     C_full = None
     if multi and args.allgather != "none":
         C_full = torch.empty((N, M), dtype=torch.float32, device=dev).t()
         if args.allgather == "fused":
-            comm.register_output(C_full)
+            try:
+                comm.register_output(C_full)
+            except emm.EmmError as e:
+                print(f"rank {rank}: C_full registration failed ({e}); NCCL all-gather", file=sys.stderr)
+                args.allgather = "nccl"
 
     def make_step(math):
         def step():

@@ -144,6 +144,11 @@ int64_t emm_multi_panel_cols(int64_t N);
  * caller (e.g. torch.distributed broadcast).  Returns EMM_ERR_COMM if NCCL
  * cannot be loaded. */
 int emm_get_unique_id(void *id128);
+/* Collective (NCCL communicator over `nranks` processes, one GPU each).  It
+ * also maps every peer's flag words by CUDA IPC for the copy-engine data
+ * plane; if any rank cannot map them, every rank still gets a working
+ * communicator for the NCCL data plane and the registrations below then fail
+ * with EMM_ERR_COMM on every rank. */
 int emm_comm_create(void **comm, const void *id128, int nranks, int rank);
 int emm_comm_destroy(void *comm);
 
@@ -178,16 +183,22 @@ int emm_sgemm_multi(void *comm, char transA, char transB, int64_t M, int64_t N, 
  * exchanged over NCCL and the peers' buffers mapped.  Afterwards
  * emm_sgemm_multi(..., C_full = that buffer, ldc_full) fuses the all-gather
  * into the GEMM: each rank's epilogue stores its C rows into every rank's
- * C_full over NVLink (tensor-core modes), followed by a stream-ordered
- * completion all-reduce.  The buffer must stay allocated until
- * emm_comm_unregister_output / emm_comm_destroy. */
+ * C_full over NVLink (tensor-core modes; other modes copy their rows), and
+ * each rank then stores the call's epoch into every rank's "done" words and
+ * waits for all of them (stream-ordered, no NCCL collective).  The buffer must stay allocated until
+ * emm_comm_unregister_output / emm_comm_destroy.  The outcome is agreed
+ * across ranks: 0 on every rank, or EMM_ERR_COMM on every rank (a rank could
+ * not export or map a buffer; nothing stays registered, and emm_sgemm_multi
+ * with that C_full uses the NCCL all-gather). */
 int emm_comm_register_output(void *comm, float *C_full, int64_t ld_full);
 int emm_comm_unregister_output(void *comm);
 
 /* Collective: register this rank's B buffer (`bytes` >= the stored size of
  * B of the calls that use it; the source on root, the receive buffer
  * elsewhere).  Only the ring successor's buffer is mapped (CUDA IPC).  Must
- * stay allocated until emm_comm_unregister_input / emm_comm_destroy. */
+ * stay allocated until emm_comm_unregister_input / emm_comm_destroy.  The
+ * outcome is agreed across ranks as for emm_comm_register_output (on
+ * EMM_ERR_COMM, B is broadcast by NCCL). */
 int emm_comm_register_input(void *comm, float *B, size_t bytes);
 int emm_comm_unregister_input(void *comm);
 

@@ -150,6 +150,7 @@ struct Comm {
     // flag words: own array and every peer's (IPC-mapped; own = flags)
     uint32_t *flags = nullptr;
     uint32_t *peer_flags[MAXR] = {};
+    bool ce_ok = true;   // peers' flag words mapped (copy-engine data plane possible; same on every rank)
     void *flags_opened[MAXR] = {};
     // registered input (B receive buffer) and the successor's, mapped
     float *in_local = nullptr;
@@ -182,6 +183,7 @@ struct IpcBlob {
     cudaIpcMemHandle_t h;
     int64_t offset;   // bytes from the allocation base to the registered pointer
     int64_t a, b;     // ld / size, checked for consistency
+    int64_t st;       // the sender's local status (0: the handle is valid)
 };
 
 int nccl_status(ncclResult_t r) { return r == ncclSuccess ? 0 : EMM_ERR_NCCL_BASE + (int)r; }
@@ -208,27 +210,57 @@ cudaEvent_t ev_at(Comm *c, size_t i) {
 }
 
 // IPC handle of the allocation holding `p` (+ offset), all-gathered over NCCL.
+// Every rank takes part in the exchange even when its own handle could not be
+// made (its blob then carries the failure), so a local error never leaves the
+// other ranks waiting in the collective; the result is uniform: 0 on every
+// rank, or an error on every rank.
 int ipc_allgather(Comm *c, const void *p, int64_t a, int64_t b, std::vector<IpcBlob> &all) {
     Nccl &n = nccl();
     auto rf = range_fn();
     CUdeviceptr base = 0;
     size_t size = 0;
-    if (!rf || rf(&base, &size, reinterpret_cast<CUdeviceptr>(p)) != CUDA_SUCCESS) return EMM_ERR_COMM;
     IpcBlob mine{};
-    int st = cuda_st(cudaIpcGetMemHandle(&mine.h, reinterpret_cast<void *>(base)));
-    if (st) return st;
+    int lst = (!rf || rf(&base, &size, reinterpret_cast<CUdeviceptr>(p)) != CUDA_SUCCESS) ? EMM_ERR_COMM : 0;
+    if (!lst) lst = cuda_st(cudaIpcGetMemHandle(&mine.h, reinterpret_cast<void *>(base)));
     mine.offset = (int64_t)(reinterpret_cast<CUdeviceptr>(p) - base);
     mine.a = a;
     mine.b = b;
+    mine.st = lst;
     IpcBlob *dev = nullptr;
-    if ((st = cuda_st(cudaMalloc(&dev, sizeof(IpcBlob) * (c->nranks + 1))))) return st;
+    int st = cuda_st(cudaMalloc(&dev, sizeof(IpcBlob) * (c->nranks + 1)));
+    if (st) return st;   // no buffer to take part with (device out of memory)
     all.assign(c->nranks, IpcBlob{});
     st = cuda_st(cudaMemcpy(dev + c->nranks, &mine, sizeof mine, cudaMemcpyHostToDevice));
     if (!st) st = nccl_status(n.allGather(dev + c->nranks, dev, sizeof(IpcBlob), ncclUint8, c->nc, c->comm_stream));
     if (!st) st = cuda_st(cudaStreamSynchronize(c->comm_stream));
     if (!st) st = cuda_st(cudaMemcpy(all.data(), dev, sizeof(IpcBlob) * c->nranks, cudaMemcpyDeviceToHost));
     cudaFree(dev);
-    return st;
+    if (st) return st;
+    for (const IpcBlob &x : all)   // (own blob included: the same code on every rank)
+        if (x.st) return EMM_ERR_COMM;   // some rank could not export its buffer
+    return 0;
+}
+
+// Collective agreement on a registration's outcome: every rank contributes
+// its local status (e.g. of opening the peers' handles) and returns the same
+// verdict (0 only if every rank succeeded).
+int agree(Comm *c, int lst) {
+    if (c->nranks == 1) return lst;
+    Nccl &n = nccl();
+    int64_t *dev = nullptr;
+    int st = cuda_st(cudaMalloc(&dev, sizeof(int64_t) * (c->nranks + 1)));
+    if (st) return st;
+    const int64_t mine = lst;
+    std::vector<int64_t> all(c->nranks, 0);
+    st = cuda_st(cudaMemcpy(dev + c->nranks, &mine, sizeof mine, cudaMemcpyHostToDevice));
+    if (!st) st = nccl_status(n.allGather(dev + c->nranks, dev, sizeof(int64_t), ncclUint8, c->nc, c->comm_stream));
+    if (!st) st = cuda_st(cudaStreamSynchronize(c->comm_stream));
+    if (!st) st = cuda_st(cudaMemcpy(all.data(), dev, sizeof(int64_t) * c->nranks, cudaMemcpyDeviceToHost));
+    cudaFree(dev);
+    if (st) return st;
+    for (int64_t x : all)   // (own status included: the same code on every rank)
+        if (x) return EMM_ERR_COMM;
+    return 0;
 }
 
 int ipc_open(const IpcBlob &b, void **opened, void **ptr) {
@@ -353,14 +385,32 @@ extern "C" int emm_comm_create(void **comm, const void *id128, int nranks, int r
     if (!st && nranks > 1) {
         std::vector<IpcBlob> all;
         st = ipc_allgather(c, c->flags, FL_WORDS, 0, all);
-        for (int r = 0; r < nranks && !st; ++r) {
-            if (r == rank) {
-                c->peer_flags[r] = c->flags;
-                continue;
+        if (!st) {   // (an exchange error is uniform; an open error is agreed below)
+            int ost = 0;
+            for (int r = 0; r < nranks && !ost; ++r) {
+                if (r == rank) {
+                    c->peer_flags[r] = c->flags;
+                    continue;
+                }
+                void *p = nullptr;
+                ost = ipc_open(all[r], &c->flags_opened[r], &p);
+                c->peer_flags[r] = static_cast<uint32_t *>(p);
             }
-            void *p = nullptr;
-            st = ipc_open(all[r], &c->flags_opened[r], &p);
-            c->peer_flags[r] = static_cast<uint32_t *>(p);
+            st = agree(c, ost);
+        }
+        if (st && st != EMM_ERR_COMM) {
+            // (NCCL / CUDA failure of the exchange itself: the communicator is unusable)
+        } else if (st) {
+            // some rank cannot map its peers' memory (no CUDA IPC / P2P): every
+            // rank keeps the communicator for the NCCL data plane only; the
+            // registrations of the copy-engine plane then fail on every rank
+            for (int r = 0; r < nranks; ++r) {
+                if (c->flags_opened[r]) cudaIpcCloseMemHandle(c->flags_opened[r]);
+                c->flags_opened[r] = nullptr;
+                c->peer_flags[r] = nullptr;
+            }
+            c->ce_ok = false;
+            st = 0;
         }
     } else if (!st) {
         c->peer_flags[0] = c->flags;
@@ -435,18 +485,24 @@ extern "C" int emm_comm_register_output(void *comm, float *C_full, int64_t ld_fu
         c->out_ld = ld_full;
         return 0;   // peers resolved at call time (registration order is free)
     }
-    if (!nccl().ok) return EMM_ERR_COMM;
+    if (!nccl().ok || !c->ce_ok) return EMM_ERR_COMM;
     std::vector<IpcBlob> all;
     int st = c->nranks > 1 ? ipc_allgather(c, C_full, ld_full, 0, all) : 0;
-    for (int r = 0; r < c->nranks && !st; ++r) {
-        if (r == c->rank) {
-            c->out_peer[r] = C_full;
-            continue;
+    if (!st && c->nranks > 1) {
+        int ost = 0;
+        for (int r = 0; r < c->nranks && !ost; ++r) {
+            if (r == c->rank) {
+                c->out_peer[r] = C_full;
+                continue;
+            }
+            if (all[r].a != ld_full) ost = EMM_ERR_COMM;   // identical layouts required
+            void *p = nullptr;
+            if (!ost) ost = ipc_open(all[r], &c->out_opened[r], &p);
+            c->out_peer[r] = static_cast<float *>(p);
         }
-        if (all[r].a != ld_full) st = EMM_ERR_COMM;   // identical layouts required
-        void *p = nullptr;
-        if (!st) st = ipc_open(all[r], &c->out_opened[r], &p);
-        c->out_peer[r] = static_cast<float *>(p);
+        st = agree(c, ost);
+    } else if (!st) {
+        c->out_peer[0] = C_full;
     }
     if (st) {
         emm_comm_unregister_output(comm);
@@ -488,17 +544,21 @@ extern "C" int emm_comm_register_input(void *comm, float *B, size_t bytes) {
         c->in_bytes = bytes;
         return 0;
     }
-    if (!nccl().ok) return EMM_ERR_COMM;
+    if (!nccl().ok || !c->ce_ok) return EMM_ERR_COMM;
     int st = 0;
     if (c->nranks > 1) {
         std::vector<IpcBlob> all;
         st = ipc_allgather(c, B, 0, (int64_t)bytes, all);
-        const int succ = (c->rank + 1) % c->nranks;
-        for (int r = 0; r < c->nranks && !st; ++r)
-            if ((size_t)all[r].b != bytes) st = EMM_ERR_COMM;
-        void *p = nullptr;
-        if (!st) st = ipc_open(all[succ], &c->in_opened, &p);
-        c->in_succ = static_cast<float *>(p);
+        if (!st) {
+            const int succ = (c->rank + 1) % c->nranks;
+            int ost = 0;
+            for (int r = 0; r < c->nranks && !ost; ++r)
+                if ((size_t)all[r].b != bytes) ost = EMM_ERR_COMM;
+            void *p = nullptr;
+            if (!ost) ost = ipc_open(all[succ], &c->in_opened, &p);
+            c->in_succ = static_cast<float *>(p);
+            st = agree(c, ost);
+        }
     }
     if (st) {
         emm_comm_unregister_input(comm);
