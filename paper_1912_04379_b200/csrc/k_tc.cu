@@ -206,6 +206,24 @@ __device__ __forceinline__ void pack_lines(const PackOperand &op, int64_t blk) {
         return keep ? __ldg(reinterpret_cast<const float4 *>(p)) : __ldcs(reinterpret_cast<const float4 *>(p));
     };
     auto ld1 = [](const float *p) { return keep ? __ldg(p) : __ldcs(p); };
+    if (MODE == PK_RAW && !op.vec) {
+        // re-pitch of a line that is not 16-byte aligned: scalar copies with
+        // consecutive threads on consecutive elements (one 128-B segment per
+        // warp access, all 16 loads in flight before the stores); the 8-wide
+        // groups below would touch each sector from 8 instructions
+        float w[PK_GROUPS * 8];
+#pragma unroll
+        for (int i = 0; i < PK_GROUPS * 8; ++i) {
+            const int64_t e = e0 + (int64_t)i * PK_THREADS + threadIdx.x;
+            w[i] = e < L ? ld1(src + e) : 0.0f;
+        }
+#pragma unroll
+        for (int i = 0; i < PK_GROUPS * 8; ++i) {
+            const int64_t e = e0 + (int64_t)i * PK_THREADS + threadIdx.x;
+            if (e < Lext) o0[e] = w[i];
+        }
+        return;
+    }
     float v[PK_GROUPS][8];
 #pragma unroll
     for (int g = 0; g < PK_GROUPS; ++g) {
