@@ -215,28 +215,35 @@ def test_cluster_splitk_bitwise_equal_to_global_splitk(emm, monkeypatch, shape, 
     assert_close(case, Cc, R, S, T, 1e-5, rows=rows)
 
 
+@pytest.mark.parametrize("math", ["3xtf32", "1xtf32"])
 @pytest.mark.parametrize("tA", ["N", "T"])
 @pytest.mark.parametrize("tB", ["N", "T"])
 @pytest.mark.parametrize("shape", [(1531, 997, 2049), (520, 388, 200), (3000, 2100, 700)])
-def test_repitched_illegal_ld_bitwise_equal_to_legal(emm, tA, tB, shape):
+def test_repitched_illegal_ld_bitwise_equal_to_legal(emm, math, tA, tB, shape):
     """A TMA-illegal leading dimension (stored rows + 13 / + 7, c3's reading)
-    makes KN1X run on a raw re-pitched copy (PK_RAW): the same operand values
-    as a TMA-legal layout of the same matrices, so the same bits."""
+    makes KN1X (3xTF32) run on a raw re-pitched copy (PK_RAW): the same
+    operand values as a TMA-legal layout of the same matrices, so the same
+    bits.  1xTF32 re-buffers an illegal layout into TF32 planes (the pass
+    rounds exactly as the direct path's TMA does, R7c): the same bits as the
+    legal layout's direct call.  (A re-pitch + direct 1xTF32 variant gave the
+    same bits and measured no faster at c3: TN 35.8 = 35.8 us, TT 35.8 ->
+    37.9 us; not kept.)"""
     M, N, K = shape
     bad = Case(tA, tB, M, N, K, -0.75, 1.25, kind="normal", pad=(13, 7, 5))
     ar = M if tA == "N" else K
     br = K if tB == "N" else N
     good = Case(tA, tB, M, N, K, -0.75, 1.25, kind="normal", pad=((-ar) % 4 + 4, (-br) % 4, 5))
     n0 = emm.launch_count()
-    Cb = bad.run(emm, "3xtf32")
+    Cb = bad.run(emm, math)
     nb = emm.launch_count() - n0
-    Cg = good.run(emm, "3xtf32")
+    Cg = good.run(emm, math)
     bad.check_untouched(Cb)
     assert torch.equal(torch.from_numpy(bad.logical(Cb)), torch.from_numpy(good.logical(Cg)))
     assert nb <= 3   # re-pitch + GEMM (+ split-K reduce)
     rows = np.r_[0:8, M - 8:M]
     R, S, T, _ = bad.oracle(rows=rows)
-    assert_close(bad, Cb, R, S, T, 1e-5, rows=rows)
+    assert_close(bad, Cb, R, S, T, 1e-5 if math == "3xtf32" else 5e-3, rows=rows)
+
 
 
 @pytest.mark.parametrize("which", ["A", "B", "AB"])
