@@ -12,7 +12,7 @@ import sys
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-FINAL = os.path.join(ROOT, "profiles", "r02_bench_v5.jsonl")
+FINAL = os.path.join(ROOT, "profiles", "r02_bench_v6.jsonl")
 
 
 def last_line(path):
