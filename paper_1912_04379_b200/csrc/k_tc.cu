@@ -560,7 +560,9 @@ int tc_num_sms() {
 }
 
 // Split-K factor for sub-wave problems: enough (tile,
-// split) units to fill the CTA pairs, each split >= 4 K-stages (128 of K).
+// split) units to fill the CTA pairs, each split >= 2 K-stages (64 of K;
+// late round 2: 4 stages measured slower at 512^3 3xTF32, 19.4 vs 17.4 us
+// with S = 8, profiles/r02_ab_kn8.md).
 // units = tiles * S <= CTA pairs (one wave).
 int tc_splits(int64_t M, int64_t N, int64_t K) {
     const int64_t tiles = ((M + 2 * TC_BM - 1) / (2 * TC_BM)) * ((N + TC_BN - 1) / TC_BN);
@@ -573,7 +575,7 @@ int tc_splits(int64_t M, int64_t N, int64_t K) {
     } else {
         if (tiles <= 0 || tiles * 2 > clusters) return 1;
         s = clusters / tiles;
-        if (s > nkb / 4) s = nkb / 4;
+        if (s > nkb / 2) s = nkb / 2;
     }
     if (s > 16) s = 16;   // KN8_SMAX: the reduce keeps every split's loads in flight
     if (s < 1) s = 1;

@@ -197,6 +197,7 @@ def test_cluster_splitk_bitwise_equal_to_global_splitk(emm, monkeypatch, shape, 
     pairs per tile, reduced over DSMEM (CSK, opt-in EMM_CSK=1); EMM_CSK=0 runs
     the same splits through HBM slots + the fixed-order reduce launch: same
     order, same bits, one launch less."""
+    monkeypatch.setenv("EMM_SPLITS", "4")   # CSK covers S <= 4 (the policy gives 512^3 S = 8); clamped per shape
     M, N, K = shape
     case = cached_case("N", "N", M, N, K, -0.75, beta, kind="normal", pad=((-M) % 4, (-K) % 4, 1))
     monkeypatch.setenv("EMM_CSK", "1")
